@@ -1,0 +1,50 @@
+// Shared host/device helpers of libpgti (error plumbing, launch helpers, small math).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstddef>
+
+#include "pgti.h"
+
+namespace pgti {
+
+// Records `st` with a printf-style message in the thread-local error buffer and returns it.
+pgti_status fail(pgti_status st, const char *fmt, ...);
+void clear_error();
+// Device address of the sticky error-flag word (bit 1: out of range, bit 2: non-finite).
+unsigned *device_error_flag();
+
+enum : unsigned { kDevErrRange = 1u, kDevErrNonfinite = 2u };
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+constexpr int kNumSMs = 148;  // B200
+
+}  // namespace pgti
+
+#define PGTI_REQUIRE(cond, status, ...)                     \
+  do {                                                      \
+    if (!(cond)) return ::pgti::fail((status), __VA_ARGS__); \
+  } while (0)
+
+#define PGTI_CUDA_TRY(call)                                                                 \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return ::pgti::fail(PGTI_ERR_CUDA, "%s failed: %s (%s:%d)", #call,                   \
+                          cudaGetErrorString(e_), __FILE__, __LINE__);                      \
+  } while (0)
+
+#define PGTI_LAUNCH_TRY() PGTI_CUDA_TRY(cudaGetLastError())
+
+#define PGTI_STATUS_TRY(expr)              \
+  do {                                     \
+    pgti_status s_ = (expr);               \
+    if (s_ != PGTI_OK) return s_;          \
+  } while (0)

@@ -1,0 +1,418 @@
+// pgti_dcrnn_step: one forward + BPTT pass of the stepwise stacked DCGRU over one gathered
+// batch, plus the diffusion test hooks.  Orchestration only: every arithmetic step runs in the
+// kernels of spmm.cu (K2), gemm_simt.cu (K3'/K4/K5) and elementwise.cu.
+//
+// Workspace (all device, caller-owned; R = N*B rows ordered n*B + b; M = 2K+1):
+//   Dx        [M][T_in][R*F]        diffusion blocks of every x_t (layer-0 input)
+//   DH[l]     [T_in][M][R*H]        diffusion blocks of H^l_t (block 0 = H^l_t itself)
+//   DrH[l]    [T_in][M][R*H]        diffusion blocks of r*H^l_{t-1}
+//   Rg/Ug/Cg  [l][T_in][R*H]        saved gates r, u and candidate c
+//   dG[l]     [T_in][R*2H], dC[l] [T_in][R*H]   gate / candidate pre-activation grads (wgrad)
+//   yhat, dyhat [T_out][R*F_out]; loss partials; BPTT accumulators and temporaries;
+//   split-K partial sums of the weight gradients.
+// "Only new columns are diffused": T(Z) = [T(in), T(H)] is column-separable,
+// so each H^l_t is diffused once when produced and reused by layer l+1 at t and layer l at t+1.
+#include <algorithm>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace pgti {
+namespace {
+
+struct Dims {
+  int N, F, F_out, L, H, K, T_in, T_out, B, M;
+  int64_t R, ld;
+};
+
+struct Layout {
+  size_t Dx, yhat, dyhat, lossp, dU, drH, dTin, dTH, wpart, total;
+  size_t tmp[8];
+  std::vector<size_t> DH, DrH, Rg, Ug, Cg, dG, dC, dHa, dHb;
+  size_t tmp_floats, wpart_floats;
+};
+
+// parameter offsets (floats) in the flat layout of pgti.h
+struct ParamOffsets {
+  std::vector<size_t> Wru, bru, Wc, bc;
+  size_t Wout, bout, total;
+};
+
+ParamOffsets param_offsets(const Dims &d) {
+  ParamOffsets o;
+  size_t off = 0;
+  for (int l = 0; l < d.L; ++l) {
+    const size_t C = size_t((l == 0 ? d.F : d.H) + d.H);
+    o.Wru.push_back(off), off += size_t(d.M) * C * 2 * d.H;
+    o.bru.push_back(off), off += 2 * d.H;
+    o.Wc.push_back(off), off += size_t(d.M) * C * d.H;
+    o.bc.push_back(off), off += d.H;
+  }
+  o.Wout = off, off += size_t(d.H) * d.F_out;
+  o.bout = off, off += d.F_out;
+  o.total = off;
+  return o;
+}
+
+pgti_status check_desc(const pgti_dcrnn_desc *desc, Dims *out) {
+  PGTI_REQUIRE(desc, PGTI_ERR_INVALID_ARG, "null pgti_dcrnn_desc");
+  const pgti_dcrnn_desc &g = *desc;
+  PGTI_REQUIRE(g.N > 0 && g.F > 0 && g.L > 0 && g.K >= 0 && g.T_in > 0 && g.B > 0,
+               PGTI_ERR_SHAPE, "desc: N=%d F=%d L=%d K=%d T_in=%d B=%d", g.N, g.F, g.L, g.K,
+               g.T_in, g.B);
+  PGTI_REQUIRE(g.T_out >= 1 && g.T_out <= g.T_in, PGTI_ERR_SHAPE,
+               "desc: need 1 <= T_out=%d <= T_in=%d (stepwise readout, reading c6)", g.T_out,
+               g.T_in);
+  PGTI_REQUIRE(g.F_out >= 1 && g.F_out <= g.F && g.F_out <= 4, PGTI_ERR_SHAPE,
+               "desc: F_out=%d must be in [1, min(F, 4)]", g.F_out);
+  PGTI_REQUIRE(g.H == 8 || g.H == 16 || g.H == 32 || g.H == 64, PGTI_ERR_UNSUPPORTED,
+               "desc: H=%d (this build supports 8, 16, 32, 64)", g.H);
+  PGTI_REQUIRE(g.ld >= int64_t(g.N) * g.F && g.ld % 4 == 0, PGTI_ERR_ALIGNMENT,
+               "desc: ld=%lld must be >= N*F and a multiple of 4", (long long)g.ld);
+  PGTI_REQUIRE(g.precision == 0, PGTI_ERR_UNSUPPORTED,
+               "desc: precision=%d not available in this build (0 = fp32)", g.precision);
+  PGTI_REQUIRE(int64_t(g.N) * g.B * 2 * g.H < (int64_t(1) << 31), PGTI_ERR_SHAPE,
+               "desc: N*B*2H exceeds int32 row indexing");
+  if (g.K > 0)
+    PGTI_REQUIRE(g.a_rowptr && g.a_col && g.Pf_val && g.PbT_val && g.at_rowptr && g.at_col &&
+                     g.Pb_val && g.PfT_val && g.nnz >= 0,
+                 PGTI_ERR_INVALID_ARG, "desc: CSR pointers must be set when K > 0");
+  Dims d{g.N, g.F, g.F_out, g.L, g.H, g.K, g.T_in, g.T_out, g.B, 2 * g.K + 1,
+         int64_t(g.N) * g.B, g.ld};
+  *out = d;
+  return PGTI_OK;
+}
+
+Layout make_layout(const Dims &d) {
+  Layout L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += round_up(int64_t(bytes), 256);
+    return o;
+  };
+  const size_t R = size_t(d.R), H = size_t(d.H), M = size_t(d.M), T = size_t(d.T_in);
+  L.Dx = take(M * T * R * d.F * 4);
+  for (int l = 0; l < d.L; ++l) {
+    L.DH.push_back(take(T * M * R * H * 4));
+    L.DrH.push_back(take(T * M * R * H * 4));
+    L.Rg.push_back(take(T * R * H * 4));
+    L.Ug.push_back(take(T * R * H * 4));
+    L.Cg.push_back(take(T * R * H * 4));
+    L.dG.push_back(take(T * R * 2 * H * 4));
+    L.dC.push_back(take(T * R * H * 4));
+    L.dHa.push_back(take(R * H * 4));
+    L.dHb.push_back(take(R * H * 4));
+  }
+  L.yhat = take(size_t(d.T_out) * R * d.F_out * 4);
+  L.dyhat = take(size_t(d.T_out) * R * d.F_out * 4);
+  L.lossp = take(size_t(kLossBlocks) * 8);
+  L.dU = take(R * H * 4);
+  L.drH = take(R * H * 4);
+  const size_t fin_max = d.L > 1 ? H : size_t(d.F);
+  L.dTin = take(M * R * fin_max * 4);
+  L.dTH = take(M * R * H * 4);
+  L.tmp_floats = R * std::max(H, fin_max);
+  for (int i = 0; i < 8; ++i) L.tmp[i] = take(L.tmp_floats * 4);
+  size_t wp = readout_partial_floats(d.H, d.F_out, d.T_out, int(d.R));
+  for (int l = 0; l < d.L; ++l) {
+    const int C = (l == 0 ? d.F : d.H) + d.H;
+    wp = std::max(wp, wgrad_partial_floats(d.M, C, 2 * d.H, d.T_in, int(d.R)));
+  }
+  L.wpart_floats = wp;
+  L.wpart = take(wp * 4);
+  L.total = off;
+  return L;
+}
+
+// forward diffusion: blocks base + m*mstride (m = 0 given), G groups of stride gstride, width W
+cudaError_t diffuse_fwd(const pgti_dcrnn_desc &g, const Dims &d, float *base, int64_t mstride,
+                        int G, int64_t gstride, int64_t W, cudaStream_t s) {
+  for (int k = 1; k <= d.K; ++k) {
+    SpmmJob j[2] = {};
+    j[0].rowptr[0] = g.a_rowptr, j[0].col[0] = g.a_col, j[0].val[0] = g.Pf_val;
+    j[0].X[0] = base + (k - 1) * mstride;
+    j[0].Y = base + k * mstride;
+    j[1].rowptr[0] = g.at_rowptr, j[1].col[0] = g.at_col, j[1].val[0] = g.Pb_val;
+    j[1].X[0] = k == 1 ? base : base + (d.K + k - 1) * mstride;
+    j[1].Y = base + (d.K + k) * mstride;
+    for (auto &jb : j) jb.nterms = 1, jb.W = W, jb.G = G, jb.gstride = gstride;
+    cudaError_t e = launch_spmm(j, 2, d.N, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// Adjoint of the diffusion features (Horner form):
+//   out (+)= dT_0 + P_f^T (dT_1 + P_f^T (... + P_f^T dT_K)) + P_b^T (dT_{K+1} + ... P_b^T dT_2K)
+struct AdjChain {
+  const float *dT;
+  int64_t mstride, W;
+  float *out;
+  int accumulate;
+  float *tf[2], *tb[2];
+};
+
+cudaError_t diffuse_adj(const pgti_dcrnn_desc &g, const Dims &d, AdjChain *ch, int nch,
+                        cudaStream_t s) {
+  if (nch == 0) return cudaSuccess;
+  const int K = d.K;
+  SpmmJob jobs[kMaxSpmmJobs];
+  if (K == 0) {
+    for (int c = 0; c < nch; ++c) {
+      jobs[c] = SpmmJob{};
+      jobs[c].nterms = 0, jobs[c].add = ch[c].dT, jobs[c].Y = ch[c].out;
+      jobs[c].accumulate = ch[c].accumulate, jobs[c].W = ch[c].W, jobs[c].G = 1;
+    }
+    return launch_spmm(jobs, nch, d.N, s);
+  }
+  std::vector<const float *> af(nch), ab(nch);
+  for (int c = 0; c < nch; ++c) af[c] = ch[c].dT + K * ch[c].mstride, ab[c] = ch[c].dT + 2 * K * ch[c].mstride;
+  int pp = 0;
+  for (int k = K - 1; k >= 1; --k) {
+    int nj = 0;
+    for (int c = 0; c < nch; ++c) {
+      SpmmJob f{}, b{};
+      f.rowptr[0] = g.at_rowptr, f.col[0] = g.at_col, f.val[0] = g.PfT_val, f.X[0] = af[c];
+      f.add = ch[c].dT + k * ch[c].mstride, f.Y = ch[c].tf[pp];
+      b.rowptr[0] = g.a_rowptr, b.col[0] = g.a_col, b.val[0] = g.PbT_val, b.X[0] = ab[c];
+      b.add = ch[c].dT + (K + k) * ch[c].mstride, b.Y = ch[c].tb[pp];
+      for (SpmmJob *jb : {&f, &b}) jb->nterms = 1, jb->W = ch[c].W, jb->G = 1;
+      jobs[nj++] = f, jobs[nj++] = b;
+      af[c] = ch[c].tf[pp], ab[c] = ch[c].tb[pp];
+    }
+    cudaError_t e = launch_spmm(jobs, nj, d.N, s);
+    if (e != cudaSuccess) return e;
+    pp ^= 1;
+  }
+  for (int c = 0; c < nch; ++c) {
+    SpmmJob j{};
+    j.rowptr[0] = g.at_rowptr, j.col[0] = g.at_col, j.val[0] = g.PfT_val, j.X[0] = af[c];
+    j.rowptr[1] = g.a_rowptr, j.col[1] = g.a_col, j.val[1] = g.PbT_val, j.X[1] = ab[c];
+    j.nterms = 2, j.add = ch[c].dT, j.Y = ch[c].out, j.accumulate = ch[c].accumulate;
+    j.W = ch[c].W, j.G = 1;
+    jobs[c] = j;
+  }
+  return launch_spmm(jobs, nch, d.N, s);
+}
+
+#define CU(expr)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(PGTI_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__,  \
+                  __LINE__);                                                                  \
+  } while (0)
+
+pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *params, float *grads,
+                     const float *x, const float *y, float *loss_dev, char *ws, float *act_dump,
+                     cudaStream_t s) {
+  const Layout Ly = make_layout(d);
+  const ParamOffsets P = param_offsets(d);
+  auto Fp = [&](size_t off) { return reinterpret_cast<float *>(ws + off); };
+  const int64_t R = d.R, H = d.H, M = d.M, RH = R * H, MRH = M * RH;
+  const int T = d.T_in, L = d.L;
+  float *Dx = Fp(Ly.Dx);
+  const int64_t RF = R * d.F;
+  unsigned *err = device_error_flag();
+  PGTI_REQUIRE(err, PGTI_ERR_CUDA, "device error flag unavailable");
+
+  // ------------------------------------------------------------------ forward
+  CU(launch_x_prep(x, d.B, T, d.ld, d.N, d.F, Dx, s));
+  CU(diffuse_fwd(g, d, Dx, int64_t(T) * RF, T, RF, int64_t(d.B) * d.F, s));
+  for (int t = 0; t < T; ++t) {
+    for (int l = 0; l < L; ++l) {
+      const int Fin = l == 0 ? d.F : d.H;
+      const float *Din = l == 0 ? Dx + t * RF : Fp(Ly.DH[l - 1]) + t * MRH;
+      const int64_t din_ms = l == 0 ? int64_t(T) * RF : RH;
+      float *DHt = Fp(Ly.DH[l]) + t * MRH;
+      const float *DHp = t > 0 ? Fp(Ly.DH[l]) + (t - 1) * MRH : nullptr;
+      float *DrHt = Fp(Ly.DrH[l]) + t * MRH;
+      float *r = Fp(Ly.Rg[l]) + t * RH, *u = Fp(Ly.Ug[l]) + t * RH, *c = Fp(Ly.Cg[l]) + t * RH;
+
+      GconvFwd gate{};
+      gate.a = GconvA{Din, din_ms, DHp, RH, Fin, d.H, d.M};
+      gate.R = int(R), gate.W = params + P.Wru[l], gate.bias = params + P.bru[l];
+      gate.Nout = 2 * d.H, gate.mode = kEpiGate, gate.Hprev = DHp;
+      gate.out_r = r, gate.out_u = u, gate.out_rH = DrHt;
+      CU(launch_gconv_fwd(gate, s));
+      CU(diffuse_fwd(g, d, DrHt, RH, 1, 0, int64_t(d.B) * d.H, s));
+
+      GconvFwd cand{};
+      cand.a = GconvA{Din, din_ms, DrHt, RH, Fin, d.H, d.M};
+      cand.R = int(R), cand.W = params + P.Wc[l], cand.bias = params + P.bc[l];
+      cand.Nout = d.H, cand.mode = kEpiCand, cand.Hprev = DHp;
+      cand.u_in = u, cand.out_c = c, cand.out_H = DHt;
+      if (l == L - 1 && t >= T - d.T_out) {
+        cand.Wout = params + P.Wout, cand.bout = params + P.bout, cand.F_out = d.F_out;
+        cand.yhat = Fp(Ly.yhat) + int64_t(t - (T - d.T_out)) * R * d.F_out;
+      }
+      CU(launch_gconv_fwd(cand, s));
+      if (!(l == L - 1 && t == T - 1)) CU(diffuse_fwd(g, d, DHt, RH, 1, 0, int64_t(d.B) * d.H, s));
+    }
+  }
+  CU(launch_loss(Fp(Ly.yhat), y, d.T_out, d.N, d.B, d.F, d.F_out, d.ld, Fp(Ly.dyhat),
+                 reinterpret_cast<double *>(ws + Ly.lossp), loss_dev, err, s));
+
+  // ------------------------------------------------------------------ backward (BPTT)
+  std::vector<float *> dHcur(L), dHprev(L);
+  for (int l = 0; l < L; ++l) {
+    dHcur[l] = Fp(Ly.dHa[l]), dHprev[l] = Fp(Ly.dHb[l]);
+    CU(cudaMemsetAsync(dHcur[l], 0, size_t(RH) * 4, s));
+  }
+  float *dU = Fp(Ly.dU), *drH = Fp(Ly.drH), *dTin = Fp(Ly.dTin), *dTH = Fp(Ly.dTH);
+  float *tmp[8];
+  for (int i = 0; i < 8; ++i) tmp[i] = Fp(Ly.tmp[i]);
+  for (int t = T - 1; t >= 0; --t) {
+    for (int l = L - 1; l >= 0; --l) {
+      const int Fin = l == 0 ? d.F : d.H, C = Fin + d.H;
+      const bool need_in = l > 0, need_h = t > 0;
+      const float *Hprev = t > 0 ? Fp(Ly.DH[l]) + (t - 1) * MRH : nullptr;
+      const float *r = Fp(Ly.Rg[l]) + t * RH, *u = Fp(Ly.Ug[l]) + t * RH, *c = Fp(Ly.Cg[l]) + t * RH;
+      float *dC = Fp(Ly.dC[l]) + t * RH, *dG = Fp(Ly.dG[l]) + t * 2 * RH;
+      const float *dy = (l == L - 1 && t >= T - d.T_out)
+                            ? Fp(Ly.dyhat) + int64_t(t - (T - d.T_out)) * R * d.F_out
+                            : nullptr;
+      CU(launch_cand_bwd(RH, d.H, dHcur[l], dy, params + P.Wout, d.F_out, u, c, Hprev, dU, dC,
+                         need_h ? dHprev[l] : nullptr, s));
+      const int64_t tin_ms = R * Fin;
+      if (need_in || need_h) {
+        GconvDgrad dg{};
+        dg.G = dC, dg.R = int(R), dg.Nout = d.H, dg.W = params + P.Wc[l];
+        dg.M = d.M, dg.Fin = Fin, dg.Hd = d.H;
+        dg.c_lo = need_in ? 0 : Fin, dg.c_hi = need_h ? C : Fin;
+        dg.Tin = dTin, dg.tin_mstride = tin_ms, dg.acc_in = 0, dg.Th = dTH, dg.th_mstride = RH;
+        CU(launch_gconv_dgrad(dg, s));
+      }
+      if (need_h) {
+        AdjChain ch{dTH, RH, int64_t(d.B) * d.H, drH, 0, {tmp[0], tmp[1]}, {tmp[2], tmp[3]}};
+        CU(diffuse_adj(g, d, &ch, 1, s));
+      }
+      CU(launch_gate_bwd(RH, d.H, need_h ? drH : nullptr, Hprev, r, u, dU,
+                         need_h ? dHprev[l] : nullptr, dG, s));
+      if (need_in || need_h) {
+        GconvDgrad dg{};
+        dg.G = dG, dg.R = int(R), dg.Nout = 2 * d.H, dg.W = params + P.Wru[l];
+        dg.M = d.M, dg.Fin = Fin, dg.Hd = d.H;
+        dg.c_lo = need_in ? 0 : Fin, dg.c_hi = need_h ? C : Fin;
+        dg.Tin = dTin, dg.tin_mstride = tin_ms, dg.acc_in = 1, dg.Th = dTH, dg.th_mstride = RH;
+        CU(launch_gconv_dgrad(dg, s));
+        AdjChain ch[2];
+        int nch = 0;
+        if (need_h)
+          ch[nch++] = AdjChain{dTH, RH, int64_t(d.B) * d.H, dHprev[l], 1, {tmp[0], tmp[1]},
+                               {tmp[2], tmp[3]}};
+        if (need_in)
+          ch[nch++] = AdjChain{dTin, tin_ms, int64_t(d.B) * Fin, dHcur[l - 1], 1,
+                               {tmp[4], tmp[5]}, {tmp[6], tmp[7]}};
+        CU(diffuse_adj(g, d, ch, nch, s));
+      }
+      std::swap(dHcur[l], dHprev[l]);
+    }
+  }
+
+  // ------------------------------------------------------------------ weight gradients
+  for (int l = 0; l < L; ++l) {
+    const int Fin = l == 0 ? d.F : d.H;
+    GconvWgrad w{};
+    w.in = l == 0 ? Dx : Fp(Ly.DH[l - 1]);
+    w.in_tstride = l == 0 ? RF : MRH;
+    w.in_mstride = l == 0 ? int64_t(T) * RF : RH;
+    w.Fin = Fin, w.Hd = d.H, w.M = d.M, w.T = T, w.R = int(R);
+    w.partial = Fp(Ly.wpart), w.partial_cap = int64_t(Ly.wpart_floats);
+    // r|u gate: Z_t = [in_t, H_{t-1}]
+    w.h = Fp(Ly.DH[l]), w.h_tstride = MRH, w.h_mstride = RH, w.h_toff = -1;
+    w.G = Fp(Ly.dG[l]), w.g_tstride = 2 * RH, w.Nout = 2 * d.H, w.out = grads + P.Wru[l];
+    CU(launch_gconv_wgrad(w, s));
+    // candidate: Z'_t = [in_t, r*H_{t-1}]
+    w.h = Fp(Ly.DrH[l]), w.h_toff = 0;
+    w.G = Fp(Ly.dC[l]), w.g_tstride = RH, w.Nout = d.H, w.out = grads + P.Wc[l];
+    CU(launch_gconv_wgrad(w, s));
+  }
+  ReadoutWgrad rw{};
+  rw.Hs = Fp(Ly.DH[L - 1]) + int64_t(T - d.T_out) * MRH, rw.h_tstride = MRH;
+  rw.dy = Fp(Ly.dyhat), rw.T = d.T_out, rw.R = int(R), rw.H = d.H, rw.F_out = d.F_out;
+  rw.partial = Fp(Ly.wpart), rw.out = grads + P.Wout;
+  CU(launch_readout_wgrad(rw, s));
+
+  // ------------------------------------------------------------------ test-only dump
+  if (act_dump) {
+    for (int t = 0; t < T; ++t)
+      for (int l = 0; l < L; ++l) {
+        float *dst = act_dump + (int64_t(t) * L + l) * 4 * RH;
+        const float *src[4] = {Fp(Ly.DH[l]) + t * MRH, Fp(Ly.Rg[l]) + t * RH,
+                               Fp(Ly.Ug[l]) + t * RH, Fp(Ly.Cg[l]) + t * RH};
+        for (int q = 0; q < 4; ++q)
+          CU(cudaMemcpyAsync(dst + q * RH, src[q], size_t(RH) * 4, cudaMemcpyDeviceToDevice, s));
+      }
+    CU(cudaMemcpyAsync(act_dump + int64_t(T) * L * 4 * RH, Fp(Ly.yhat),
+                       size_t(d.T_out) * R * d.F_out * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  return PGTI_OK;
+}
+
+}  // namespace
+}  // namespace pgti
+
+using namespace pgti;
+
+extern "C" size_t pgti_dcrnn_num_params(const pgti_dcrnn_desc *desc) {
+  Dims d;
+  if (check_desc(desc, &d) != PGTI_OK) return 0;
+  return param_offsets(d).total;
+}
+
+extern "C" size_t pgti_dcrnn_workspace_bytes(const pgti_dcrnn_desc *desc) {
+  Dims d;
+  if (check_desc(desc, &d) != PGTI_OK) return 0;
+  return make_layout(d).total;
+}
+
+extern "C" pgti_status pgti_dcrnn_step(const pgti_dcrnn_desc *desc, const float *params,
+                                       float *grads, const float *x, const float *y,
+                                       float *loss_dev, void *workspace, size_t ws_bytes,
+                                       float *act_dump, void *stream) {
+  clear_error();
+  Dims d;
+  PGTI_STATUS_TRY(check_desc(desc, &d));
+  PGTI_REQUIRE(params && grads && x && y && loss_dev && workspace, PGTI_ERR_INVALID_ARG,
+               "pgti_dcrnn_step: null pointer");
+  PGTI_REQUIRE(aligned16(params) && aligned16(grads) && aligned16(workspace), PGTI_ERR_ALIGNMENT,
+               "pgti_dcrnn_step: params / grads / workspace must be 16-byte aligned");
+  const size_t need = make_layout(d).total;
+  PGTI_REQUIRE(ws_bytes >= need, PGTI_ERR_WORKSPACE,
+               "pgti_dcrnn_step: workspace %zu bytes < %zu needed", ws_bytes, need);
+  return run_step(*desc, d, params, grads, x, y, loss_dev, static_cast<char *>(workspace),
+                  act_dump, as_stream(stream));
+}
+
+extern "C" pgti_status pgti_diffuse(const pgti_dcrnn_desc *desc, const float *X, int64_t W,
+                                    float *out, void *stream) {
+  clear_error();
+  Dims d;
+  PGTI_STATUS_TRY(check_desc(desc, &d));
+  PGTI_REQUIRE(X && out && W > 0, PGTI_ERR_INVALID_ARG, "pgti_diffuse: bad arguments");
+  cudaStream_t s = as_stream(stream);
+  const int64_t NW = int64_t(d.N) * W;
+  CU(cudaMemcpyAsync(out, X, size_t(NW) * 4, cudaMemcpyDeviceToDevice, s));
+  CU(diffuse_fwd(*desc, d, out, NW, 1, 0, W, s));
+  return PGTI_OK;
+}
+
+extern "C" pgti_status pgti_diffuse_adjoint(const pgti_dcrnn_desc *desc, const float *dT,
+                                            int64_t W, float *dZ, void *stream) {
+  clear_error();
+  Dims d;
+  PGTI_STATUS_TRY(check_desc(desc, &d));
+  PGTI_REQUIRE(dT && dZ && W > 0, PGTI_ERR_INVALID_ARG, "pgti_diffuse_adjoint: bad arguments");
+  cudaStream_t s = as_stream(stream);
+  const int64_t NW = int64_t(d.N) * W;
+  float *tmp = nullptr;
+  CU(cudaMallocAsync(reinterpret_cast<void **>(&tmp), size_t(4 * NW) * 4, s));
+  AdjChain ch{dT, NW, W, dZ, 0, {tmp, tmp + NW}, {tmp + 2 * NW, tmp + 3 * NW}};
+  cudaError_t e = diffuse_adj(*desc, d, &ch, 1, s);
+  cudaError_t e2 = cudaFreeAsync(tmp, s);
+  CU(e);
+  CU(e2);
+  return PGTI_OK;
+}

@@ -1,0 +1,150 @@
+// Small fused elementwise kernels of the step: x re-layout, MAE loss (K5), GRU backward.
+#include "kernels.cuh"
+
+namespace pgti {
+namespace {
+
+constexpr int kT = 256;
+
+inline unsigned grid_for(int64_t n, int cap = 148 * 16) {
+  return unsigned(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kT), cap)));
+}
+
+// x[b][t][ld] (gathered batch, sample-major) -> X0[t][n][b][f] (node-major rows = n*B + b,
+// the dense-operand layout of the diffusion SpMM and the row order of the gate GEMMs).
+__global__ void k_x_prep(const float *__restrict__ x, int B, int T_in, int64_t ld, int N, int F,
+                         float *__restrict__ X0) {
+  const int64_t total = int64_t(T_in) * N * B * F;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    int64_t q = i;
+    const int f = int(q % F);
+    q /= F;
+    const int b = int(q % B);
+    q /= B;
+    const int n = int(q % N);
+    const int t = int(q / N);
+    X0[i] = x[(int64_t(b) * T_in + t) * ld + int64_t(n) * F + f];
+  }
+}
+
+// loss = mean |yhat - y[..., :F_out]|; dyhat = sign(resid) / count (0 at ties).
+// yhat/dyhat [T_out][N*B][F_out] (row n*B + b); y [B][T_out][ld].
+__global__ void k_loss_partial(const float *__restrict__ yhat, const float *__restrict__ y,
+                               int T_out, int N, int B, int F, int F_out, int64_t ld,
+                               float *__restrict__ dyhat, double *__restrict__ partials) {
+  const int64_t R = int64_t(N) * B, total = int64_t(T_out) * R * F_out;
+  const float inv = float(1.0 / double(total));
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int o = int(i % F_out);
+    const int64_t rt = i / F_out;
+    const int64_t row = rt % R;
+    const int tt = int(rt / R);
+    const int n = int(row / B), b = int(row % B);
+    const float yv = y[(int64_t(b) * T_out + tt) * ld + int64_t(n) * F + o];
+    const float r = yhat[i] - yv;
+    dyhat[i] = r > 0.f ? inv : (r < 0.f ? -inv : 0.f);
+    acc += double(fabsf(r));
+  }
+  __shared__ double red[kT / 32];
+  for (int q = 16; q > 0; q >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, q);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kT / 32; ++w) s += red[w];
+    partials[blockIdx.x] = s;
+  }
+}
+
+__global__ void k_loss_final(const double *__restrict__ partials, int n, int64_t count,
+                             float *__restrict__ loss, unsigned *__restrict__ err) {
+  if (threadIdx.x != 0) return;
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) s += partials[i];
+  const float l = float(s / double(count));
+  *loss = l;
+  if (!isfinite(l)) atomicOr(err, kDevErrNonfinite);
+}
+
+// Candidate / update backward:  H' = u H + (1-u) c,  c = tanh(pre)
+//   dH' = dHcur (+ dyhat W_out^T);  dU = dH' (H - c);  dCpre = dH' (1-u)(1-c^2);  dHprev = dH' u
+__global__ void k_cand_bwd(int64_t RH, int H, const float *__restrict__ dHcur,
+                           const float *__restrict__ dy, const float *__restrict__ Wout, int F_out,
+                           const float *__restrict__ u, const float *__restrict__ c,
+                           const float *__restrict__ Hprev, float *__restrict__ dU,
+                           float *__restrict__ dC, float *__restrict__ dHprev) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < RH;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    float dh = dHcur[i];
+    if (dy) {
+      const int64_t row = i / H;
+      const int j = int(i - row * H);
+      for (int o = 0; o < F_out; ++o) dh = fmaf(dy[row * F_out + o], Wout[j * F_out + o], dh);
+    }
+    const float uu = u[i], cc = c[i], hp = Hprev ? Hprev[i] : 0.f;
+    dU[i] = dh * (hp - cc);
+    dC[i] = dh * (1.0f - uu) * (1.0f - cc * cc);
+    if (dHprev) dHprev[i] = dh * uu;
+  }
+}
+
+// Gate backward: rH = r*H;  dr = d(rH) H;  dHprev += d(rH) r;
+//   dG[:, :H] = dr r (1-r),  dG[:, H:] = dU u (1-u)
+__global__ void k_gate_bwd(int64_t RH, int H, const float *__restrict__ drH,
+                           const float *__restrict__ Hprev, const float *__restrict__ r,
+                           const float *__restrict__ u, const float *__restrict__ dU,
+                           float *__restrict__ dHprev, float *__restrict__ dG) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < RH;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t row = i / H;
+    const int j = int(i - row * H);
+    const float rr = r[i], uu = u[i];
+    float dr = 0.f;
+    if (drH) {
+      const float d = drH[i];
+      dr = Hprev ? d * Hprev[i] : 0.f;
+      if (dHprev) dHprev[i] += d * rr;
+    }
+    dG[row * 2 * H + j] = dr * rr * (1.0f - rr);
+    dG[row * 2 * H + H + j] = dU[i] * uu * (1.0f - uu);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_x_prep(const float *x, int B, int T_in, int64_t ld, int N, int F, float *X0,
+                          cudaStream_t s) {
+  k_x_prep<<<grid_for(int64_t(T_in) * N * B * F), kT, 0, s>>>(x, B, T_in, ld, N, F, X0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_loss(const float *yhat, const float *y, int T_out, int N, int B, int F,
+                        int F_out, int64_t ld, float *dyhat, double *partials, float *loss,
+                        unsigned *err, cudaStream_t s) {
+  k_loss_partial<<<kLossBlocks, kT, 0, s>>>(yhat, y, T_out, N, B, F, F_out, ld, dyhat, partials);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_loss_final<<<1, 32, 0, s>>>(partials, kLossBlocks, int64_t(T_out) * N * B * F_out, loss, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cand_bwd(int64_t RH, int H, const float *dHcur, const float *dy,
+                            const float *Wout, int F_out, const float *u, const float *c,
+                            const float *Hprev, float *dU, float *dC, float *dHprev_out,
+                            cudaStream_t s) {
+  k_cand_bwd<<<grid_for(RH), kT, 0, s>>>(RH, H, dHcur, dy, Wout, F_out, u, c, Hprev, dU, dC,
+                                         dHprev_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gate_bwd(int64_t RH, int H, const float *drH, const float *Hprev,
+                            const float *r, const float *u, const float *dU, float *dHprev,
+                            float *dG, cudaStream_t s) {
+  k_gate_bwd<<<grid_for(RH), kT, 0, s>>>(RH, H, drH, Hprev, r, u, dU, dHprev, dG);
+  return cudaGetLastError();
+}
+
+}  // namespace pgti

@@ -1,0 +1,126 @@
+// Internal launch interfaces shared by the step orchestration (dcrnn.cu) and the kernels.
+#pragma once
+
+#include "common.cuh"
+
+namespace pgti {
+
+// ------------------------------------------------------------------ K2 CSR SpMM (diffusion)
+// Y[g][n][:] = add[g][n][:] + sum_t sum_{e in row n of A_t} val_t[e] * X_t[g][col_t[e]][:]
+//              (+ Y[g][n][:] if accumulate)
+// Every buffer of a job is [G][N][W] with group stride gstride (floats).
+struct SpmmJob {
+  const int32_t *rowptr[2];
+  const int32_t *col[2];
+  const float *val[2];
+  const float *X[2];
+  int nterms;
+  const float *add;   // nullable
+  float *Y;
+  int accumulate;
+  int64_t W;
+  int G;
+  int64_t gstride;
+  // filled by launch_spmm
+  int64_t warp_begin, chunks;
+};
+constexpr int kMaxSpmmJobs = 4;
+cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s);
+
+// ------------------------------------------------------------------ K3' fp32 SIMT GEMMs
+// Virtual A operand of the diffusion convolution: row r, column k = m*C_in + c reads
+//   c <  Fin : in[m*in_mstride + r*Fin + c]
+//   c >= Fin : h [m*h_mstride  + r*Hd  + (c-Fin)]   (h == nullptr -> 0)
+struct GconvA {
+  const float *in;
+  int64_t in_mstride;
+  const float *h;
+  int64_t h_mstride;
+  int Fin, Hd, M;
+};
+
+enum EpiMode { kEpiGate = 0, kEpiCand = 1 };
+
+struct GconvFwd {
+  GconvA a;
+  int R;                 // rows = N*B
+  const float *W;        // [M*C_in][Nout]
+  const float *bias;     // [Nout]
+  int Nout;              // 2H (gate) or H (cand)
+  int mode;
+  const float *Hprev;    // [R][H] nullable (zeros)
+  // gate epilogue
+  float *out_r, *out_u, *out_rH;
+  // cand epilogue
+  const float *u_in;
+  float *out_c, *out_H;
+  // optional readout yhat[R][F_out] = H' W_out + b_out
+  const float *Wout, *bout;
+  int F_out;
+  float *yhat;
+};
+cudaError_t launch_gconv_fwd(const GconvFwd &p, cudaStream_t s);
+
+// dgrad: out[r][(m,c)] = sum_j G[r][j] * W[m*C_in + c][j] for c in [c_lo, c_hi),
+// written to Tin (c < Fin, layout [M][R][Fin], += if acc_in) or Th (layout [M][R][Hd]).
+struct GconvDgrad {
+  const float *G;   // [R][Nout]
+  int R, Nout;
+  const float *W;   // [M*C_in][Nout]
+  int M, Fin, Hd, c_lo, c_hi;
+  float *Tin;       // nullable when c_lo >= Fin
+  int64_t tin_mstride;
+  int acc_in;
+  float *Th;
+  int64_t th_mstride;
+};
+cudaError_t launch_gconv_dgrad(const GconvDgrad &p, cudaStream_t s);
+
+// wgrad: dW[(m,c)][j] = sum_t sum_r A_t[r][(m,c)] * G_t[r][j]; row M*C_in = bias (A = 1).
+// A_t: in part  in + t*in_tstride + m*in_mstride + r*Fin + c
+//      h  part  h + (t+h_toff)*h_tstride + m*h_mstride + r*Hd + c-Fin  (t+h_toff < 0 -> 0)
+struct GconvWgrad {
+  const float *in;
+  int64_t in_tstride, in_mstride;
+  const float *h;
+  int64_t h_tstride, h_mstride;
+  int h_toff;
+  int Fin, Hd, M;
+  const float *G;        // + t*g_tstride, [R][Nout]
+  int64_t g_tstride;
+  int T, R, Nout;
+  float *partial;        // [nchunks][M*C_in+1][Nout]
+  int64_t partial_cap;   // floats available
+  float *out;            // [M*C_in+1][Nout]
+};
+cudaError_t launch_gconv_wgrad(const GconvWgrad &p, cudaStream_t s);
+size_t wgrad_partial_floats(int M, int C_in, int Nout, int T, int R);
+
+// readout wgrad: dW_out[j][o] = sum_tt sum_r Hs_tt[r][j] dy[tt][r][o], j = H -> bias
+struct ReadoutWgrad {
+  const float *Hs;       // + tt*h_tstride, [R][H]
+  int64_t h_tstride;
+  const float *dy;       // [T][R][F_out]
+  int T, R, H, F_out;
+  float *partial;
+  float *out;            // [H+1][F_out] (W_out then b_out)
+};
+cudaError_t launch_readout_wgrad(const ReadoutWgrad &p, cudaStream_t s);
+size_t readout_partial_floats(int H, int F_out, int T, int R);
+
+// ------------------------------------------------------------------ elementwise
+cudaError_t launch_x_prep(const float *x, int B, int T_in, int64_t ld, int N, int F, float *X0,
+                          cudaStream_t s);
+cudaError_t launch_loss(const float *yhat, const float *y, int T_out, int N, int B, int F,
+                        int F_out, int64_t ld, float *dyhat, double *partials, float *loss,
+                        unsigned *err, cudaStream_t s);
+constexpr int kLossBlocks = 296;
+cudaError_t launch_cand_bwd(int64_t RH, int H, const float *dHcur, const float *dy,
+                            const float *Wout, int F_out, const float *u, const float *c,
+                            const float *Hprev, float *dU, float *dC, float *dHprev_out,
+                            cudaStream_t s);
+cudaError_t launch_gate_bwd(int64_t RH, int H, const float *drH, const float *Hprev,
+                            const float *r, const float *u, const float *dU, float *dHprev,
+                            float *dG, cudaStream_t s);
+
+}  // namespace pgti

@@ -1,0 +1,178 @@
+"""Host driver of the index-batched training step (distributed-index-batching).
+
+Host-side arithmetic here is bookkeeping only (window counts, shard ranges, Adam step count);
+every value the model sees is produced by libpgti kernels:
+
+  load (one H2D copy) -> stats (window-weighted Alg. 1) -> normalise
+   -> per-epoch index plan -> per step: gather -> DCGRU
+  forward/backward -> NCCL all-reduce -> Adam.
+
+Halo sharding (BASELINE.json north_star): rank r of R owns window starts
+[r S_r, (r+1) S_r), S_r = floor(S_tr / R), and holds series rows [r S_r, (r+1) S_r + T_in +
+T_out - 1).  The last rank additionally holds the rows the statistics need up to S_tr + T_in - 1.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+
+from . import pgti
+
+
+def window_count(E: int, T_in: int, T_out: int) -> int:
+    """S = E - T_in - T_out + 1 windows (Eq. 2; DESIGN reading c11)."""
+    return max(0, E - T_in - T_out + 1)
+
+
+def train_windows(S: int) -> int:
+    """round(S * 0.70) (Alg. 1)."""
+    return round(S * 0.70)
+
+
+@dataclasses.dataclass(frozen=True)
+class ShardPlan:
+    win_lo: int     # first global window start of this rank
+    win_hi: int     # one past the last
+    row_lo: int     # first global series row held
+    row_hi: int     # one past the last row held
+    stat_lo: int    # rows whose Alg. 1 statistics this rank contributes
+    stat_hi: int
+
+
+def shard_plan(S_tr: int, R: int, r: int, T_in: int, T_out: int) -> ShardPlan:
+    S_r = S_tr // R
+    win_lo, win_hi = r * S_r, (r + 1) * S_r
+    row_lo, row_hi = win_lo, win_hi + T_in + T_out - 1
+    stat_lo = win_lo
+    stat_hi = win_hi if r < R - 1 else S_tr + T_in - 1
+    row_hi = max(row_hi, stat_hi)
+    return ShardPlan(win_lo, win_hi, row_lo, row_hi, stat_lo, stat_hi)
+
+
+def row_pitch(N: int, F: int) -> int:
+    """ld = roundup(N F, 4) floats: 16-byte aligned time rows (SURVEY decision 5)."""
+    return (N * F + 3) // 4 * 4
+
+
+class Trainer:
+    """One rank of distributed-index-batching.
+
+    cfg: any object with N, E, F, F_out, T_in, T_out, L, H, K, B.
+    graph: (src, dst, w) edge list.  series_fn(row_lo, row_hi) -> float32 [rows][N][F] raw
+    values of those global rows.  params0: float32 [num_params] initial parameters.
+    """
+
+    def __init__(self, cfg, graph, series_fn, params0, rank=0, world=1, device=0, comm=None,
+                 seed=3, lr=1e-2, precision=0, shuffle=True, use_cuda_graph=True):
+        import torch
+
+        self.torch = torch
+        self.cfg, self.rank, self.world, self.comm = cfg, rank, world, comm
+        self.dev = torch.device("cuda", device)
+        torch.cuda.set_device(self.dev)
+        self.seed, self.lr, self.shuffle = seed, lr, shuffle
+        self.S = window_count(cfg.E, cfg.T_in, cfg.T_out)
+        self.S_tr = train_windows(self.S)
+        self.plan = shard_plan(self.S_tr, world, rank, cfg.T_in, cfg.T_out)
+        self.ld = row_pitch(cfg.N, cfg.F)
+        p = self.plan
+        rows = np.ascontiguousarray(series_fn(p.row_lo, p.row_hi), dtype=np.float32)
+        assert rows.shape == (p.row_hi - p.row_lo, cfg.N, cfg.F), rows.shape
+        self.host_rows = torch.from_numpy(rows).pin_memory()
+        self.series_buf = torch.empty((p.row_hi - p.row_lo) * self.ld, dtype=torch.float32,
+                                      device=self.dev)
+        self.series = pgti.Series(self.host_rows, p.row_lo, cfg.N, cfg.F, self.series_buf,
+                                  self.ld)
+        self.mu, self.sigma = self._stats()
+        self.series.normalize(self.mu, self.sigma)
+
+        csr = pgti.graph_build(cfg.N, *graph)
+        self.csr = pgti.csr_to_device(csr, self.dev)
+        self.model = pgti.DCRNN(cfg.N, cfg.F, cfg.F_out, cfg.L, cfg.H, cfg.K, cfg.T_in,
+                                cfg.T_out, cfg.B, self.ld, self.csr, precision)
+        n = self.model.num_params()
+        assert params0.size == n, (params0.size, n)
+        f32 = dict(dtype=torch.float32, device=self.dev)
+        self.params = torch.from_numpy(np.ascontiguousarray(params0, np.float32)).to(self.dev)
+        self.grads = torch.zeros(n, **f32)
+        self.m = torch.zeros(n, **f32)
+        self.v = torch.zeros(n, **f32)
+        self.ws = torch.empty(self.model.workspace_bytes(), dtype=torch.uint8, device=self.dev)
+        self.loss = torch.zeros(1, **f32)
+        B, T_in, T_out = cfg.B, cfg.T_in, cfg.T_out
+        self.x = torch.empty(B * T_in * self.ld, **f32)
+        self.y = torch.empty(B * T_out * self.ld, **f32)
+        self.idx = torch.empty(max(1, p.win_hi - p.win_lo), dtype=torch.int32, device=self.dev)
+        self.idx_cur = torch.empty(B, dtype=torch.int32, device=self.dev)
+        self.dev_step = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.n_used = 0
+        self.use_cuda_graph = use_cuda_graph
+        self.graph = None
+
+    # ------------------------------------------------------------------ setup
+    def _stats(self):
+        torch = self.torch
+        p, cfg = self.plan, self.cfg
+        out = []
+        shift = 0.0
+        for _ in range(2):   # pass 1: mean; pass 2: variance about the mean (no cancellation)
+            sums = torch.zeros(3, dtype=torch.float64, device=self.dev)
+            self.series.stats(self.S_tr, cfg.T_in, p.stat_lo, p.stat_hi, shift, sums)
+            if self.comm is not None and self.world > 1:
+                self.comm.allreduce_f64(sums)
+            s0, s1, s2 = sums.cpu().tolist()
+            mean_d = s1 / s0
+            out.append((shift, mean_d, s2 / s0 - mean_d * mean_d))
+            shift = shift + mean_d
+        mu = out[1][0] + out[1][1]
+        var = out[1][2]
+        return mu, math.sqrt(max(var, 0.0))
+
+    def steps_per_epoch(self) -> int:
+        return (self.plan.win_hi - self.plan.win_lo) // self.cfg.B
+
+    def start_epoch(self, epoch: int) -> int:
+        p, cfg = self.plan, self.cfg
+        self.n_used = self.series.make_index(p.win_lo, p.win_hi, cfg.T_in, cfg.T_out, cfg.B,
+                                             self.seed, epoch, self.rank, self.shuffle, self.idx)
+        return self.n_used // cfg.B
+
+    # ------------------------------------------------------------------ one step
+    def _body(self, idx):
+        cfg = self.cfg
+        self.series.gather(idx, cfg.B, cfg.T_in, cfg.T_out, self.x, self.y)
+        self.model.step(self.params, self.grads, self.x, self.y, self.loss, self.ws)
+        if self.comm is not None and self.world > 1:
+            self.comm.allreduce_grads(self.grads)
+        pgti.adam_step(self.params, self.grads, self.m, self.v, 0, self.lr,
+                       grad_scale=1.0 / self.world, dev_step=self.dev_step)
+
+    def step(self, j: int):
+        """Batch j of the current epoch (gather -> fwd/bwd -> all-reduce -> Adam)."""
+        B = self.cfg.B
+        sl = self.idx[j * B:(j + 1) * B]
+        if not self.use_cuda_graph:
+            self._body(sl)
+            return
+        self.idx_cur.copy_(sl)
+        if self.graph is None:
+            torch = self.torch
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):      # warm-up outside capture (loads every kernel)
+                snap = [t.clone() for t in (self.params, self.m, self.v, self.dev_step)]
+                self._body(self.idx_cur)
+                for t, c in zip((self.params, self.m, self.v, self.dev_step), snap):
+                    t.copy_(c)
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._body(self.idx_cur)
+            self.graph = g
+        self.graph.replay()
+
+    def check(self):
+        pgti.check_device_error()

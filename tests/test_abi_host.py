@@ -1,0 +1,104 @@
+"""CPU checks of the C ABI: the library builds, loads and exports every symbol include/pgti.h
+declares; host-only entry points (pgti_graph_build) agree with the oracle; host shard logic."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import philox, transitions, windows
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="session")
+def pgti():
+    from paper_2507_11683_b200 import build
+    build.build()
+    from paper_2507_11683_b200 import pgti as mod
+    return mod
+
+
+def test_exports_every_declared_symbol(pgti):
+    import ctypes
+    hdr = open(os.path.join(ROOT, "include", "pgti.h")).read()
+    declared = set(re.findall(r"\b(pgti_[a-z0-9_]+)\s*\(", hdr))
+    assert len(declared) >= 20
+    lib = ctypes.CDLL(pgti.LIB_PATH)
+    missing = [s for s in sorted(declared) if not hasattr(lib, s)]
+    assert not missing, missing
+    assert pgti.version().startswith("libpgti")
+
+
+def test_sm100a_cubin_and_no_fallback(pgti):
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", pgti.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out, out
+
+
+@pytest.mark.parametrize("N,p,seed", [(7, 0.4, 1), (30, 0.1, 2), (1, 1.0, 3)])
+def test_graph_build_matches_oracle(pgti, N, p, seed):
+    src, dst, w = synth.random_graph(N, p, seed)
+    csr = pgti.graph_build(N, src, dst, w)
+    Pf, Pb = transitions.transition_matrices(N, src, dst, w, dense=True)
+
+    def dense(rowptr, col, val):
+        D = np.zeros((N, N))
+        for i in range(N):
+            for e in range(rowptr[i], rowptr[i + 1]):
+                D[i, col[e]] = val[e]
+            assert np.all(np.diff(col[rowptr[i]:rowptr[i + 1]]) > 0)  # ascending columns
+        return D
+
+    tol = dict(rtol=1e-7, atol=0)
+    assert np.allclose(dense(csr["a_rowptr"], csr["a_col"], csr["Pf_val"]), Pf, **tol)
+    assert np.allclose(dense(csr["a_rowptr"], csr["a_col"], csr["PbT_val"]), Pb.T, **tol)
+    assert np.allclose(dense(csr["at_rowptr"], csr["at_col"], csr["Pb_val"]), Pb, **tol)
+    assert np.allclose(dense(csr["at_rowptr"], csr["at_col"], csr["PfT_val"]), Pf.T, **tol)
+
+
+def test_graph_build_errors(pgti):
+    with pytest.raises(pgti.PgtiError) as e:
+        pgti.graph_build(3, [0, 0], [1, 1], [1.0, 2.0])
+    assert e.value.name == "INVALID_ARG" and "duplicate" in str(e.value)
+    with pytest.raises(pgti.PgtiError):
+        pgti.graph_build(3, [0], [5], [1.0])
+    with pytest.raises(pgti.PgtiError):
+        pgti.graph_build(3, [0], [1], [-1.0])
+
+
+def test_desc_validation_without_gpu(pgti):
+    m = pgti.DCRNN(207, 2, 1, 2, 64, 2, 12, 12, 64, 416, None)
+    with pytest.raises(pgti.PgtiError):  # K > 0 needs CSR pointers
+        m.num_params()
+    m = pgti.DCRNN(207, 2, 1, 2, 64, 0, 12, 12, 64, 416, None)
+    assert m.num_params() == 2 * 0 + synth.num_params(synth.CONFIGS["metr_la"].replace(K=0))
+    bad = pgti.DCRNN(207, 2, 1, 2, 64, 0, 12, 13, 64, 416, None)  # T_out > T_in
+    with pytest.raises(pgti.PgtiError):
+        bad.workspace_bytes()
+
+
+@pytest.mark.parametrize("name", list(synth.CONFIGS))
+def test_shard_plan_vs_oracle(pgti, name):
+    from paper_2507_11683_b200 import trainer
+    cfg = synth.CONFIGS[name]
+    S = windows.num_windows(cfg.E, cfg.T_in, cfg.T_out)
+    assert trainer.window_count(cfg.E, cfg.T_in, cfg.T_out) == S
+    S_tr = windows.split_counts(S)[0]
+    assert trainer.train_windows(S) == S_tr
+    for R in (1, 2, 4, 8):
+        covered = []
+        for r in range(R):
+            p = trainer.shard_plan(S_tr, R, r, cfg.T_in, cfg.T_out)
+            a, S_r = philox.shard(S_tr, R, r)
+            assert (p.win_lo, p.win_hi) == (a, a + S_r)
+            r0, r1 = philox.shard_rows(S_tr, R, r, cfg.T_in, cfg.T_out)
+            assert p.row_lo == r0 and p.row_hi >= r1 and p.row_hi <= cfg.E
+            assert p.row_lo <= p.stat_lo <= p.stat_hi <= p.row_hi
+            covered.append((p.stat_lo, p.stat_hi))
+        # the statistics row ranges tile every row a training window reads
+        assert covered[0][0] == 0 and covered[-1][1] == S_tr + cfg.T_in - 1
+        assert all(covered[i][1] == covered[i + 1][0] for i in range(R - 1))
+    assert trainer.row_pitch(207, 2) == 416 and trainer.row_pitch(325, 2) == 652

@@ -1,0 +1,341 @@
+"""CUDA path (through the C ABI) vs the float64 oracle, element by element.
+
+Bars (BASELINE.json north_star): gathers, index plans and the normalised series bit-exact;
+loss / activations / gradients within 1e-5 scale-relative (fp32 path, reading c19).
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import adam, dcgru, philox, pipeline, transitions, windows
+
+from gpu_util import (SMALL_CONFIGS, ld_of, load_series, model_for, run_step, scale_rel,
+                      split_dump)
+
+pytestmark = pytest.mark.gpu
+
+TOL32 = 1e-5
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    from paper_2507_11683_b200 import build
+    build.build()
+    from paper_2507_11683_b200 import pgti
+    return pgti, torch
+
+
+_REFS = {}
+
+
+def ref_for(cfg):
+    if cfg.name not in _REFS:
+        _REFS[cfg.name] = pipeline.Reference(cfg)
+    return _REFS[cfg.name]
+
+
+# ------------------------------------------------------------------ series / stats / index
+@pytest.mark.parametrize("name", ["tiny2", "cp", "odd", "metr_la", "pems_bay"])
+def test_normalized_series_bitexact(env, name):
+    pgti, torch = env
+    cfg = SMALL_CONFIGS.get(name) or synth.CONFIGS[name]
+    ref = ref_for(cfg)
+    s = load_series(pgti, torch, ref.v, 0, cfg, ref.mu, ref.sigma)
+    got = s.buf.cpu().numpy().reshape(cfg.E, ld_of(cfg))
+    want = windows.standardize32(ref.v, ref.mu, ref.sigma).reshape(cfg.E, -1)
+    nf = cfg.N * cfg.F
+    assert np.array_equal(got[:, :nf].view(np.uint32), want.view(np.uint32))
+    assert not np.any(got[:, nf:].view(np.uint32))  # pads are +0.0
+
+
+@pytest.mark.parametrize("name", ["cp", "odd", "metr_la", "pems_bay"])
+@pytest.mark.parametrize("R", [1, 2, 4, 8])
+def test_stats_match_alg1(env, name, R):
+    """Window-weighted device statistics of every rank's shard, summed, equal Alg. 1's
+    stacked mu / sigma to 1e-12."""
+    pgti, torch = env
+    from paper_2507_11683_b200 import trainer
+    cfg = SMALL_CONFIGS.get(name) or synth.CONFIGS[name]
+    ref = ref_for(cfg)
+    S_tr = ref.n_train
+    shift = 0.0
+    for _ in range(2):
+        tot = np.zeros(3)
+        for r in range(R):
+            p = trainer.shard_plan(S_tr, R, r, cfg.T_in, cfg.T_out)
+            s = load_series(pgti, torch, ref.v[p.row_lo:p.row_hi], p.row_lo, cfg)
+            sums = torch.zeros(3, dtype=torch.float64, device="cuda")
+            s.stats(S_tr, cfg.T_in, p.stat_lo, p.stat_hi, shift, sums)
+            tot += sums.cpu().numpy()
+        mean_d = tot[1] / tot[0]
+        var = tot[2] / tot[0] - mean_d ** 2
+        mu, shift = shift + mean_d, shift + mean_d
+    assert abs(mu - ref.mu) <= 1e-12 * abs(ref.mu)
+    assert abs(np.sqrt(var) - ref.sigma) <= 1e-12 * ref.sigma
+
+
+@pytest.mark.parametrize("name", ["cp", "metr_la", "pems_bay"])
+@pytest.mark.parametrize("R", [1, 2, 4, 8])
+def test_index_plan_bitexact(env, name, R):
+    pgti, torch = env
+    from paper_2507_11683_b200 import trainer
+    cfg = SMALL_CONFIGS.get(name) or synth.CONFIGS[name]
+    ref = ref_for(cfg)
+    for r in sorted({0, R - 1}):
+        p = trainer.shard_plan(ref.n_train, R, r, cfg.T_in, cfg.T_out)
+        s = load_series(pgti, torch, ref.v[p.row_lo:p.row_hi], p.row_lo, cfg, ref.mu, ref.sigma)
+        idx = torch.empty(p.win_hi - p.win_lo, dtype=torch.int32, device="cuda")
+        for epoch in (0, 1, 7):
+            n_used = s.make_index(p.win_lo, p.win_hi, cfg.T_in, cfg.T_out, cfg.B, 3, epoch, r, 1, idx)
+            want = ref.plan(R, r, seed=3, epoch=epoch)
+            assert n_used == want.size
+            assert np.array_equal(idx.cpu().numpy()[:n_used], want)
+            full = p.win_lo + philox.epoch_permutation(3, epoch, r, p.win_hi - p.win_lo)
+            assert np.array_equal(idx.cpu().numpy(), full)
+        n_used = s.make_index(p.win_lo, p.win_hi, cfg.T_in, cfg.T_out, cfg.B, 3, 0, r, 0, idx)
+        assert np.array_equal(idx.cpu().numpy(), np.arange(p.win_lo, p.win_hi))
+
+
+@pytest.mark.parametrize("name", ["tiny2", "cp", "odd", "metr_la", "pems_bay"])
+@pytest.mark.parametrize("R", [1, 2, 4, 8])
+@pytest.mark.parametrize("mode", ["ldg", "tma"])
+def test_gather_bitexact(env, name, R, mode, monkeypatch):
+    """Index-batched batch == the materialised Alg. 1 snapshots, bitwise,
+    including each shard's first and last window (y ends on the shard's last row)."""
+    pgti, torch = env
+    from paper_2507_11683_b200 import trainer
+    cfg = SMALL_CONFIGS.get(name) or synth.CONFIGS[name]
+    ref = ref_for(cfg)
+    if ref.n_train // R < 2:
+        pytest.skip("too few windows per rank")
+    pgti.set_gather_mode(mode)
+    try:
+        ld, nf = ld_of(cfg), cfg.N * cfg.F
+        for r in sorted({0, R // 2, R - 1}):
+            p = trainer.shard_plan(ref.n_train, R, r, cfg.T_in, cfg.T_out)
+            s = load_series(pgti, torch, ref.v[p.row_lo:p.row_hi], p.row_lo, cfg, ref.mu,
+                            ref.sigma)
+            plan = ref.plan(R, r)
+            idx_np = np.concatenate([[p.win_lo, p.win_hi - 1], plan[:max(1, cfg.B - 2)]])
+            B = idx_np.size
+            idx = torch.from_numpy(idx_np.astype(np.int32)).cuda()
+            x = torch.full((B * cfg.T_in * ld,), float("nan"), device="cuda")
+            y = torch.full((B * cfg.T_out * ld,), float("nan"), device="cuda")
+            s.gather(idx, B, cfg.T_in, cfg.T_out, x, y)
+            pgti.check_device_error()
+            fx, fy = ref.batch(idx_np)
+            xg = x.cpu().numpy().reshape(B, cfg.T_in, ld)
+            yg = y.cpu().numpy().reshape(B, cfg.T_out, ld)
+            assert np.array_equal(xg[..., :nf].view(np.uint32), fx.reshape(B, cfg.T_in, nf).view(np.uint32))
+            assert np.array_equal(yg[..., :nf].view(np.uint32), fy.reshape(B, cfg.T_out, nf).view(np.uint32))
+            assert not np.any(xg[..., nf:].view(np.uint32)) and not np.any(yg[..., nf:].view(np.uint32))
+    finally:
+        pgti.set_gather_mode("ldg")
+
+
+def test_gather_out_of_range_sets_flag(env):
+    pgti, torch = env
+    cfg = SMALL_CONFIGS["tiny2"]
+    ref = ref_for(cfg)
+    s = load_series(pgti, torch, ref.v[10:30], 10, cfg, ref.mu, ref.sigma)
+    ld = ld_of(cfg)
+    x = torch.zeros(2 * cfg.T_in * ld, device="cuda")
+    y = torch.zeros(2 * cfg.T_out * ld, device="cuda")
+    ok = torch.tensor([10, 30 - cfg.T_in - cfg.T_out], dtype=torch.int32, device="cuda")
+    s.gather(ok, 2, cfg.T_in, cfg.T_out, x, y)
+    pgti.check_device_error()
+    for bad in ([9, 12], [12, 30 - cfg.T_in - cfg.T_out + 1]):
+        s.gather(torch.tensor(bad, dtype=torch.int32, device="cuda"), 2, cfg.T_in, cfg.T_out, x, y)
+        with pytest.raises(pgti.PgtiError) as e:
+            pgti.check_device_error()
+        assert e.value.name == "OUT_OF_RANGE"
+    idx = torch.zeros(20, dtype=torch.int32, device="cuda")
+    with pytest.raises(pgti.PgtiError) as e:   # windows reaching past the held rows
+        s.make_index(10, 30, cfg.T_in, cfg.T_out, 2, 0, 0, 0, 1, idx)
+    assert e.value.name == "OUT_OF_RANGE"
+
+
+# ------------------------------------------------------------------ diffusion (K2)
+@pytest.mark.parametrize("N,W,K,graph", [(37, 24, 3, "er"), (37, 7, 2, "er"), (207, 4096, 2, "knn"),
+                                          (64, 128, 1, "ring"), (5, 3, 0, "er")])
+def test_diffusion_vs_oracle(env, N, W, K, graph):
+    pgti, torch = env
+    g = {"er": lambda: synth.random_graph(N, 0.15, seed=N),
+         "knn": lambda: synth.make_graph(N, 8),
+         "ring": lambda: synth.ring_graph(N)}[graph]()
+    cfg = synth.Config("d", N=N, E=10, F=1, T_in=1, T_out=1, L=1, H=8, K=K, B=1)
+    model = model_for(pgti, torch, cfg, g)
+    Pf, Pb = transitions.transition_matrices(N, *g)
+    rng = np.random.default_rng(0)
+    Z = rng.normal(size=(N, W)).astype(np.float32)
+    M = 2 * K + 1
+    out = torch.empty(M * N * W, device="cuda")
+    model.diffuse(torch.from_numpy(Z).cuda(), W, out)
+    want = dcgru.diffusion_features(Pf, Pb, Z.astype(np.float64), K)
+    got = out.cpu().numpy().reshape(M, N, W)
+    for m in range(M):
+        assert scale_rel(got[m], want[m]) <= 1e-6, m
+    dT = rng.normal(size=(M, N, W)).astype(np.float32)
+    dZ = torch.empty(N * W, device="cuda")
+    model.diffuse_adjoint(torch.from_numpy(dT).cuda(), W, dZ)
+    want = dcgru.diffusion_adjoint(Pf, Pb, dT.astype(np.float64), K)
+    assert scale_rel(dZ.cpu().numpy().reshape(N, W), want) <= 1e-6
+
+
+# ------------------------------------------------------------------ full step (K1..K5)
+def _step_case(env, cfg, seed=0, B=None, scale=1.0):
+    pgti, torch = env
+    B = B or cfg.B
+    cfg = cfg.replace(B=B)
+    ref = ref_for(cfg)
+    s = load_series(pgti, torch, ref.v, 0, cfg, ref.mu, ref.sigma)
+    idx_np = ref.plan(1, 0, epoch=seed)[:B]
+    idx = torch.from_numpy(idx_np.astype(np.int32)).cuda()
+    ld = ld_of(cfg)
+    x = torch.empty(B * cfg.T_in * ld, device="cuda")
+    y = torch.empty(B * cfg.T_out * ld, device="cuda")
+    s.gather(idx, B, cfg.T_in, cfg.T_out, x, y)
+    model = model_for(pgti, torch, cfg, ref.graph)
+    theta = synth.make_params(cfg, seed=synth.SEED_PARAMS + seed, kind="random", scale=scale)
+    assert model.num_params() == theta.size == dcgru.num_params(ref.d)
+    loss, g, act = run_step(pgti, torch, model, theta, x, y)
+    xo, yo = ref.batch(idx_np)
+    loss_ref, g_ref, fwd = dcgru.backward(theta.astype(np.float64), ref.d, ref.Pf, ref.Pb,
+                                          xo.astype(np.float64), yo.astype(np.float64))
+    resid = np.abs(fwd["yhat"] - yo[..., :cfg.F_out])
+    return dict(loss=loss, g=g, act=act, loss_ref=loss_ref, g_ref=g_ref, fwd=fwd, cfg=cfg,
+                ref=ref, margin=float(resid.min()), B=B)
+
+
+def _check_step(c, tol=TOL32):
+    cfg, B = c["cfg"], c["B"]
+    assert c["margin"] > 1e-5, "a residual sits at an |.| kink; pick another seed"
+    assert abs(c["loss"] - c["loss_ref"]) <= tol * abs(c["loss_ref"])
+    acts, yhat = split_dump(c["act"], cfg, B)
+    acts_ref, yhat_ref = dcgru.activations(c["fwd"], dcgru.Dims.of(cfg))
+    # oracle [T][L][4][B][N][H] vs dump [T][L][4][N][B][H]
+    acts_ref = acts_ref.transpose(0, 1, 2, 4, 3, 5)
+    for t in range(cfg.T_in):
+        for l in range(cfg.L):
+            for q, nm in enumerate("Hruc"):
+                e = scale_rel(acts[t, l, q], acts_ref[t, l, q])
+                assert e <= tol, (t, l, nm, e)
+    assert scale_rel(yhat, yhat_ref.transpose(1, 2, 0, 3)) <= tol
+    off = 0
+    for name, shp in synth.param_shapes(cfg):
+        n = int(np.prod(shp))
+        e = scale_rel(c["g"][off:off + n], c["g_ref"][off:off + n])
+        assert e <= tol, (name, e)
+        off += n
+    assert scale_rel(c["g"], c["g_ref"]) <= tol
+
+
+@pytest.mark.parametrize("name", list(SMALL_CONFIGS))
+@pytest.mark.parametrize("seed", [0, 1])
+def test_step_parity_small(env, name, seed):
+    _check_step(_step_case(env, SMALL_CONFIGS[name], seed=seed))
+
+
+@pytest.mark.parametrize("name,B", [("metr_la", 64), ("metr_la", 13), ("pems_bay", 16)])
+def test_step_parity_traffic(env, name, B):
+    """METR-LA at its full per-GPU batch (the bench's launch configuration)."""
+    _check_step(_step_case(env, synth.CONFIGS[name], B=B))
+
+
+def test_step_is_deterministic(env):
+    c1 = _step_case(env, SMALL_CONFIGS["odd"])
+    c2 = _step_case(env, SMALL_CONFIGS["odd"])
+    assert c1["loss"] == c2["loss"] and np.array_equal(c1["g"].view(np.uint32), c2["g"].view(np.uint32))
+
+
+def test_step_errors(env):
+    pgti, torch = env
+    cfg = SMALL_CONFIGS["tiny2"]
+    ref = ref_for(cfg)
+    model = model_for(pgti, torch, cfg, ref.graph)
+    n = model.num_params()
+    p = torch.zeros(n, device="cuda")
+    ws = torch.empty(model.workspace_bytes() - 256, dtype=torch.uint8, device="cuda")
+    x = torch.zeros(cfg.B * cfg.T_in * ld_of(cfg), device="cuda")
+    y = torch.zeros(cfg.B * cfg.T_out * ld_of(cfg), device="cuda")
+    with pytest.raises(pgti.PgtiError) as e:
+        model.step(p, p.clone(), x, y, torch.zeros(1, device="cuda"), ws)
+    assert e.value.name == "WORKSPACE" and "needed" in str(e.value)
+
+
+# ------------------------------------------------------------------ data parallel + Adam
+@pytest.mark.parametrize("R", [2, 4])
+def test_ddp_equivalence_emulated(env, R):
+    """R virtual ranks on one GPU, each on its own halo shard and first batch; their gradient
+    mean equals the oracle gradient of the union batch."""
+    pgti, torch = env
+    from paper_2507_11683_b200 import trainer
+    cfg = synth.CONFIGS["metr_la"].replace(B=8)
+    ref = ref_for(cfg)
+    theta = synth.make_params(cfg, kind="random")
+    gsum = np.zeros(theta.size)
+    union = []
+    for r in range(R):
+        p = trainer.shard_plan(ref.n_train, R, r, cfg.T_in, cfg.T_out)
+        s = load_series(pgti, torch, ref.v[p.row_lo:p.row_hi], p.row_lo, cfg, ref.mu, ref.sigma)
+        idx = torch.empty(p.win_hi - p.win_lo, dtype=torch.int32, device="cuda")
+        s.make_index(p.win_lo, p.win_hi, cfg.T_in, cfg.T_out, cfg.B, 3, 0, r, 1, idx)
+        ld = ld_of(cfg)
+        x = torch.empty(cfg.B * cfg.T_in * ld, device="cuda")
+        y = torch.empty(cfg.B * cfg.T_out * ld, device="cuda")
+        s.gather(idx[:cfg.B], cfg.B, cfg.T_in, cfg.T_out, x, y)
+        model = model_for(pgti, torch, cfg, ref.graph)
+        _, g, _ = run_step(pgti, torch, model, theta, x, y, dump=False)
+        gsum += g
+        union.append(idx[:cfg.B].cpu().numpy())
+    union = np.concatenate(union)
+    _, g_union, _ = ref.loss_and_grad(theta, union)
+    assert scale_rel(gsum / R, g_union) <= TOL32
+
+
+def test_adam_vs_oracle(env):
+    pgti, torch = env
+    rng = np.random.default_rng(0)
+    n = 1001  # ragged tail
+    th = rng.normal(size=n).astype(np.float32)
+    p = torch.from_numpy(th).cuda()
+    m = torch.zeros(n, device="cuda")
+    v = torch.zeros(n, device="cuda")
+    dev_step = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tho, mo, vo = th.astype(np.float64), np.zeros(n), np.zeros(n)
+    for step in range(1, 7):
+        g = rng.normal(size=n).astype(np.float32)
+        use_dev = step % 2 == 0
+        if use_dev:
+            dev_step.fill_(step - 1)
+        pgti.adam_step(p, torch.from_numpy(g).cuda(), m, v, 0 if use_dev else step, 1e-2,
+                       grad_scale=0.25, dev_step=dev_step if use_dev else None)
+        tho, mo, vo = adam.adam_step(tho, g, mo, vo, step, 1e-2, grad_scale=0.25)
+        assert scale_rel(p.cpu().numpy() - th, tho - th) <= 1e-5
+    assert int(dev_step.item()) == 6
+
+
+def test_trainer_cuda_graph_matches_eager(env):
+    """The captured step (gather -> fwd/bwd -> Adam) replays to the same parameters, bit for
+    bit, as eager launches; and the Trainer's own statistics match Alg. 1."""
+    pgti, torch = env
+    from paper_2507_11683_b200.trainer import Trainer
+    cfg = SMALL_CONFIGS["cp"]
+    ref = ref_for(cfg)
+    theta = synth.make_params(cfg, kind="train")
+    outs = []
+    for use_graph in (False, True):
+        tr = Trainer(cfg, ref.graph, lambda a, b: ref.v[a:b], theta, use_cuda_graph=use_graph)
+        assert abs(tr.mu - ref.mu) <= 1e-12 * abs(ref.mu)
+        assert abs(tr.sigma - ref.sigma) <= 1e-12 * ref.sigma
+        steps = tr.start_epoch(0)
+        losses = []
+        for j in range(min(steps, 12)):
+            tr.step(j)
+            losses.append(float(tr.loss.item()))
+        tr.check()
+        outs.append((tr.params.cpu().numpy(), losses))
+    assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
+    assert outs[0][1] == outs[1][1]
