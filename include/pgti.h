@@ -214,6 +214,20 @@ pgti_status pgti_adam_step(float *params, const float *grads, float *m, float *v
                            int64_t step, int64_t *dev_step, float lr, float beta1, float beta2,
                            float eps, float grad_scale, void *stream);
 
+/* ----------------------------------------------------------------- instrumentation */
+/* Per-kernel-class timing for the roofline report (bench.py).  While enabled, every EAGER
+ * launch (not while a stream is being captured into a CUDA graph) is bracketed by two CUDA
+ * events on its own stream and attributed to one class (gather, spmm, gemm_fwd, ...) with its
+ * ALGORITHMIC bytes and flops.  pgti_profile_read synchronises on the
+ * recorded events, writes per-class totals (ms, bytes, flops, launches; arrays of >=
+ * pgti_profile_num_classes() entries) and clears the record.  Errors: INVALID_ARG, CUDA. */
+pgti_status pgti_profile_enable(int on);
+int pgti_profile_num_classes(void);
+const char *pgti_profile_class_name(int c);
+pgti_status pgti_profile_read(double *ms, double *bytes, double *flops, int64_t *launches, int n);
+/* Number of kernel launches libpgti has issued (captured launches included) since load. */
+uint64_t pgti_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

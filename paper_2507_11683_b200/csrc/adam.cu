@@ -3,6 +3,7 @@
 #include <cmath>
 
 #include "common.cuh"
+#include "profile.cuh"
 
 namespace {
 
@@ -65,6 +66,9 @@ extern "C" pgti_status pgti_adam_step(float *params, const float *grads, float *
   cudaStream_t s = pgti::as_stream(stream);
   const int64_t *ds = step > 0 ? nullptr : dev_step;
   const int64_t n4 = int64_t(n) / 4;
+  // algorithmic bytes: read params, grads, m, v; write params, m, v
+  pgti::ProfScope prof(pgti::kProfAdam, s, 28.0 * double(n), 10.0 * double(n),
+                       (n4 > 0) + (int64_t(n) > n4 * 4) + (ds != nullptr));
   if (n4 > 0) {
     const int grid = int(std::min<int64_t>(pgti::ceil_div(n4, 256), 148 * 8));
     k_adam<<<grid, 256, 0, s>>>(reinterpret_cast<float4 *>(params),

@@ -7,6 +7,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "profile.cuh"
 
 struct pgti_comm {
   ncclComm_t comm;
@@ -48,6 +49,9 @@ extern "C" pgti_status pgti_comm_init(pgti_comm **out, const uint8_t id[128], in
 extern "C" pgti_status pgti_allreduce_grads(pgti_comm *c, float *grads, size_t n, void *stream) {
   pgti::clear_error();
   PGTI_REQUIRE(c && grads, PGTI_ERR_INVALID_ARG, "pgti_allreduce_grads: null pointer");
+  // bytes each rank must move in a ring all-reduce: 2 (R-1)/R n 4 (reported as "bus" bytes)
+  pgti::ProfScope prof(pgti::kProfAllreduce, pgti::as_stream(stream),
+                       2.0 * (c->world - 1) / c->world * double(n) * 4.0, double(n));
   PGTI_NCCL_TRY(ncclAllReduce(grads, grads, n, ncclFloat32, ncclSum, c->comm,
                               pgti::as_stream(stream)));
   return PGTI_OK;

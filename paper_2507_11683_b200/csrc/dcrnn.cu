@@ -65,8 +65,8 @@ pgti_status check_desc(const pgti_dcrnn_desc *desc, Dims *out) {
                g.T_in);
   PGTI_REQUIRE(g.F_out >= 1 && g.F_out <= g.F && g.F_out <= 4, PGTI_ERR_SHAPE,
                "desc: F_out=%d must be in [1, min(F, 4)]", g.F_out);
-  PGTI_REQUIRE(g.H == 8 || g.H == 16 || g.H == 32 || g.H == 64, PGTI_ERR_UNSUPPORTED,
-               "desc: H=%d (this build supports 8, 16, 32, 64)", g.H);
+  PGTI_REQUIRE(g.H == 16 || g.H == 32 || g.H == 64, PGTI_ERR_UNSUPPORTED,
+               "desc: H=%d (this build supports 16, 32, 64)", g.H);
   PGTI_REQUIRE(g.ld >= int64_t(g.N) * g.F && g.ld % 4 == 0, PGTI_ERR_ALIGNMENT,
                "desc: ld=%lld must be >= N*F and a multiple of 4", (long long)g.ld);
   PGTI_REQUIRE(g.precision == 0, PGTI_ERR_UNSUPPORTED,
@@ -130,10 +130,10 @@ cudaError_t diffuse_fwd(const pgti_dcrnn_desc &g, const Dims &d, float *base, in
                         int G, int64_t gstride, int64_t W, cudaStream_t s) {
   for (int k = 1; k <= d.K; ++k) {
     SpmmJob j[2] = {};
-    j[0].rowptr[0] = g.a_rowptr, j[0].col[0] = g.a_col, j[0].val[0] = g.Pf_val;
+    j[0].rowptr[0] = g.a_rowptr, j[0].col[0] = g.a_col, j[0].val[0] = g.Pf_val, j[0].nnz[0] = g.nnz;
     j[0].X[0] = base + (k - 1) * mstride;
     j[0].Y = base + k * mstride;
-    j[1].rowptr[0] = g.at_rowptr, j[1].col[0] = g.at_col, j[1].val[0] = g.Pb_val;
+    j[1].rowptr[0] = g.at_rowptr, j[1].col[0] = g.at_col, j[1].val[0] = g.Pb_val, j[1].nnz[0] = g.nnz;
     j[1].X[0] = k == 1 ? base : base + (d.K + k - 1) * mstride;
     j[1].Y = base + (d.K + k) * mstride;
     for (auto &jb : j) jb.nterms = 1, jb.W = W, jb.G = G, jb.gstride = gstride;
@@ -174,6 +174,7 @@ cudaError_t diffuse_adj(const pgti_dcrnn_desc &g, const Dims &d, AdjChain *ch, i
     for (int c = 0; c < nch; ++c) {
       SpmmJob f{}, b{};
       f.rowptr[0] = g.at_rowptr, f.col[0] = g.at_col, f.val[0] = g.PfT_val, f.X[0] = af[c];
+      f.nnz[0] = b.nnz[0] = g.nnz;
       f.add = ch[c].dT + k * ch[c].mstride, f.Y = ch[c].tf[pp];
       b.rowptr[0] = g.a_rowptr, b.col[0] = g.a_col, b.val[0] = g.PbT_val, b.X[0] = ab[c];
       b.add = ch[c].dT + (K + k) * ch[c].mstride, b.Y = ch[c].tb[pp];
@@ -189,6 +190,7 @@ cudaError_t diffuse_adj(const pgti_dcrnn_desc &g, const Dims &d, AdjChain *ch, i
     SpmmJob j{};
     j.rowptr[0] = g.at_rowptr, j.col[0] = g.at_col, j.val[0] = g.PfT_val, j.X[0] = af[c];
     j.rowptr[1] = g.a_rowptr, j.col[1] = g.a_col, j.val[1] = g.PbT_val, j.X[1] = ab[c];
+    j.nnz[0] = j.nnz[1] = g.nnz;
     j.nterms = 2, j.add = ch[c].dT, j.Y = ch[c].out, j.accumulate = ch[c].accumulate;
     j.W = ch[c].W, j.G = 1;
     jobs[c] = j;

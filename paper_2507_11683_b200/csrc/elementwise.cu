@@ -1,5 +1,6 @@
 // Small fused elementwise kernels of the step: x re-layout, MAE loss (K5), GRU backward.
 #include "kernels.cuh"
+#include "profile.cuh"
 
 namespace pgti {
 namespace {
@@ -117,13 +118,16 @@ __global__ void k_gate_bwd(int64_t RH, int H, const float *__restrict__ drH,
 
 cudaError_t launch_x_prep(const float *x, int B, int T_in, int64_t ld, int N, int F, float *X0,
                           cudaStream_t s) {
-  k_x_prep<<<grid_for(int64_t(T_in) * N * B * F), kT, 0, s>>>(x, B, T_in, ld, N, F, X0);
+  const int64_t n = int64_t(T_in) * N * B * F;
+  ProfScope prof(kProfElementwise, s, 8.0 * double(n), 0.0);
+  k_x_prep<<<grid_for(n), kT, 0, s>>>(x, B, T_in, ld, N, F, X0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_loss(const float *yhat, const float *y, int T_out, int N, int B, int F,
                         int F_out, int64_t ld, float *dyhat, double *partials, float *loss,
                         unsigned *err, cudaStream_t s) {
+  ProfScope prof(kProfLoss, s, 12.0 * double(T_out) * N * B * F_out, 0.0, 2);
   k_loss_partial<<<kLossBlocks, kT, 0, s>>>(yhat, y, T_out, N, B, F, F_out, ld, dyhat, partials);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -135,6 +139,7 @@ cudaError_t launch_cand_bwd(int64_t RH, int H, const float *dHcur, const float *
                             const float *Wout, int F_out, const float *u, const float *c,
                             const float *Hprev, float *dU, float *dC, float *dHprev_out,
                             cudaStream_t s) {
+  ProfScope prof(kProfElementwise, s, 4.0 * double(RH) * (3 + (Hprev ? 1 : 0) + 2 + (dHprev_out ? 1 : 0)), 0.0);
   k_cand_bwd<<<grid_for(RH), kT, 0, s>>>(RH, H, dHcur, dy, Wout, F_out, u, c, Hprev, dU, dC,
                                          dHprev_out);
   return cudaGetLastError();
@@ -143,6 +148,8 @@ cudaError_t launch_cand_bwd(int64_t RH, int H, const float *dHcur, const float *
 cudaError_t launch_gate_bwd(int64_t RH, int H, const float *drH, const float *Hprev,
                             const float *r, const float *u, const float *dU, float *dHprev,
                             float *dG, cudaStream_t s) {
+  ProfScope prof(kProfElementwise, s,
+                 4.0 * double(RH) * (3 + (drH ? 1 : 0) + (Hprev ? 1 : 0) + (dHprev ? 2 : 0) + 2), 0.0);
   k_gate_bwd<<<grid_for(RH), kT, 0, s>>>(RH, H, drH, Hprev, r, u, dU, dHprev, dG);
   return cudaGetLastError();
 }

@@ -6,6 +6,7 @@
 // from the diffusion buffers (multi-source A operand), never concatenated in memory.
 // Equations: Li et al. Eq. 2-3 [ext]; readings c1-c7.
 #include "kernels.cuh"
+#include "profile.cuh"
 
 namespace pgti {
 namespace {
@@ -303,6 +304,11 @@ __global__ void __launch_bounds__(256) k_readout_wgrad(const __grid_constant__ R
 
 cudaError_t launch_gconv_fwd(const GconvFwd &p, cudaStream_t s) {
   const dim3 grid(unsigned(ceil_div(p.R, BM)));
+  const double Kt = double(p.a.M) * (p.a.Fin + p.a.Hd), R = p.R, H = p.mode == kEpiGate ? p.Nout / 2 : p.Nout;
+  // algorithmic bytes: A blocks + W + bias read once; epilogue reads Hprev (+u), writes outputs
+  const double io = p.mode == kEpiGate ? (p.Hprev ? 1 : 0) + 3 : (p.Hprev ? 1 : 0) + 1 + 2;
+  const double bytes = 4.0 * (R * Kt + Kt * p.Nout + p.Nout + R * H * io + (p.yhat ? R * p.F_out : 0));
+  ProfScope prof(kProfGemmFwd, s, bytes, 2.0 * R * Kt * p.Nout);
   switch (p.Nout) {
     case 16: k_gconv_fwd<16><<<grid, NT, 0, s>>>(p); break;
     case 32: k_gconv_fwd<32><<<grid, NT, 0, s>>>(p); break;
@@ -317,6 +323,9 @@ cudaError_t launch_gconv_dgrad(const GconvDgrad &p, cudaStream_t s) {
   const int Vtot = p.M * (p.c_hi - p.c_lo);
   if (Vtot <= 0) return cudaSuccess;
   const dim3 grid(unsigned(ceil_div(p.R, BM)), unsigned(ceil_div(Vtot, DBN)));
+  const double R = p.R;
+  const double bytes = 4.0 * (R * p.Nout + double(Vtot) * p.Nout + R * Vtot);
+  ProfScope prof(kProfGemmDgrad, s, bytes, 2.0 * R * p.Nout * Vtot);
   k_gconv_dgrad<<<grid, NT, 0, s>>>(p);
   return cudaGetLastError();
 }
@@ -331,16 +340,22 @@ cudaError_t launch_gconv_wgrad(const GconvWgrad &p, cudaStream_t s) {
   const int nchunks = p.T * cpt;
   if (int64_t(nchunks) * Vr * p.Nout > p.partial_cap) return cudaErrorInvalidValue;
   const dim3 grid(unsigned(ceil_div(Vr, BM)), unsigned(nchunks));
-  switch (p.Nout) {
-    case 16: k_gconv_wgrad<16><<<grid, NT, 0, s>>>(p, cpt); break;
-    case 32: k_gconv_wgrad<32><<<grid, NT, 0, s>>>(p, cpt); break;
-    case 64: k_gconv_wgrad<64><<<grid, NT, 0, s>>>(p, cpt); break;
-    case 128: k_gconv_wgrad<128><<<grid, NT, 0, s>>>(p, cpt); break;
-    default: return cudaErrorInvalidValue;
+  const int64_t n = int64_t(Vr) * p.Nout;
+  {
+    const double TR = double(p.T) * p.R;
+    const double bytes = 4.0 * (TR * (Vr - 1) + TR * p.Nout + double(nchunks) * n);
+    ProfScope prof(kProfGemmWgrad, s, bytes, 2.0 * TR * Vr * p.Nout);
+    switch (p.Nout) {
+      case 16: k_gconv_wgrad<16><<<grid, NT, 0, s>>>(p, cpt); break;
+      case 32: k_gconv_wgrad<32><<<grid, NT, 0, s>>>(p, cpt); break;
+      case 64: k_gconv_wgrad<64><<<grid, NT, 0, s>>>(p, cpt); break;
+      case 128: k_gconv_wgrad<128><<<grid, NT, 0, s>>>(p, cpt); break;
+      default: return cudaErrorInvalidValue;
+    }
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const int64_t n = int64_t(Vr) * p.Nout;
+  ProfScope prof(kProfReduce, s, 4.0 * double(n) * (nchunks + 1), double(n) * nchunks);
   k_reduce_chunks<<<unsigned(std::min<int64_t>(ceil_div(n, 256), 1184)), 256, 0, s>>>(
       p.partial, nchunks, n, p.out);
   return cudaGetLastError();
@@ -354,10 +369,16 @@ cudaError_t launch_readout_wgrad(const ReadoutWgrad &p, cudaStream_t s) {
   if (p.F_out > 4) return cudaErrorInvalidValue;
   const int cpt = int(ceil_div(p.R, RKC));
   const int nchunks = p.T * cpt;
-  k_readout_wgrad<<<unsigned(nchunks), 256, 0, s>>>(p, cpt);
+  const int64_t n = int64_t(p.H + 1) * p.F_out;
+  {
+    const double TR = double(p.T) * p.R;
+    ProfScope prof(kProfGemmWgrad, s, 4.0 * (TR * p.H + TR * p.F_out + double(nchunks) * n),
+                   2.0 * TR * n);
+    k_readout_wgrad<<<unsigned(nchunks), 256, 0, s>>>(p, cpt);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const int64_t n = int64_t(p.H + 1) * p.F_out;
+  ProfScope prof(kProfReduce, s, 4.0 * double(n) * (nchunks + 1), double(n) * nchunks);
   k_reduce_chunks<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(p.partial, nchunks, n, p.out);
   return cudaGetLastError();
 }

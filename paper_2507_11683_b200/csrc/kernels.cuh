@@ -14,6 +14,7 @@ struct SpmmJob {
   const int32_t *col[2];
   const float *val[2];
   const float *X[2];
+  int64_t nnz[2];     // entries of each term's CSR (algorithmic-byte accounting)
   int nterms;
   const float *add;   // nullable
   float *Y;

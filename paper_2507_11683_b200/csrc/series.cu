@@ -11,6 +11,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "profile.cuh"
 
 struct pgti_series {
   int64_t row0, nrows, N, F, ld;
@@ -260,6 +261,7 @@ extern "C" pgti_status pgti_load_series(pgti_series **out, const float *host_row
   if (ld > N * F) {
     int64_t total = nrows * (ld - N * F);
     int grid = int(std::min<int64_t>(pgti::ceil_div(total, 256), 4 * 148 * 8));
+    pgti::ProfScope prof(pgti::kProfSeries, s, 4.0 * double(total), 0.0);
     k_zero_pads<<<grid, 256, 0, s>>>(dev_buf, nrows, ld, N * F);
     PGTI_LAUNCH_TRY();
   }
@@ -281,6 +283,8 @@ extern "C" pgti_status pgti_series_stats(const pgti_series *sr, int64_t S_tr, in
                (long long)(sr->row0 + sr->nrows));
   if (row_hi == row_lo) return PGTI_OK;
   int grid = int(std::min<int64_t>(row_hi - row_lo, 148 * 16));
+  pgti::ProfScope prof(pgti::kProfSeries, pgti::as_stream(stream),
+                       4.0 * double(row_hi - row_lo) * double(sr->N * sr->F), 0.0);
   k_stats<<<grid, 256, 0, pgti::as_stream(stream)>>>(sr->buf, sr->row0, sr->ld, sr->N * sr->F,
                                                       row_lo, row_hi, S_tr, T_in, shift, dev_sums);
   PGTI_LAUNCH_TRY();
@@ -296,6 +300,7 @@ extern "C" pgti_status pgti_series_normalize(pgti_series *sr, double mu, double 
                "sigma=%g must be finite and > 0", sigma);
   int64_t total = sr->nrows * (sr->ld / 4);
   int grid = int(std::min<int64_t>(pgti::ceil_div(total, 256), 148 * 16));
+  pgti::ProfScope prof(pgti::kProfSeries, pgti::as_stream(stream), 8.0 * double(total) * 4, 0.0);
   k_normalize<<<grid, 256, 0, pgti::as_stream(stream)>>>(sr->buf, sr->nrows, sr->ld,
                                                           sr->N * sr->F, float(mu), float(sigma));
   PGTI_LAUNCH_TRY();
@@ -344,6 +349,8 @@ extern "C" pgti_status pgti_make_index(const pgti_series *sr, int64_t win_lo, in
   PGTI_REQUIRE(n >= B, PGTI_ERR_TOO_FEW_WINDOWS, "%lld windows < batch %d", (long long)n, B);
   cudaStream_t s = pgti::as_stream(stream);
   const int grid = int(std::min<int64_t>(pgti::ceil_div(n, 256), 148 * 8));
+  pgti::ProfScope prof(pgti::kProfIndex, s, double(n) * (shuffle ? 48.0 : 4.0), 0.0,
+                       shuffle ? 5 : 1);
   if (!shuffle) {
     k_keys<<<grid, 256, 0, s>>>(n, int32_t(win_lo), seed, epoch, uint32_t(rank), 0, nullptr,
                                 dev_idx);
@@ -385,6 +392,9 @@ extern "C" pgti_status pgti_gather_batch(const pgti_series *sr, const int32_t *d
   unsigned *err = pgti::device_error_flag();
   PGTI_REQUIRE(err, PGTI_ERR_CUDA, "device error flag unavailable");
   cudaStream_t s = pgti::as_stream(stream);
+  // algorithmic bytes: 2 B (T_in+T_out) N F 4 -- read + write, pads excluded
+  pgti::ProfScope prof(pgti::kProfGather, s, 8.0 * B * (T_in + T_out) * double(sr->N * sr->F),
+                       0.0);
   if (gather_mode() == 1) {
     const int64_t xb = int64_t(T_in) * sr->ld * 4, yb = int64_t(T_out) * sr->ld * 4;
     const int64_t xc = pgti::ceil_div(xb, kChunk), yc = pgti::ceil_div(yb, kChunk);

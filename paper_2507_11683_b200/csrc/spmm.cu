@@ -5,6 +5,7 @@
 // registers and broadcast with shuffles; the neighbour slices are read with 128-bit loads,
 // kUnroll of them in flight; fp32 accumulation in CSR order (deterministic).
 #include "kernels.cuh"
+#include "profile.cuh"
 
 namespace pgti {
 namespace {
@@ -127,6 +128,19 @@ cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s) {
   p.N = N;
   p.total_warps = w;
   if (w == 0) return cudaSuccess;
+  // algorithmic bytes (SURVEY 8(d) K2 model): each dense operand row read once per term,
+  // output written once, addend / accumulator read once, CSR (col, val, rowptr) once per group
+  double bytes = 0.0, flops = 0.0;
+  for (int i = 0; i < njobs; ++i) {
+    const SpmmJob &j = jobs[i];
+    const double nw = double(N) * double(j.W) * 4.0 * j.G;
+    bytes += nw * (1 + j.nterms + (j.add ? 1 : 0) + (j.accumulate ? 1 : 0));
+    for (int t = 0; t < j.nterms; ++t) {
+      bytes += (double(j.nnz[t]) * 8.0 + double(N + 1) * 4.0) * j.G;
+      flops += 2.0 * double(j.nnz[t]) * double(j.W) * j.G;
+    }
+  }
+  ProfScope prof(kProfSpmm, s, bytes, flops);
   const int64_t blocks = ceil_div(w, 8);
   if (vec4)
     k_spmm<4><<<unsigned(blocks), 256, 0, s>>>(p);

@@ -62,6 +62,6 @@ SMALL_CONFIGS = {
     "tiny2": synth.Config("tiny2", N=12, E=60, F=2, T_in=3, T_out=2, L=2, H=16, K=2, B=3),
     "cp": synth.CONFIGS["chickenpox"],
     "odd": synth.Config("odd", N=33, E=80, F=3, T_in=5, T_out=5, L=2, H=64, K=1, B=5, F_out=2),
-    "k0": synth.Config("k0", N=9, E=40, F=1, T_in=4, T_out=3, L=3, H=8, K=0, B=2),
+    "k0": synth.Config("k0", N=9, E=40, F=1, T_in=4, T_out=3, L=3, H=16, K=0, B=2),
     "k3": synth.Config("k3", N=17, E=50, F=2, T_in=4, T_out=2, L=1, H=32, K=3, B=7),
 }

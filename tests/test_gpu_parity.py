@@ -165,7 +165,7 @@ def test_diffusion_vs_oracle(env, N, W, K, graph):
     g = {"er": lambda: synth.random_graph(N, 0.15, seed=N),
          "knn": lambda: synth.make_graph(N, 8),
          "ring": lambda: synth.ring_graph(N)}[graph]()
-    cfg = synth.Config("d", N=N, E=10, F=1, T_in=1, T_out=1, L=1, H=8, K=K, B=1)
+    cfg = synth.Config("d", N=N, E=10, F=1, T_in=1, T_out=1, L=1, H=16, K=K, B=1)
     model = model_for(pgti, torch, cfg, g)
     Pf, Pb = transitions.transition_matrices(N, *g)
     rng = np.random.default_rng(0)
@@ -224,9 +224,14 @@ def _check_step(c, tol=TOL32):
                 assert e <= tol, (t, l, nm, e)
     assert scale_rel(yhat, yhat_ref.transpose(1, 2, 0, 3)) <= tol
     off = 0
+    gscale = np.max(np.abs(c["g_ref"]))
     for name, shp in synth.param_shapes(cfg):
         n = int(np.prod(shp))
-        e = scale_rel(c["g"][off:off + n], c["g_ref"][off:off + n])
+        g, gr = c["g"][off:off + n], c["g_ref"][off:off + n]
+        # per tensor scale-relative; a tensor whose reference is (near) zero -- e.g. db_out =
+        # sum of +-1/count with balanced signs -- is measured against 1e-3 of the gradient scale
+        den = max(np.max(np.abs(gr)), 1e-3 * gscale)
+        e = np.max(np.abs(g.astype(np.float64) - gr)) / den
         assert e <= tol, (name, e)
         off += n
     assert scale_rel(c["g"], c["g_ref"]) <= tol
