@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""bench.py -- training samples/s and peak HBM per GPU of the index-batched DCRNN step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config metr_la] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...       (one rank per GPU, NCCL)
+
+A step = gather (index batching) -> DCGRU forward + BPTT -> NCCL gradient all-reduce -> Adam,
+replayed as one CUDA graph per step, on synthetic seeded inputs of the named workload shape
+(BASELINE.json configs; METR-LA-shaped by default = configs[1]).  Timing: W untimed warm-up
+steps, then exactly K steps between barrier + synchronize, CUDA events on the launching stream,
+max over ranks.  Prints ONE JSON line on rank 0 (contract: see DESIGN.md "Measurement").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "training samples/sec and peak HBM per GPU, index-batched DCRNN, at 1/2/4/8 B200"
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # SIMT FFMA peak at max clock
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="metr_la")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", type=int, default=0)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def env_ranks():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ------------------------------------------------------------------------------ clocks
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200", "-i",
+                                       str(gpu)], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.f.flush()
+        sm, mx, reasons, pw = [], [], set(), []
+        for line in open(self.f.name):
+            c = [x.strip() for x in line.split(",")]
+            if len(c) < 8:
+                continue
+            try:
+                sm.append(float(c[1]))
+                mx.append(float(c[2]))
+                pw.append(float(c[3]))
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, c[4:8]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(pw) if pw else None}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except (OSError, ValueError):
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+            "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------------------ oracle legs
+def blas_threads():
+    try:
+        import threadpoolctl
+        return sum(i.get("num_threads", 0) for i in threadpoolctl.threadpool_info()
+                   if i.get("user_api") == "blas") or 1
+    except Exception:
+        return 1
+
+
+def oracle_samples_per_s(cfg, n_windows: int, repeats: int, warm: int = 1):
+    """Time the float64 oracle (Alg. 1 materialisation of the sampled windows + DCGRU forward/
+    backward + Adam) on a bounded sample of the workload.  Returns (samples/s, details)."""
+    import numpy as np
+
+    import synth
+    from oracle import adam, dcgru, pipeline
+
+    t0 = time.perf_counter()
+    ref = pipeline.Reference(cfg, materialize_all=False)
+    setup_s = time.perf_counter() - t0
+    theta = synth.make_params(cfg, kind="train").astype(np.float64)
+    m = np.zeros_like(theta)
+    v = np.zeros_like(theta)
+    plan = ref.plan(1, 0)
+    done, t_run, j = 0, 0.0, 0
+    for it in range(warm + repeats):
+        idx = plan[j:j + n_windows]
+        j += n_windows
+        t1 = time.perf_counter()
+        x, y = ref.batch(idx)
+        _, g, _ = dcgru.backward(theta, ref.d, ref.Pf, ref.Pb, x.astype(np.float64),
+                                 y.astype(np.float64))
+        theta, m, v = adam.adam_step(theta, g, m, v, it + 1, 1e-2)
+        if it >= warm:
+            t_run += time.perf_counter() - t1
+            done += len(idx)
+    return done / t_run, dict(setup_s=round(setup_s, 2), timed_s=round(t_run, 2),
+                              windows=done, per_batch=n_windows)
+
+
+def run_reference(args, cfg):
+    """--impl reference: the oracle is this tier's reference arm (rank 0 only, host cores)."""
+    rank, world, _ = env_ranks()
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+    K, W = args.steps, args.warmup
+    # calibrate the per-window cost, then size each step so the whole run ends in ~3 min
+    sps1, _ = oracle_samples_per_s(cfg, 1, 1, warm=0)
+    per_step_budget = 150.0 / max(1, K + W)
+    b = int(max(1, min(cfg.B, math.floor(per_step_budget * sps1))))
+    sps, det = oracle_samples_per_s(cfg, b, K, warm=W)
+    cores = blas_threads()
+    line = {"metric": METRIC, "value": round(sps, 4), "unit": "samples/s", "n_gpus": args.gpus,
+            "steps": K, "warmup": W, "ms_per_step": round(1000.0 * b / sps, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": config_dict(cfg, world, args),
+            "cpu_baseline": {"value": round(sps, 4), "unit": "samples/s", "cores": cores,
+                             "kind": "oracle",
+                             "sample": f"{K} steps x {b} windows of the {cfg.name} workload "
+                                       f"(after {W} warm-up steps), float64 oracle"},
+            "e2e": {"value": round(sps, 4), "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "oracle": det}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(cfg, world, args):
+    return {"workload": cfg.name, "N": cfg.N, "E": cfg.E, "F": cfg.F, "T_in": cfg.T_in,
+            "T_out": cfg.T_out, "layers": cfg.L, "hidden": cfg.H, "K_hops": cfg.K,
+            "per_gpu_batch": cfg.B, "global_batch": cfg.B * world,
+            "parallelism": f"dp{world} (halo-sharded distributed-index-batching)",
+            "precision": "fp32" if args.precision == 0 else "bf16",
+            "l2": "no flush: each step writes >= 1 GB of fresh activations (>> 126 MB L2)",
+            "cuda_graph": not args.no_graph}
+
+
+# ------------------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    import synth
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_11683_b200 import pgti
+    from paper_2507_11683_b200.trainer import Trainer
+
+    rank, world, local = env_ranks()
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    comm = None
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(pgti.comm_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        comm = pgti.Comm(bytes(uid.cpu().numpy().tolist()), rank, world, local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---------------------------------------------------------------- setup (untimed)
+    graph = synth.make_graph(cfg.N, cfg.knn)
+    params0 = synth.make_params(cfg, kind="train")
+    from paper_2507_11683_b200.trainer import shard_plan, train_windows, window_count
+    p = shard_plan(train_windows(window_count(cfg.E, cfg.T_in, cfg.T_out)), world, rank,
+                   cfg.T_in, cfg.T_out)
+    rows = synth.make_series(cfg, row_lo=p.row_lo, row_hi=p.row_hi)
+    barrier()
+    t0 = time.perf_counter()
+    tr = Trainer(cfg, graph, lambda a, b: rows, params0, rank, world, local, comm,
+                 precision=args.precision, use_cuda_graph=not args.no_graph)
+    torch.cuda.synchronize()
+    load_s = time.perf_counter() - t0
+    spe = tr.start_epoch(0)
+    state = {"epoch": 0}
+
+    def run(jg):
+        e, j = divmod(jg, spe)
+        if e != state["epoch"]:
+            tr.start_epoch(e)
+            state["epoch"] = e
+        tr.step(j)
+
+    for j in range(args.warmup):
+        run(j)
+    tr.check()
+    barrier()
+    torch.cuda.synchronize()
+
+    # ---------------------------------------------------------------- timed region
+    clocks = Clocks(local)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    ev0.record()
+    for j in range(args.warmup, args.warmup + args.steps):
+        run(j)
+    ev1.record()
+    torch.cuda.synchronize()
+    barrier()
+    ck = clocks.stop()
+    ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    t_ms = float(ms.item())
+    value = world * cfg.B * args.steps / (t_ms / 1000.0)
+    tr.check()
+    loss_last = float(tr.loss.item())
+
+    # ---------------------------------------------------------------- per-kernel breakdown
+    # an instrumented eager replay of the same step right after the timed region: every libpgti
+    # launch bracketed by CUDA events on its own stream
+    use_graph = tr.use_cuda_graph
+    tr.use_cuda_graph = False
+    pgti.profile_read()
+    pgti.profile_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    base = args.warmup + args.steps
+    for j in range(base, base + args.profile_steps):
+        run(j)
+    e1.record()
+    torch.cuda.synchronize()
+    prof = pgti.profile_read()
+    pgti.profile_enable(False)
+    tr.use_cuda_graph = use_graph
+    eager_ms = e0.elapsed_time(e1) / args.profile_steps
+    P = args.profile_steps
+    kernels = {k: {"ms_per_step": round(v["ms"] / P, 4), "launches_per_step": v["launches"] // P,
+                   "GB_per_step": round(v["bytes"] / P / 1e9, 4),
+                   "GFLOP_per_step": round(v["flops"] / P / 1e9, 3)}
+               for k, v in prof.items() if v["launches"]}
+    ours = {k: v for k, v in prof.items() if k != "allreduce" and v["launches"]}
+    launches_per_step = sum(v["launches"] for v in ours.values()) // P
+    dom = max(ours, key=lambda k: ours[k]["ms"])
+    d = prof[dom]
+    peaks, src = measured_peaks()
+    if dom.startswith("gemm") and args.precision == 0:
+        ach = d["flops"] / (d["ms"] / 1e3) / 1e12
+        roof = {"bound": "alu", "achieved": round(ach, 3), "peak": round(FP32_PEAK_TFLOPS, 1),
+                "unit": "TFLOP/s", "frac": round(ach / FP32_PEAK_TFLOPS, 4), "traffic": None,
+                "kernel": dom, "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz"}
+    elif dom.startswith("gemm"):
+        ach = d["flops"] / (d["ms"] / 1e3) / 1e12
+        pk = peaks.get("bf16_tflops_sustained") or peaks["bf16_tflops"]
+        roof = {"bound": "tensor", "achieved": round(ach, 3), "peak": pk, "unit": "TFLOP/s",
+                "frac": round(ach / pk, 4), "traffic": None, "kernel": dom, "peak_source": src}
+    else:
+        ach = d["bytes"] / (d["ms"] / 1e3) / 1e9
+        pk = peaks["hbm_gbs"]
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": pk, "unit": "GB/s",
+                "frac": round(ach / pk, 4), "traffic": None, "kernel": dom, "peak_source": src}
+    roof["share_of_step"] = round(d["ms"] / P / eager_ms, 4)
+    roof["per_launch_ms"] = round(d["ms"] / d["launches"], 5)
+    roof["algorithmic_per_launch"] = {"bytes": d["bytes"] / d["launches"],
+                                      "flops": d["flops"] / d["launches"]}
+
+    # ---------------------------------------------------------------- end to end (host buffers)
+    e2e = None
+    if not args.no_e2e:
+        B = cfg.B
+        tr.start_epoch(1)
+        plan_host = tr.idx[:tr.n_used].cpu().pin_memory()
+        loss_host = torch.zeros(1, dtype=torch.float32).pin_memory()
+        n_e2e = min(args.steps, tr.n_used // B)
+        for j in range(min(3, n_e2e)):
+            tr.step_from_host(plan_host[j * B:(j + 1) * B])
+        torch.cuda.synchronize()
+        barrier()
+        t1 = time.perf_counter()
+        for j in range(n_e2e):
+            tr.step_from_host(plan_host[j * B:(j + 1) * B])
+            loss_host.copy_(tr.loss, non_blocking=True)
+            torch.cuda.current_stream().synchronize()   # the host reads this step's loss
+        barrier()
+        te = torch.tensor([time.perf_counter() - t1], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(world * B * n_e2e / float(te.item()), 2), "unit": "samples/s",
+               "h2d_bytes_per_step": 4 * B, "d2h_bytes_per_step": 4, "steps": n_e2e,
+               "what": "per step: pinned H2D of the batch's window starts, graph replay of "
+                       "gather+fwd+bwd+allreduce+Adam, D2H of the loss, host sync",
+               "load_s": round(load_s, 3)}
+
+    # ---------------------------------------------------------------- memory + gather
+    peak_alloc = torch.cuda.max_memory_allocated(dev) / 1e9
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(local)
+        nvml_used = pynvml.nvmlDeviceGetMemoryInfo(h).used / 1e9
+    except Exception:
+        nvml_used = None
+    mem = torch.tensor([peak_alloc, nvml_used or 0.0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(mem, op=dist.ReduceOp.MAX)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, ck)
+        reasons = sorted({r for g in gathered for r in g.get("reasons", [])})
+        ck["reasons"] = reasons
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sps, det = oracle_samples_per_s(cfg, 8, 3)
+        cpu = {"value": round(sps, 4), "unit": "samples/s", "cores": blas_threads(),
+               "kind": "oracle",
+               "sample": f"3 batches x 8 windows of {cfg.name} (+1 warm-up), float64 Alg. 1 "
+                         f"materialisation + DCGRU fwd/bwd + Adam; host os.cpu_count()="
+                         f"{os.cpu_count()}", "details": det}
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 2), "unit": "samples/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": round(t_ms / args.steps, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32" if args.precision == 0 else "bf16",
+                "data": "synthetic (seeded series + kNN sensor graph of the workload's shape, "
+                        "random-init parameters)",
+                "config": config_dict(cfg, world, args),
+                "peak_hbm_gb": {"torch_max_allocated": round(float(mem[0]), 3),
+                                "nvml_used": round(float(mem[1]), 3) if nvml_used else None},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches_per_step * args.steps,
+                "launches_per_step": launches_per_step, "clocks": ck,
+                "kernels": kernels, "eager_ms_per_step": round(eager_ms, 4),
+                "loss_last": loss_last, "steps_per_epoch": spe}
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -81,6 +81,31 @@ _adam = _sig("pgti_adam_step", C.c_int, _vp, _vp, _vp, _vp, _sz, _i64, _vp, _f32
              _f32, _f32, _vp)
 
 
+_prof_enable = _sig("pgti_profile_enable", C.c_int, C.c_int)
+_prof_n = _sig("pgti_profile_num_classes", C.c_int)
+_prof_name = _sig("pgti_profile_class_name", C.c_char_p, C.c_int)
+_prof_read = _sig("pgti_profile_read", C.c_int, _vp, _vp, _vp, _vp, C.c_int)
+_launch_count = _sig("pgti_launch_count", C.c_uint64)
+
+
+def profile_enable(on: bool = True):
+    _ok(_prof_enable(int(on)))
+
+
+def profile_read() -> dict:
+    """{class: dict(ms, bytes, flops, launches)} of eager launches since the last read."""
+    n = _prof_n()
+    ms, by, fl = (np.zeros(n) for _ in range(3))
+    la = np.zeros(n, np.int64)
+    _ok(_prof_read(ms.ctypes.data, by.ctypes.data, fl.ctypes.data, la.ctypes.data, n))
+    return {_prof_name(i).decode(): dict(ms=float(ms[i]), bytes=float(by[i]), flops=float(fl[i]),
+                                         launches=int(la[i])) for i in range(n)}
+
+
+def launch_count() -> int:
+    return int(_launch_count())
+
+
 def last_error() -> str:
     return _lib_last_error().decode()
 

@@ -157,6 +157,17 @@ class Trainer:
             self._body(sl)
             return
         self.idx_cur.copy_(sl)
+        self._replay()
+
+    def step_from_host(self, idx_host):
+        """End-to-end form: this step's B window starts come from (pinned) host memory."""
+        self.idx_cur.copy_(idx_host, non_blocking=True)
+        if not self.use_cuda_graph:
+            self._body(self.idx_cur)
+            return
+        self._replay()
+
+    def _replay(self):
         if self.graph is None:
             torch = self.torch
             s = torch.cuda.Stream()
