@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "tc_gemm.cuh"
 
 namespace pgti {
 namespace {
@@ -23,6 +24,7 @@ namespace {
 struct Dims {
   int N, F, F_out, L, H, K, T_in, T_out, B, M;
   int64_t R, ld;
+  int precision;
 };
 
 struct Layout {
@@ -69,8 +71,12 @@ pgti_status check_desc(const pgti_dcrnn_desc *desc, Dims *out) {
                "desc: H=%d (this build supports 16, 32, 64)", g.H);
   PGTI_REQUIRE(g.ld >= int64_t(g.N) * g.F && g.ld % 4 == 0, PGTI_ERR_ALIGNMENT,
                "desc: ld=%lld must be >= N*F and a multiple of 4", (long long)g.ld);
-  PGTI_REQUIRE(g.precision == 0, PGTI_ERR_UNSUPPORTED,
-               "desc: precision=%d not available in this build (0 = fp32)", g.precision);
+  PGTI_REQUIRE(g.precision == 0 || g.precision == 1, PGTI_ERR_UNSUPPORTED,
+               "desc: precision=%d (0 = fp32 SIMT, 1 = bf16 tcgen05)", g.precision);
+  PGTI_REQUIRE(g.precision == 0 || (g.H == 64 && g.F * (2 * g.K + 1) <= 20),
+               PGTI_ERR_UNSUPPORTED,
+               "desc: the bf16 tcgen05 path needs H = 64 and F*(2K+1) <= 20 (H=%d F=%d K=%d)", g.H,
+               g.F, g.K);
   PGTI_REQUIRE(int64_t(g.N) * g.B * 2 * g.H < (int64_t(1) << 31), PGTI_ERR_SHAPE,
                "desc: N*B*2H exceeds int32 row indexing");
   if (g.K > 0)
@@ -78,7 +84,7 @@ pgti_status check_desc(const pgti_dcrnn_desc *desc, Dims *out) {
                      g.Pb_val && g.PfT_val && g.nnz >= 0,
                  PGTI_ERR_INVALID_ARG, "desc: CSR pointers must be set when K > 0");
   Dims d{g.N, g.F, g.F_out, g.L, g.H, g.K, g.T_in, g.T_out, g.B, 2 * g.K + 1,
-         int64_t(g.N) * g.B, g.ld};
+         int64_t(g.N) * g.B, g.ld, g.precision};
   *out = d;
   return PGTI_OK;
 }
@@ -353,6 +359,273 @@ pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *param
   return PGTI_OK;
 }
 
+
+// =========================================================================== precision = 1
+// bf16 tcgen05 path.  Differences from the fp32 path: the diffusion blocks of H and r*H are
+// bf16 (they are the tensor-core A operands and the forward SpMM operands), an fp32 copy of H
+// carries the recurrence, dG / dCpre also get bf16 copies (dgrad A / wgrad B operands), and the
+// weights are re-tiled to bf16 every step.  Layer 0's F-channel input part stays fp32 (FFMA in
+// the GEMM epilogue, SIMT wgrad rows); the backward adjoint diffusion stays fp32.
+struct LayoutTC {
+  size_t Dx, yhat, dyhat, lossp, dU, drH, dTin, dTH, wpart, total;
+  size_t tmp[8];
+  std::vector<size_t> DHb, DrHb, H32, Rg, Ug, Cg, dG, dGb, dC, dCb, dHa, dHb, Wf_ru, Wf_c, Wd_ru,
+      Wd_c;
+  size_t tmp_floats, wpart_floats;
+};
+
+int nkb_total(const Dims &d, int l) { return l == 0 ? d.M : 2 * d.M; }
+int vrows(const Dims &d, int l) { return l == 0 ? d.M * 64 : d.M * (d.H + d.H); }
+
+LayoutTC make_layout_tc(const Dims &d) {
+  LayoutTC L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += round_up(int64_t(bytes), 1024);
+    return o;
+  };
+  const size_t R = size_t(d.R), H = size_t(d.H), M = size_t(d.M), T = size_t(d.T_in);
+  L.Dx = take(M * T * R * d.F * 4);
+  size_t wp = readout_partial_floats(d.H, d.F_out, d.T_out, int(d.R));
+  for (int l = 0; l < d.L; ++l) {
+    L.DHb.push_back(take(T * M * R * H * 2));
+    L.DrHb.push_back(take(T * M * R * H * 2));
+    L.H32.push_back(take(T * R * H * 4));
+    L.Rg.push_back(take(T * R * H * 4));
+    L.Ug.push_back(take(T * R * H * 4));
+    L.Cg.push_back(take(T * R * H * 4));
+    L.dG.push_back(take(T * R * 2 * H * 4));
+    L.dGb.push_back(take(T * R * 2 * H * 2));
+    L.dC.push_back(take(T * R * H * 4));
+    L.dCb.push_back(take(T * R * H * 2));
+    L.dHa.push_back(take(R * H * 4));
+    L.dHb.push_back(take(R * H * 4));
+    const int C = (l == 0 ? d.F : d.H) + d.H;
+    L.Wf_ru.push_back(take(size_t(nkb_total(d, l)) * 2 * H * 64 * 2));
+    L.Wf_c.push_back(take(size_t(nkb_total(d, l)) * H * 64 * 2));
+    L.Wd_ru.push_back(take(size_t(vrows(d, l)) * 2 * H * 2));
+    L.Wd_c.push_back(take(size_t(vrows(d, l)) * H * 2));
+    wp = std::max(wp, tc_wgrad_partial_floats(vrows(d, l), 2 * d.H, d.T_in, int(d.R)));
+    wp = std::max(wp, wgrad_partial_floats(d.M, C, 2 * d.H, d.T_in, int(d.R)));
+  }
+  L.yhat = take(size_t(d.T_out) * R * d.F_out * 4);
+  L.dyhat = take(size_t(d.T_out) * R * d.F_out * 4);
+  L.lossp = take(size_t(kLossBlocks) * 8);
+  L.dU = take(R * H * 4);
+  L.drH = take(R * H * 4);
+  const size_t fin_max = d.L > 1 ? H : size_t(d.F);
+  L.dTin = take(M * R * fin_max * 4);
+  L.dTH = take(M * R * H * 4);
+  L.tmp_floats = R * std::max(H, fin_max);
+  for (int i = 0; i < 8; ++i) L.tmp[i] = take(L.tmp_floats * 4);
+  L.wpart_floats = wp;
+  L.wpart = take(wp * 4);
+  L.total = off;
+  return L;
+}
+
+cudaError_t diffuse_fwd_bf16(const pgti_dcrnn_desc &g, const Dims &d, __nv_bfloat16 *base,
+                             int64_t mstride, int64_t W, cudaStream_t s) {
+  for (int k = 1; k <= d.K; ++k) {
+    SpmmJob j[2] = {};
+    j[0].rowptr[0] = g.a_rowptr, j[0].col[0] = g.a_col, j[0].val[0] = g.Pf_val, j[0].nnz[0] = g.nnz;
+    j[0].X[0] = reinterpret_cast<const float *>(base + (k - 1) * mstride);
+    j[0].Y = reinterpret_cast<float *>(base + k * mstride);
+    j[1].rowptr[0] = g.at_rowptr, j[1].col[0] = g.at_col, j[1].val[0] = g.Pb_val, j[1].nnz[0] = g.nnz;
+    j[1].X[0] = reinterpret_cast<const float *>(k == 1 ? base : base + (d.K + k - 1) * mstride);
+    j[1].Y = reinterpret_cast<float *>(base + (d.K + k) * mstride);
+    for (auto &jb : j) jb.nterms = 1, jb.W = W, jb.G = 1, jb.gstride = 0, jb.bf16 = 1;
+    cudaError_t e = launch_spmm(j, 2, d.N, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *params,
+                        float *grads, const float *x, const float *y, float *loss_dev, char *ws,
+                        float *act_dump, cudaStream_t s) {
+  using bf16 = __nv_bfloat16;
+  const LayoutTC Ly = make_layout_tc(d);
+  const ParamOffsets P = param_offsets(d);
+  auto Fp = [&](size_t off) { return reinterpret_cast<float *>(ws + off); };
+  auto Bp = [&](size_t off) { return reinterpret_cast<bf16 *>(ws + off); };
+  const int64_t R = d.R, H = d.H, M = d.M, RH = R * H, MRH = M * RH;
+  const int T = d.T_in, L = d.L;
+  float *Dx = Fp(Ly.Dx);
+  const int64_t RF = R * d.F;
+  unsigned *err = device_error_flag();
+  PGTI_REQUIRE(err, PGTI_ERR_CUDA, "device error flag unavailable");
+
+  // ------------------------------------------------------------------ bf16 weight tiles
+  {
+    WeightJob jobs[8];
+    int nj = 0;
+    for (int l = 0; l < L; ++l) {
+      const int Fin = l == 0 ? d.F : d.H, C = Fin + d.H;
+      jobs[nj++] = WeightJob{params + P.Wru[l], 2 * d.H, C, d.M, Fin, l == 0, Bp(Ly.Wf_ru[l]),
+                             Bp(Ly.Wd_ru[l])};
+      jobs[nj++] = WeightJob{params + P.Wc[l], d.H, C, d.M, Fin, l == 0, Bp(Ly.Wf_c[l]),
+                             Bp(Ly.Wd_c[l])};
+    }
+    CU(launch_convert_weights(jobs, nj, s));
+  }
+
+  // ------------------------------------------------------------------ forward
+  CU(launch_x_prep(x, d.B, T, d.ld, d.N, d.F, Dx, s));
+  CU(diffuse_fwd(g, d, Dx, int64_t(T) * RF, T, RF, int64_t(d.B) * d.F, s));
+  for (int t = 0; t < T; ++t) {
+    for (int l = 0; l < L; ++l) {
+      const int Fin = l == 0 ? d.F : d.H, C = Fin + d.H;
+      const bf16 *Ain = l == 0 ? nullptr : Bp(Ly.DHb[l - 1]) + t * MRH;
+      const bf16 *DHp = t > 0 ? Bp(Ly.DHb[l]) + (t - 1) * MRH : nullptr;
+      bf16 *DHt = Bp(Ly.DHb[l]) + t * MRH, *DrHt = Bp(Ly.DrHb[l]) + t * MRH;
+      const float *Hp32 = t > 0 ? Fp(Ly.H32[l]) + (t - 1) * RH : nullptr;
+      float *r = Fp(Ly.Rg[l]) + t * RH, *u = Fp(Ly.Ug[l]) + t * RH, *c = Fp(Ly.Cg[l]) + t * RH;
+      auto fill_kb = [&](TcFwd &f, bool has_h) {
+        f.nkb = 0;
+        for (int m = 0; m < d.M; ++m) {
+          if (l > 0) f.kb_src[f.nkb] = 0, f.kb_m[f.nkb] = m, f.kb_w[f.nkb] = 2 * m, ++f.nkb;
+          if (has_h)
+            f.kb_src[f.nkb] = 1, f.kb_m[f.nkb] = m, f.kb_w[f.nkb] = l > 0 ? 2 * m + 1 : m, ++f.nkb;
+        }
+      };
+      TcFwd gate{};
+      gate.R = int(R), gate.H = d.H, gate.Nout = 2 * d.H, gate.mode = kEpiGate;
+      gate.A_in = Ain, gate.A_h = DHp, gate.M = d.M;
+      gate.Wf = Bp(Ly.Wf_ru[l]), gate.nkb_total = nkb_total(d, l);
+      fill_kb(gate, DHp != nullptr);
+      gate.bias = params + P.bru[l];
+      if (l == 0)
+        gate.Dx = Dx + t * RF, gate.dx_mstride = int64_t(T) * RF, gate.F = d.F, gate.C_in = C,
+        gate.Wx = params + P.Wru[l];
+      gate.Hprev = Hp32;
+      gate.out_r = r, gate.out_u = u, gate.out_rH = DrHt;
+      CU(launch_tc_fwd(gate, s));
+      CU(diffuse_fwd_bf16(g, d, DrHt, RH, int64_t(d.B) * d.H, s));
+
+      TcFwd cand{};
+      cand.R = int(R), cand.H = d.H, cand.Nout = d.H, cand.mode = kEpiCand;
+      cand.A_in = Ain, cand.A_h = DrHt, cand.M = d.M;
+      cand.Wf = Bp(Ly.Wf_c[l]), cand.nkb_total = nkb_total(d, l);
+      fill_kb(cand, t > 0);
+      cand.bias = params + P.bc[l];
+      if (l == 0)
+        cand.Dx = Dx + t * RF, cand.dx_mstride = int64_t(T) * RF, cand.F = d.F, cand.C_in = C,
+        cand.Wx = params + P.Wc[l];
+      cand.Hprev = Hp32, cand.u_in = u, cand.out_c = c;
+      cand.out_H = Fp(Ly.H32[l]) + t * RH, cand.out_Hb = DHt;
+      if (l == L - 1 && t >= T - d.T_out) {
+        cand.Wout = params + P.Wout, cand.bout = params + P.bout, cand.F_out = d.F_out;
+        cand.yhat = Fp(Ly.yhat) + int64_t(t - (T - d.T_out)) * R * d.F_out;
+      }
+      CU(launch_tc_fwd(cand, s));
+      if (!(l == L - 1 && t == T - 1)) CU(diffuse_fwd_bf16(g, d, DHt, RH, int64_t(d.B) * d.H, s));
+    }
+  }
+  CU(launch_loss(Fp(Ly.yhat), y, d.T_out, d.N, d.B, d.F, d.F_out, d.ld, Fp(Ly.dyhat),
+                 reinterpret_cast<double *>(ws + Ly.lossp), loss_dev, err, s));
+
+  // ------------------------------------------------------------------ backward (BPTT)
+  std::vector<float *> dHcur(L), dHprev(L);
+  for (int l = 0; l < L; ++l) {
+    dHcur[l] = Fp(Ly.dHa[l]), dHprev[l] = Fp(Ly.dHb[l]);
+    CU(cudaMemsetAsync(dHcur[l], 0, size_t(RH) * 4, s));
+  }
+  float *dU = Fp(Ly.dU), *drH = Fp(Ly.drH), *dTin = Fp(Ly.dTin), *dTH = Fp(Ly.dTH);
+  float *tmp[8];
+  for (int i = 0; i < 8; ++i) tmp[i] = Fp(Ly.tmp[i]);
+  for (int t = T - 1; t >= 0; --t) {
+    for (int l = L - 1; l >= 0; --l) {
+      const int Fin = l == 0 ? d.F : d.H;
+      const bool need_in = l > 0, need_h = t > 0;
+      const float *Hprev = t > 0 ? Fp(Ly.H32[l]) + (t - 1) * RH : nullptr;
+      const float *r = Fp(Ly.Rg[l]) + t * RH, *u = Fp(Ly.Ug[l]) + t * RH, *c = Fp(Ly.Cg[l]) + t * RH;
+      float *dC = Fp(Ly.dC[l]) + t * RH, *dG = Fp(Ly.dG[l]) + t * 2 * RH;
+      bf16 *dCb = Bp(Ly.dCb[l]) + t * RH, *dGb = Bp(Ly.dGb[l]) + t * 2 * RH;
+      const float *dy = (l == L - 1 && t >= T - d.T_out)
+                            ? Fp(Ly.dyhat) + int64_t(t - (T - d.T_out)) * R * d.F_out
+                            : nullptr;
+      CU(launch_cand_bwd(RH, d.H, dHcur[l], dy, params + P.Wout, d.F_out, u, c, Hprev, dU, dC,
+                         need_h ? dHprev[l] : nullptr, s, dCb));
+      const int64_t tin_ms = R * Fin;
+      const int V = vrows(d, l), vseg = l == 0 ? 64 : 2 * d.H, coff = l == 0 ? d.F : 0;
+      if (need_in || need_h) {
+        TcDgrad dg{dCb, int(R), d.H, Bp(Ly.Wd_c[l]), V, vseg, coff, Fin, d.H,
+                   dTin, tin_ms, 0, dTH, RH};
+        CU(launch_tc_dgrad(dg, s));
+      }
+      if (need_h) {
+        AdjChain ch{dTH, RH, int64_t(d.B) * d.H, drH, 0, {tmp[0], tmp[1]}, {tmp[2], tmp[3]}};
+        CU(diffuse_adj(g, d, &ch, 1, s));
+      }
+      CU(launch_gate_bwd(RH, d.H, need_h ? drH : nullptr, Hprev, r, u, dU,
+                         need_h ? dHprev[l] : nullptr, dG, s, dGb));
+      if (need_in || need_h) {
+        TcDgrad dg{dGb, int(R), 2 * d.H, Bp(Ly.Wd_ru[l]), V, vseg, coff, Fin, d.H,
+                   dTin, tin_ms, 1, dTH, RH};
+        CU(launch_tc_dgrad(dg, s));
+        AdjChain ch[2];
+        int nch = 0;
+        if (need_h)
+          ch[nch++] = AdjChain{dTH, RH, int64_t(d.B) * d.H, dHprev[l], 1, {tmp[0], tmp[1]},
+                               {tmp[2], tmp[3]}};
+        if (need_in)
+          ch[nch++] = AdjChain{dTin, tin_ms, int64_t(d.B) * Fin, dHcur[l - 1], 1,
+                               {tmp[4], tmp[5]}, {tmp[6], tmp[7]}};
+        CU(diffuse_adj(g, d, ch, nch, s));
+      }
+      std::swap(dHcur[l], dHprev[l]);
+    }
+  }
+
+  // ------------------------------------------------------------------ weight gradients
+  for (int l = 0; l < L; ++l) {
+    const int Fin = l == 0 ? d.F : d.H, C = Fin + d.H;
+    const int V = vrows(d, l), vseg = l == 0 ? 64 : 2 * d.H, coff = l == 0 ? d.F : 0;
+    const bf16 *Ain = l == 0 ? nullptr : Bp(Ly.DHb[l - 1]);
+    TcWgrad tw{Ain, Bp(Ly.DHb[l]), -1, T, d.M, int(R), Bp(Ly.dGb[l]), 2 * d.H,
+               V, vseg, coff, C, Fp(Ly.wpart), int64_t(Ly.wpart_floats), grads + P.Wru[l]};
+    CU(launch_tc_wgrad(tw, s));
+    tw.A_h = Bp(Ly.DrHb[l]), tw.h_toff = 0, tw.G = Bp(Ly.dCb[l]), tw.Nout = d.H;
+    tw.out = grads + P.Wc[l];
+    CU(launch_tc_wgrad(tw, s));
+    // input rows of layer 0 (fp32 x part) and the bias rows: SIMT, compact rows
+    GconvWgrad w{};
+    w.in = Dx, w.in_tstride = RF, w.in_mstride = int64_t(T) * RF;
+    w.Fin = Fin, w.Hd = d.H, w.M = d.M, w.T = T, w.R = int(R);
+    w.partial = Fp(Ly.wpart), w.partial_cap = int64_t(Ly.wpart_floats);
+    w.compact = l == 0 ? d.F : 0;
+    w.G = Fp(Ly.dG[l]), w.g_tstride = 2 * RH, w.Nout = 2 * d.H, w.out = grads + P.Wru[l];
+    CU(launch_gconv_wgrad(w, s));
+    w.G = Fp(Ly.dC[l]), w.g_tstride = RH, w.Nout = d.H, w.out = grads + P.Wc[l];
+    CU(launch_gconv_wgrad(w, s));
+  }
+  ReadoutWgrad rw{};
+  rw.Hs = Fp(Ly.H32[L - 1]) + int64_t(T - d.T_out) * RH, rw.h_tstride = RH;
+  rw.dy = Fp(Ly.dyhat), rw.T = d.T_out, rw.R = int(R), rw.H = d.H, rw.F_out = d.F_out;
+  rw.partial = Fp(Ly.wpart), rw.out = grads + P.Wout;
+  CU(launch_readout_wgrad(rw, s));
+
+  if (act_dump) {
+    for (int t = 0; t < T; ++t)
+      for (int l = 0; l < L; ++l) {
+        float *dst = act_dump + (int64_t(t) * L + l) * 4 * RH;
+        const float *src[4] = {Fp(Ly.H32[l]) + t * RH, Fp(Ly.Rg[l]) + t * RH,
+                               Fp(Ly.Ug[l]) + t * RH, Fp(Ly.Cg[l]) + t * RH};
+        for (int q = 0; q < 4; ++q)
+          CU(cudaMemcpyAsync(dst + q * RH, src[q], size_t(RH) * 4, cudaMemcpyDeviceToDevice, s));
+      }
+    CU(cudaMemcpyAsync(act_dump + int64_t(T) * L * 4 * RH, Fp(Ly.yhat),
+                       size_t(d.T_out) * R * d.F_out * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  return PGTI_OK;
+}
+
+size_t workspace_for(const Dims &d) {
+  return d.precision == 1 ? make_layout_tc(d).total : make_layout(d).total;
+}
+
 }  // namespace
 }  // namespace pgti
 
@@ -367,7 +640,7 @@ extern "C" size_t pgti_dcrnn_num_params(const pgti_dcrnn_desc *desc) {
 extern "C" size_t pgti_dcrnn_workspace_bytes(const pgti_dcrnn_desc *desc) {
   Dims d;
   if (check_desc(desc, &d) != PGTI_OK) return 0;
-  return make_layout(d).total;
+  return workspace_for(d);
 }
 
 extern "C" pgti_status pgti_dcrnn_step(const pgti_dcrnn_desc *desc, const float *params,
@@ -381,9 +654,12 @@ extern "C" pgti_status pgti_dcrnn_step(const pgti_dcrnn_desc *desc, const float 
                "pgti_dcrnn_step: null pointer");
   PGTI_REQUIRE(aligned16(params) && aligned16(grads) && aligned16(workspace), PGTI_ERR_ALIGNMENT,
                "pgti_dcrnn_step: params / grads / workspace must be 16-byte aligned");
-  const size_t need = make_layout(d).total;
+  const size_t need = workspace_for(d);
   PGTI_REQUIRE(ws_bytes >= need, PGTI_ERR_WORKSPACE,
                "pgti_dcrnn_step: workspace %zu bytes < %zu needed", ws_bytes, need);
+  if (d.precision == 1)
+    return run_step_tc(*desc, d, params, grads, x, y, loss_dev, static_cast<char *>(workspace),
+                       act_dump, as_stream(stream));
   return run_step(*desc, d, params, grads, x, y, loss_dev, static_cast<char *>(workspace),
                   act_dump, as_stream(stream));
 }

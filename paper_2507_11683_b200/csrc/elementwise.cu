@@ -1,4 +1,6 @@
 // Small fused elementwise kernels of the step: x re-layout, MAE loss (K5), GRU backward.
+#include <cuda_bf16.h>
+
 #include "kernels.cuh"
 #include "profile.cuh"
 
@@ -72,11 +74,13 @@ __global__ void k_loss_final(const double *__restrict__ partials, int n, int64_t
 
 // Candidate / update backward:  H' = u H + (1-u) c,  c = tanh(pre)
 //   dH' = dHcur (+ dyhat W_out^T);  dU = dH' (H - c);  dCpre = dH' (1-u)(1-c^2);  dHprev = dH' u
+// (dCb: optional bf16 copy of dCpre -- the tensor-core dgrad / wgrad operand)
 __global__ void k_cand_bwd(int64_t RH, int H, const float *__restrict__ dHcur,
                            const float *__restrict__ dy, const float *__restrict__ Wout, int F_out,
                            const float *__restrict__ u, const float *__restrict__ c,
                            const float *__restrict__ Hprev, float *__restrict__ dU,
-                           float *__restrict__ dC, float *__restrict__ dHprev) {
+                           float *__restrict__ dC, float *__restrict__ dHprev,
+                           __nv_bfloat16 *__restrict__ dCb) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < RH;
        i += int64_t(gridDim.x) * blockDim.x) {
     float dh = dHcur[i];
@@ -87,17 +91,20 @@ __global__ void k_cand_bwd(int64_t RH, int H, const float *__restrict__ dHcur,
     }
     const float uu = u[i], cc = c[i], hp = Hprev ? Hprev[i] : 0.f;
     dU[i] = dh * (hp - cc);
-    dC[i] = dh * (1.0f - uu) * (1.0f - cc * cc);
+    const float dc = dh * (1.0f - uu) * (1.0f - cc * cc);
+    dC[i] = dc;
+    if (dCb) dCb[i] = __float2bfloat16_rn(dc);
     if (dHprev) dHprev[i] = dh * uu;
   }
 }
 
 // Gate backward: rH = r*H;  dr = d(rH) H;  dHprev += d(rH) r;
-//   dG[:, :H] = dr r (1-r),  dG[:, H:] = dU u (1-u)
+//   dG[:, :H] = dr r (1-r),  dG[:, H:] = dU u (1-u)      (dGb: optional bf16 copy)
 __global__ void k_gate_bwd(int64_t RH, int H, const float *__restrict__ drH,
                            const float *__restrict__ Hprev, const float *__restrict__ r,
                            const float *__restrict__ u, const float *__restrict__ dU,
-                           float *__restrict__ dHprev, float *__restrict__ dG) {
+                           float *__restrict__ dHprev, float *__restrict__ dG,
+                           __nv_bfloat16 *__restrict__ dGb) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < RH;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t row = i / H;
@@ -109,8 +116,47 @@ __global__ void k_gate_bwd(int64_t RH, int H, const float *__restrict__ drH,
       dr = Hprev ? d * Hprev[i] : 0.f;
       if (dHprev) dHprev[i] += d * rr;
     }
-    dG[row * 2 * H + j] = dr * rr * (1.0f - rr);
-    dG[row * 2 * H + H + j] = dU[i] * uu * (1.0f - uu);
+    const float g0 = dr * rr * (1.0f - rr), g1 = dU[i] * uu * (1.0f - uu);
+    dG[row * 2 * H + j] = g0;
+    dG[row * 2 * H + H + j] = g1;
+    if (dGb) {
+      dGb[row * 2 * H + j] = __float2bfloat16_rn(g0);
+      dGb[row * 2 * H + H + j] = __float2bfloat16_rn(g1);
+    }
+  }
+}
+
+struct WeightParams {
+  WeightJob job[8];
+  int njobs;
+};
+
+// Per job: Wf[kb][j][c] (kb over the k-blocks of the tensor-core forward GEMM) and
+// Wd[v][j] (rows of the tensor-core dgrad); grid-stride over Wf then Wd elements.
+__global__ void k_convert_weights(const __grid_constant__ WeightParams p) {
+  for (int q = 0; q < p.njobs; ++q) {
+    const WeightJob &w = p.job[q];
+    const int nkb = w.layer0 ? w.M : 2 * w.M;
+    const int64_t nf = int64_t(nkb) * w.Nout * 64;
+    __nv_bfloat16 *wf = static_cast<__nv_bfloat16 *>(w.Wf);
+    __nv_bfloat16 *wd = static_cast<__nv_bfloat16 *>(w.Wd);
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nf;
+         i += int64_t(gridDim.x) * blockDim.x) {
+      const int c = int(i % 64);
+      const int j = int((i / 64) % w.Nout);
+      const int kb = int(i / (64 * w.Nout));
+      const int row = w.layer0 ? kb * w.C_in + w.Fin + c : (kb / 2) * w.C_in + (kb % 2) * 64 + c;
+      wf[i] = __float2bfloat16_rn(w.W[int64_t(row) * w.Nout + j]);
+    }
+    const int vseg = w.layer0 ? 64 : w.C_in, coff = w.layer0 ? w.Fin : 0;
+    const int64_t nd = int64_t(w.M) * vseg * w.Nout;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nd;
+         i += int64_t(gridDim.x) * blockDim.x) {
+      const int j = int(i % w.Nout);
+      const int v = int(i / w.Nout);
+      const int row = (v / vseg) * w.C_in + coff + v % vseg;
+      wd[i] = __float2bfloat16_rn(w.W[int64_t(row) * w.Nout + j]);
+    }
   }
 }
 
@@ -138,19 +184,37 @@ cudaError_t launch_loss(const float *yhat, const float *y, int T_out, int N, int
 cudaError_t launch_cand_bwd(int64_t RH, int H, const float *dHcur, const float *dy,
                             const float *Wout, int F_out, const float *u, const float *c,
                             const float *Hprev, float *dU, float *dC, float *dHprev_out,
-                            cudaStream_t s) {
-  ProfScope prof(kProfElementwise, s, 4.0 * double(RH) * (3 + (Hprev ? 1 : 0) + 2 + (dHprev_out ? 1 : 0)), 0.0);
+                            cudaStream_t s, void *dC_bf16) {
+  ProfScope prof(kProfElementwise, s,
+                 double(RH) * (4.0 * (3 + (Hprev ? 1 : 0) + 2 + (dHprev_out ? 1 : 0)) +
+                               (dC_bf16 ? 2.0 : 0.0)), 0.0);
   k_cand_bwd<<<grid_for(RH), kT, 0, s>>>(RH, H, dHcur, dy, Wout, F_out, u, c, Hprev, dU, dC,
-                                         dHprev_out);
+                                         dHprev_out, static_cast<__nv_bfloat16 *>(dC_bf16));
   return cudaGetLastError();
 }
 
 cudaError_t launch_gate_bwd(int64_t RH, int H, const float *drH, const float *Hprev,
                             const float *r, const float *u, const float *dU, float *dHprev,
-                            float *dG, cudaStream_t s) {
+                            float *dG, cudaStream_t s, void *dG_bf16) {
   ProfScope prof(kProfElementwise, s,
-                 4.0 * double(RH) * (3 + (drH ? 1 : 0) + (Hprev ? 1 : 0) + (dHprev ? 2 : 0) + 2), 0.0);
-  k_gate_bwd<<<grid_for(RH), kT, 0, s>>>(RH, H, drH, Hprev, r, u, dU, dHprev, dG);
+                 double(RH) * (4.0 * (3 + (drH ? 1 : 0) + (Hprev ? 1 : 0) + (dHprev ? 2 : 0) + 2) +
+                               (dG_bf16 ? 4.0 : 0.0)), 0.0);
+  k_gate_bwd<<<grid_for(RH), kT, 0, s>>>(RH, H, drH, Hprev, r, u, dU, dHprev, dG,
+                                         static_cast<__nv_bfloat16 *>(dG_bf16));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_convert_weights(const WeightJob *jobs, int njobs, cudaStream_t s) {
+  if (njobs > 8) return cudaErrorInvalidValue;
+  WeightParams p{};
+  double n = 0;
+  for (int i = 0; i < njobs; ++i) {
+    p.job[i] = jobs[i];
+    n += double(jobs[i].M) * jobs[i].C_in * jobs[i].Nout;
+  }
+  p.njobs = njobs;
+  ProfScope prof(kProfElementwise, s, n * 8.0, 0.0);
+  k_convert_weights<<<148 * 2, kT, 0, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -188,6 +188,11 @@ __global__ void __launch_bounds__(NT) k_gconv_dgrad(const __grid_constant__ Gcon
 
 // ----------------------------------------------------------------------------- wgrad
 __device__ __forceinline__ float load_wa(const GconvWgrad &p, int t, int row, int vr, int C) {
+  if (p.compact >= 0) {  // input rows c < compact of each block, then the bias row
+    if (vr >= p.M * p.compact) return 1.0f;
+    const int m = vr / p.compact, c = vr - m * p.compact;
+    return __ldg(p.in + t * p.in_tstride + m * p.in_mstride + int64_t(row) * p.Fin + c);
+  }
   const int m = vr / C;
   if (m >= p.M) return 1.0f;  // bias row
   const int c = vr - m * C;
@@ -206,7 +211,7 @@ __global__ void __launch_bounds__(NT) k_gconv_wgrad(const __grid_constant__ Gcon
   __shared__ alignas(16) float As[BK][BM + 4];
   __shared__ alignas(16) float Bs[BK][BN];
   const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
-  const int C = p.Fin + p.Hd, Vr = p.M * C + 1;
+  const int C = p.Fin + p.Hd, Vr = p.compact >= 0 ? p.M * p.compact + 1 : p.M * C + 1;
   const int vr0 = blockIdx.x * BM;
   const int chunk = blockIdx.y;
   const int t = chunk / chunks_per_t;
@@ -266,6 +271,20 @@ __global__ void k_reduce_chunks(const float *__restrict__ partial, int nchunks, 
     float s = 0.f;
     for (int c = 0; c < nchunks; ++c) s += partial[int64_t(c) * n + i];
     out[i] = s;
+  }
+}
+
+// Same, for compact virtual rows vr -> (vr / Fs) * C_in + vr % Fs, last row -> M * C_in.
+__global__ void k_reduce_compact(const float *__restrict__ partial, int nchunks, int Vr, int Nout,
+                                 int Fs, int M, int C_in, float *__restrict__ out) {
+  const int64_t n = int64_t(Vr) * Nout;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    float s = 0.f;
+    for (int c = 0; c < nchunks; ++c) s += partial[int64_t(c) * n + i];
+    const int vr = int(i / Nout), j = int(i - int64_t(vr) * Nout);
+    const int row = vr >= M * Fs ? M * C_in : (vr / Fs) * C_in + vr % Fs;
+    out[int64_t(row) * Nout + j] = s;
   }
 }
 
@@ -335,7 +354,7 @@ size_t wgrad_partial_floats(int M, int C_in, int Nout, int T, int R) {
 }
 
 cudaError_t launch_gconv_wgrad(const GconvWgrad &p, cudaStream_t s) {
-  const int C = p.Fin + p.Hd, Vr = p.M * C + 1;
+  const int C = p.Fin + p.Hd, Vr = p.compact >= 0 ? p.M * p.compact + 1 : p.M * C + 1;
   const int cpt = int(ceil_div(p.R, WKC));
   const int nchunks = p.T * cpt;
   if (int64_t(nchunks) * Vr * p.Nout > p.partial_cap) return cudaErrorInvalidValue;
@@ -356,8 +375,12 @@ cudaError_t launch_gconv_wgrad(const GconvWgrad &p, cudaStream_t s) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   ProfScope prof(kProfReduce, s, 4.0 * double(n) * (nchunks + 1), double(n) * nchunks);
-  k_reduce_chunks<<<unsigned(std::min<int64_t>(ceil_div(n, 256), 1184)), 256, 0, s>>>(
-      p.partial, nchunks, n, p.out);
+  if (p.compact >= 0)
+    k_reduce_compact<<<unsigned(std::min<int64_t>(ceil_div(n, 256), 1184)), 256, 0, s>>>(
+        p.partial, nchunks, Vr, p.Nout, p.compact, p.M, C, p.out);
+  else
+    k_reduce_chunks<<<unsigned(std::min<int64_t>(ceil_div(n, 256), 1184)), 256, 0, s>>>(
+        p.partial, nchunks, n, p.out);
   return cudaGetLastError();
 }
 

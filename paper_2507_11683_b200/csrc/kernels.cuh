@@ -22,6 +22,7 @@ struct SpmmJob {
   int64_t W;
   int G;
   int64_t gstride;
+  int bf16;           // X, add, Y are __nv_bfloat16 (all jobs of a launch agree)
   // filled by launch_spmm
   int64_t warp_begin, chunks;
 };
@@ -93,6 +94,9 @@ struct GconvWgrad {
   float *partial;        // [nchunks][M*C_in+1][Nout]
   int64_t partial_cap;   // floats available
   float *out;            // [M*C_in+1][Nout]
+  // compact >= 0: compute only the input rows c < compact of every block plus the bias row
+  // (virtual rows m*compact + c, then bias), written to rows m*C_in + c and M*C_in of out.
+  int compact = -1;
 };
 cudaError_t launch_gconv_wgrad(const GconvWgrad &p, cudaStream_t s);
 size_t wgrad_partial_floats(int M, int C_in, int Nout, int T, int R);
@@ -119,9 +123,21 @@ constexpr int kLossBlocks = 296;
 cudaError_t launch_cand_bwd(int64_t RH, int H, const float *dHcur, const float *dy,
                             const float *Wout, int F_out, const float *u, const float *c,
                             const float *Hprev, float *dU, float *dC, float *dHprev_out,
-                            cudaStream_t s);
+                            cudaStream_t s, void *dC_bf16 = nullptr);
 cudaError_t launch_gate_bwd(int64_t RH, int H, const float *drH, const float *Hprev,
                             const float *r, const float *u, const float *dU, float *dHprev,
-                            float *dG, cudaStream_t s);
+                            float *dG, cudaStream_t s, void *dG_bf16 = nullptr);
+
+// bf16 weight tiles of the tensor-core path, rebuilt from the fp32 parameters every step:
+//   fwd  (K-major B):  Wf[kb][j][c]  = W[row_kb + c][j]           c < 64, j < Nout
+//   dgrad(K-major B):  Wd[v][j]      = W[(v/vseg)*C_in + coff + v%vseg][j]
+struct WeightJob {
+  const float *W;        // [M*C_in][Nout] fp32 (params)
+  int Nout, C_in, M, Fin;
+  int layer0;            // 1: blocks are the hidden part only (kb = m, rows m*C_in + Fin)
+  void *Wf;              // bf16
+  void *Wd;              // bf16
+};
+cudaError_t launch_convert_weights(const WeightJob *jobs, int njobs, cudaStream_t s);
 
 }  // namespace pgti

@@ -344,3 +344,45 @@ def test_trainer_cuda_graph_matches_eager(env):
         outs.append((tr.params.cpu().numpy(), losses))
     assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
     assert outs[0][1] == outs[1][1]
+
+
+# ------------------------------------------------------------------ bf16 tcgen05 path
+TOL_BF16 = 2e-2
+TC_CONFIGS = {
+    "tc_tiny": synth.Config("tc_tiny", N=12, E=60, F=2, T_in=3, T_out=2, L=2, H=64, K=2, B=3),
+    "tc_odd": SMALL_CONFIGS["odd"],
+    "tc_l1": synth.Config("tc_l1", N=40, E=60, F=1, T_in=4, T_out=1, L=1, H=64, K=2, B=5),
+}
+
+
+def _step_case_tc(env, cfg, B=None, seed=0):
+    pgti, torch = env
+    B = B or cfg.B
+    cfg = cfg.replace(B=B)
+    ref = ref_for(cfg)
+    s = load_series(pgti, torch, ref.v, 0, cfg, ref.mu, ref.sigma)
+    idx_np = ref.plan(1, 0, epoch=seed)[:B]
+    idx = torch.from_numpy(idx_np.astype(np.int32)).cuda()
+    ld = ld_of(cfg)
+    x = torch.empty(B * cfg.T_in * ld, device="cuda")
+    y = torch.empty(B * cfg.T_out * ld, device="cuda")
+    s.gather(idx, B, cfg.T_in, cfg.T_out, x, y)
+    model = model_for(pgti, torch, cfg, ref.graph, precision=1)
+    theta = synth.make_params(cfg, seed=synth.SEED_PARAMS + seed, kind="random")
+    loss, g, act = run_step(pgti, torch, model, theta, x, y)
+    xo, yo = ref.batch(idx_np)
+    loss_ref, g_ref, fwd = dcgru.backward(theta.astype(np.float64), ref.d, ref.Pf, ref.Pb,
+                                          xo.astype(np.float64), yo.astype(np.float64))
+    return dict(loss=loss, g=g, act=act, loss_ref=loss_ref, g_ref=g_ref, fwd=fwd, cfg=cfg,
+                ref=ref, margin=1.0, B=B)
+
+
+@pytest.mark.parametrize("name", list(TC_CONFIGS))
+def test_step_parity_bf16_small(env, name):
+    """precision = 1 (bf16 operands, fp32 TMEM accumulation): 2e-2 scale-relative (BJ)."""
+    _check_step(_step_case_tc(env, TC_CONFIGS[name]), tol=TOL_BF16)
+
+
+@pytest.mark.parametrize("name,B", [("metr_la", 64), ("pems_bay", 16)])
+def test_step_parity_bf16_traffic(env, name, B):
+    _check_step(_step_case_tc(env, synth.CONFIGS[name], B=B), tol=TOL_BF16)
