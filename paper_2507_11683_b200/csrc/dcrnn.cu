@@ -1,8 +1,10 @@
 // pgti_dcrnn_step: one forward + BPTT pass of the stepwise stacked DCGRU over one gathered
 // batch, plus the diffusion test hooks.  Orchestration only: every arithmetic step runs in the
-// kernels of spmm.cu (K2), gemm_simt.cu (K3'/K4/K5) and elementwise.cu.
+// kernels of spmm.cu (K2), gemm_simt.cu / tc_gemm.cu (K3/K3'/K4/K5), small_wgrad.cu and
+// elementwise.cu.
 //
-// Workspace (all device, caller-owned; R = N*B rows ordered n*B + b; M = 2K+1):
+// Workspace of the fp32 path (precision 0; all device, caller-owned; R = N*B rows ordered
+// n*B + b; M = 2K+1):
 //   Dx        [M][T_in][R*F]        diffusion blocks of every x_t (layer-0 input)
 //   DH[l]     [T_in][M][R*H]        diffusion blocks of H^l_t (block 0 = H^l_t itself)
 //   DrH[l]    [T_in][M][R*H]        diffusion blocks of r*H^l_{t-1}
@@ -73,10 +75,10 @@ pgti_status check_desc(const pgti_dcrnn_desc *desc, Dims *out) {
                "desc: ld=%lld must be >= N*F and a multiple of 4", (long long)g.ld);
   PGTI_REQUIRE(g.precision == 0 || g.precision == 1, PGTI_ERR_UNSUPPORTED,
                "desc: precision=%d (0 = fp32 SIMT, 1 = bf16 tcgen05)", g.precision);
-  PGTI_REQUIRE(g.precision == 0 || (g.H == 64 && g.F * (2 * g.K + 1) <= 20),
+  PGTI_REQUIRE(g.precision == 0 || (g.H == 64 && g.F * (2 * g.K + 1) <= 11 && 2 * g.K + 1 <= 8),
                PGTI_ERR_UNSUPPORTED,
-               "desc: the bf16 tcgen05 path needs H = 64 and F*(2K+1) <= 20 (H=%d F=%d K=%d)", g.H,
-               g.F, g.K);
+               "desc: the bf16 tcgen05 path needs H = 64, F*(2K+1) <= 11 and K <= 3 (H=%d F=%d K=%d)",
+               g.H, g.F, g.K);
   PGTI_REQUIRE(int64_t(g.N) * g.B * 2 * g.H < (int64_t(1) << 31), PGTI_ERR_SHAPE,
                "desc: N*B*2H exceeds int32 row indexing");
   if (g.K > 0)
@@ -120,7 +122,7 @@ Layout make_layout(const Dims &d) {
   L.dTH = take(M * R * H * 4);
   L.tmp_floats = R * std::max(H, fin_max);
   for (int i = 0; i < 8; ++i) L.tmp[i] = take(L.tmp_floats * 4);
-  size_t wp = readout_partial_floats(d.H, d.F_out, d.T_out, int(d.R));
+  size_t wp = small_wgrad_partial_floats(d.T_out, int(d.R), d.H);
   for (int l = 0; l < d.L; ++l) {
     const int C = (l == 0 ? d.F : d.H) + d.H;
     wp = std::max(wp, wgrad_partial_floats(d.M, C, 2 * d.H, d.T_in, int(d.R)));
@@ -131,18 +133,31 @@ Layout make_layout(const Dims &d) {
   return L;
 }
 
-// forward diffusion: blocks base + m*mstride (m = 0 given), G groups of stride gstride, width W
+// Forward diffusion: blocks base + m*mstride (m = 0 given), G groups of stride gstride, width W.
+// transposed = 1 diffuses with P_f^T / P_b^T instead (the backward "diffuse-then-GEMM" dgrad).
+// bf16 = 1: blocks are __nv_bfloat16 (base / src0 reinterpreted).
 cudaError_t diffuse_fwd(const pgti_dcrnn_desc &g, const Dims &d, float *base, int64_t mstride,
-                        int G, int64_t gstride, int64_t W, cudaStream_t s) {
+                        int G, int64_t gstride, int64_t W, cudaStream_t s, int bf16 = 0,
+                        int transposed = 0, const void *src0 = nullptr) {
+  const int es = bf16 ? 2 : 4;
+  char *b = reinterpret_cast<char *>(base);
+  const char *z = src0 ? static_cast<const char *>(src0) : b;
+  auto blk = [&](int m) { return b + int64_t(m) * mstride * es; };
   for (int k = 1; k <= d.K; ++k) {
     SpmmJob j[2] = {};
-    j[0].rowptr[0] = g.a_rowptr, j[0].col[0] = g.a_col, j[0].val[0] = g.Pf_val, j[0].nnz[0] = g.nnz;
-    j[0].X[0] = base + (k - 1) * mstride;
-    j[0].Y = base + k * mstride;
-    j[1].rowptr[0] = g.at_rowptr, j[1].col[0] = g.at_col, j[1].val[0] = g.Pb_val, j[1].nnz[0] = g.nnz;
-    j[1].X[0] = k == 1 ? base : base + (d.K + k - 1) * mstride;
-    j[1].Y = base + (d.K + k) * mstride;
-    for (auto &jb : j) jb.nterms = 1, jb.W = W, jb.G = G, jb.gstride = gstride;
+    if (!transposed) {
+      j[0].rowptr[0] = g.a_rowptr, j[0].col[0] = g.a_col, j[0].val[0] = g.Pf_val;
+      j[1].rowptr[0] = g.at_rowptr, j[1].col[0] = g.at_col, j[1].val[0] = g.Pb_val;
+    } else {
+      j[0].rowptr[0] = g.at_rowptr, j[0].col[0] = g.at_col, j[0].val[0] = g.PfT_val;
+      j[1].rowptr[0] = g.a_rowptr, j[1].col[0] = g.a_col, j[1].val[0] = g.PbT_val;
+    }
+    j[0].X[0] = reinterpret_cast<const float *>(k == 1 ? z : blk(k - 1));
+    j[0].Y = reinterpret_cast<float *>(blk(k));
+    j[1].X[0] = reinterpret_cast<const float *>(k == 1 ? z : blk(d.K + k - 1));
+    j[1].Y = reinterpret_cast<float *>(blk(d.K + k));
+    for (auto &jb : j)
+      jb.nterms = 1, jb.nnz[0] = g.nnz, jb.W = W, jb.G = G, jb.gstride = gstride, jb.bf16 = bf16;
     cudaError_t e = launch_spmm(j, 2, d.N, s);
     if (e != cudaSuccess) return e;
   }
@@ -173,18 +188,18 @@ cudaError_t diffuse_adj(const pgti_dcrnn_desc &g, const Dims &d, AdjChain *ch, i
     return launch_spmm(jobs, nch, d.N, s);
   }
   std::vector<const float *> af(nch), ab(nch);
-  for (int c = 0; c < nch; ++c) af[c] = ch[c].dT + K * ch[c].mstride, ab[c] = ch[c].dT + 2 * K * ch[c].mstride;
+  for (int c = 0; c < nch; ++c)
+    af[c] = ch[c].dT + K * ch[c].mstride, ab[c] = ch[c].dT + 2 * K * ch[c].mstride;
   int pp = 0;
   for (int k = K - 1; k >= 1; --k) {
     int nj = 0;
     for (int c = 0; c < nch; ++c) {
       SpmmJob f{}, b{};
       f.rowptr[0] = g.at_rowptr, f.col[0] = g.at_col, f.val[0] = g.PfT_val, f.X[0] = af[c];
-      f.nnz[0] = b.nnz[0] = g.nnz;
       f.add = ch[c].dT + k * ch[c].mstride, f.Y = ch[c].tf[pp];
       b.rowptr[0] = g.a_rowptr, b.col[0] = g.a_col, b.val[0] = g.PbT_val, b.X[0] = ab[c];
       b.add = ch[c].dT + (K + k) * ch[c].mstride, b.Y = ch[c].tb[pp];
-      for (SpmmJob *jb : {&f, &b}) jb->nterms = 1, jb->W = ch[c].W, jb->G = 1;
+      for (SpmmJob *jb : {&f, &b}) jb->nterms = 1, jb->nnz[0] = g.nnz, jb->W = ch[c].W, jb->G = 1;
       jobs[nj++] = f, jobs[nj++] = b;
       af[c] = ch[c].tf[pp], ab[c] = ch[c].tb[pp];
     }
@@ -212,6 +227,7 @@ cudaError_t diffuse_adj(const pgti_dcrnn_desc &g, const Dims &d, AdjChain *ch, i
                   __LINE__);                                                                  \
   } while (0)
 
+// =========================================================================== precision = 0
 pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *params, float *grads,
                      const float *x, const float *y, float *loss_dev, char *ws, float *act_dump,
                      cudaStream_t s) {
@@ -337,11 +353,12 @@ pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *param
     w.G = Fp(Ly.dC[l]), w.g_tstride = RH, w.Nout = d.H, w.out = grads + P.Wc[l];
     CU(launch_gconv_wgrad(w, s));
   }
-  ReadoutWgrad rw{};
-  rw.Hs = Fp(Ly.DH[L - 1]) + int64_t(T - d.T_out) * MRH, rw.h_tstride = MRH;
-  rw.dy = Fp(Ly.dyhat), rw.T = d.T_out, rw.R = int(R), rw.H = d.H, rw.F_out = d.F_out;
-  rw.partial = Fp(Ly.wpart), rw.out = grads + P.Wout;
-  CU(launch_readout_wgrad(rw, s));
+  SmallWgrad rw{};
+  rw.mode = kSmallReadout, rw.T = d.T_out, rw.R = int(R);
+  rw.dy = Fp(Ly.dyhat), rw.F_out = d.F_out;
+  rw.G = Fp(Ly.DH[L - 1]) + int64_t(T - d.T_out) * MRH, rw.g_tstride = MRH, rw.NG = d.H;
+  rw.partial = Fp(Ly.wpart), rw.partial_cap = int64_t(Ly.wpart_floats), rw.out = grads + P.Wout;
+  CU(launch_small_wgrad(rw, s));
 
   // ------------------------------------------------------------------ test-only dump
   if (act_dump) {
@@ -359,19 +376,20 @@ pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *param
   return PGTI_OK;
 }
 
-
 // =========================================================================== precision = 1
-// bf16 tcgen05 path.  Differences from the fp32 path: the diffusion blocks of H and r*H are
-// bf16 (they are the tensor-core A operands and the forward SpMM operands), an fp32 copy of H
-// carries the recurrence, dG / dCpre also get bf16 copies (dgrad A / wgrad B operands), and the
-// weights are re-tiled to bf16 every step.  Layer 0's F-channel input part stays fp32 (FFMA in
-// the GEMM epilogue, SIMT wgrad rows); the backward adjoint diffusion stays fp32.
+// bf16 tcgen05 path.  Differences from the fp32 path:
+//  * the diffusion blocks of H and r*H are bf16 (tensor-core A operands, forward SpMM
+//    operands); an fp32 copy of H carries the recurrence; weights are re-tiled to bf16 per step;
+//  * layer 0's F-channel input part stays fp32 (FFMA in the GEMM epilogue; skinny wgrad rows);
+//  * backward "diffuse-then-GEMM": dZ = sum_m (P^m)^T dG W_m^T = sum_m ((P^m)^T dG) W_m^T, so
+//    the gate gradient (2H wide, bf16) is diffused with the transposed operators and ONE
+//    multi-block tcgen05 GEMM accumulates dZ straight into the fp32 BPTT accumulators -- no
+//    M*C_in-wide dT intermediate and no Horner chains.
 struct LayoutTC {
-  size_t Dx, yhat, dyhat, lossp, dU, drH, dTin, dTH, wpart, total;
-  size_t tmp[8];
+  size_t Dx, yhat, dyhat, lossp, dU, drH, Q, wpart, total;
   std::vector<size_t> DHb, DrHb, H32, Rg, Ug, Cg, dG, dGb, dC, dCb, dHa, dHb, Wf_ru, Wf_c, Wd_ru,
       Wd_c;
-  size_t tmp_floats, wpart_floats;
+  size_t wpart_floats;
 };
 
 int nkb_total(const Dims &d, int l) { return l == 0 ? d.M : 2 * d.M; }
@@ -387,7 +405,7 @@ LayoutTC make_layout_tc(const Dims &d) {
   };
   const size_t R = size_t(d.R), H = size_t(d.H), M = size_t(d.M), T = size_t(d.T_in);
   L.Dx = take(M * T * R * d.F * 4);
-  size_t wp = readout_partial_floats(d.H, d.F_out, d.T_out, int(d.R));
+  size_t wp = small_wgrad_partial_floats(d.T_in, int(d.R), 2 * d.H);
   for (int l = 0; l < d.L; ++l) {
     L.DHb.push_back(take(T * M * R * H * 2));
     L.DrHb.push_back(take(T * M * R * H * 2));
@@ -401,45 +419,22 @@ LayoutTC make_layout_tc(const Dims &d) {
     L.dCb.push_back(take(T * R * H * 2));
     L.dHa.push_back(take(R * H * 4));
     L.dHb.push_back(take(R * H * 4));
-    const int C = (l == 0 ? d.F : d.H) + d.H;
     L.Wf_ru.push_back(take(size_t(nkb_total(d, l)) * 2 * H * 64 * 2));
     L.Wf_c.push_back(take(size_t(nkb_total(d, l)) * H * 64 * 2));
     L.Wd_ru.push_back(take(size_t(vrows(d, l)) * 2 * H * 2));
     L.Wd_c.push_back(take(size_t(vrows(d, l)) * H * 2));
     wp = std::max(wp, tc_wgrad_partial_floats(vrows(d, l), 2 * d.H, d.T_in, int(d.R)));
-    wp = std::max(wp, wgrad_partial_floats(d.M, C, 2 * d.H, d.T_in, int(d.R)));
   }
   L.yhat = take(size_t(d.T_out) * R * d.F_out * 4);
   L.dyhat = take(size_t(d.T_out) * R * d.F_out * 4);
   L.lossp = take(size_t(kLossBlocks) * 8);
   L.dU = take(R * H * 4);
   L.drH = take(R * H * 4);
-  const size_t fin_max = d.L > 1 ? H : size_t(d.F);
-  L.dTin = take(M * R * fin_max * 4);
-  L.dTH = take(M * R * H * 4);
-  L.tmp_floats = R * std::max(H, fin_max);
-  for (int i = 0; i < 8; ++i) L.tmp[i] = take(L.tmp_floats * 4);
+  L.Q = take(M * R * 2 * H * 2);
   L.wpart_floats = wp;
   L.wpart = take(wp * 4);
   L.total = off;
   return L;
-}
-
-cudaError_t diffuse_fwd_bf16(const pgti_dcrnn_desc &g, const Dims &d, __nv_bfloat16 *base,
-                             int64_t mstride, int64_t W, cudaStream_t s) {
-  for (int k = 1; k <= d.K; ++k) {
-    SpmmJob j[2] = {};
-    j[0].rowptr[0] = g.a_rowptr, j[0].col[0] = g.a_col, j[0].val[0] = g.Pf_val, j[0].nnz[0] = g.nnz;
-    j[0].X[0] = reinterpret_cast<const float *>(base + (k - 1) * mstride);
-    j[0].Y = reinterpret_cast<float *>(base + k * mstride);
-    j[1].rowptr[0] = g.at_rowptr, j[1].col[0] = g.at_col, j[1].val[0] = g.Pb_val, j[1].nnz[0] = g.nnz;
-    j[1].X[0] = reinterpret_cast<const float *>(k == 1 ? base : base + (d.K + k - 1) * mstride);
-    j[1].Y = reinterpret_cast<float *>(base + (d.K + k) * mstride);
-    for (auto &jb : j) jb.nterms = 1, jb.W = W, jb.G = 1, jb.gstride = 0, jb.bf16 = 1;
-    cudaError_t e = launch_spmm(j, 2, d.N, s);
-    if (e != cudaSuccess) return e;
-  }
-  return cudaSuccess;
 }
 
 pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *params,
@@ -482,37 +477,43 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
       bf16 *DHt = Bp(Ly.DHb[l]) + t * MRH, *DrHt = Bp(Ly.DrHb[l]) + t * MRH;
       const float *Hp32 = t > 0 ? Fp(Ly.H32[l]) + (t - 1) * RH : nullptr;
       float *r = Fp(Ly.Rg[l]) + t * RH, *u = Fp(Ly.Ug[l]) + t * RH, *c = Fp(Ly.Cg[l]) + t * RH;
-      auto fill_kb = [&](TcFwd &f, bool has_h) {
+      // k-blocks: (input block m: map A0) and (hidden block m: map A1), B = Wf[kb] tiles
+      auto fill_kb = [&](TcFwd &f, const bf16 *Ah, int Nout) {
+        f.A0 = Ain, f.A1 = Ah, f.CA = 64, f.M0 = d.M, f.M1 = d.M;
+        f.bX = 64, f.bY = Nout, f.bZ = nkb_total(d, l);
         f.nkb = 0;
         for (int m = 0; m < d.M; ++m) {
-          if (l > 0) f.kb_src[f.nkb] = 0, f.kb_m[f.nkb] = m, f.kb_w[f.nkb] = 2 * m, ++f.nkb;
-          if (has_h)
-            f.kb_src[f.nkb] = 1, f.kb_m[f.nkb] = m, f.kb_w[f.nkb] = l > 0 ? 2 * m + 1 : m, ++f.nkb;
+          if (l > 0) {
+            f.kb_as[f.nkb] = 0, f.kb_am[f.nkb] = m, f.kb_ac[f.nkb] = 0;
+            f.kb_bx[f.nkb] = 0, f.kb_by[f.nkb] = 0, f.kb_bz[f.nkb] = 2 * m, ++f.nkb;
+          }
+          if (Ah) {
+            f.kb_as[f.nkb] = 1, f.kb_am[f.nkb] = m, f.kb_ac[f.nkb] = 0;
+            f.kb_bx[f.nkb] = 0, f.kb_by[f.nkb] = 0, f.kb_bz[f.nkb] = l > 0 ? 2 * m + 1 : m, ++f.nkb;
+          }
         }
       };
       TcFwd gate{};
-      gate.R = int(R), gate.H = d.H, gate.Nout = 2 * d.H, gate.mode = kEpiGate;
-      gate.A_in = Ain, gate.A_h = DHp, gate.M = d.M;
-      gate.Wf = Bp(Ly.Wf_ru[l]), gate.nkb_total = nkb_total(d, l);
-      fill_kb(gate, DHp != nullptr);
+      gate.R = int(R), gate.H = d.H, gate.Nout = 2 * d.H, gate.mode = kEpiGate, gate.ntiles = 2;
+      fill_kb(gate, DHp, 2 * d.H);
+      gate.Bw = Bp(Ly.Wf_ru[l]);
       gate.bias = params + P.bru[l];
       if (l == 0)
         gate.Dx = Dx + t * RF, gate.dx_mstride = int64_t(T) * RF, gate.F = d.F, gate.C_in = C,
-        gate.Wx = params + P.Wru[l];
+        gate.M = d.M, gate.Wx = params + P.Wru[l];
       gate.Hprev = Hp32;
       gate.out_r = r, gate.out_u = u, gate.out_rH = DrHt;
       CU(launch_tc_fwd(gate, s));
-      CU(diffuse_fwd_bf16(g, d, DrHt, RH, int64_t(d.B) * d.H, s));
+      CU(diffuse_fwd(g, d, reinterpret_cast<float *>(DrHt), RH, 1, 0, int64_t(d.B) * d.H, s, 1));
 
       TcFwd cand{};
-      cand.R = int(R), cand.H = d.H, cand.Nout = d.H, cand.mode = kEpiCand;
-      cand.A_in = Ain, cand.A_h = DrHt, cand.M = d.M;
-      cand.Wf = Bp(Ly.Wf_c[l]), cand.nkb_total = nkb_total(d, l);
-      fill_kb(cand, t > 0);
+      cand.R = int(R), cand.H = d.H, cand.Nout = d.H, cand.mode = kEpiCand, cand.ntiles = 1;
+      fill_kb(cand, t > 0 ? DrHt : nullptr, d.H);
+      cand.Bw = Bp(Ly.Wf_c[l]);
       cand.bias = params + P.bc[l];
       if (l == 0)
         cand.Dx = Dx + t * RF, cand.dx_mstride = int64_t(T) * RF, cand.F = d.F, cand.C_in = C,
-        cand.Wx = params + P.Wc[l];
+        cand.M = d.M, cand.Wx = params + P.Wc[l];
       cand.Hprev = Hp32, cand.u_in = u, cand.out_c = c;
       cand.out_H = Fp(Ly.H32[l]) + t * RH, cand.out_Hb = DHt;
       if (l == L - 1 && t >= T - d.T_out) {
@@ -520,7 +521,8 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
         cand.yhat = Fp(Ly.yhat) + int64_t(t - (T - d.T_out)) * R * d.F_out;
       }
       CU(launch_tc_fwd(cand, s));
-      if (!(l == L - 1 && t == T - 1)) CU(diffuse_fwd_bf16(g, d, DHt, RH, int64_t(d.B) * d.H, s));
+      if (!(l == L - 1 && t == T - 1))
+        CU(diffuse_fwd(g, d, reinterpret_cast<float *>(DHt), RH, 1, 0, int64_t(d.B) * d.H, s, 1));
     }
   }
   CU(launch_loss(Fp(Ly.yhat), y, d.T_out, d.N, d.B, d.F, d.F_out, d.ld, Fp(Ly.dyhat),
@@ -532,12 +534,35 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
     dHcur[l] = Fp(Ly.dHa[l]), dHprev[l] = Fp(Ly.dHb[l]);
     CU(cudaMemsetAsync(dHcur[l], 0, size_t(RH) * 4, s));
   }
-  float *dU = Fp(Ly.dU), *drH = Fp(Ly.drH), *dTin = Fp(Ly.dTin), *dTH = Fp(Ly.dTH);
-  float *tmp[8];
-  for (int i = 0; i < 8; ++i) tmp[i] = Fp(Ly.tmp[i]);
+  float *dU = Fp(Ly.dU), *drH = Fp(Ly.drH);
+  bf16 *Q = Bp(Ly.Q);
+  // dZ = sum_m Q_m W_m^T, Q_0 = gradient itself (map A0), Q_{m>0} = (P^m)^T grad (map A1)
+  auto bwd_gemm = [&](int l, const bf16 *grad, int NG, const bf16 *Wd, bool need_in,
+                      bool need_h, float *dst_in, float *dst_h, int acc_h) -> pgti_status {
+    const int vseg = l == 0 ? 64 : 2 * d.H;
+    TcFwd b{};
+    b.R = int(R), b.H = d.H, b.Nout = NG, b.mode = kEpiBwd;
+    b.A0 = grad, b.A1 = Q, b.CA = NG, b.M0 = 1, b.M1 = d.M;
+    b.Bw = Wd, b.bX = NG, b.bY = vrows(d, l), b.bZ = 1;
+    b.nkb = 0;
+    for (int m = 0; m < d.M; ++m)
+      for (int jb = 0; jb < NG / 64; ++jb) {
+        b.kb_as[b.nkb] = m > 0, b.kb_am[b.nkb] = m, b.kb_ac[b.nkb] = jb * 64;
+        b.kb_bx[b.nkb] = jb * 64, b.kb_by[b.nkb] = m * vseg, b.kb_bz[b.nkb] = 0, ++b.nkb;
+      }
+    // column tiles: l > 0 -> [input (64), hidden (64)]; l = 0 -> [hidden]
+    int nt = 0;
+    if (need_in) b.dst[nt] = dst_in, b.dst_acc[nt] = 1, ++nt;
+    if (need_h) b.dst[nt] = dst_h, b.dst_acc[nt] = acc_h, ++nt;
+    if (nt == 0) return PGTI_OK;
+    if (l > 0 && !need_in)  // skip the input tile: shift B rows by one 64-column tile
+      for (int k = 0; k < b.nkb; ++k) b.kb_by[k] += 64;
+    b.ntiles = nt;
+    CU(launch_tc_fwd(b, s));
+    return PGTI_OK;
+  };
   for (int t = T - 1; t >= 0; --t) {
     for (int l = L - 1; l >= 0; --l) {
-      const int Fin = l == 0 ? d.F : d.H;
       const bool need_in = l > 0, need_h = t > 0;
       const float *Hprev = t > 0 ? Fp(Ly.H32[l]) + (t - 1) * RH : nullptr;
       const float *r = Fp(Ly.Rg[l]) + t * RH, *u = Fp(Ly.Ug[l]) + t * RH, *c = Fp(Ly.Cg[l]) + t * RH;
@@ -546,34 +571,21 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
       const float *dy = (l == L - 1 && t >= T - d.T_out)
                             ? Fp(Ly.dyhat) + int64_t(t - (T - d.T_out)) * R * d.F_out
                             : nullptr;
+      float *dIn = need_in ? dHcur[l - 1] : nullptr;
       CU(launch_cand_bwd(RH, d.H, dHcur[l], dy, params + P.Wout, d.F_out, u, c, Hprev, dU, dC,
                          need_h ? dHprev[l] : nullptr, s, dCb));
-      const int64_t tin_ms = R * Fin;
-      const int V = vrows(d, l), vseg = l == 0 ? 64 : 2 * d.H, coff = l == 0 ? d.F : 0;
       if (need_in || need_h) {
-        TcDgrad dg{dCb, int(R), d.H, Bp(Ly.Wd_c[l]), V, vseg, coff, Fin, d.H,
-                   dTin, tin_ms, 0, dTH, RH};
-        CU(launch_tc_dgrad(dg, s));
-      }
-      if (need_h) {
-        AdjChain ch{dTH, RH, int64_t(d.B) * d.H, drH, 0, {tmp[0], tmp[1]}, {tmp[2], tmp[3]}};
-        CU(diffuse_adj(g, d, &ch, 1, s));
+        CU(diffuse_fwd(g, d, reinterpret_cast<float *>(Q), RH, 1, 0, int64_t(d.B) * d.H, s, 1, 1,
+                       dCb));
+        PGTI_STATUS_TRY(bwd_gemm(l, dCb, d.H, Bp(Ly.Wd_c[l]), need_in, need_h, dIn, drH, 0));
       }
       CU(launch_gate_bwd(RH, d.H, need_h ? drH : nullptr, Hprev, r, u, dU,
                          need_h ? dHprev[l] : nullptr, dG, s, dGb));
       if (need_in || need_h) {
-        TcDgrad dg{dGb, int(R), 2 * d.H, Bp(Ly.Wd_ru[l]), V, vseg, coff, Fin, d.H,
-                   dTin, tin_ms, 1, dTH, RH};
-        CU(launch_tc_dgrad(dg, s));
-        AdjChain ch[2];
-        int nch = 0;
-        if (need_h)
-          ch[nch++] = AdjChain{dTH, RH, int64_t(d.B) * d.H, dHprev[l], 1, {tmp[0], tmp[1]},
-                               {tmp[2], tmp[3]}};
-        if (need_in)
-          ch[nch++] = AdjChain{dTin, tin_ms, int64_t(d.B) * Fin, dHcur[l - 1], 1,
-                               {tmp[4], tmp[5]}, {tmp[6], tmp[7]}};
-        CU(diffuse_adj(g, d, ch, nch, s));
+        CU(diffuse_fwd(g, d, reinterpret_cast<float *>(Q), 2 * RH, 1, 0, int64_t(d.B) * 2 * d.H, s,
+                       1, 1, dGb));
+        PGTI_STATUS_TRY(bwd_gemm(l, dGb, 2 * d.H, Bp(Ly.Wd_ru[l]), need_in, need_h, dIn,
+                                 need_h ? dHprev[l] : nullptr, 1));
       }
       std::swap(dHcur[l], dHprev[l]);
     }
@@ -590,22 +602,23 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
     tw.A_h = Bp(Ly.DrHb[l]), tw.h_toff = 0, tw.G = Bp(Ly.dCb[l]), tw.Nout = d.H;
     tw.out = grads + P.Wc[l];
     CU(launch_tc_wgrad(tw, s));
-    // input rows of layer 0 (fp32 x part) and the bias rows: SIMT, compact rows
-    GconvWgrad w{};
-    w.in = Dx, w.in_tstride = RF, w.in_mstride = int64_t(T) * RF;
-    w.Fin = Fin, w.Hd = d.H, w.M = d.M, w.T = T, w.R = int(R);
-    w.partial = Fp(Ly.wpart), w.partial_cap = int64_t(Ly.wpart_floats);
-    w.compact = l == 0 ? d.F : 0;
-    w.G = Fp(Ly.dG[l]), w.g_tstride = 2 * RH, w.Nout = 2 * d.H, w.out = grads + P.Wru[l];
-    CU(launch_gconv_wgrad(w, s));
-    w.G = Fp(Ly.dC[l]), w.g_tstride = RH, w.Nout = d.H, w.out = grads + P.Wc[l];
-    CU(launch_gconv_wgrad(w, s));
+    // input rows of layer 0 (fp32 x part) and the bias rows: skinny reduction over T*R rows
+    SmallWgrad sw{};
+    sw.mode = kSmallBiasX, sw.T = T, sw.R = int(R);
+    if (l == 0) sw.Dx = Dx, sw.dx_mstride = int64_t(T) * RF, sw.dx_tstride = RF;
+    sw.M = d.M, sw.F = d.F, sw.C_in = C;
+    sw.partial = Fp(Ly.wpart), sw.partial_cap = int64_t(Ly.wpart_floats);
+    sw.G = Fp(Ly.dG[l]), sw.g_tstride = 2 * RH, sw.NG = 2 * d.H, sw.out = grads + P.Wru[l];
+    CU(launch_small_wgrad(sw, s));
+    sw.G = Fp(Ly.dC[l]), sw.g_tstride = RH, sw.NG = d.H, sw.out = grads + P.Wc[l];
+    CU(launch_small_wgrad(sw, s));
   }
-  ReadoutWgrad rw{};
-  rw.Hs = Fp(Ly.H32[L - 1]) + int64_t(T - d.T_out) * RH, rw.h_tstride = RH;
-  rw.dy = Fp(Ly.dyhat), rw.T = d.T_out, rw.R = int(R), rw.H = d.H, rw.F_out = d.F_out;
-  rw.partial = Fp(Ly.wpart), rw.out = grads + P.Wout;
-  CU(launch_readout_wgrad(rw, s));
+  SmallWgrad rw{};
+  rw.mode = kSmallReadout, rw.T = d.T_out, rw.R = int(R);
+  rw.dy = Fp(Ly.dyhat), rw.F_out = d.F_out;
+  rw.G = Fp(Ly.H32[L - 1]) + int64_t(T - d.T_out) * RH, rw.g_tstride = RH, rw.NG = d.H;
+  rw.partial = Fp(Ly.wpart), rw.partial_cap = int64_t(Ly.wpart_floats), rw.out = grads + P.Wout;
+  CU(launch_small_wgrad(rw, s));
 
   if (act_dump) {
     for (int t = 0; t < T; ++t)

@@ -41,7 +41,7 @@ struct GconvA {
   int Fin, Hd, M;
 };
 
-enum EpiMode { kEpiGate = 0, kEpiCand = 1 };
+enum EpiMode { kEpiGate = 0, kEpiCand = 1, kEpiBwd = 2 };
 
 struct GconvFwd {
   GconvA a;
@@ -112,6 +112,32 @@ struct ReadoutWgrad {
 };
 cudaError_t launch_readout_wgrad(const ReadoutWgrad &p, cudaStream_t s);
 size_t readout_partial_floats(int H, int F_out, int T, int R);
+
+// Skinny weight gradients: out[s][j] = sum_t sum_r S_t[r][s] * G_t[r][j] for a handful of
+// "small" rows s (ns <= 12) against a wide operand G (NG <= 128 columns), split over row chunks
+// with a fixed-order reduction.
+//   mode kSmallBiasX : S = [x part of layer 0 (M*F values from Dx), 1]; G = dG or dCpre;
+//                      row s < M*F -> out row (s/F)*C_in + s%F, s = last -> bias row M*C_in.
+//   mode kSmallReadout: S = dyhat [T][R][F_out]; G = H^L_t (+ a ones column for b_out);
+//                      W_out[j][o] = sum, b_out[o] = sum over the ones column.
+enum SmallMode { kSmallBiasX = 0, kSmallReadout = 1 };
+struct SmallWgrad {
+  int mode;
+  int T, R;
+  const float *Dx;        // kSmallBiasX: + m*dx_mstride + t*dx_tstride + r*F + f (nullable)
+  int64_t dx_mstride, dx_tstride;
+  int M, F, C_in;
+  const float *dy;        // kSmallReadout: [T][R][F_out]
+  int F_out;
+  const float *G;         // + t*g_tstride, [R][NG]
+  int64_t g_tstride;
+  int NG;
+  float *partial;
+  int64_t partial_cap;
+  float *out;             // kSmallBiasX: layer's [M*C_in+1][NG] grads block; readout: W_out
+};
+cudaError_t launch_small_wgrad(const SmallWgrad &p, cudaStream_t s);
+size_t small_wgrad_partial_floats(int T, int R, int NG);
 
 // ------------------------------------------------------------------ elementwise
 cudaError_t launch_x_prep(const float *x, int B, int T_in, int64_t ld, int N, int F, float *X0,

@@ -1,8 +1,10 @@
 // K3: tcgen05 gate GEMMs (bf16 operands staged by TMA into SWIZZLE_128B shared memory, fp32
 // accumulators in TMEM, one elected thread issuing tcgen05.mma) with the GRU math fused into
-// the TMEM -> register epilogue.  Warp roles per CTA (192 threads):
-//   warp 0: TMA producer (one lane)      warp 1: TMEM alloc + MMA issuer (one lane)
-//   warps 2-5: epilogue, thread i of the 128 owns accumulator row i (TMEM lane i)
+// the TMEM -> register epilogue.
+//   k_tc_fwd   : multi-block GEMM (forward gates, and the backward "diffuse-then-GEMM" dgrad)
+//                10 warps: warp 0 TMA producer, warp 1 TMEM alloc + MMA issuer, warps 2-9
+//                epilogue (thread = one accumulator row x 32 of the tile's 64 columns)
+//   k_tc_wgrad : split-K weight gradient, MN-major A (diffusion blocks) and B (gate gradients)
 // 4-stage mbarrier ring between TMA and MMA (full / empty), one commit barrier MMA -> epilogue.
 // Equations: Li et al. Eq. 2-3 [ext], PAPER.md P:168, P:222 (readings c1-c7).
 #include <cudaTypedefs.h>
@@ -21,7 +23,7 @@ namespace {
 using namespace tc;
 using bf16 = __nv_bfloat16;
 
-constexpr int kBM = 128, kBK = 64, kStages = 4, kThreads = 192;
+constexpr int kBM = 128, kBK = 64, kStages = 4;
 
 struct Barriers {
   uint64_t full[kStages], empty[kStages], tfull;
@@ -59,12 +61,10 @@ __device__ __forceinline__ void teardown(Barriers *bar, uint32_t ncols) {
   }
 }
 
-// ================================================================== forward (gate / cand)
-// One CTA = 128 rows x one 64-column tile of the gate output (gate: tile 0 = r, tile 1 = u;
-// cand: tile 0 = c).  10 warps: TMA, MMA, and 8 epilogue warps -- thread (quarter q, half hh)
-// owns row q*32+lane and 32 of the 64 columns.  Everything the epilogue needs that does not
-// depend on the accumulator (bias, layer-0 x part by FFMA, H_{t-1}, u) is gathered while the
-// MMAs run; after the commit barrier only TMEM -> activation -> stores remain.
+// ================================================================== multi-block GEMM
+// One CTA = 128 rows x one 64-column tile.  Everything the epilogue needs that does not depend
+// on the accumulator (bias, layer-0 x part by FFMA, H_{t-1}, u, the bwd destination) is
+// gathered while the MMAs run; after the commit barrier only TMEM -> math -> stores remain.
 constexpr int kFwdThreads = 320, kEpiThreads = 256;
 
 __device__ __forceinline__ void epi_bar() {
@@ -72,7 +72,7 @@ __device__ __forceinline__ void epi_bar() {
 }
 
 __global__ void __launch_bounds__(kFwdThreads, 1)
-    k_tc_fwd(const __grid_constant__ CUtensorMap mA_in, const __grid_constant__ CUtensorMap mA_h,
+    k_tc_fwd(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
              const __grid_constant__ CUtensorMap mB, const __grid_constant__ TcFwd p) {
   constexpr int A_BYTES = kBM * kBK * 2, B_BYTES = 64 * kBK * 2, STAGE = A_BYTES + B_BYTES;
   extern __shared__ uint8_t smem_raw[];
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   float *y_s = wx_s + 20 * 64;                                                       // [128][4]
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int row0 = blockIdx.x * kBM, ct = blockIdx.y;
-  if (threadIdx.x == 0) tma_prefetch(&mA_in), tma_prefetch(&mA_h), tma_prefetch(&mB);
+  if (threadIdx.x == 0) tma_prefetch(&mA0), tma_prefetch(&mA1), tma_prefetch(&mB);
   setup(bar, 64);
   const uint32_t tmem = bar->tmem;
 
@@ -93,8 +93,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         mbar_wait(&bar->empty[s], ((kb / kStages) & 1) ^ 1);
         mbar_expect_tx(&bar->full[s], STAGE);
         uint8_t *a = smem + s * STAGE;
-        tma_load_3d(a, p.kb_src[kb] ? &mA_h : &mA_in, &bar->full[s], 0, row0, p.kb_m[kb]);
-        tma_load_3d(a + A_BYTES, &mB, &bar->full[s], 0, ct * 64, p.kb_w[kb]);
+        tma_load_3d(a, p.kb_as[kb] ? &mA1 : &mA0, &bar->full[s], p.kb_ac[kb], row0, p.kb_am[kb]);
+        tma_load_3d(a + A_BYTES, &mB, &bar->full[s], p.kb_bx[kb], p.kb_by[kb] + ct * 64,
+                    p.kb_bz[kb]);
       }
     }
   } else if (warp == 1) {
@@ -118,187 +119,136 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int r = q * 32 + lane, row = row0 + r;
     const bool valid = row < p.R;
     const int H = p.H;
-    const int nx = p.Dx ? p.F * p.M : 0;
-    // stage this tile's x-part weight rows (fp32) in shared memory
-    for (int i = e * 32 + lane; i < nx * 64; i += kEpiThreads) {
-      const int mf = i / 64, j = i % 64, m = mf / p.F, f = mf % p.F;
-      wx_s[i] = __ldg(p.Wx + int64_t(m * p.C_in + f) * p.Nout + ct * 64 + j);
-    }
-    epi_bar();
-    const int jc = hh * 32;                 // first tile column of this thread
-    const int jg = ct * 64 + jc;            // first gate column
-    float pre[32];
+    const int jc = hh * 32;   // first tile column of this thread
+    if (p.mode == kEpiBwd) {
+      float *dst = p.dst[ct];
+      const int64_t ro = int64_t(row) * 64 + jc;
+      float old[32];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) pre[i] = __ldg(p.bias + jg + i);
-    if (nx && valid) {
-      for (int mf = 0; mf < nx; ++mf) {
-        const int m = mf / p.F, f = mf % p.F;
-        const float xv = __ldg(p.Dx + m * p.dx_mstride + int64_t(row) * p.F + f);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) pre[i] = fmaf(xv, wx_s[mf * 64 + jc + i], pre[i]);
+      for (int i = 0; i < 32; i += 4) {
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid && p.dst_acc[ct]) a = *reinterpret_cast<const float4 *>(dst + ro + i);
+        old[i] = a.x, old[i + 1] = a.y, old[i + 2] = a.z, old[i + 3] = a.w;
       }
-    }
-    const int jh = (p.mode == kEpiGate ? 0 : ct * 64) + jc;   // hidden-unit index of column 0
-    const int64_t ro = int64_t(row) * H + jh;
-    const bool need_h = p.mode == kEpiCand || ct == 0;
-    float hp[32], uu[32];
-#pragma unroll
-    for (int i = 0; i < 32; i += 4) {
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-      if (valid && need_h && p.Hprev) a = *reinterpret_cast<const float4 *>(p.Hprev + ro + i);
-      if (valid && p.mode == kEpiCand) b = *reinterpret_cast<const float4 *>(p.u_in + ro + i);
-      hp[i] = a.x, hp[i + 1] = a.y, hp[i + 2] = a.z, hp[i + 3] = a.w;
-      uu[i] = b.x, uu[i + 1] = b.y, uu[i + 2] = b.z, uu[i + 3] = b.w;
-    }
-    mbar_wait(&bar->tfull, 0);
-    tc_fence_after();
-    float acc[32];
-    if (p.nkb) {
+      mbar_wait(&bar->tfull, 0);
+      tc_fence_after();
+      float acc[32];
       const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + jc;
       tmem_ld16(taddr, acc);
       tmem_ld16(taddr + 16, acc + 16);
       tmem_wait_ld();
-    } else {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) acc[i] = 0.f;
-    }
-    __align__(16) bf16 hb[32];
-    if (p.mode == kEpiGate) {
-      float *out = ct == 0 ? p.out_r : p.out_u;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) acc[i] = sigmoid_f(acc[i] + pre[i]);
       if (valid) {
 #pragma unroll
         for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<float4 *>(out + ro + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
-        if (ct == 0) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) hb[i] = __float2bfloat16_rn(acc[i] * hp[i]);
-#pragma unroll
-          for (int i = 0; i < 32; i += 8)
-            *reinterpret_cast<uint4 *>(p.out_rH + ro + i) = *reinterpret_cast<const uint4 *>(hb + i);
-        }
+          *reinterpret_cast<float4 *>(dst + ro + i) =
+              make_float4(old[i] + acc[i], old[i + 1] + acc[i + 1], old[i + 2] + acc[i + 2],
+                          old[i + 3] + acc[i + 3]);
       }
     } else {
-      float ys[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float c = tanhf(acc[i] + pre[i]);
-        acc[i] = c;
-        pre[i] = uu[i] * hp[i] + (1.0f - uu[i]) * c;   // H_t
-        hb[i] = __float2bfloat16_rn(pre[i]);
+      const int nx = p.Dx ? p.F * p.M : 0;
+      // stage this tile's x-part weight rows (fp32) in shared memory
+      for (int i = e * 32 + lane; i < nx * 64; i += kEpiThreads) {
+        const int mf = i / 64, j = i % 64, m = mf / p.F, f = mf % p.F;
+        wx_s[i] = __ldg(p.Wx + int64_t(m * p.C_in + f) * p.Nout + ct * 64 + j);
       }
-      if (p.yhat)
-        for (int o = 0; o < p.F_out; ++o)
+      epi_bar();
+      const int jg = ct * 64 + jc;  // first gate column
+      float pre[32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) ys[o] = fmaf(pre[i], __ldg(p.Wout + (jh + i) * p.F_out + o), ys[o]);
-      if (valid) {
+      for (int i = 0; i < 32; ++i) pre[i] = __ldg(p.bias + jg + i);
+      if (nx && valid) {
+        for (int mf = 0; mf < nx; ++mf) {
+          const int m = mf / p.F, f = mf % p.F;
+          const float xv = __ldg(p.Dx + m * p.dx_mstride + int64_t(row) * p.F + f);
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          *reinterpret_cast<float4 *>(p.out_c + ro + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
-          *reinterpret_cast<float4 *>(p.out_H + ro + i) = make_float4(pre[i], pre[i + 1], pre[i + 2], pre[i + 3]);
+          for (int i = 0; i < 32; ++i) pre[i] = fmaf(xv, wx_s[mf * 64 + jc + i], pre[i]);
         }
-#pragma unroll
-        for (int i = 0; i < 32; i += 8)
-          *reinterpret_cast<uint4 *>(p.out_Hb + ro + i) = *reinterpret_cast<const uint4 *>(hb + i);
       }
-      if (p.yhat) {
-        if (hh == 1)
-          for (int o = 0; o < p.F_out; ++o) y_s[r * 4 + o] = ys[o];
-        epi_bar();
-        if (hh == 0 && valid)
+      const int jh = (p.mode == kEpiGate ? 0 : ct * 64) + jc;  // hidden index of column 0
+      const int64_t ro = int64_t(row) * H + jh;
+      const bool need_h = p.mode == kEpiCand || ct == 0;
+      float hp[32], uu[32];
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+        if (valid && need_h && p.Hprev) a = *reinterpret_cast<const float4 *>(p.Hprev + ro + i);
+        if (valid && p.mode == kEpiCand) b = *reinterpret_cast<const float4 *>(p.u_in + ro + i);
+        hp[i] = a.x, hp[i + 1] = a.y, hp[i + 2] = a.z, hp[i + 3] = a.w;
+        uu[i] = b.x, uu[i + 1] = b.y, uu[i + 2] = b.z, uu[i + 3] = b.w;
+      }
+      mbar_wait(&bar->tfull, 0);
+      tc_fence_after();
+      float acc[32];
+      if (p.nkb) {
+        const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + jc;
+        tmem_ld16(taddr, acc);
+        tmem_ld16(taddr + 16, acc + 16);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+      }
+      __align__(16) bf16 hb[32];
+      if (p.mode == kEpiGate) {
+        float *out = ct == 0 ? p.out_r : p.out_u;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] = sigmoid_f(acc[i] + pre[i]);
+        if (valid) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4 *>(out + ro + i) =
+                make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+          if (ct == 0) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) hb[i] = __float2bfloat16_rn(acc[i] * hp[i]);
+#pragma unroll
+            for (int i = 0; i < 32; i += 8)
+              *reinterpret_cast<uint4 *>(p.out_rH + ro + i) = *reinterpret_cast<const uint4 *>(hb + i);
+          }
+        }
+      } else {
+        float ys[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float c = tanhf(acc[i] + pre[i]);
+          acc[i] = c;
+          pre[i] = uu[i] * hp[i] + (1.0f - uu[i]) * c;  // H_t
+          hb[i] = __float2bfloat16_rn(pre[i]);
+        }
+        if (p.yhat)
           for (int o = 0; o < p.F_out; ++o)
-            p.yhat[int64_t(row) * p.F_out + o] = (ys[o] + y_s[r * 4 + o]) + __ldg(p.bout + o);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) ys[o] = fmaf(pre[i], __ldg(p.Wout + (jh + i) * p.F_out + o), ys[o]);
+        if (valid) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            *reinterpret_cast<float4 *>(p.out_c + ro + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+            *reinterpret_cast<float4 *>(p.out_H + ro + i) = make_float4(pre[i], pre[i + 1], pre[i + 2], pre[i + 3]);
+          }
+#pragma unroll
+          for (int i = 0; i < 32; i += 8)
+            *reinterpret_cast<uint4 *>(p.out_Hb + ro + i) = *reinterpret_cast<const uint4 *>(hb + i);
+        }
+        if (p.yhat) {
+          if (hh == 1)
+            for (int o = 0; o < p.F_out; ++o) y_s[r * 4 + o] = ys[o];
+          epi_bar();
+          if (hh == 0 && valid)
+            for (int o = 0; o < p.F_out; ++o)
+              p.yhat[int64_t(row) * p.F_out + o] = (ys[o] + y_s[r * 4 + o]) + __ldg(p.bout + o);
+        }
       }
     }
   }
   teardown(bar, 64);
 }
 
-// ================================================================== dgrad
-// One CTA = 128 rows x 128 output columns v; 8 epilogue warps, thread (q, hh) owns 64 columns.
-// 16-column chunks never straddle an input/hidden boundary (segments are 64-aligned), so each
-// chunk is decoded once and stored as 4 float4.
-__global__ void __launch_bounds__(kFwdThreads, 1)
-    k_tc_dgrad(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
-               const __grid_constant__ TcDgrad p) {
-  constexpr int BN = 128;
-  constexpr int A_BYTES = kBM * kBK * 2, B_BYTES = BN * kBK * 2, STAGE = A_BYTES + B_BYTES;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = align1024(smem_raw);
-  Barriers *bar = carve<A_BYTES, B_BYTES>(smem);
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int row0 = blockIdx.x * kBM, v0 = blockIdx.y * BN;
-  const int nkb = p.Nout / kBK;
-  if (threadIdx.x == 0) tma_prefetch(&mA), tma_prefetch(&mB);
-  setup(bar, BN);
-  const uint32_t tmem = bar->tmem;
-  if (warp == 0) {
-    if (lane == 0)
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % kStages;
-        mbar_wait(&bar->empty[s], ((kb / kStages) & 1) ^ 1);
-        mbar_expect_tx(&bar->full[s], STAGE);
-        uint8_t *a = smem + s * STAGE;
-        tma_load_2d(a, &mA, &bar->full[s], kb * kBK, row0);
-        tma_load_2d(a + A_BYTES, &mB, &bar->full[s], kb * kBK, v0);
-      }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16(kBM, BN, false, false);
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % kStages;
-        mbar_wait(&bar->full[s], (kb / kStages) & 1);
-        tc_fence_after();
-        const uint32_t a = smem_u32(smem + s * STAGE), b = a + A_BYTES;
-#pragma unroll
-        for (int k = 0; k < kBK / 16; ++k)
-          mma_bf16(tmem, desc_sw128(a + 32 * k, 16, 1024), desc_sw128(b + 32 * k, 16, 1024), idesc,
-                   (kb | k) != 0);
-        mma_commit(&bar->empty[s]);
-      }
-      mma_commit(&bar->tfull);
-    }
-  } else {
-    const int e = warp - 2, q = warp & 3, hh = e >> 2;
-    const int row = row0 + q * 32 + lane;
-    const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + hh * 64;
-    mbar_wait(&bar->tfull, 0);
-    tc_fence_after();
-#pragma unroll 1
-    for (int c0 = 0; c0 < 64; c0 += 16) {
-      float d[16];
-      tmem_ld16(taddr + c0, d);
-      tmem_wait_ld();
-      const int v = v0 + hh * 64 + c0;
-      if (row >= p.R || v >= p.V) continue;
-      const int m = v / p.vseg, c = p.coff + (v - m * p.vseg);
-      if (c < p.Fin) {
-        float4 *dst = reinterpret_cast<float4 *>(p.Tin + m * p.tin_mstride + int64_t(row) * p.Fin + c);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          float4 o = make_float4(d[4 * i], d[4 * i + 1], d[4 * i + 2], d[4 * i + 3]);
-          if (p.acc_in) {
-            const float4 a = dst[i];
-            o.x += a.x, o.y += a.y, o.z += a.z, o.w += a.w;
-          }
-          dst[i] = o;
-        }
-      } else {
-        float4 *dst = reinterpret_cast<float4 *>(p.Th + m * p.th_mstride + int64_t(row) * p.Hd + (c - p.Fin));
-#pragma unroll
-        for (int i = 0; i < 4; ++i) dst[i] = make_float4(d[4 * i], d[4 * i + 1], d[4 * i + 2], d[4 * i + 3]);
-      }
-    }
-  }
-  teardown(bar, BN);
-}
-
 // ================================================================== wgrad (MN-major A and B)
+constexpr int kWgThreads = 192;
 constexpr int kWKC = 2048;  // rows per split-K chunk
 
 template <int NOUT>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kWgThreads, 1)
     k_tc_wgrad(const __grid_constant__ CUtensorMap mA_in, const __grid_constant__ CUtensorMap mA_h,
                const __grid_constant__ CUtensorMap mG, const __grid_constant__ TcWgrad p,
                int chunks_per_t) {
@@ -423,53 +373,39 @@ cudaError_t set_smem(K kernel, int bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
-constexpr int smem_bytes(int b_rows) { return kStages * (kBM * kBK * 2 + b_rows * kBK * 2) + 1024 + 256; }
+constexpr int wg_smem_bytes(int b_rows) { return kStages * (kBM * kBK * 2 + b_rows * kBK * 2) + 1024 + 256; }
+constexpr int fwd_smem_bytes() {
+  return kStages * (kBM * kBK * 2 + 64 * kBK * 2) + 1024 + 256 + (20 * 64 + 128 * 4) * 4;
+}
 
 }  // namespace
 
-constexpr int fwd_smem_bytes() { return kStages * (kBM * kBK * 2 + 64 * kBK * 2) + 1024 + 256 + (20 * 64 + 128 * 4) * 4; }
-
 cudaError_t launch_tc_fwd(const TcFwd &p, cudaStream_t s) {
-  if (p.H != 64 || (p.Nout != 128 && p.Nout != 64) || p.nkb > 16 || (p.Dx && p.F * p.M > 20) ||
-      p.F_out > 4)
+  if (p.H != 64 || p.nkb > kTcMaxKb || (p.Dx && p.F * p.M > 20) || p.F_out > 4 ||
+      p.ntiles < 1 || p.ntiles > 2 || (p.CA != 64 && p.CA != 128))
     return cudaErrorInvalidValue;
-  CUtensorMap ma_in, ma_h, mb;
-  const uint64_t R = uint64_t(p.R), M = uint64_t(p.M);
-  const uint64_t dA[3] = {64, R, M}, sA[2] = {128, R * 128};
+  CUtensorMap ma0, ma1, mb;
+  const uint64_t R = uint64_t(p.R), CA = uint64_t(p.CA);
+  const uint64_t dA0[3] = {CA, R, uint64_t(p.M0)}, dA1[3] = {CA, R, uint64_t(p.M1)};
+  const uint64_t sA[2] = {CA * 2, R * CA * 2};
   const uint32_t bA[3] = {64, 128, 1};
-  const uint64_t dB[3] = {64, uint64_t(p.Nout), uint64_t(p.nkb_total)},
-                 sB[2] = {128, uint64_t(p.Nout) * 128};
+  const uint64_t dB[3] = {uint64_t(p.bX), uint64_t(p.bY), uint64_t(p.bZ)},
+                 sB[2] = {uint64_t(p.bX) * 2, uint64_t(p.bX) * p.bY * 2};
   const uint32_t bB[3] = {64, 64, 1};
-  if (!make_map(&ma_in, p.A_in, 3, dA, sA, bA) || !make_map(&ma_h, p.A_h, 3, dA, sA, bA) ||
-      !make_map(&mb, p.Wf, 3, dB, sB, bB))
+  if (!make_map(&ma0, p.A0, 3, dA0, sA, bA) || !make_map(&ma1, p.A1, 3, dA1, sA, bA) ||
+      !make_map(&mb, p.Bw, 3, dB, sB, bB))
     return cudaErrorInvalidValue;
-  const dim3 grid(unsigned(ceil_div(p.R, kBM)), unsigned(p.Nout / 64));
+  const dim3 grid(unsigned(ceil_div(p.R, kBM)), unsigned(p.ntiles));
+  const double N = 64.0 * p.ntiles;
   const double Kt = double(p.nkb) * 64 + (p.Dx ? p.F * p.M : 0);
-  const double bytes = 2.0 * p.R * 64 * p.nkb + 2.0 * p.nkb * 64 * p.Nout +
-                       4.0 * p.R * p.H * (p.mode == kEpiGate ? 2 + (p.Hprev ? 1 : 0) + 0.5 : 4.5 + (p.Hprev ? 1 : 0));
-  ProfScope prof(kProfGemmFwd, s, bytes, 2.0 * p.R * Kt * p.Nout);
+  double io = p.mode == kEpiGate ? 2 + (p.Hprev ? 1 : 0) + 0.5
+            : p.mode == kEpiCand ? 4.5 + (p.Hprev ? 1 : 0)
+                                 : 1.0 + (p.dst_acc[0] ? 1.0 : 0.0);
+  const double bytes = 2.0 * p.R * 64 * p.nkb + 2.0 * p.nkb * 64 * N + 4.0 * p.R * N * io / 2 * 2;
+  ProfScope prof(p.mode == kEpiBwd ? kProfGemmDgrad : kProfGemmFwd, s, bytes, 2.0 * p.R * Kt * N);
   static cudaError_t once = set_smem(k_tc_fwd, fwd_smem_bytes());
   if (once != cudaSuccess) return once;
-  k_tc_fwd<<<grid, kFwdThreads, fwd_smem_bytes(), s>>>(ma_in, ma_h, mb, p);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_tc_dgrad(const TcDgrad &p, cudaStream_t s) {
-  if ((p.Nout != 128 && p.Nout != 64) || p.V <= 0 || p.V % 64 || p.vseg % 64)
-    return p.V == 0 ? cudaSuccess : cudaErrorInvalidValue;
-  CUtensorMap ma, mb;
-  const uint64_t dA[2] = {uint64_t(p.Nout), uint64_t(p.R)}, sA[1] = {uint64_t(p.Nout) * 2};
-  const uint32_t bA[2] = {64, 128};
-  const uint64_t dB[2] = {uint64_t(p.Nout), uint64_t(p.V)}, sB[1] = {uint64_t(p.Nout) * 2};
-  const uint32_t bB[2] = {64, 128};
-  if (!make_map(&ma, p.G, 2, dA, sA, bA) || !make_map(&mb, p.Wd, 2, dB, sB, bB))
-    return cudaErrorInvalidValue;
-  const dim3 grid(unsigned(ceil_div(p.R, kBM)), unsigned(ceil_div(p.V, 128)));
-  const double bytes = 2.0 * p.R * p.Nout + 2.0 * p.V * p.Nout + 4.0 * p.R * p.V;
-  ProfScope prof(kProfGemmDgrad, s, bytes, 2.0 * p.R * p.Nout * p.V);
-  static cudaError_t once = set_smem(k_tc_dgrad, smem_bytes(128));
-  if (once != cudaSuccess) return once;
-  k_tc_dgrad<<<grid, kFwdThreads, smem_bytes(128), s>>>(ma, mb, p);
+  k_tc_fwd<<<grid, kFwdThreads, fwd_smem_bytes(), s>>>(ma0, ma1, mb, p);
   return cudaGetLastError();
 }
 
@@ -498,13 +434,13 @@ cudaError_t launch_tc_wgrad(const TcWgrad &p, cudaStream_t s) {
     ProfScope prof(kProfGemmWgrad, s, 2.0 * TR * p.V + 2.0 * TR * p.Nout + 4.0 * nchunks * n,
                    2.0 * TR * p.V * p.Nout);
     if (p.Nout == 128) {
-      static cudaError_t once = set_smem(k_tc_wgrad<128>, smem_bytes(128));
+      static cudaError_t once = set_smem(k_tc_wgrad<128>, wg_smem_bytes(128));
       if (once != cudaSuccess) return once;
-      k_tc_wgrad<128><<<grid, kThreads, smem_bytes(128), s>>>(ma_in, ma_h, mg, p, cpt);
+      k_tc_wgrad<128><<<grid, kWgThreads, wg_smem_bytes(128), s>>>(ma_in, ma_h, mg, p, cpt);
     } else {
-      static cudaError_t once = set_smem(k_tc_wgrad<64>, smem_bytes(64));
+      static cudaError_t once = set_smem(k_tc_wgrad<64>, wg_smem_bytes(64));
       if (once != cudaSuccess) return once;
-      k_tc_wgrad<64><<<grid, kThreads, smem_bytes(64), s>>>(ma_in, ma_h, mg, p, cpt);
+      k_tc_wgrad<64><<<grid, kWgThreads, wg_smem_bytes(64), s>>>(ma_in, ma_h, mg, p, cpt);
     }
   }
   cudaError_t e = cudaGetLastError();

@@ -1,6 +1,7 @@
 // Host interfaces of the tcgen05 (bf16 -> fp32 TMEM) gate GEMMs of the precision = 1 path.
-// All diffusion blocks handled here are 64 channels wide (hidden state H = 64, or the 64-wide
-// input of layer > 0): one 128-byte SWIZZLE_128B row per row of A, so one k-block = one block.
+// All diffusion blocks handled here are 64-channel slices (hidden state H = 64, the 64-wide
+// input of layer > 0, or 64-column slices of the diffused gradients): one 128-byte
+// SWIZZLE_128B row per row of A, so one k-block = one 64-channel slice of one block.
 #pragma once
 
 #include <cuda_bf16.h>
@@ -9,24 +10,33 @@
 
 namespace pgti {
 
-constexpr int kTcC = 64;  // channels per k-block
+constexpr int kTcC = 64;   // channels per k-block
+constexpr int kTcMaxKb = 16;
 
-// Forward gate / candidate GEMM with fused GRU epilogue (K3 + K4 + K5).
-//   G[r][j] = sum_kb A_kb[r][0:64] . Wf[kb][j][0:64] + bias[j] (+ layer-0 x part by FFMA)
+// Multi-block GEMM with a fused epilogue, one CTA per (128 rows, 64-column tile):
+//   acc[r][n] = sum_kb A_kb[r][0:64] . B_kb[n][0:64]
+// A_kb = slice kb_ac of block kb_am of operand map kb_as (0: A0, 1: A1), each [blocks][R][CA].
+// B_kb = rows (kb_by + 64*tile) and columns kb_bx of the 3-D bf16 map Bw ([Z][Y][X]) at z=kb_bz.
+// Epilogues (mode):
+//   kEpiGate: gate = acc + bias (+ layer-0 x part by FFMA); tile 0 -> r = sigma(.), writes r
+//             and r*H_{t-1} (bf16); tile 1 -> u = sigma(.).
+//   kEpiCand: c = tanh(acc + bias + x part); H_t = u H_{t-1} + (1-u) c (fp32 and bf16);
+//             optional readout yhat = H_t W_out + b_out.
+//   kEpiBwd : dst[tile][r][0:64] (+)= acc  (the adjoint-diffused gradient, fp32).
 struct TcFwd {
-  int R, H, Nout, mode;             // mode: kEpiGate / kEpiCand (kernels.cuh)
-  const __nv_bfloat16 *A_in;        // [M][R][64] (layer > 0 input blocks) or null
-  const __nv_bfloat16 *A_h;         // [M][R][64] hidden blocks (H_{t-1} or r*H) or null (= 0)
-  int M;
-  const __nv_bfloat16 *Wf;          // [nkb_total][Nout][64]: K-major B tiles
-  int nkb_total;
-  int nkb;                          // active k-blocks
-  signed char kb_src[16], kb_m[16], kb_w[16];
+  int R, H, Nout, mode, ntiles;
+  const __nv_bfloat16 *A0, *A1;     // [blocks][R][CA] (null -> unused)
+  int CA, M0, M1;                   // channels per row of A0/A1; block counts
+  const __nv_bfloat16 *Bw;          // bf16 weights viewed as [Z][Y][X] (X contiguous)
+  int bX, bY, bZ;
+  int nkb;
+  signed char kb_as[kTcMaxKb], kb_am[kTcMaxKb], kb_ac[kTcMaxKb];
+  short kb_bx[kTcMaxKb], kb_by[kTcMaxKb], kb_bz[kTcMaxKb];
   const float *bias;
   // layer-0 x part (fp32, FFMA): Dx[m*dx_mstride + r*F + f] * Wx[(m*C_in + f)*Nout + j]
   const float *Dx;
   int64_t dx_mstride;
-  int F, C_in;
+  int F, C_in, M;
   const float *Wx;
   const float *Hprev;               // fp32 [R][H] or null
   float *out_r, *out_u;             // gate
@@ -37,23 +47,10 @@ struct TcFwd {
   const float *Wout, *bout;
   int F_out;
   float *yhat;
+  float *dst[2];                    // bwd
+  int dst_acc[2];
 };
 cudaError_t launch_tc_fwd(const TcFwd &p, cudaStream_t s);
-
-// dgrad: dT[r][v] = sum_j G[r][j] Wd[v][j]; v -> (m, c) = (v / vseg, coff + v % vseg);
-// c < Fin -> Tin[m][r][c] (+= if acc_in), else Th[m][r][c - Fin]   (fp32 outputs)
-struct TcDgrad {
-  const __nv_bfloat16 *G;           // [R][Nout]
-  int R, Nout;
-  const __nv_bfloat16 *Wd;          // [V][Nout]
-  int V, vseg, coff, Fin, Hd;
-  float *Tin;
-  int64_t tin_mstride;
-  int acc_in;
-  float *Th;
-  int64_t th_mstride;
-};
-cudaError_t launch_tc_dgrad(const TcDgrad &p, cudaStream_t s);
 
 // wgrad: partial[chunk][v][j] = sum_{rows of chunk} A[v][row] G_t[row][j], then a fixed-order
 // reduction over chunks into out rows (v / vseg) * C_in + coff + v % vseg.
