@@ -1,10 +1,11 @@
 // pgti_dcrnn_step: one forward + BPTT pass of the stepwise stacked DCGRU over one gathered
 // batch, plus the diffusion test hooks.  Orchestration only: every arithmetic step runs in the
 // kernels of spmm.cu (K2), gemm_simt.cu / tc_gemm.cu (K3/K3'/K4/K5), small_wgrad.cu and
-// elementwise.cu.
+// elementwise.cu.  This file holds the fp32 parity path (precision 0) and the C ABI; the bf16
+// tcgen05 path (precision 1) is dcrnn_tc.cu.
 //
-// Workspace of the fp32 path (precision 0; all device, caller-owned; R = N*B rows ordered
-// n*B + b; M = 2K+1):
+// Workspace of the fp32 path (all device, caller-owned; R = N*B rows ordered n*B + b;
+// M = 2K+1):
 //   Dx        [M][T_in][R*F]        diffusion blocks of every x_t (layer-0 input)
 //   DH[l]     [T_in][M][R*H]        diffusion blocks of H^l_t (block 0 = H^l_t itself)
 //   DrH[l]    [T_in][M][R*H]        diffusion blocks of r*H^l_{t-1}
@@ -17,30 +18,10 @@
 #include <algorithm>
 #include <vector>
 
-#include "kernels.cuh"
-#include "tc_gemm.cuh"
+#include "dcrnn_common.cuh"
 
 namespace pgti {
-namespace {
-
-struct Dims {
-  int N, F, F_out, L, H, K, T_in, T_out, B, M;
-  int64_t R, ld;
-  int precision;
-};
-
-struct Layout {
-  size_t Dx, yhat, dyhat, lossp, dU, drH, dTin, dTH, wpart, total;
-  size_t tmp[8];
-  std::vector<size_t> DH, DrH, Rg, Ug, Cg, dG, dC, dHa, dHb;
-  size_t tmp_floats, wpart_floats;
-};
-
-// parameter offsets (floats) in the flat layout of pgti.h
-struct ParamOffsets {
-  std::vector<size_t> Wru, bru, Wc, bc;
-  size_t Wout, bout, total;
-};
+namespace detail {
 
 ParamOffsets param_offsets(const Dims &d) {
   ParamOffsets o;
@@ -75,10 +56,12 @@ pgti_status check_desc(const pgti_dcrnn_desc *desc, Dims *out) {
                "desc: ld=%lld must be >= N*F and a multiple of 4", (long long)g.ld);
   PGTI_REQUIRE(g.precision == 0 || g.precision == 1, PGTI_ERR_UNSUPPORTED,
                "desc: precision=%d (0 = fp32 SIMT, 1 = bf16 tcgen05)", g.precision);
-  PGTI_REQUIRE(g.precision == 0 || (g.H == 64 && g.F * (2 * g.K + 1) <= 11 && 2 * g.K + 1 <= 8),
+  PGTI_REQUIRE(g.precision == 0 || (g.H == 64 && g.F * (2 * g.K + 1) <= 11 && 2 * g.K + 1 <= 8 &&
+                                    g.L <= 8),
                PGTI_ERR_UNSUPPORTED,
-               "desc: the bf16 tcgen05 path needs H = 64, F*(2K+1) <= 11 and K <= 3 (H=%d F=%d K=%d)",
-               g.H, g.F, g.K);
+               "desc: the bf16 tcgen05 path needs H = 64, F*(2K+1) <= 11, K <= 3, L <= 8 "
+               "(H=%d F=%d K=%d L=%d)",
+               g.H, g.F, g.K, g.L);
   PGTI_REQUIRE(int64_t(g.N) * g.B * 2 * g.H < (int64_t(1) << 31), PGTI_ERR_SHAPE,
                "desc: N*B*2H exceeds int32 row indexing");
   if (g.K > 0)
@@ -91,54 +74,9 @@ pgti_status check_desc(const pgti_dcrnn_desc *desc, Dims *out) {
   return PGTI_OK;
 }
 
-Layout make_layout(const Dims &d) {
-  Layout L{};
-  size_t off = 0;
-  auto take = [&](size_t bytes) {
-    size_t o = off;
-    off += round_up(int64_t(bytes), 256);
-    return o;
-  };
-  const size_t R = size_t(d.R), H = size_t(d.H), M = size_t(d.M), T = size_t(d.T_in);
-  L.Dx = take(M * T * R * d.F * 4);
-  for (int l = 0; l < d.L; ++l) {
-    L.DH.push_back(take(T * M * R * H * 4));
-    L.DrH.push_back(take(T * M * R * H * 4));
-    L.Rg.push_back(take(T * R * H * 4));
-    L.Ug.push_back(take(T * R * H * 4));
-    L.Cg.push_back(take(T * R * H * 4));
-    L.dG.push_back(take(T * R * 2 * H * 4));
-    L.dC.push_back(take(T * R * H * 4));
-    L.dHa.push_back(take(R * H * 4));
-    L.dHb.push_back(take(R * H * 4));
-  }
-  L.yhat = take(size_t(d.T_out) * R * d.F_out * 4);
-  L.dyhat = take(size_t(d.T_out) * R * d.F_out * 4);
-  L.lossp = take(size_t(kLossBlocks) * 8);
-  L.dU = take(R * H * 4);
-  L.drH = take(R * H * 4);
-  const size_t fin_max = d.L > 1 ? H : size_t(d.F);
-  L.dTin = take(M * R * fin_max * 4);
-  L.dTH = take(M * R * H * 4);
-  L.tmp_floats = R * std::max(H, fin_max);
-  for (int i = 0; i < 8; ++i) L.tmp[i] = take(L.tmp_floats * 4);
-  size_t wp = small_wgrad_partial_floats(d.T_out, int(d.R), d.H);
-  for (int l = 0; l < d.L; ++l) {
-    const int C = (l == 0 ? d.F : d.H) + d.H;
-    wp = std::max(wp, wgrad_partial_floats(d.M, C, 2 * d.H, d.T_in, int(d.R)));
-  }
-  L.wpart_floats = wp;
-  L.wpart = take(wp * 4);
-  L.total = off;
-  return L;
-}
-
-// Forward diffusion: blocks base + m*mstride (m = 0 given), G groups of stride gstride, width W.
-// transposed = 1 diffuses with P_f^T / P_b^T instead (the backward "diffuse-then-GEMM" dgrad).
-// bf16 = 1: blocks are __nv_bfloat16 (base / src0 reinterpreted).
 cudaError_t diffuse_fwd(const pgti_dcrnn_desc &g, const Dims &d, float *base, int64_t mstride,
-                        int G, int64_t gstride, int64_t W, cudaStream_t s, int bf16 = 0,
-                        int transposed = 0, const void *src0 = nullptr) {
+                        int G, int64_t gstride, int64_t W, cudaStream_t s, int bf16,
+                        int transposed, const void *src0) {
   const int es = bf16 ? 2 : 4;
   char *b = reinterpret_cast<char *>(base);
   const char *z = src0 ? static_cast<const char *>(src0) : b;
@@ -163,16 +101,6 @@ cudaError_t diffuse_fwd(const pgti_dcrnn_desc &g, const Dims &d, float *base, in
   }
   return cudaSuccess;
 }
-
-// Adjoint of the diffusion features (Horner form):
-//   out (+)= dT_0 + P_f^T (dT_1 + P_f^T (... + P_f^T dT_K)) + P_b^T (dT_{K+1} + ... P_b^T dT_2K)
-struct AdjChain {
-  const float *dT;
-  int64_t mstride, W;
-  float *out;
-  int accumulate;
-  float *tf[2], *tb[2];
-};
 
 cudaError_t diffuse_adj(const pgti_dcrnn_desc &g, const Dims &d, AdjChain *ch, int nch,
                         cudaStream_t s) {
@@ -219,15 +147,57 @@ cudaError_t diffuse_adj(const pgti_dcrnn_desc &g, const Dims &d, AdjChain *ch, i
   return launch_spmm(jobs, nch, d.N, s);
 }
 
-#define CU(expr)                                                                              \
-  do {                                                                                        \
-    cudaError_t e_ = (expr);                                                                  \
-    if (e_ != cudaSuccess)                                                                    \
-      return fail(PGTI_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__,  \
-                  __LINE__);                                                                  \
-  } while (0)
+namespace {
 
-// =========================================================================== precision = 0
+struct Layout {
+  size_t Dx, yhat, dyhat, lossp, dU, drH, dTin, dTH, wpart, total;
+  size_t tmp[8];
+  std::vector<size_t> DH, DrH, Rg, Ug, Cg, dG, dC, dHa, dHb;
+  size_t tmp_floats, wpart_floats;
+};
+
+Layout make_layout(const Dims &d) {
+  Layout L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += round_up(int64_t(bytes), 256);
+    return o;
+  };
+  const size_t R = size_t(d.R), H = size_t(d.H), M = size_t(d.M), T = size_t(d.T_in);
+  L.Dx = take(M * T * R * d.F * 4);
+  for (int l = 0; l < d.L; ++l) {
+    L.DH.push_back(take(T * M * R * H * 4));
+    L.DrH.push_back(take(T * M * R * H * 4));
+    L.Rg.push_back(take(T * R * H * 4));
+    L.Ug.push_back(take(T * R * H * 4));
+    L.Cg.push_back(take(T * R * H * 4));
+    L.dG.push_back(take(T * R * 2 * H * 4));
+    L.dC.push_back(take(T * R * H * 4));
+    L.dHa.push_back(take(R * H * 4));
+    L.dHb.push_back(take(R * H * 4));
+  }
+  L.yhat = take(size_t(d.T_out) * R * d.F_out * 4);
+  L.dyhat = take(size_t(d.T_out) * R * d.F_out * 4);
+  L.lossp = take(size_t(kLossBlocks) * 8);
+  L.dU = take(R * H * 4);
+  L.drH = take(R * H * 4);
+  const size_t fin_max = d.L > 1 ? H : size_t(d.F);
+  L.dTin = take(M * R * fin_max * 4);
+  L.dTH = take(M * R * H * 4);
+  L.tmp_floats = R * std::max(H, fin_max);
+  for (int i = 0; i < 8; ++i) L.tmp[i] = take(L.tmp_floats * 4);
+  size_t wp = small_wgrad_partial_floats(d.T_out, int(d.R), d.H);
+  for (int l = 0; l < d.L; ++l) {
+    const int C = (l == 0 ? d.F : d.H) + d.H;
+    wp = std::max(wp, wgrad_partial_floats(d.M, C, 2 * d.H, d.T_in, int(d.R)));
+  }
+  L.wpart_floats = wp;
+  L.wpart = take(wp * 4);
+  L.total = off;
+  return L;
+}
+
 pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *params, float *grads,
                      const float *x, const float *y, float *loss_dev, char *ws, float *act_dump,
                      cudaStream_t s) {
@@ -297,8 +267,8 @@ pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *param
       const float *dy = (l == L - 1 && t >= T - d.T_out)
                             ? Fp(Ly.dyhat) + int64_t(t - (T - d.T_out)) * R * d.F_out
                             : nullptr;
-      CU(launch_cand_bwd(RH, d.H, dHcur[l], dy, params + P.Wout, d.F_out, u, c, Hprev, dU, dC,
-                         need_h ? dHprev[l] : nullptr, s));
+      CU(launch_cand_bwd(RH, d.H, dHcur[l], nullptr, dy, params + P.Wout, d.F_out, u, c, Hprev,
+                         dU, dC, need_h ? dHprev[l] : nullptr, s));
       const int64_t tin_ms = R * Fin;
       if (need_in || need_h) {
         GconvDgrad dg{};
@@ -376,273 +346,16 @@ pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *param
   return PGTI_OK;
 }
 
-// =========================================================================== precision = 1
-// bf16 tcgen05 path.  Differences from the fp32 path:
-//  * the diffusion blocks of H and r*H are bf16 (tensor-core A operands, forward SpMM
-//    operands); an fp32 copy of H carries the recurrence; weights are re-tiled to bf16 per step;
-//  * layer 0's F-channel input part stays fp32 (FFMA in the GEMM epilogue; skinny wgrad rows);
-//  * backward "diffuse-then-GEMM": dZ = sum_m (P^m)^T dG W_m^T = sum_m ((P^m)^T dG) W_m^T, so
-//    the gate gradient (2H wide, bf16) is diffused with the transposed operators and ONE
-//    multi-block tcgen05 GEMM accumulates dZ straight into the fp32 BPTT accumulators -- no
-//    M*C_in-wide dT intermediate and no Horner chains.
-struct LayoutTC {
-  size_t Dx, yhat, dyhat, lossp, dU, drH, Q, wpart, total;
-  std::vector<size_t> DHb, DrHb, H32, Rg, Ug, Cg, dG, dGb, dC, dCb, dHa, dHb, Wf_ru, Wf_c, Wd_ru,
-      Wd_c;
-  size_t wpart_floats;
-};
-
-int nkb_total(const Dims &d, int l) { return l == 0 ? d.M : 2 * d.M; }
-int vrows(const Dims &d, int l) { return l == 0 ? d.M * 64 : d.M * (d.H + d.H); }
-
-LayoutTC make_layout_tc(const Dims &d) {
-  LayoutTC L{};
-  size_t off = 0;
-  auto take = [&](size_t bytes) {
-    size_t o = off;
-    off += round_up(int64_t(bytes), 1024);
-    return o;
-  };
-  const size_t R = size_t(d.R), H = size_t(d.H), M = size_t(d.M), T = size_t(d.T_in);
-  L.Dx = take(M * T * R * d.F * 4);
-  size_t wp = small_wgrad_partial_floats(d.T_in, int(d.R), 2 * d.H);
-  for (int l = 0; l < d.L; ++l) {
-    L.DHb.push_back(take(T * M * R * H * 2));
-    L.DrHb.push_back(take(T * M * R * H * 2));
-    L.H32.push_back(take(T * R * H * 4));
-    L.Rg.push_back(take(T * R * H * 4));
-    L.Ug.push_back(take(T * R * H * 4));
-    L.Cg.push_back(take(T * R * H * 4));
-    L.dG.push_back(take(T * R * 2 * H * 4));
-    L.dGb.push_back(take(T * R * 2 * H * 2));
-    L.dC.push_back(take(T * R * H * 4));
-    L.dCb.push_back(take(T * R * H * 2));
-    L.dHa.push_back(take(R * H * 4));
-    L.dHb.push_back(take(R * H * 4));
-    L.Wf_ru.push_back(take(size_t(nkb_total(d, l)) * 2 * H * 64 * 2));
-    L.Wf_c.push_back(take(size_t(nkb_total(d, l)) * H * 64 * 2));
-    L.Wd_ru.push_back(take(size_t(vrows(d, l)) * 2 * H * 2));
-    L.Wd_c.push_back(take(size_t(vrows(d, l)) * H * 2));
-    wp = std::max(wp, tc_wgrad_partial_floats(vrows(d, l), 2 * d.H, d.T_in, int(d.R)));
-  }
-  L.yhat = take(size_t(d.T_out) * R * d.F_out * 4);
-  L.dyhat = take(size_t(d.T_out) * R * d.F_out * 4);
-  L.lossp = take(size_t(kLossBlocks) * 8);
-  L.dU = take(R * H * 4);
-  L.drH = take(R * H * 4);
-  L.Q = take(M * R * 2 * H * 2);
-  L.wpart_floats = wp;
-  L.wpart = take(wp * 4);
-  L.total = off;
-  return L;
-}
-
-pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *params,
-                        float *grads, const float *x, const float *y, float *loss_dev, char *ws,
-                        float *act_dump, cudaStream_t s) {
-  using bf16 = __nv_bfloat16;
-  const LayoutTC Ly = make_layout_tc(d);
-  const ParamOffsets P = param_offsets(d);
-  auto Fp = [&](size_t off) { return reinterpret_cast<float *>(ws + off); };
-  auto Bp = [&](size_t off) { return reinterpret_cast<bf16 *>(ws + off); };
-  const int64_t R = d.R, H = d.H, M = d.M, RH = R * H, MRH = M * RH;
-  const int T = d.T_in, L = d.L;
-  float *Dx = Fp(Ly.Dx);
-  const int64_t RF = R * d.F;
-  unsigned *err = device_error_flag();
-  PGTI_REQUIRE(err, PGTI_ERR_CUDA, "device error flag unavailable");
-
-  // ------------------------------------------------------------------ bf16 weight tiles
-  {
-    WeightJob jobs[8];
-    int nj = 0;
-    for (int l = 0; l < L; ++l) {
-      const int Fin = l == 0 ? d.F : d.H, C = Fin + d.H;
-      jobs[nj++] = WeightJob{params + P.Wru[l], 2 * d.H, C, d.M, Fin, l == 0, Bp(Ly.Wf_ru[l]),
-                             Bp(Ly.Wd_ru[l])};
-      jobs[nj++] = WeightJob{params + P.Wc[l], d.H, C, d.M, Fin, l == 0, Bp(Ly.Wf_c[l]),
-                             Bp(Ly.Wd_c[l])};
-    }
-    CU(launch_convert_weights(jobs, nj, s));
-  }
-
-  // ------------------------------------------------------------------ forward
-  CU(launch_x_prep(x, d.B, T, d.ld, d.N, d.F, Dx, s));
-  CU(diffuse_fwd(g, d, Dx, int64_t(T) * RF, T, RF, int64_t(d.B) * d.F, s));
-  for (int t = 0; t < T; ++t) {
-    for (int l = 0; l < L; ++l) {
-      const int Fin = l == 0 ? d.F : d.H, C = Fin + d.H;
-      const bf16 *Ain = l == 0 ? nullptr : Bp(Ly.DHb[l - 1]) + t * MRH;
-      const bf16 *DHp = t > 0 ? Bp(Ly.DHb[l]) + (t - 1) * MRH : nullptr;
-      bf16 *DHt = Bp(Ly.DHb[l]) + t * MRH, *DrHt = Bp(Ly.DrHb[l]) + t * MRH;
-      const float *Hp32 = t > 0 ? Fp(Ly.H32[l]) + (t - 1) * RH : nullptr;
-      float *r = Fp(Ly.Rg[l]) + t * RH, *u = Fp(Ly.Ug[l]) + t * RH, *c = Fp(Ly.Cg[l]) + t * RH;
-      // k-blocks: (input block m: map A0) and (hidden block m: map A1), B = Wf[kb] tiles
-      auto fill_kb = [&](TcFwd &f, const bf16 *Ah, int Nout) {
-        f.A0 = Ain, f.A1 = Ah, f.CA = 64, f.M0 = d.M, f.M1 = d.M;
-        f.bX = 64, f.bY = Nout, f.bZ = nkb_total(d, l);
-        f.nkb = 0;
-        for (int m = 0; m < d.M; ++m) {
-          if (l > 0) {
-            f.kb_as[f.nkb] = 0, f.kb_am[f.nkb] = m, f.kb_ac[f.nkb] = 0;
-            f.kb_bx[f.nkb] = 0, f.kb_by[f.nkb] = 0, f.kb_bz[f.nkb] = 2 * m, ++f.nkb;
-          }
-          if (Ah) {
-            f.kb_as[f.nkb] = 1, f.kb_am[f.nkb] = m, f.kb_ac[f.nkb] = 0;
-            f.kb_bx[f.nkb] = 0, f.kb_by[f.nkb] = 0, f.kb_bz[f.nkb] = l > 0 ? 2 * m + 1 : m, ++f.nkb;
-          }
-        }
-      };
-      TcFwd gate{};
-      gate.R = int(R), gate.H = d.H, gate.Nout = 2 * d.H, gate.mode = kEpiGate, gate.ntiles = 2;
-      fill_kb(gate, DHp, 2 * d.H);
-      gate.Bw = Bp(Ly.Wf_ru[l]);
-      gate.bias = params + P.bru[l];
-      if (l == 0)
-        gate.Dx = Dx + t * RF, gate.dx_mstride = int64_t(T) * RF, gate.F = d.F, gate.C_in = C,
-        gate.M = d.M, gate.Wx = params + P.Wru[l];
-      gate.Hprev = Hp32;
-      gate.out_r = r, gate.out_u = u, gate.out_rH = DrHt;
-      CU(launch_tc_fwd(gate, s));
-      CU(diffuse_fwd(g, d, reinterpret_cast<float *>(DrHt), RH, 1, 0, int64_t(d.B) * d.H, s, 1));
-
-      TcFwd cand{};
-      cand.R = int(R), cand.H = d.H, cand.Nout = d.H, cand.mode = kEpiCand, cand.ntiles = 1;
-      fill_kb(cand, t > 0 ? DrHt : nullptr, d.H);
-      cand.Bw = Bp(Ly.Wf_c[l]);
-      cand.bias = params + P.bc[l];
-      if (l == 0)
-        cand.Dx = Dx + t * RF, cand.dx_mstride = int64_t(T) * RF, cand.F = d.F, cand.C_in = C,
-        cand.M = d.M, cand.Wx = params + P.Wc[l];
-      cand.Hprev = Hp32, cand.u_in = u, cand.out_c = c;
-      cand.out_H = Fp(Ly.H32[l]) + t * RH, cand.out_Hb = DHt;
-      if (l == L - 1 && t >= T - d.T_out) {
-        cand.Wout = params + P.Wout, cand.bout = params + P.bout, cand.F_out = d.F_out;
-        cand.yhat = Fp(Ly.yhat) + int64_t(t - (T - d.T_out)) * R * d.F_out;
-      }
-      CU(launch_tc_fwd(cand, s));
-      if (!(l == L - 1 && t == T - 1))
-        CU(diffuse_fwd(g, d, reinterpret_cast<float *>(DHt), RH, 1, 0, int64_t(d.B) * d.H, s, 1));
-    }
-  }
-  CU(launch_loss(Fp(Ly.yhat), y, d.T_out, d.N, d.B, d.F, d.F_out, d.ld, Fp(Ly.dyhat),
-                 reinterpret_cast<double *>(ws + Ly.lossp), loss_dev, err, s));
-
-  // ------------------------------------------------------------------ backward (BPTT)
-  std::vector<float *> dHcur(L), dHprev(L);
-  for (int l = 0; l < L; ++l) {
-    dHcur[l] = Fp(Ly.dHa[l]), dHprev[l] = Fp(Ly.dHb[l]);
-    CU(cudaMemsetAsync(dHcur[l], 0, size_t(RH) * 4, s));
-  }
-  float *dU = Fp(Ly.dU), *drH = Fp(Ly.drH);
-  bf16 *Q = Bp(Ly.Q);
-  // dZ = sum_m Q_m W_m^T, Q_0 = gradient itself (map A0), Q_{m>0} = (P^m)^T grad (map A1)
-  auto bwd_gemm = [&](int l, const bf16 *grad, int NG, const bf16 *Wd, bool need_in,
-                      bool need_h, float *dst_in, float *dst_h, int acc_h) -> pgti_status {
-    const int vseg = l == 0 ? 64 : 2 * d.H;
-    TcFwd b{};
-    b.R = int(R), b.H = d.H, b.Nout = NG, b.mode = kEpiBwd;
-    b.A0 = grad, b.A1 = Q, b.CA = NG, b.M0 = 1, b.M1 = d.M;
-    b.Bw = Wd, b.bX = NG, b.bY = vrows(d, l), b.bZ = 1;
-    b.nkb = 0;
-    for (int m = 0; m < d.M; ++m)
-      for (int jb = 0; jb < NG / 64; ++jb) {
-        b.kb_as[b.nkb] = m > 0, b.kb_am[b.nkb] = m, b.kb_ac[b.nkb] = jb * 64;
-        b.kb_bx[b.nkb] = jb * 64, b.kb_by[b.nkb] = m * vseg, b.kb_bz[b.nkb] = 0, ++b.nkb;
-      }
-    // column tiles: l > 0 -> [input (64), hidden (64)]; l = 0 -> [hidden]
-    int nt = 0;
-    if (need_in) b.dst[nt] = dst_in, b.dst_acc[nt] = 1, ++nt;
-    if (need_h) b.dst[nt] = dst_h, b.dst_acc[nt] = acc_h, ++nt;
-    if (nt == 0) return PGTI_OK;
-    if (l > 0 && !need_in)  // skip the input tile: shift B rows by one 64-column tile
-      for (int k = 0; k < b.nkb; ++k) b.kb_by[k] += 64;
-    b.ntiles = nt;
-    CU(launch_tc_fwd(b, s));
-    return PGTI_OK;
-  };
-  for (int t = T - 1; t >= 0; --t) {
-    for (int l = L - 1; l >= 0; --l) {
-      const bool need_in = l > 0, need_h = t > 0;
-      const float *Hprev = t > 0 ? Fp(Ly.H32[l]) + (t - 1) * RH : nullptr;
-      const float *r = Fp(Ly.Rg[l]) + t * RH, *u = Fp(Ly.Ug[l]) + t * RH, *c = Fp(Ly.Cg[l]) + t * RH;
-      float *dC = Fp(Ly.dC[l]) + t * RH, *dG = Fp(Ly.dG[l]) + t * 2 * RH;
-      bf16 *dCb = Bp(Ly.dCb[l]) + t * RH, *dGb = Bp(Ly.dGb[l]) + t * 2 * RH;
-      const float *dy = (l == L - 1 && t >= T - d.T_out)
-                            ? Fp(Ly.dyhat) + int64_t(t - (T - d.T_out)) * R * d.F_out
-                            : nullptr;
-      float *dIn = need_in ? dHcur[l - 1] : nullptr;
-      CU(launch_cand_bwd(RH, d.H, dHcur[l], dy, params + P.Wout, d.F_out, u, c, Hprev, dU, dC,
-                         need_h ? dHprev[l] : nullptr, s, dCb));
-      if (need_in || need_h) {
-        CU(diffuse_fwd(g, d, reinterpret_cast<float *>(Q), RH, 1, 0, int64_t(d.B) * d.H, s, 1, 1,
-                       dCb));
-        PGTI_STATUS_TRY(bwd_gemm(l, dCb, d.H, Bp(Ly.Wd_c[l]), need_in, need_h, dIn, drH, 0));
-      }
-      CU(launch_gate_bwd(RH, d.H, need_h ? drH : nullptr, Hprev, r, u, dU,
-                         need_h ? dHprev[l] : nullptr, dG, s, dGb));
-      if (need_in || need_h) {
-        CU(diffuse_fwd(g, d, reinterpret_cast<float *>(Q), 2 * RH, 1, 0, int64_t(d.B) * 2 * d.H, s,
-                       1, 1, dGb));
-        PGTI_STATUS_TRY(bwd_gemm(l, dGb, 2 * d.H, Bp(Ly.Wd_ru[l]), need_in, need_h, dIn,
-                                 need_h ? dHprev[l] : nullptr, 1));
-      }
-      std::swap(dHcur[l], dHprev[l]);
-    }
-  }
-
-  // ------------------------------------------------------------------ weight gradients
-  for (int l = 0; l < L; ++l) {
-    const int Fin = l == 0 ? d.F : d.H, C = Fin + d.H;
-    const int V = vrows(d, l), vseg = l == 0 ? 64 : 2 * d.H, coff = l == 0 ? d.F : 0;
-    const bf16 *Ain = l == 0 ? nullptr : Bp(Ly.DHb[l - 1]);
-    TcWgrad tw{Ain, Bp(Ly.DHb[l]), -1, T, d.M, int(R), Bp(Ly.dGb[l]), 2 * d.H,
-               V, vseg, coff, C, Fp(Ly.wpart), int64_t(Ly.wpart_floats), grads + P.Wru[l]};
-    CU(launch_tc_wgrad(tw, s));
-    tw.A_h = Bp(Ly.DrHb[l]), tw.h_toff = 0, tw.G = Bp(Ly.dCb[l]), tw.Nout = d.H;
-    tw.out = grads + P.Wc[l];
-    CU(launch_tc_wgrad(tw, s));
-    // input rows of layer 0 (fp32 x part) and the bias rows: skinny reduction over T*R rows
-    SmallWgrad sw{};
-    sw.mode = kSmallBiasX, sw.T = T, sw.R = int(R);
-    if (l == 0) sw.Dx = Dx, sw.dx_mstride = int64_t(T) * RF, sw.dx_tstride = RF;
-    sw.M = d.M, sw.F = d.F, sw.C_in = C;
-    sw.partial = Fp(Ly.wpart), sw.partial_cap = int64_t(Ly.wpart_floats);
-    sw.G = Fp(Ly.dG[l]), sw.g_tstride = 2 * RH, sw.NG = 2 * d.H, sw.out = grads + P.Wru[l];
-    CU(launch_small_wgrad(sw, s));
-    sw.G = Fp(Ly.dC[l]), sw.g_tstride = RH, sw.NG = d.H, sw.out = grads + P.Wc[l];
-    CU(launch_small_wgrad(sw, s));
-  }
-  SmallWgrad rw{};
-  rw.mode = kSmallReadout, rw.T = d.T_out, rw.R = int(R);
-  rw.dy = Fp(Ly.dyhat), rw.F_out = d.F_out;
-  rw.G = Fp(Ly.H32[L - 1]) + int64_t(T - d.T_out) * RH, rw.g_tstride = RH, rw.NG = d.H;
-  rw.partial = Fp(Ly.wpart), rw.partial_cap = int64_t(Ly.wpart_floats), rw.out = grads + P.Wout;
-  CU(launch_small_wgrad(rw, s));
-
-  if (act_dump) {
-    for (int t = 0; t < T; ++t)
-      for (int l = 0; l < L; ++l) {
-        float *dst = act_dump + (int64_t(t) * L + l) * 4 * RH;
-        const float *src[4] = {Fp(Ly.H32[l]) + t * RH, Fp(Ly.Rg[l]) + t * RH,
-                               Fp(Ly.Ug[l]) + t * RH, Fp(Ly.Cg[l]) + t * RH};
-        for (int q = 0; q < 4; ++q)
-          CU(cudaMemcpyAsync(dst + q * RH, src[q], size_t(RH) * 4, cudaMemcpyDeviceToDevice, s));
-      }
-    CU(cudaMemcpyAsync(act_dump + int64_t(T) * L * 4 * RH, Fp(Ly.yhat),
-                       size_t(d.T_out) * R * d.F_out * 4, cudaMemcpyDeviceToDevice, s));
-  }
-  return PGTI_OK;
-}
-
 size_t workspace_for(const Dims &d) {
-  return d.precision == 1 ? make_layout_tc(d).total : make_layout(d).total;
+  return d.precision == 1 ? workspace_tc(d) : make_layout(d).total;
 }
 
 }  // namespace
+}  // namespace detail
 }  // namespace pgti
 
 using namespace pgti;
+using namespace pgti::detail;
 
 extern "C" size_t pgti_dcrnn_num_params(const pgti_dcrnn_desc *desc) {
   Dims d;

@@ -1,0 +1,353 @@
+// pgti_dcrnn_step, precision = 1: bf16 operands on the 5th-gen tensor cores (tcgen05, fp32 TMEM
+// accumulation).  Differences from the fp32 path (dcrnn.cu):
+//  * the diffusion blocks of H and r*H are bf16 (tensor-core A operands, forward SpMM
+//    operands); an fp32 copy of H carries the recurrence; weights are re-tiled to bf16 per step;
+//  * layer 0's F-channel input part stays fp32 (FFMA in the GEMM epilogue; skinny wgrad rows);
+//  * backward "diffuse-then-GEMM": dZ = sum_m (P^m)^T dG W_m^T = sum_m ((P^m)^T dG) W_m^T, so
+//    the gate gradient (2H wide, bf16) is diffused with the transposed operators and ONE
+//    multi-block tcgen05 GEMM accumulates dZ straight into the fp32 BPTT accumulators;
+//  * layer pipelining: layer l runs on its own stream; (l+1, t) depends only on (l, t) and
+//    (l+1, t-1), so layer l at t+1 overlaps layer l+1 at t (and the reverse wavefront in BPTT).
+//    Cross-layer gradients use per-layer, time-parity double buffers (dHup) so no two streams
+//    ever write the same accumulator.  Captured into one CUDA graph this is a DAG, not a chain.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <map>
+#include <vector>
+
+#include "dcrnn_common.cuh"
+#include "tc_gemm.cuh"
+
+namespace pgti {
+namespace detail {
+namespace {
+
+using bf16 = __nv_bfloat16;
+
+// ------------------------------------------------------------------ streams / events
+struct StreamPool {
+  std::vector<cudaStream_t> side;
+  std::vector<cudaEvent_t> ev;
+  size_t next = 0;
+};
+
+// One pool per (host thread, device): side streams for layers 1.., a ring of events.
+StreamPool *pool(int nside, cudaError_t *err) {
+  thread_local std::map<int, StreamPool> pools;
+  int dev = 0;
+  *err = cudaGetDevice(&dev);
+  if (*err != cudaSuccess) return nullptr;
+  StreamPool &p = pools[dev];
+  while (int(p.side.size()) < nside) {
+    cudaStream_t st;
+    *err = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (*err != cudaSuccess) return nullptr;
+    p.side.push_back(st);
+  }
+  while (p.ev.size() < 1024) {
+    cudaEvent_t e;
+    *err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (*err != cudaSuccess) return nullptr;
+    p.ev.push_back(e);
+  }
+  return &p;
+}
+
+// `to` waits for all work enqueued so far on `from`.
+cudaError_t depend(StreamPool *p, cudaStream_t from, cudaStream_t to) {
+  if (from == to) return cudaSuccess;
+  cudaEvent_t e = p->ev[p->next++ % p->ev.size()];
+  cudaError_t r = cudaEventRecord(e, from);
+  if (r != cudaSuccess) return r;
+  return cudaStreamWaitEvent(to, e, 0);
+}
+
+cudaError_t record(StreamPool *p, cudaStream_t st, cudaEvent_t *out) {
+  *out = p->ev[p->next++ % p->ev.size()];
+  return cudaEventRecord(*out, st);
+}
+
+// ------------------------------------------------------------------ workspace
+struct LayoutTC {
+  size_t Dx, yhat, dyhat, lossp, total;
+  std::vector<size_t> DHb, DrHb, H32, Rg, Ug, Cg, dG, dGb, dC, dCb, Wf_ru, Wf_c, Wd_ru, Wd_c;
+  std::vector<size_t> dU, drH, Q, wpart, dHrec0, dHrec1, dHup0, dHup1;
+  size_t wpart_floats;
+};
+
+int nkb_total(const Dims &d, int l) { return l == 0 ? d.M : 2 * d.M; }
+int vrows(const Dims &d, int l) { return l == 0 ? d.M * 64 : d.M * (d.H + d.H); }
+
+LayoutTC make_layout_tc(const Dims &d) {
+  LayoutTC L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += round_up(int64_t(bytes), 1024);
+    return o;
+  };
+  const size_t R = size_t(d.R), H = size_t(d.H), M = size_t(d.M), T = size_t(d.T_in);
+  L.Dx = take(M * T * R * d.F * 4);
+  size_t wp = small_wgrad_partial_floats(d.T_in, int(d.R), 2 * d.H);
+  for (int l = 0; l < d.L; ++l)
+    wp = std::max(wp, tc_wgrad_partial_floats(vrows(d, l), 2 * d.H, d.T_in, int(d.R)));
+  L.wpart_floats = wp;
+  for (int l = 0; l < d.L; ++l) {
+    L.DHb.push_back(take(T * M * R * H * 2));
+    L.DrHb.push_back(take(T * M * R * H * 2));
+    L.H32.push_back(take(T * R * H * 4));
+    L.Rg.push_back(take(T * R * H * 4));
+    L.Ug.push_back(take(T * R * H * 4));
+    L.Cg.push_back(take(T * R * H * 4));
+    L.dG.push_back(take(T * R * 2 * H * 4));
+    L.dGb.push_back(take(T * R * 2 * H * 2));
+    L.dC.push_back(take(T * R * H * 4));
+    L.dCb.push_back(take(T * R * H * 2));
+    L.Wf_ru.push_back(take(size_t(nkb_total(d, l)) * 2 * H * 64 * 2));
+    L.Wf_c.push_back(take(size_t(nkb_total(d, l)) * H * 64 * 2));
+    L.Wd_ru.push_back(take(size_t(vrows(d, l)) * 2 * H * 2));
+    L.Wd_c.push_back(take(size_t(vrows(d, l)) * H * 2));
+    // per-layer (= per-stream) scratch
+    L.dU.push_back(take(R * H * 4));
+    L.drH.push_back(take(R * H * 4));
+    L.Q.push_back(take(M * R * 2 * H * 2));
+    L.wpart.push_back(take(wp * 4));
+    L.dHrec0.push_back(take(R * H * 4));
+    L.dHrec1.push_back(take(R * H * 4));
+    L.dHup0.push_back(take(R * H * 4));
+    L.dHup1.push_back(take(R * H * 4));
+  }
+  L.yhat = take(size_t(d.T_out) * R * d.F_out * 4);
+  L.dyhat = take(size_t(d.T_out) * R * d.F_out * 4);
+  L.lossp = take(size_t(kLossBlocks) * 8);
+  L.total = off;
+  return L;
+}
+
+}  // namespace
+
+size_t workspace_tc(const Dims &d) { return make_layout_tc(d).total; }
+
+pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *params,
+                        float *grads, const float *x, const float *y, float *loss_dev, char *ws,
+                        float *act_dump, cudaStream_t s) {
+  const LayoutTC Ly = make_layout_tc(d);
+  const ParamOffsets P = param_offsets(d);
+  auto Fp = [&](size_t off) { return reinterpret_cast<float *>(ws + off); };
+  auto Bp = [&](size_t off) { return reinterpret_cast<bf16 *>(ws + off); };
+  const int64_t R = d.R, H = d.H, M = d.M, RH = R * H, MRH = M * RH;
+  const int T = d.T_in, L = d.L;
+  float *Dx = Fp(Ly.Dx);
+  const int64_t RF = R * d.F;
+  unsigned *err = device_error_flag();
+  PGTI_REQUIRE(err, PGTI_ERR_CUDA, "device error flag unavailable");
+  cudaError_t perr = cudaSuccess;
+  StreamPool *sp = pool(L - 1, &perr);
+  CU(perr);
+  std::vector<cudaStream_t> st(L);
+  st[0] = s;
+  for (int l = 1; l < L; ++l) st[l] = sp->side[l - 1];
+
+  // ------------------------------------------------------------------ prologue on s
+  {
+    WeightJob jobs[16];
+    int nj = 0;
+    for (int l = 0; l < L; ++l) {
+      const int Fin = l == 0 ? d.F : d.H, C = Fin + d.H;
+      jobs[nj++] = WeightJob{params + P.Wru[l], 2 * d.H, C, d.M, Fin, l == 0, Bp(Ly.Wf_ru[l]),
+                             Bp(Ly.Wd_ru[l])};
+      jobs[nj++] = WeightJob{params + P.Wc[l], d.H, C, d.M, Fin, l == 0, Bp(Ly.Wf_c[l]),
+                             Bp(Ly.Wd_c[l])};
+    }
+    for (int i = 0; i < nj; i += 8) CU(launch_convert_weights(jobs + i, std::min(8, nj - i), s));
+  }
+  CU(launch_x_prep(x, d.B, T, d.ld, d.N, d.F, Dx, s));
+  CU(diffuse_fwd(g, d, Dx, int64_t(T) * RF, T, RF, int64_t(d.B) * d.F, s));
+  for (int l = 1; l < L; ++l) CU(depend(sp, s, st[l]));  // fork
+
+  // ------------------------------------------------------------------ forward
+  std::vector<std::vector<cudaEvent_t>> fdone(L, std::vector<cudaEvent_t>(T));
+  for (int t = 0; t < T; ++t) {
+    for (int l = 0; l < L; ++l) {
+      cudaStream_t ss = st[l];
+      if (l > 0) CU(cudaStreamWaitEvent(ss, fdone[l - 1][t], 0));
+      const int Fin = l == 0 ? d.F : d.H, C = Fin + d.H;
+      const bf16 *Ain = l == 0 ? nullptr : Bp(Ly.DHb[l - 1]) + t * MRH;
+      const bf16 *DHp = t > 0 ? Bp(Ly.DHb[l]) + (t - 1) * MRH : nullptr;
+      bf16 *DHt = Bp(Ly.DHb[l]) + t * MRH, *DrHt = Bp(Ly.DrHb[l]) + t * MRH;
+      const float *Hp32 = t > 0 ? Fp(Ly.H32[l]) + (t - 1) * RH : nullptr;
+      float *r = Fp(Ly.Rg[l]) + t * RH, *u = Fp(Ly.Ug[l]) + t * RH, *c = Fp(Ly.Cg[l]) + t * RH;
+      // k-blocks: (input block m: map A0) and (hidden block m: map A1), B = Wf[kb] tiles
+      auto fill_kb = [&](TcFwd &f, const bf16 *Ah, int Nout) {
+        f.A0 = Ain, f.A1 = Ah, f.CA = 64, f.M0 = d.M, f.M1 = d.M;
+        f.bX = 64, f.bY = Nout, f.bZ = nkb_total(d, l);
+        f.nkb = 0;
+        for (int m = 0; m < d.M; ++m) {
+          if (l > 0) {
+            f.kb_as[f.nkb] = 0, f.kb_am[f.nkb] = m, f.kb_ac[f.nkb] = 0;
+            f.kb_bx[f.nkb] = 0, f.kb_by[f.nkb] = 0, f.kb_bz[f.nkb] = 2 * m, ++f.nkb;
+          }
+          if (Ah) {
+            f.kb_as[f.nkb] = 1, f.kb_am[f.nkb] = m, f.kb_ac[f.nkb] = 0;
+            f.kb_bx[f.nkb] = 0, f.kb_by[f.nkb] = 0, f.kb_bz[f.nkb] = l > 0 ? 2 * m + 1 : m, ++f.nkb;
+          }
+        }
+      };
+      TcFwd gate{};
+      gate.R = int(R), gate.H = d.H, gate.Nout = 2 * d.H, gate.mode = kEpiGate, gate.ntiles = 2;
+      fill_kb(gate, DHp, 2 * d.H);
+      gate.Bw = Bp(Ly.Wf_ru[l]);
+      gate.bias = params + P.bru[l];
+      if (l == 0)
+        gate.Dx = Dx + t * RF, gate.dx_mstride = int64_t(T) * RF, gate.F = d.F, gate.C_in = C,
+        gate.M = d.M, gate.Wx = params + P.Wru[l];
+      gate.Hprev = Hp32;
+      gate.out_r = r, gate.out_u = u, gate.out_rH = DrHt;
+      CU(launch_tc_fwd(gate, ss));
+      CU(diffuse_fwd(g, d, reinterpret_cast<float *>(DrHt), RH, 1, 0, int64_t(d.B) * d.H, ss, 1));
+
+      TcFwd cand{};
+      cand.R = int(R), cand.H = d.H, cand.Nout = d.H, cand.mode = kEpiCand, cand.ntiles = 1;
+      fill_kb(cand, t > 0 ? DrHt : nullptr, d.H);
+      cand.Bw = Bp(Ly.Wf_c[l]);
+      cand.bias = params + P.bc[l];
+      if (l == 0)
+        cand.Dx = Dx + t * RF, cand.dx_mstride = int64_t(T) * RF, cand.F = d.F, cand.C_in = C,
+        cand.M = d.M, cand.Wx = params + P.Wc[l];
+      cand.Hprev = Hp32, cand.u_in = u, cand.out_c = c;
+      cand.out_H = Fp(Ly.H32[l]) + t * RH, cand.out_Hb = DHt;
+      if (l == L - 1 && t >= T - d.T_out) {
+        cand.Wout = params + P.Wout, cand.bout = params + P.bout, cand.F_out = d.F_out;
+        cand.yhat = Fp(Ly.yhat) + int64_t(t - (T - d.T_out)) * R * d.F_out;
+      }
+      CU(launch_tc_fwd(cand, ss));
+      if (!(l == L - 1 && t == T - 1))
+        CU(diffuse_fwd(g, d, reinterpret_cast<float *>(DHt), RH, 1, 0, int64_t(d.B) * d.H, ss, 1));
+      if (l + 1 < L) CU(record(sp, ss, &fdone[l][t]));
+    }
+  }
+  cudaStream_t top = st[L - 1];
+  CU(launch_loss(Fp(Ly.yhat), y, d.T_out, d.N, d.B, d.F, d.F_out, d.ld, Fp(Ly.dyhat),
+                 reinterpret_cast<double *>(ws + Ly.lossp), loss_dev, err, top));
+
+  // ------------------------------------------------------------------ backward (BPTT)
+  // dZ = sum_m Q_m W_m^T, Q_0 = gradient itself (map A0), Q_{m>0} = (P^m)^T grad (map A1)
+  auto bwd_gemm = [&](int l, const bf16 *grad, int NG, const bf16 *Wd, bf16 *Q, bool need_in,
+                      bool need_h, float *dst_in, int acc_in, float *dst_h, int acc_h,
+                      cudaStream_t ss) -> pgti_status {
+    const int vseg = l == 0 ? 64 : 2 * d.H;
+    TcFwd b{};
+    b.R = int(R), b.H = d.H, b.Nout = NG, b.mode = kEpiBwd;
+    b.A0 = grad, b.A1 = Q, b.CA = NG, b.M0 = 1, b.M1 = d.M;
+    b.Bw = Wd, b.bX = NG, b.bY = vrows(d, l), b.bZ = 1;
+    b.nkb = 0;
+    for (int m = 0; m < d.M; ++m)
+      for (int jb = 0; jb < NG / 64; ++jb) {
+        b.kb_as[b.nkb] = m > 0, b.kb_am[b.nkb] = m, b.kb_ac[b.nkb] = jb * 64;
+        b.kb_bx[b.nkb] = jb * 64, b.kb_by[b.nkb] = m * vseg, b.kb_bz[b.nkb] = 0, ++b.nkb;
+      }
+    // column tiles: l > 0 -> [input (64), hidden (64)]; l = 0 -> [hidden]
+    int nt = 0;
+    if (need_in) b.dst[nt] = dst_in, b.dst_acc[nt] = acc_in, ++nt;
+    if (need_h) b.dst[nt] = dst_h, b.dst_acc[nt] = acc_h, ++nt;
+    if (nt == 0) return PGTI_OK;
+    if (l > 0 && !need_in)  // skip the input tile: shift B rows by one 64-column tile
+      for (int k = 0; k < b.nkb; ++k) b.kb_by[k] += 64;
+    b.ntiles = nt;
+    CU(launch_tc_fwd(b, ss));
+    return PGTI_OK;
+  };
+  std::vector<std::vector<cudaEvent_t>> bdone(L, std::vector<cudaEvent_t>(T));
+  auto rec_buf = [&](int l, int t) { return Fp((t & 1) ? Ly.dHrec1[l] : Ly.dHrec0[l]); };
+  auto up_buf = [&](int l, int t) { return Fp((t & 1) ? Ly.dHup1[l] : Ly.dHup0[l]); };
+  for (int t = T - 1; t >= 0; --t) {
+    for (int l = L - 1; l >= 0; --l) {
+      cudaStream_t ss = st[l];
+      // d(H^l_t) from above is ready; the parity buffer this step writes (for layer l-1) was
+      // last read by (l-1, t+2)
+      if (l + 1 < L) CU(cudaStreamWaitEvent(ss, bdone[l + 1][t], 0));
+      if (l > 0 && t + 2 < T) CU(cudaStreamWaitEvent(ss, bdone[l - 1][t + 2], 0));
+      const bool need_in = l > 0, need_h = t > 0;
+      const float *Hprev = t > 0 ? Fp(Ly.H32[l]) + (t - 1) * RH : nullptr;
+      const float *r = Fp(Ly.Rg[l]) + t * RH, *u = Fp(Ly.Ug[l]) + t * RH, *c = Fp(Ly.Cg[l]) + t * RH;
+      float *dC = Fp(Ly.dC[l]) + t * RH, *dG = Fp(Ly.dG[l]) + t * 2 * RH;
+      bf16 *dCb = Bp(Ly.dCb[l]) + t * RH, *dGb = Bp(Ly.dGb[l]) + t * 2 * RH;
+      const float *dy = (l == L - 1 && t >= T - d.T_out)
+                            ? Fp(Ly.dyhat) + int64_t(t - (T - d.T_out)) * R * d.F_out
+                            : nullptr;
+      const float *dH_rec = t + 1 < T ? rec_buf(l, t) : nullptr;   // from (l, t+1)
+      const float *dH_up = l + 1 < L ? up_buf(l, t) : nullptr;     // from (l+1, t)
+      float *dH_prev = need_h ? rec_buf(l, t - 1) : nullptr;       // to (l, t-1)
+      float *dIn = need_in ? up_buf(l - 1, t) : nullptr;           // to (l-1, t)
+      float *dU = Fp(Ly.dU[l]), *drH = Fp(Ly.drH[l]);
+      bf16 *Q = Bp(Ly.Q[l]);
+      CU(launch_cand_bwd(RH, d.H, dH_rec, dH_up, dy, params + P.Wout, d.F_out, u, c, Hprev, dU, dC,
+                         dH_prev, ss, dCb));
+      if (need_in || need_h) {
+        CU(diffuse_fwd(g, d, reinterpret_cast<float *>(Q), RH, 1, 0, int64_t(d.B) * d.H, ss, 1, 1,
+                       dCb));
+        PGTI_STATUS_TRY(bwd_gemm(l, dCb, d.H, Bp(Ly.Wd_c[l]), Q, need_in, need_h, dIn, 0, drH, 0,
+                                 ss));
+      }
+      CU(launch_gate_bwd(RH, d.H, need_h ? drH : nullptr, Hprev, r, u, dU, dH_prev, dG, ss, dGb));
+      if (need_in || need_h) {
+        CU(diffuse_fwd(g, d, reinterpret_cast<float *>(Q), 2 * RH, 1, 0, int64_t(d.B) * 2 * d.H,
+                       ss, 1, 1, dGb));
+        PGTI_STATUS_TRY(bwd_gemm(l, dGb, 2 * d.H, Bp(Ly.Wd_ru[l]), Q, need_in, need_h, dIn, 1,
+                                 dH_prev, 1, ss));
+      }
+      CU(record(sp, ss, &bdone[l][t]));
+    }
+  }
+
+  // ------------------------------------------------------------------ weight gradients
+  for (int l = 0; l < L; ++l) {
+    cudaStream_t ss = st[l];  // layer l's backward is complete in stream order
+    const int Fin = l == 0 ? d.F : d.H, C = Fin + d.H;
+    const int V = vrows(d, l), vseg = l == 0 ? 64 : 2 * d.H, coff = l == 0 ? d.F : 0;
+    const bf16 *Ain = l == 0 ? nullptr : Bp(Ly.DHb[l - 1]);
+    float *wpart = Fp(Ly.wpart[l]);
+    TcWgrad tw{Ain, Bp(Ly.DHb[l]), -1, T, d.M, int(R), Bp(Ly.dGb[l]), 2 * d.H,
+               V, vseg, coff, C, wpart, int64_t(Ly.wpart_floats), grads + P.Wru[l]};
+    CU(launch_tc_wgrad(tw, ss));
+    tw.A_h = Bp(Ly.DrHb[l]), tw.h_toff = 0, tw.G = Bp(Ly.dCb[l]), tw.Nout = d.H;
+    tw.out = grads + P.Wc[l];
+    CU(launch_tc_wgrad(tw, ss));
+    // input rows of layer 0 (fp32 x part) and the bias rows: skinny reduction over T*R rows
+    SmallWgrad sw{};
+    sw.mode = kSmallBiasX, sw.T = T, sw.R = int(R);
+    if (l == 0) sw.Dx = Dx, sw.dx_mstride = int64_t(T) * RF, sw.dx_tstride = RF;
+    sw.M = d.M, sw.F = d.F, sw.C_in = C;
+    sw.partial = wpart, sw.partial_cap = int64_t(Ly.wpart_floats);
+    sw.G = Fp(Ly.dG[l]), sw.g_tstride = 2 * RH, sw.NG = 2 * d.H, sw.out = grads + P.Wru[l];
+    CU(launch_small_wgrad(sw, ss));
+    sw.G = Fp(Ly.dC[l]), sw.g_tstride = RH, sw.NG = d.H, sw.out = grads + P.Wc[l];
+    CU(launch_small_wgrad(sw, ss));
+  }
+  SmallWgrad rw{};
+  rw.mode = kSmallReadout, rw.T = d.T_out, rw.R = int(R);
+  rw.dy = Fp(Ly.dyhat), rw.F_out = d.F_out;
+  rw.G = Fp(Ly.H32[L - 1]) + int64_t(T - d.T_out) * RH, rw.g_tstride = RH, rw.NG = d.H;
+  rw.partial = Fp(Ly.wpart[L - 1]), rw.partial_cap = int64_t(Ly.wpart_floats);
+  rw.out = grads + P.Wout;
+  CU(launch_small_wgrad(rw, top));
+  for (int l = 1; l < L; ++l) CU(depend(sp, st[l], s));  // join
+
+  if (act_dump) {
+    for (int t = 0; t < T; ++t)
+      for (int l = 0; l < L; ++l) {
+        float *dst = act_dump + (int64_t(t) * L + l) * 4 * RH;
+        const float *src[4] = {Fp(Ly.H32[l]) + t * RH, Fp(Ly.Rg[l]) + t * RH,
+                               Fp(Ly.Ug[l]) + t * RH, Fp(Ly.Cg[l]) + t * RH};
+        for (int q = 0; q < 4; ++q)
+          CU(cudaMemcpyAsync(dst + q * RH, src[q], size_t(RH) * 4, cudaMemcpyDeviceToDevice, s));
+      }
+    CU(cudaMemcpyAsync(act_dump + int64_t(T) * L * 4 * RH, Fp(Ly.yhat),
+                       size_t(d.T_out) * R * d.F_out * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  return PGTI_OK;
+}
+
+}  // namespace detail
+}  // namespace pgti

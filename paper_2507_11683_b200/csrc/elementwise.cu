@@ -76,6 +76,7 @@ __global__ void k_loss_final(const double *__restrict__ partials, int n, int64_t
 //   dH' = dHcur (+ dyhat W_out^T);  dU = dH' (H - c);  dCpre = dH' (1-u)(1-c^2);  dHprev = dH' u
 // (dCb: optional bf16 copy of dCpre -- the tensor-core dgrad / wgrad operand)
 __global__ void k_cand_bwd(int64_t RH, int H, const float *__restrict__ dHcur,
+                           const float *__restrict__ dHcur2,
                            const float *__restrict__ dy, const float *__restrict__ Wout, int F_out,
                            const float *__restrict__ u, const float *__restrict__ c,
                            const float *__restrict__ Hprev, float *__restrict__ dU,
@@ -83,7 +84,8 @@ __global__ void k_cand_bwd(int64_t RH, int H, const float *__restrict__ dHcur,
                            __nv_bfloat16 *__restrict__ dCb) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < RH;
        i += int64_t(gridDim.x) * blockDim.x) {
-    float dh = dHcur[i];
+    float dh = dHcur ? dHcur[i] : 0.f;
+    if (dHcur2) dh += dHcur2[i];
     if (dy) {
       const int64_t row = i / H;
       const int j = int(i - row * H);
@@ -181,15 +183,16 @@ cudaError_t launch_loss(const float *yhat, const float *y, int T_out, int N, int
   return cudaGetLastError();
 }
 
-cudaError_t launch_cand_bwd(int64_t RH, int H, const float *dHcur, const float *dy,
-                            const float *Wout, int F_out, const float *u, const float *c,
-                            const float *Hprev, float *dU, float *dC, float *dHprev_out,
-                            cudaStream_t s, void *dC_bf16) {
+cudaError_t launch_cand_bwd(int64_t RH, int H, const float *dHcur, const float *dHcur2,
+                            const float *dy, const float *Wout, int F_out, const float *u,
+                            const float *c, const float *Hprev, float *dU, float *dC,
+                            float *dHprev_out, cudaStream_t s, void *dC_bf16) {
   ProfScope prof(kProfElementwise, s,
-                 double(RH) * (4.0 * (3 + (Hprev ? 1 : 0) + 2 + (dHprev_out ? 1 : 0)) +
+                 double(RH) * (4.0 * ((dHcur ? 1 : 0) + (dHcur2 ? 1 : 0) + 2 + (Hprev ? 1 : 0) +
+                                      2 + (dHprev_out ? 1 : 0)) +
                                (dC_bf16 ? 2.0 : 0.0)), 0.0);
-  k_cand_bwd<<<grid_for(RH), kT, 0, s>>>(RH, H, dHcur, dy, Wout, F_out, u, c, Hprev, dU, dC,
-                                         dHprev_out, static_cast<__nv_bfloat16 *>(dC_bf16));
+  k_cand_bwd<<<grid_for(RH), kT, 0, s>>>(RH, H, dHcur, dHcur2, dy, Wout, F_out, u, c, Hprev, dU,
+                                         dC, dHprev_out, static_cast<__nv_bfloat16 *>(dC_bf16));
   return cudaGetLastError();
 }
 

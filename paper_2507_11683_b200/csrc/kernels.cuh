@@ -146,7 +146,9 @@ cudaError_t launch_loss(const float *yhat, const float *y, int T_out, int N, int
                         int F_out, int64_t ld, float *dyhat, double *partials, float *loss,
                         unsigned *err, cudaStream_t s);
 constexpr int kLossBlocks = 296;
-cudaError_t launch_cand_bwd(int64_t RH, int H, const float *dHcur, const float *dy,
+// dH' = dHcur (+ dHcur2 if non-null) (+ dyhat W_out^T if dy non-null); dHcur nullable (= 0)
+cudaError_t launch_cand_bwd(int64_t RH, int H, const float *dHcur, const float *dHcur2,
+                            const float *dy,
                             const float *Wout, int F_out, const float *u, const float *c,
                             const float *Hprev, float *dU, float *dC, float *dHprev_out,
                             cudaStream_t s, void *dC_bf16 = nullptr);

@@ -72,11 +72,17 @@ __global__ void __launch_bounds__(kThr) k_small_wgrad(const __grid_constant__ Sm
       p.partial[(int64_t(chunk) * q.ns + s) * q.ngt + j] = red[0][s][j] + red[1][s][j];
 }
 
+// One warp per output: lane l sums chunks l, l+32, ... (fixed order), then a fixed xor-tree.
 __global__ void k_small_reduce(const __grid_constant__ SmallWgrad p, Plan q) {
   const int n = q.ns * q.ngt;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+       i += (gridDim.x * blockDim.x) >> 5) {
     float sum = 0.f;
-    for (int c = 0; c < q.nchunks; ++c) sum += p.partial[int64_t(c) * n + i];
+    for (int c = lane; c < q.nchunks; c += 32) sum += p.partial[int64_t(c) * n + i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane) continue;
     const int s = i / q.ngt, j = i % q.ngt;
     if (p.mode == kSmallBiasX) {
       const int row = s == q.ns - 1 ? p.M * p.C_in : (s / p.F) * p.C_in + s % p.F;
@@ -109,7 +115,7 @@ cudaError_t launch_small_wgrad(const SmallWgrad &p, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   ProfScope prof(kProfReduce, s, 4.0 * double(q.nchunks + 1) * q.ns * q.ngt,
                  double(q.nchunks) * q.ns * q.ngt);
-  k_small_reduce<<<unsigned(ceil_div(q.ns * q.ngt, 256)), 256, 0, s>>>(p, q);
+  k_small_reduce<<<unsigned(ceil_div(q.ns * q.ngt, 8)), 256, 0, s>>>(p, q);
   return cudaGetLastError();
 }
 

@@ -71,7 +71,7 @@ __device__ __forceinline__ void epi_bar() {
   asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
 }
 
-__global__ void __launch_bounds__(kFwdThreads, 1)
+__global__ void __launch_bounds__(kFwdThreads, 2)
     k_tc_fwd(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
              const __grid_constant__ CUtensorMap mB, const __grid_constant__ TcFwd p) {
   constexpr int A_BYTES = kBM * kBK * 2, B_BYTES = 64 * kBK * 2, STAGE = A_BYTES + B_BYTES;
@@ -188,7 +188,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) acc[i] = 0.f;
       }
-      __align__(16) bf16 hb[32];
       if (p.mode == kEpiGate) {
         float *out = ct == 0 ? p.out_r : p.out_u;
 #pragma unroll
@@ -200,25 +199,31 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                 make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
           if (ct == 0) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) hb[i] = __float2bfloat16_rn(acc[i] * hp[i]);
+            for (int i = 0; i < 32; ++i) hp[i] *= acc[i];
 #pragma unroll
             for (int i = 0; i < 32; i += 8)
-              *reinterpret_cast<uint4 *>(p.out_rH + ro + i) = *reinterpret_cast<const uint4 *>(hb + i);
+              *reinterpret_cast<uint4 *>(p.out_rH + ro + i) = pack8_bf16(hp + i);
           }
         }
       } else {
-        float ys[4] = {0.f, 0.f, 0.f, 0.f};
+        float ys0 = 0.f, ys1 = 0.f, ys2 = 0.f, ys3 = 0.f;
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           const float c = tanhf(acc[i] + pre[i]);
           acc[i] = c;
           pre[i] = uu[i] * hp[i] + (1.0f - uu[i]) * c;  // H_t
-          hb[i] = __float2bfloat16_rn(pre[i]);
         }
-        if (p.yhat)
-          for (int o = 0; o < p.F_out; ++o)
+        if (p.yhat) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) ys[o] = fmaf(pre[i], __ldg(p.Wout + (jh + i) * p.F_out + o), ys[o]);
+          for (int i = 0; i < 32; ++i) {
+            const float *w = p.Wout + (jh + i) * p.F_out;
+            ys0 = fmaf(pre[i], __ldg(w), ys0);
+            if (p.F_out > 1) ys1 = fmaf(pre[i], __ldg(w + 1), ys1);
+            if (p.F_out > 2) ys2 = fmaf(pre[i], __ldg(w + 2), ys2);
+            if (p.F_out > 3) ys3 = fmaf(pre[i], __ldg(w + 3), ys3);
+          }
+        }
+        const float ys[4] = {ys0, ys1, ys2, ys3};
         if (valid) {
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
@@ -227,15 +232,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           }
 #pragma unroll
           for (int i = 0; i < 32; i += 8)
-            *reinterpret_cast<uint4 *>(p.out_Hb + ro + i) = *reinterpret_cast<const uint4 *>(hb + i);
+            *reinterpret_cast<uint4 *>(p.out_Hb + ro + i) = pack8_bf16(pre + i);
         }
         if (p.yhat) {
-          if (hh == 1)
-            for (int o = 0; o < p.F_out; ++o) y_s[r * 4 + o] = ys[o];
+          if (hh == 1) {
+#pragma unroll
+            for (int o = 0; o < 4; ++o) y_s[r * 4 + o] = ys[o];
+          }
           epi_bar();
-          if (hh == 0 && valid)
-            for (int o = 0; o < p.F_out; ++o)
-              p.yhat[int64_t(row) * p.F_out + o] = (ys[o] + y_s[r * 4 + o]) + __ldg(p.bout + o);
+          if (hh == 0 && valid) {
+#pragma unroll
+            for (int o = 0; o < 4; ++o)
+              if (o < p.F_out)
+                p.yhat[int64_t(row) * p.F_out + o] = (ys[o] + y_s[r * 4 + o]) + __ldg(p.bout + o);
+          }
         }
       }
     }

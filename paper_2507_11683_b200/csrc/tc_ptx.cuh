@@ -145,5 +145,20 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool 
 
 __device__ __forceinline__ float sigmoid_f(float a) { return 1.0f / (1.0f + __expf(-a)); }
 
+// 8 floats -> 8 bf16 (round to nearest) packed in 16 bytes, register-only.
+__device__ __forceinline__ uint4 pack8_bf16(const float *v) {
+  uint4 r;
+  __nv_bfloat162 h;
+  h = __floats2bfloat162_rn(v[0], v[1]);
+  r.x = *reinterpret_cast<uint32_t *>(&h);
+  h = __floats2bfloat162_rn(v[2], v[3]);
+  r.y = *reinterpret_cast<uint32_t *>(&h);
+  h = __floats2bfloat162_rn(v[4], v[5]);
+  r.z = *reinterpret_cast<uint32_t *>(&h);
+  h = __floats2bfloat162_rn(v[6], v[7]);
+  r.w = *reinterpret_cast<uint32_t *>(&h);
+  return r;
+}
+
 }  // namespace tc
 }  // namespace pgti
