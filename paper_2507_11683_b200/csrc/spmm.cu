@@ -1,10 +1,12 @@
 // K2: CSR SpMM for the diffusion convolution (Li et al. Eq. 2 [ext]).
 // Dense operand layout [G][N][W]: node-major, every node's W = B*C values contiguous, so one
-// CSR row of the transition matrix multiplies whole warp-wide slices.
-// One warp per (row, run of CPW column chunks): the row's (col, val) pairs are loaded once
-// (lane e holds entry e), broadcast with shuffles, and reused for every chunk of the run;
-// neighbour slices are read with 128-bit loads (4 fp32 or 8 bf16 per lane), 4 in flight, and
-// accumulated in fp32 with packed FFMA2 (sm_100) in CSR order (deterministic).
+// CSR row of the transition matrix multiplies whole contiguous slices.
+// One thread per (row, 16-byte column vector: 4 fp32 or 8 bf16): the row's CSR entries are read
+// through the read-only path (all threads of a row hit the same lines -> L1 broadcast), each
+// neighbour slice is one 128-bit load, accumulation is fp32 with packed FFMA2 (sm_100) in CSR
+// order (deterministic).  Consecutive threads cover consecutive columns of one row, so every
+// neighbour read of a warp is a contiguous 512-byte segment.  (A warp-per-row design that
+// broadcast the CSR with shuffles measured 1.3-2.3x slower: tests/cuda/spmm_microbench.cu.)
 // Element type per launch: fp32 (parity path, backward adjoint) or bf16 (tensor-core path's
 // diffusion blocks, which are the GEMM A operands).
 #include <cuda_bf16.h>
@@ -17,37 +19,27 @@ namespace {
 
 struct SpmmParams {
   SpmmJob job[kMaxSpmmJobs];
-  int warp_begin[kMaxSpmmJobs + 1];
-  int runs[kMaxSpmmJobs];   // runs (of CPW chunks) per row
-  int chunks[kMaxSpmmJobs];
+  int thread_begin[kMaxSpmmJobs + 1];
+  int vecs[kMaxSpmmJobs];  // 16-byte vectors per row
   int njobs;
   int N;
 };
-
-constexpr int kCPW = 1;   // chunks per warp run
-constexpr int kGrp = 4;   // neighbour loads in flight per lane
 
 template <typename T>
 struct Lane;
 template <>
 struct Lane<float> {
   static constexpr int V = 4;
-  using Raw = float4;
-  static __device__ __forceinline__ Raw ld_raw(const float *p) {
-    return __ldg(reinterpret_cast<const float4 *>(p));
-  }
-  static __device__ __forceinline__ void fma_raw(float2 *acc, float w, const Raw &a) {
+  static __device__ __forceinline__ void fma(float2 *acc, float w, const float *p) {
+    const float4 a = __ldg(reinterpret_cast<const float4 *>(p));
     const float2 ww = make_float2(w, w);
     acc[0] = __ffma2_rn(ww, make_float2(a.x, a.y), acc[0]);
     acc[1] = __ffma2_rn(ww, make_float2(a.z, a.w), acc[1]);
   }
-  static __device__ __forceinline__ void load(const float *p, float2 *v) {
-    const float4 a = __ldg(reinterpret_cast<const float4 *>(p));
-    v[0] = make_float2(a.x, a.y), v[1] = make_float2(a.z, a.w);
-  }
-  static __device__ __forceinline__ void load_plain(const float *p, float2 *v) {
+  static __device__ __forceinline__ void add(float2 *acc, const float *p) {
     const float4 a = *reinterpret_cast<const float4 *>(p);
-    v[0] = make_float2(a.x, a.y), v[1] = make_float2(a.z, a.w);
+    acc[0] = __fadd2_rn(acc[0], make_float2(a.x, a.y));
+    acc[1] = __fadd2_rn(acc[1], make_float2(a.z, a.w));
   }
   static __device__ __forceinline__ void store(float *p, const float2 *v) {
     *reinterpret_cast<float4 *>(p) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
@@ -59,24 +51,20 @@ struct Lane<__nv_bfloat16> {
   static __device__ __forceinline__ float2 unpack(uint32_t w) {
     return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
   }
-  using Raw = uint4;
-  static __device__ __forceinline__ Raw ld_raw(const __nv_bfloat16 *p) {
-    return __ldg(reinterpret_cast<const uint4 *>(p));
-  }
-  static __device__ __forceinline__ void fma_raw(float2 *acc, float w, const Raw &a) {
+  static __device__ __forceinline__ void fma(float2 *acc, float w, const __nv_bfloat16 *p) {
+    const uint4 a = __ldg(reinterpret_cast<const uint4 *>(p));
     const float2 ww = make_float2(w, w);
     acc[0] = __ffma2_rn(ww, unpack(a.x), acc[0]);
     acc[1] = __ffma2_rn(ww, unpack(a.y), acc[1]);
     acc[2] = __ffma2_rn(ww, unpack(a.z), acc[2]);
     acc[3] = __ffma2_rn(ww, unpack(a.w), acc[3]);
   }
-  static __device__ __forceinline__ void load(const __nv_bfloat16 *p, float2 *v) {
-    const uint4 a = __ldg(reinterpret_cast<const uint4 *>(p));
-    v[0] = unpack(a.x), v[1] = unpack(a.y), v[2] = unpack(a.z), v[3] = unpack(a.w);
-  }
-  static __device__ __forceinline__ void load_plain(const __nv_bfloat16 *p, float2 *v) {
+  static __device__ __forceinline__ void add(float2 *acc, const __nv_bfloat16 *p) {
     const uint4 a = *reinterpret_cast<const uint4 *>(p);
-    v[0] = unpack(a.x), v[1] = unpack(a.y), v[2] = unpack(a.z), v[3] = unpack(a.w);
+    acc[0] = __fadd2_rn(acc[0], unpack(a.x));
+    acc[1] = __fadd2_rn(acc[1], unpack(a.y));
+    acc[2] = __fadd2_rn(acc[2], unpack(a.z));
+    acc[3] = __fadd2_rn(acc[3], unpack(a.w));
   }
   static __device__ __forceinline__ void store(__nv_bfloat16 *p, const float2 *v) {
     uint4 a;
@@ -90,103 +78,75 @@ struct Lane<__nv_bfloat16> {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(256, 4) k_spmm(const __grid_constant__ SpmmParams p) {
+__global__ void __launch_bounds__(256) k_spmm(const __grid_constant__ SpmmParams p) {
   using L = Lane<T>;
   constexpr int V = L::V, P = V / 2;
-  const int wid = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const int lane = threadIdx.x & 31;
-  if (wid >= p.warp_begin[p.njobs]) return;
+  const int tid = int(blockIdx.x * blockDim.x + threadIdx.x);
+  if (tid >= p.thread_begin[p.njobs]) return;
   int j = 0;
 #pragma unroll
   for (int q = 1; q < kMaxSpmmJobs; ++q)
-    if (q < p.njobs && wid >= p.warp_begin[q]) j = q;
+    if (q < p.njobs && tid >= p.thread_begin[q]) j = q;
   const SpmmJob &jb = p.job[j];
-  const int runs = p.runs[j], chunks = p.chunks[j];
-  int rem = wid - p.warp_begin[j];
-  const int per_group = p.N * runs;
+  const int vecs = p.vecs[j];
+  int rem = tid - p.thread_begin[j];
+  const int per_group = p.N * vecs;
   const int g = rem / per_group;
   rem -= g * per_group;
-  const int n = rem / runs;
-  const int run = rem - n * runs;
+  const int n = rem / vecs;
+  const int col0 = (rem - n * vecs) * V;
   const int W = int(jb.W);
-  const int64_t orow = int64_t(g) * jb.gstride + int64_t(n) * W;
-  for (int c = run * kCPW; c < min(chunks, run * kCPW + kCPW); ++c) {
-    const int col0 = c * 32 * V + lane * V;
-    const bool active = col0 < W;
-    float2 acc[P];
+  const int64_t goff = int64_t(g) * jb.gstride;
+
+  float2 acc[P];
 #pragma unroll
-    for (int i = 0; i < P; ++i) acc[i] = make_float2(0.f, 0.f);
-    for (int t = 0; t < jb.nterms; ++t) {
-      const T *base = reinterpret_cast<const T *>(jb.X[t]) + int64_t(g) * jb.gstride + col0;
-      const int beg = __ldg(jb.rowptr[t] + n), cnt = __ldg(jb.rowptr[t] + n + 1) - beg;
-      for (int e0 = 0; e0 < cnt; e0 += 32) {
-        // lane e holds CSR entry e0 + e of the row; broadcast with shuffles
-        const int ce = min(32, cnt - e0);
-        int cc = 0;
-        float vv = 0.f;
-        if (lane < ce) cc = __ldg(jb.col[t] + beg + e0 + lane), vv = __ldg(jb.val[t] + beg + e0 + lane);
-        // all (up to kGrp) neighbour slices of the group in flight before any FMA
-        for (int e = 0; e < ce; e += kGrp) {
-          typename L::Raw xr[kGrp];
-          float w[kGrp];
-#pragma unroll
-          for (int u = 0; u < kGrp; ++u) {
-            const int col = __shfl_sync(0xffffffffu, cc, (e + u) & 31);
-            w[u] = __shfl_sync(0xffffffffu, vv, (e + u) & 31);
-            if (active && e + u < ce) xr[u] = L::ld_raw(base + col * W);
-          }
-          if (active) {
-#pragma unroll
-            for (int u = 0; u < kGrp; ++u)
-              if (e + u < ce) L::fma_raw(acc, w[u], xr[u]);
-          }
-        }
-      }
+  for (int i = 0; i < P; ++i) acc[i] = make_float2(0.f, 0.f);
+  for (int t = 0; t < jb.nterms; ++t) {
+    const T *X = reinterpret_cast<const T *>(jb.X[t]) + goff + col0;
+    const int beg = __ldg(jb.rowptr[t] + n), end = __ldg(jb.rowptr[t] + n + 1);
+    int e = beg;
+    for (; e + 4 <= end; e += 4) {  // 4 independent neighbour loads in flight
+      const int c0 = __ldg(jb.col[t] + e), c1 = __ldg(jb.col[t] + e + 1);
+      const int c2 = __ldg(jb.col[t] + e + 2), c3 = __ldg(jb.col[t] + e + 3);
+      const float w0 = __ldg(jb.val[t] + e), w1 = __ldg(jb.val[t] + e + 1);
+      const float w2 = __ldg(jb.val[t] + e + 2), w3 = __ldg(jb.val[t] + e + 3);
+      L::fma(acc, w0, X + c0 * W);
+      L::fma(acc, w1, X + c1 * W);
+      L::fma(acc, w2, X + c2 * W);
+      L::fma(acc, w3, X + c3 * W);
     }
-    if (!active) continue;
-    float2 tmp[P];
-    if (jb.add) {
-      L::load_plain(reinterpret_cast<const T *>(jb.add) + orow + col0, tmp);
-#pragma unroll
-      for (int i = 0; i < P; ++i) acc[i] = __fadd2_rn(acc[i], tmp[i]);
-    }
-    T *Y = reinterpret_cast<T *>(jb.Y) + orow + col0;
-    if (jb.accumulate) {
-      L::load_plain(Y, tmp);
-#pragma unroll
-      for (int i = 0; i < P; ++i) acc[i] = __fadd2_rn(acc[i], tmp[i]);
-    }
-    L::store(Y, acc);
+    for (; e < end; ++e) L::fma(acc, __ldg(jb.val[t] + e), X + __ldg(jb.col[t] + e) * W);
   }
+  const int64_t o = goff + int64_t(n) * W + col0;
+  if (jb.add) L::add(acc, reinterpret_cast<const T *>(jb.add) + o);
+  T *Y = reinterpret_cast<T *>(jb.Y) + o;
+  if (jb.accumulate) L::add(acc, Y);
+  L::store(Y, acc);
 }
 
 // Scalar fp32 fallback for widths that are not a multiple of 4 (test shapes only).
 __global__ void __launch_bounds__(256) k_spmm_scalar(const __grid_constant__ SpmmParams p) {
-  const int wid = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const int lane = threadIdx.x & 31;
-  if (wid >= p.warp_begin[p.njobs]) return;
+  const int tid = int(blockIdx.x * blockDim.x + threadIdx.x);
+  if (tid >= p.thread_begin[p.njobs]) return;
   int j = 0;
   for (int q = 1; q < p.njobs; ++q)
-    if (wid >= p.warp_begin[q]) j = q;
+    if (tid >= p.thread_begin[q]) j = q;
   const SpmmJob &jb = p.job[j];
-  const int runs = p.runs[j];
-  int rem = wid - p.warp_begin[j];
-  const int g = rem / (p.N * runs);
-  rem -= g * p.N * runs;
-  const int n = rem / runs, run = rem - (rem / runs) * runs;
   const int W = int(jb.W);
-  const int64_t orow = int64_t(g) * jb.gstride + int64_t(n) * W;
-  for (int col = run * 32 + lane; col < W; col += runs * 32) {
-    float acc = 0.f;
-    for (int t = 0; t < jb.nterms; ++t) {
-      const float *X = jb.X[t] + int64_t(g) * jb.gstride;
-      for (int e = jb.rowptr[t][n]; e < jb.rowptr[t][n + 1]; ++e)
-        acc = fmaf(jb.val[t][e], X[int64_t(jb.col[t][e]) * W + col], acc);
-    }
-    if (jb.add) acc += jb.add[orow + col];
-    if (jb.accumulate) acc += jb.Y[orow + col];
-    jb.Y[orow + col] = acc;
+  int rem = tid - p.thread_begin[j];
+  const int g = rem / (p.N * W);
+  rem -= g * p.N * W;
+  const int n = rem / W, col = rem - n * W;
+  const int64_t goff = int64_t(g) * jb.gstride, o = goff + int64_t(n) * W + col;
+  float acc = 0.f;
+  for (int t = 0; t < jb.nterms; ++t) {
+    const float *X = jb.X[t] + goff;
+    for (int e = jb.rowptr[t][n]; e < jb.rowptr[t][n + 1]; ++e)
+      acc = fmaf(jb.val[t][e], X[int64_t(jb.col[t][e]) * W + col], acc);
   }
+  if (jb.add) acc += jb.add[o];
+  if (jb.accumulate) acc += jb.Y[o];
+  jb.Y[o] = acc;
 }
 
 }  // namespace
@@ -206,22 +166,20 @@ cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s) {
           (j.nterms < 1 || al(j.X[0])) && (j.nterms < 2 || al(j.X[1]));
   }
   if (bf && !vec) return cudaErrorInvalidValue;  // bf16 path needs 16-byte lanes
-  const int vw = bf ? 256 : 128;
+  const int V = bf ? 8 : (vec ? 4 : 1);
   SpmmParams p{};
-  int64_t w = 0;
+  int64_t th = 0;
   for (int i = 0; i < njobs; ++i) {
     p.job[i] = jobs[i];
-    if (p.job[i].nterms < 2) p.job[i].X[1] = p.job[i].X[0];
-    p.chunks[i] = int(ceil_div(jobs[i].W, vw));
-    p.runs[i] = vec ? int(ceil_div(p.chunks[i], kCPW)) : 1;
-    p.warp_begin[i] = int(w);
-    w += int64_t(jobs[i].G) * N * p.runs[i];
+    p.vecs[i] = int(jobs[i].W / V);
+    p.thread_begin[i] = int(th);
+    th += int64_t(jobs[i].G) * N * p.vecs[i];
   }
-  if (w >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
-  p.warp_begin[njobs] = int(w);
+  if (th >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
+  p.thread_begin[njobs] = int(th);
   p.njobs = njobs;
   p.N = N;
-  if (w == 0) return cudaSuccess;
+  if (th == 0) return cudaSuccess;
   // algorithmic bytes (SURVEY 8(d) K2 model): each dense operand row read once per term,
   // output written once, addend / accumulator read once, CSR (col, val, rowptr) once per group
   const double es = bf ? 2.0 : 4.0;
@@ -236,7 +194,7 @@ cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s) {
     }
   }
   ProfScope prof(kProfSpmm, s, bytes, flops);
-  const unsigned blocks = unsigned(ceil_div(w, 8));
+  const unsigned blocks = unsigned(ceil_div(th, 256));
   if (bf)
     k_spmm<__nv_bfloat16><<<blocks, 256, 0, s>>>(p);
   else if (vec)
