@@ -71,19 +71,23 @@ __device__ __forceinline__ void epi_bar() {
   asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
 }
 
-__global__ void __launch_bounds__(kFwdThreads, 2)
+// NSUB = 64-column sub-tiles per CTA: 1 (small R: more CTAs) or 2 (large R: A read once for
+// both the r and u halves of the gate / the input and hidden tiles of the backward GEMM).
+template <int NSUB>
+__global__ void __launch_bounds__(kFwdThreads, 3 - NSUB)
     k_tc_fwd(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
              const __grid_constant__ CUtensorMap mB, const __grid_constant__ TcFwd p) {
-  constexpr int A_BYTES = kBM * kBK * 2, B_BYTES = 64 * kBK * 2, STAGE = A_BYTES + B_BYTES;
+  constexpr int NT = 64 * NSUB;
+  constexpr int A_BYTES = kBM * kBK * 2, B_BYTES = NT * kBK * 2, STAGE = A_BYTES + B_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
   Barriers *bar = carve<A_BYTES, B_BYTES>(smem);
   float *wx_s = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(bar) + 256);  // [20][64]
   float *y_s = wx_s + 20 * 64;                                                       // [128][4]
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int row0 = blockIdx.x * kBM, ct = blockIdx.y;
+  const int row0 = blockIdx.x * kBM, ct0 = blockIdx.y * NSUB;
   if (threadIdx.x == 0) tma_prefetch(&mA0), tma_prefetch(&mA1), tma_prefetch(&mB);
-  setup(bar, 64);
+  setup(bar, NT);
   const uint32_t tmem = bar->tmem;
 
   if (warp == 0) {
@@ -94,13 +98,13 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
         mbar_expect_tx(&bar->full[s], STAGE);
         uint8_t *a = smem + s * STAGE;
         tma_load_3d(a, p.kb_as[kb] ? &mA1 : &mA0, &bar->full[s], p.kb_ac[kb], row0, p.kb_am[kb]);
-        tma_load_3d(a + A_BYTES, &mB, &bar->full[s], p.kb_bx[kb], p.kb_by[kb] + ct * 64,
+        tma_load_3d(a + A_BYTES, &mB, &bar->full[s], p.kb_bx[kb], p.kb_by[kb] + ct0 * 64,
                     p.kb_bz[kb]);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16(kBM, 64, false, false);
+      constexpr uint32_t idesc = idesc_bf16(kBM, NT, false, false);
       for (int kb = 0; kb < p.nkb; ++kb) {
         const int s = kb % kStages;
         mbar_wait(&bar->full[s], (kb / kStages) & 1);
@@ -119,7 +123,12 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
     const int r = q * 32 + lane, row = row0 + r;
     const bool valid = row < p.R;
     const int H = p.H;
-    const int jc = hh * 32;   // first tile column of this thread
+#pragma unroll 1
+    for (int sub = 0; sub < NSUB; ++sub) {
+    if (sub > 0) epi_bar();                  // sub-tile 0 finished with wx_s / y_s
+    const int ct = ct0 + sub;
+    const int jc = hh * 32;                  // first tile column of this thread
+    const uint32_t tsub = uint32_t(sub * 64);  // TMEM column of this sub-tile
     if (p.mode == kEpiBwd) {
       float *dst = p.dst[ct];
       const int64_t ro = int64_t(row) * 64 + jc;
@@ -133,7 +142,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       mbar_wait(&bar->tfull, 0);
       tc_fence_after();
       float acc[32];
-      const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + jc;
+      const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + tsub + jc;
       tmem_ld16(taddr, acc);
       tmem_ld16(taddr + 16, acc + 16);
       tmem_wait_ld();
@@ -180,7 +189,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       tc_fence_after();
       float acc[32];
       if (p.nkb) {
-        const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + jc;
+        const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + tsub + jc;
         tmem_ld16(taddr, acc);
         tmem_ld16(taddr + 16, acc + 16);
         tmem_wait_ld();
@@ -249,8 +258,9 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
         }
       }
     }
+    }  // sub-tiles
   }
-  teardown(bar, 64);
+  teardown(bar, NT);
 }
 
 // ================================================================== wgrad (MN-major A and B)
@@ -384,8 +394,8 @@ cudaError_t set_smem(K kernel, int bytes) {
 }
 
 constexpr int wg_smem_bytes(int b_rows) { return kStages * (kBM * kBK * 2 + b_rows * kBK * 2) + 1024 + 256; }
-constexpr int fwd_smem_bytes() {
-  return kStages * (kBM * kBK * 2 + 64 * kBK * 2) + 1024 + 256 + (20 * 64 + 128 * 4) * 4;
+constexpr int fwd_smem_bytes(int nsub) {
+  return kStages * (kBM * kBK * 2 + 64 * nsub * kBK * 2) + 1024 + 256 + (20 * 64 + 128 * 4) * 4;
 }
 
 }  // namespace
@@ -401,11 +411,15 @@ cudaError_t launch_tc_fwd(const TcFwd &p, cudaStream_t s) {
   const uint32_t bA[3] = {64, 128, 1};
   const uint64_t dB[3] = {uint64_t(p.bX), uint64_t(p.bY), uint64_t(p.bZ)},
                  sB[2] = {uint64_t(p.bX) * 2, uint64_t(p.bX) * p.bY * 2};
-  const uint32_t bB[3] = {64, 64, 1};
+  // two 64-column sub-tiles per CTA once there are enough row tiles to fill the GPU twice:
+  // A (the dominant operand) is then staged once for both halves
+  const int row_tiles = int(ceil_div(p.R, kBM));
+  const int nsub = (p.ntiles == 2 && row_tiles >= 2 * kNumSMs) ? 2 : 1;
+  const uint32_t bB[3] = {64, uint32_t(64 * nsub), 1};
   if (!make_map(&ma0, p.A0, 3, dA0, sA, bA) || !make_map(&ma1, p.A1, 3, dA1, sA, bA) ||
       !make_map(&mb, p.Bw, 3, dB, sB, bB))
     return cudaErrorInvalidValue;
-  const dim3 grid(unsigned(ceil_div(p.R, kBM)), unsigned(p.ntiles));
+  const dim3 grid(unsigned(row_tiles), unsigned(p.ntiles / nsub));
   const double N = 64.0 * p.ntiles;
   const double Kt = double(p.nkb) * 64 + (p.Dx ? p.F * p.M : 0);
   double io = p.mode == kEpiGate ? 2 + (p.Hprev ? 1 : 0) + 0.5
@@ -413,9 +427,15 @@ cudaError_t launch_tc_fwd(const TcFwd &p, cudaStream_t s) {
                                  : 1.0 + (p.dst_acc[0] ? 1.0 : 0.0);
   const double bytes = 2.0 * p.R * 64 * p.nkb + 2.0 * p.nkb * 64 * N + 4.0 * p.R * N * io / 2 * 2;
   ProfScope prof(p.mode == kEpiBwd ? kProfGemmDgrad : kProfGemmFwd, s, bytes, 2.0 * p.R * Kt * N);
-  static cudaError_t once = set_smem(k_tc_fwd, fwd_smem_bytes());
-  if (once != cudaSuccess) return once;
-  k_tc_fwd<<<grid, kFwdThreads, fwd_smem_bytes(), s>>>(ma0, ma1, mb, p);
+  if (nsub == 2) {
+    static cudaError_t once = set_smem(k_tc_fwd<2>, fwd_smem_bytes(2));
+    if (once != cudaSuccess) return once;
+    k_tc_fwd<2><<<grid, kFwdThreads, fwd_smem_bytes(2), s>>>(ma0, ma1, mb, p);
+  } else {
+    static cudaError_t once = set_smem(k_tc_fwd<1>, fwd_smem_bytes(1));
+    if (once != cudaSuccess) return once;
+    k_tc_fwd<1><<<grid, kFwdThreads, fwd_smem_bytes(1), s>>>(ma0, ma1, mb, p);
+  }
   return cudaGetLastError();
 }
 

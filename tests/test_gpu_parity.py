@@ -353,6 +353,8 @@ TC_CONFIGS = {
     "tc_tiny": synth.Config("tc_tiny", N=12, E=60, F=2, T_in=3, T_out=2, L=2, H=64, K=2, B=3),
     "tc_odd": SMALL_CONFIGS["odd"],
     "tc_l1": synth.Config("tc_l1", N=40, E=60, F=1, T_in=4, T_out=1, L=1, H=64, K=2, B=5),
+    # >= 2*148 row tiles of 128: the GEMMs switch to two 64-column sub-tiles per CTA
+    "tc_big": synth.Config("tc_big", N=600, E=110, F=2, T_in=3, T_out=2, L=2, H=64, K=2, B=64),
 }
 
 
