@@ -32,7 +32,7 @@ FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # SIMT FFMA peak at max cloc
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="metr_la")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -169,7 +169,26 @@ def run_reference(args, cfg):
             "e2e": {"value": round(sps, 4), "unit": "samples/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
             "oracle": det}
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+# The JSON line goes to the ORIGINAL stdout; everything else written to fd 1 afterwards (NCCL's
+# version banner, library chatter) is redirected to stderr so stdout carries exactly one line.
+_JSON_OUT = None
+
+
+def _claim_stdout():
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line: dict):
+    _claim_stdout()
+    _JSON_OUT.write(json.dumps(line) + "\n")
+    _JSON_OUT.flush()
 
 
 def config_dict(cfg, world, args):
@@ -184,6 +203,7 @@ def config_dict(cfg, world, args):
 
 # ------------------------------------------------------------------------------ our arm
 def main():
+    _claim_stdout()
     args = parse()
     import synth
     cfg = synth.CONFIGS[args.config]
@@ -379,7 +399,11 @@ def main():
                 "launches_per_step": launches_per_step, "clocks": ck,
                 "kernels": kernels, "eager_ms_per_step": round(eager_ms, 4),
                 "loss_last": loss_last, "steps_per_epoch": spe}
-        print(json.dumps(line), flush=True)
+        emit(line)
+    # tear down: drop the captured graph (it holds NCCL kernels) before the communicator
+    tr.graph = None
+    torch.cuda.synchronize()
+    barrier()
     if comm is not None:
         comm.close()
     if world > 1:

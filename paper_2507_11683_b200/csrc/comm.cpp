@@ -68,7 +68,10 @@ extern "C" pgti_status pgti_allreduce_f64(pgti_comm *c, double *buf, size_t n, v
 extern "C" pgti_status pgti_comm_destroy(pgti_comm *c) {
   pgti::clear_error();
   if (!c) return PGTI_OK;
-  ncclResult_t r = ncclCommDestroy(c->comm);
+  // collective: every rank calls this (after its last enqueued all-reduce); finalize flushes
+  // outstanding work, destroy frees the resources
+  ncclResult_t r = ncclCommFinalize(c->comm);
+  if (r == ncclSuccess) r = ncclCommDestroy(c->comm);
   delete c;
   PGTI_REQUIRE(r == ncclSuccess, PGTI_ERR_NCCL, "ncclCommDestroy: %s", ncclGetErrorString(r));
   return PGTI_OK;
