@@ -75,6 +75,19 @@ pgti_status pgti_graph_build(int32_t N, int64_t nnz, const int32_t *src, const i
                              float *PbT_val, int32_t *at_rowptr, int32_t *at_col, float *Pb_val,
                              float *PfT_val);
 
+/* Shared-memory staging plan of the diffusion SpMM (the north star's "shared-
+ * memory staging of the dense operand") on ONE CSR pattern (host arrays): rows
+ * are cut into windows of rows_per_window consecutive nodes (1..64); window w
+ * stages the ascending union of its rows' columns, written to
+ * win_nodes[win_ptr[w] .. win_ptr[w+1]) (win_ptr has ceil(N/rows_per_window)+1
+ * entries; win_nodes needs at most rowptr[N] entries), and lcol[e] (rowptr[N]
+ * entries) is the position of col[e] in its window's union.  *max_union = the
+ * largest union.  Index bookkeeping only (no values).  Errors: INVALID_ARG (null,
+ * rows_per_window outside [1,64], column outside [0,N), a union > 65535). */
+pgti_status pgti_graph_windows(int32_t N, const int32_t *rowptr, const int32_t *col,
+                               int32_t rows_per_window, int32_t *win_ptr, int32_t *win_nodes,
+                               uint16_t *lcol, int32_t *max_union);
+
 /* ----------------------------------------------------------------- the series */
 typedef struct pgti_series pgti_series; /* opaque; BORROWS dev_buf */
 
@@ -160,6 +173,17 @@ typedef struct {
   const float *Pf_val, *PbT_val;     /*   values of P_f and P_b^T on it         */
   const int32_t *at_rowptr, *at_col; /* pattern(A^T) device CSR                  */
   const float *Pb_val, *PfT_val;     /*   values of P_b and P_f^T on it         */
+  /* Optional shared-memory staging plan of the SpMM (pgti_graph_windows on each
+   * pattern, same rows_per_window; device arrays).  win_rows = 0 or any null
+   * pointer -> the SpMM reads neighbour rows straight from global memory.  The
+   * plan changes where operands are read from, never the arithmetic or its order:
+   * results are bit-identical either way. */
+  int32_t win_rows;                  /* rows per window, 1..64 (0 = no plan)      */
+  int32_t win_max;                   /* max window union size over both patterns */
+  const int32_t *a_win_ptr, *a_win_nodes;   /* pattern(A) plan                   */
+  const uint16_t *a_lcol;
+  const int32_t *at_win_ptr, *at_win_nodes; /* pattern(A^T) plan                 */
+  const uint16_t *at_lcol;
 } pgti_dcrnn_desc;
 
 /* Number of float parameters of the layout above (0 if desc invalid). */

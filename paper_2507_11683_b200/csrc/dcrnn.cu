@@ -68,11 +68,34 @@ pgti_status check_desc(const pgti_dcrnn_desc *desc, Dims *out) {
     PGTI_REQUIRE(g.a_rowptr && g.a_col && g.Pf_val && g.PbT_val && g.at_rowptr && g.at_col &&
                      g.Pb_val && g.PfT_val && g.nnz >= 0,
                  PGTI_ERR_INVALID_ARG, "desc: CSR pointers must be set when K > 0");
+  if (g.K > 0 && g.win_rows != 0)
+    PGTI_REQUIRE(g.win_rows >= 1 && g.win_rows <= 64 && g.win_max >= 0 && g.a_win_ptr &&
+                     g.a_win_nodes && g.a_lcol && g.at_win_ptr && g.at_win_nodes && g.at_lcol,
+                 PGTI_ERR_INVALID_ARG,
+                 "desc: SpMM window plan needs win_rows in [1,64], win_max >= 0 and all six "
+                 "plan pointers (win_rows=%d)",
+                 g.win_rows);
   Dims d{g.N, g.F, g.F_out, g.L, g.H, g.K, g.T_in, g.T_out, g.B, 2 * g.K + 1,
          int64_t(g.N) * g.B, g.ld, g.precision};
   *out = d;
   return PGTI_OK;
 }
+
+namespace {
+// term t of a job: pattern(A) (pat 0) or pattern(A^T) (pat 1) with values val, operand X
+void set_term(SpmmJob &j, int t, const pgti_dcrnn_desc &g, int pat, const float *val,
+              const float *X) {
+  j.rowptr[t] = pat ? g.at_rowptr : g.a_rowptr;
+  j.col[t] = pat ? g.at_col : g.a_col;
+  j.val[t] = val;
+  j.X[t] = X;
+  j.nnz[t] = g.nnz;
+  j.win_ptr[t] = pat ? g.at_win_ptr : g.a_win_ptr;
+  j.win_nodes[t] = pat ? g.at_win_nodes : g.a_win_nodes;
+  j.lcol[t] = pat ? g.at_lcol : g.a_lcol;
+  j.win_rows = g.win_rows, j.win_max = g.win_max;
+}
+}  // namespace
 
 cudaError_t diffuse_fwd(const pgti_dcrnn_desc &g, const Dims &d, float *base, int64_t mstride,
                         int G, int64_t gstride, int64_t W, cudaStream_t s, int bf16,
@@ -83,19 +106,18 @@ cudaError_t diffuse_fwd(const pgti_dcrnn_desc &g, const Dims &d, float *base, in
   auto blk = [&](int m) { return b + int64_t(m) * mstride * es; };
   for (int k = 1; k <= d.K; ++k) {
     SpmmJob j[2] = {};
+    const float *xf = reinterpret_cast<const float *>(k == 1 ? z : blk(k - 1));
+    const float *xb = reinterpret_cast<const float *>(k == 1 ? z : blk(d.K + k - 1));
     if (!transposed) {
-      j[0].rowptr[0] = g.a_rowptr, j[0].col[0] = g.a_col, j[0].val[0] = g.Pf_val;
-      j[1].rowptr[0] = g.at_rowptr, j[1].col[0] = g.at_col, j[1].val[0] = g.Pb_val;
+      set_term(j[0], 0, g, 0, g.Pf_val, xf);
+      set_term(j[1], 0, g, 1, g.Pb_val, xb);
     } else {
-      j[0].rowptr[0] = g.at_rowptr, j[0].col[0] = g.at_col, j[0].val[0] = g.PfT_val;
-      j[1].rowptr[0] = g.a_rowptr, j[1].col[0] = g.a_col, j[1].val[0] = g.PbT_val;
+      set_term(j[0], 0, g, 1, g.PfT_val, xf);
+      set_term(j[1], 0, g, 0, g.PbT_val, xb);
     }
-    j[0].X[0] = reinterpret_cast<const float *>(k == 1 ? z : blk(k - 1));
     j[0].Y = reinterpret_cast<float *>(blk(k));
-    j[1].X[0] = reinterpret_cast<const float *>(k == 1 ? z : blk(d.K + k - 1));
     j[1].Y = reinterpret_cast<float *>(blk(d.K + k));
-    for (auto &jb : j)
-      jb.nterms = 1, jb.nnz[0] = g.nnz, jb.W = W, jb.G = G, jb.gstride = gstride, jb.bf16 = bf16;
+    for (auto &jb : j) jb.nterms = 1, jb.W = W, jb.G = G, jb.gstride = gstride, jb.bf16 = bf16;
     cudaError_t e = launch_spmm(j, 2, d.N, s);
     if (e != cudaSuccess) return e;
   }
@@ -123,11 +145,11 @@ cudaError_t diffuse_adj(const pgti_dcrnn_desc &g, const Dims &d, AdjChain *ch, i
     int nj = 0;
     for (int c = 0; c < nch; ++c) {
       SpmmJob f{}, b{};
-      f.rowptr[0] = g.at_rowptr, f.col[0] = g.at_col, f.val[0] = g.PfT_val, f.X[0] = af[c];
+      set_term(f, 0, g, 1, g.PfT_val, af[c]);
       f.add = ch[c].dT + k * ch[c].mstride, f.Y = ch[c].tf[pp];
-      b.rowptr[0] = g.a_rowptr, b.col[0] = g.a_col, b.val[0] = g.PbT_val, b.X[0] = ab[c];
+      set_term(b, 0, g, 0, g.PbT_val, ab[c]);
       b.add = ch[c].dT + (K + k) * ch[c].mstride, b.Y = ch[c].tb[pp];
-      for (SpmmJob *jb : {&f, &b}) jb->nterms = 1, jb->nnz[0] = g.nnz, jb->W = ch[c].W, jb->G = 1;
+      for (SpmmJob *jb : {&f, &b}) jb->nterms = 1, jb->W = ch[c].W, jb->G = 1;
       jobs[nj++] = f, jobs[nj++] = b;
       af[c] = ch[c].tf[pp], ab[c] = ch[c].tb[pp];
     }
@@ -137,9 +159,8 @@ cudaError_t diffuse_adj(const pgti_dcrnn_desc &g, const Dims &d, AdjChain *ch, i
   }
   for (int c = 0; c < nch; ++c) {
     SpmmJob j{};
-    j.rowptr[0] = g.at_rowptr, j.col[0] = g.at_col, j.val[0] = g.PfT_val, j.X[0] = af[c];
-    j.rowptr[1] = g.a_rowptr, j.col[1] = g.a_col, j.val[1] = g.PbT_val, j.X[1] = ab[c];
-    j.nnz[0] = j.nnz[1] = g.nnz;
+    set_term(j, 0, g, 1, g.PfT_val, af[c]);
+    set_term(j, 1, g, 0, g.PbT_val, ab[c]);
     j.nterms = 2, j.add = ch[c].dT, j.Y = ch[c].out, j.accumulate = ch[c].accumulate;
     j.W = ch[c].W, j.G = 1;
     jobs[c] = j;

@@ -72,7 +72,7 @@ cudaError_t record(StreamPool *p, cudaStream_t st, cudaEvent_t *out) {
 struct LayoutTC {
   size_t Dx, yhat, dyhat, lossp, total;
   std::vector<size_t> DHb, DrHb, H32, Rg, Ug, Cg, dG, dGb, dC, dCb, Wf_ru, Wf_c, Wd_ru, Wd_c;
-  std::vector<size_t> dU, drH, Q, wpart, dHrec0, dHrec1, dHup0, dHup1;
+  std::vector<size_t> Q, wpart, dHrec0, dHrec1, dHup0, dHup1;
   size_t wpart_floats;
 };
 
@@ -109,8 +109,6 @@ LayoutTC make_layout_tc(const Dims &d) {
     L.Wd_ru.push_back(take(size_t(vrows(d, l)) * 2 * H * 2));
     L.Wd_c.push_back(take(size_t(vrows(d, l)) * H * 2));
     // per-layer (= per-stream) scratch
-    L.dU.push_back(take(R * H * 4));
-    L.drH.push_back(take(R * H * 4));
     L.Q.push_back(take(M * R * 2 * H * 2));
     L.wpart.push_back(take(wp * 4));
     L.dHrec0.push_back(take(R * H * 4));
@@ -233,9 +231,15 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
 
   // ------------------------------------------------------------------ backward (BPTT)
   // dZ = sum_m Q_m W_m^T, Q_0 = gradient itself (map A0), Q_{m>0} = (P^m)^T grad (map A1)
+  struct GateFuse {
+    const float *Hprev, *r;
+    float *dG;
+    bf16 *dGb;
+    float *dHprev;
+  };
   auto bwd_gemm = [&](int l, const bf16 *grad, int NG, const bf16 *Wd, bf16 *Q, bool need_in,
                       bool need_h, float *dst_in, int acc_in, float *dst_h, int acc_h,
-                      cudaStream_t ss) -> pgti_status {
+                      const GateFuse *fuse, cudaStream_t ss) -> pgti_status {
     const int vseg = l == 0 ? 64 : 2 * d.H;
     TcFwd b{};
     b.R = int(R), b.H = d.H, b.Nout = NG, b.mode = kEpiBwd;
@@ -250,7 +254,13 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
     // column tiles: l > 0 -> [input (64), hidden (64)]; l = 0 -> [hidden]
     int nt = 0;
     if (need_in) b.dst[nt] = dst_in, b.dst_acc[nt] = acc_in, ++nt;
-    if (need_h) b.dst[nt] = dst_h, b.dst_acc[nt] = acc_h, ++nt;
+    if (need_h) {
+      if (fuse) {
+        b.fuse_tile = nt, b.Hprev = fuse->Hprev, b.g_r = fuse->r, b.g_dG = fuse->dG;
+        b.g_dGb = fuse->dGb, b.g_dHprev = fuse->dHprev;
+      }
+      b.dst[nt] = dst_h, b.dst_acc[nt] = acc_h, ++nt;
+    }
     if (nt == 0) return PGTI_OK;
     if (l > 0 && !need_in)  // skip the input tile: shift B rows by one 64-column tile
       for (int k = 0; k < b.nkb; ++k) b.kb_by[k] += 64;
@@ -280,22 +290,23 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
       const float *dH_up = l + 1 < L ? up_buf(l, t) : nullptr;     // from (l+1, t)
       float *dH_prev = need_h ? rec_buf(l, t - 1) : nullptr;       // to (l, t-1)
       float *dIn = need_in ? up_buf(l - 1, t) : nullptr;           // to (l-1, t)
-      float *dU = Fp(Ly.dU[l]), *drH = Fp(Ly.drH[l]);
       bf16 *Q = Bp(Ly.Q[l]);
-      CU(launch_cand_bwd(RH, d.H, dH_rec, dH_up, dy, params + P.Wout, d.F_out, u, c, Hprev, dU, dC,
-                         dH_prev, ss, dCb));
+      // candidate backward (+ dG_u, and dG_r = 0 at t = 0)
+      CU(launch_cand_bwd_tc(RH, d.H, dH_rec, dH_up, dy, params + P.Wout, d.F_out, u, c, Hprev,
+                            dC, dCb, dH_prev, dG, dGb, ss));
       if (need_in || need_h) {
+        // d[in, r*H] = sum_m ((P^m)^T dC) W_c[m]^T; the hidden tile's epilogue runs the gate
+        // backward (dG_r, dH_{t-1} += d(rH) r) in place of storing d(rH)
         CU(diffuse_fwd(g, d, reinterpret_cast<float *>(Q), RH, 1, 0, int64_t(d.B) * d.H, ss, 1, 1,
                        dCb));
-        PGTI_STATUS_TRY(bwd_gemm(l, dCb, d.H, Bp(Ly.Wd_c[l]), Q, need_in, need_h, dIn, 0, drH, 0,
-                                 ss));
-      }
-      CU(launch_gate_bwd(RH, d.H, need_h ? drH : nullptr, Hprev, r, u, dU, dH_prev, dG, ss, dGb));
-      if (need_in || need_h) {
+        const GateFuse fz{Hprev, r, dG, dGb, dH_prev};
+        PGTI_STATUS_TRY(bwd_gemm(l, dCb, d.H, Bp(Ly.Wd_c[l]), Q, need_in, need_h, dIn, 0, nullptr,
+                                 0, &fz, ss));
+        // d[in, H] += sum_m ((P^m)^T dG) W_ru[m]^T
         CU(diffuse_fwd(g, d, reinterpret_cast<float *>(Q), 2 * RH, 1, 0, int64_t(d.B) * 2 * d.H,
                        ss, 1, 1, dGb));
         PGTI_STATUS_TRY(bwd_gemm(l, dGb, 2 * d.H, Bp(Ly.Wd_ru[l]), Q, need_in, need_h, dIn, 1,
-                                 dH_prev, 1, ss));
+                                 dH_prev, 1, nullptr, ss));
       }
       CU(record(sp, ss, &bdone[l][t]));
     }

@@ -100,6 +100,39 @@ __global__ void k_cand_bwd(int64_t RH, int H, const float *__restrict__ dHcur,
   }
 }
 
+// Tensor-core path candidate backward: as k_cand_bwd, plus the update-gate half of the gate
+// gradient dG_u = dU u (1-u) (dU never leaves registers) and, when H_{t-1} = 0, dG_r = 0; the
+// reset half dG_r is finished by the candidate dgrad GEMM's epilogue (TcFwd::fuse_tile).
+__global__ void k_cand_bwd_tc(int64_t RH, int H, const float *__restrict__ dHa,
+                              const float *__restrict__ dHb, const float *__restrict__ dy,
+                              const float *__restrict__ Wout, int F_out,
+                              const float *__restrict__ u, const float *__restrict__ c,
+                              const float *__restrict__ Hprev, float *__restrict__ dC,
+                              __nv_bfloat16 *__restrict__ dCb, float *__restrict__ dHprev,
+                              float *__restrict__ dG, __nv_bfloat16 *__restrict__ dGb) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < RH;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t row = i / H;
+    const int j = int(i - row * H);
+    float dh = dHa ? dHa[i] : 0.f;
+    if (dHb) dh += dHb[i];
+    if (dy)
+      for (int o = 0; o < F_out; ++o) dh = fmaf(dy[row * F_out + o], Wout[j * F_out + o], dh);
+    const float uu = u[i], cc = c[i], hp = Hprev ? Hprev[i] : 0.f;
+    const float dc = dh * (1.0f - uu) * (1.0f - cc * cc);
+    dC[i] = dc;
+    dCb[i] = __float2bfloat16_rn(dc);
+    if (dHprev) dHprev[i] = dh * uu;
+    const float gu = dh * (hp - cc) * uu * (1.0f - uu);
+    dG[row * 2 * H + H + j] = gu;
+    dGb[row * 2 * H + H + j] = __float2bfloat16_rn(gu);
+    if (!Hprev) {
+      dG[row * 2 * H + j] = 0.f;
+      dGb[row * 2 * H + j] = __float2bfloat16_rn(0.f);
+    }
+  }
+}
+
 // Gate backward: rH = r*H;  dr = d(rH) H;  dHprev += d(rH) r;
 //   dG[:, :H] = dr r (1-r),  dG[:, H:] = dU u (1-u)      (dGb: optional bf16 copy)
 __global__ void k_gate_bwd(int64_t RH, int H, const float *__restrict__ drH,
@@ -193,6 +226,21 @@ cudaError_t launch_cand_bwd(int64_t RH, int H, const float *dHcur, const float *
                                (dC_bf16 ? 2.0 : 0.0)), 0.0);
   k_cand_bwd<<<grid_for(RH), kT, 0, s>>>(RH, H, dHcur, dHcur2, dy, Wout, F_out, u, c, Hprev, dU,
                                          dC, dHprev_out, static_cast<__nv_bfloat16 *>(dC_bf16));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cand_bwd_tc(int64_t RH, int H, const float *dHa, const float *dHb,
+                               const float *dy, const float *Wout, int F_out, const float *u,
+                               const float *c, const float *Hprev, float *dC, void *dCb,
+                               float *dHprev, float *dG, void *dGb, cudaStream_t s) {
+  ProfScope prof(kProfElementwise, s,
+                 double(RH) * (4.0 * ((dHa ? 1 : 0) + (dHb ? 1 : 0) + 2 + (Hprev ? 1 : 0) + 1 +
+                                      (dHprev ? 1 : 0) + (Hprev ? 1 : 2)) +
+                               2.0 * (1 + (Hprev ? 1 : 2))),
+                 0.0);
+  k_cand_bwd_tc<<<grid_for(RH), kT, 0, s>>>(RH, H, dHa, dHb, dy, Wout, F_out, u, c, Hprev, dC,
+                                            static_cast<__nv_bfloat16 *>(dCb), dHprev, dG,
+                                            static_cast<__nv_bfloat16 *>(dGb));
   return cudaGetLastError();
 }
 

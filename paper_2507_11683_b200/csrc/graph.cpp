@@ -66,3 +66,46 @@ extern "C" pgti_status pgti_graph_build(int32_t N, int64_t nnz, const int32_t *s
   for (int i = 0; i < N; ++i) at_rowptr[i + 1] += at_rowptr[i];
   return PGTI_OK;
 }
+
+// Shared-memory staging plan of the diffusion SpMM (K2) on one CSR pattern: rows are cut into
+// windows of `rows_per_window` consecutive nodes; window w stages the union of its rows' column
+// indices (ascending, win_nodes[win_ptr[w] .. win_ptr[w+1])) and every CSR entry gets its column's
+// position in that union (lcol).  Pure index bookkeeping: values and summation order unchanged.
+extern "C" pgti_status pgti_graph_windows(int32_t N, const int32_t *rowptr, const int32_t *col,
+                                          int32_t rows_per_window, int32_t *win_ptr,
+                                          int32_t *win_nodes, uint16_t *lcol,
+                                          int32_t *max_union) {
+  pgti::clear_error();
+  PGTI_REQUIRE(N > 0 && rowptr && win_ptr && max_union, PGTI_ERR_INVALID_ARG,
+               "pgti_graph_windows: null pointer or N=%d", N);
+  PGTI_REQUIRE(rows_per_window >= 1 && rows_per_window <= 64, PGTI_ERR_INVALID_ARG,
+               "pgti_graph_windows: rows_per_window=%d outside [1, 64]", rows_per_window);
+  const int64_t nnz = rowptr[N];
+  PGTI_REQUIRE(rowptr[0] == 0 && nnz >= 0 && (nnz == 0 || (col && win_nodes && lcol)),
+               PGTI_ERR_INVALID_ARG, "pgti_graph_windows: bad rowptr / null arrays");
+  for (int32_t i = 0; i < N; ++i)
+    PGTI_REQUIRE(rowptr[i + 1] >= rowptr[i], PGTI_ERR_INVALID_ARG, "rowptr not monotone at %d", i);
+  const int32_t nwin = (N + rows_per_window - 1) / rows_per_window;
+  std::vector<int32_t> u;
+  int64_t pos = 0;
+  int32_t mx = 0;
+  win_ptr[0] = 0;
+  for (int32_t w = 0; w < nwin; ++w) {
+    const int32_t r0 = w * rows_per_window, r1 = std::min(N, r0 + rows_per_window);
+    u.assign(col + rowptr[r0], col + rowptr[r1]);
+    for (int32_t c : u)
+      PGTI_REQUIRE(c >= 0 && c < N, PGTI_ERR_INVALID_ARG, "column %d outside [0, %d)", c, N);
+    std::sort(u.begin(), u.end());
+    u.erase(std::unique(u.begin(), u.end()), u.end());
+    PGTI_REQUIRE(u.size() <= 65535, PGTI_ERR_INVALID_ARG, "window %d union %zu > 65535", w,
+                 u.size());
+    for (int64_t e = rowptr[r0]; e < rowptr[r1]; ++e)
+      lcol[e] = uint16_t(std::lower_bound(u.begin(), u.end(), col[e]) - u.begin());
+    std::copy(u.begin(), u.end(), win_nodes + pos);
+    pos += int64_t(u.size());
+    win_ptr[w + 1] = int32_t(pos);
+    mx = std::max(mx, int32_t(u.size()));
+  }
+  *max_union = mx;
+  return PGTI_OK;
+}

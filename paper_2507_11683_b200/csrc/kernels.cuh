@@ -23,6 +23,12 @@ struct SpmmJob {
   int G;
   int64_t gstride;
   int bf16;           // X, add, Y are __nv_bfloat16 (all jobs of a launch agree)
+  // shared-memory staging plan of each term's pattern (pgti_graph_windows); used when every
+  // term of every job of the launch has one with the same win_rows
+  const int32_t *win_ptr[2];
+  const int32_t *win_nodes[2];
+  const uint16_t *lcol[2];
+  int win_rows, win_max;
   // filled by launch_spmm
   int64_t warp_begin, chunks;
 };
@@ -152,6 +158,11 @@ cudaError_t launch_cand_bwd(int64_t RH, int H, const float *dHcur, const float *
                             const float *Wout, int F_out, const float *u, const float *c,
                             const float *Hprev, float *dU, float *dC, float *dHprev_out,
                             cudaStream_t s, void *dC_bf16 = nullptr);
+// tensor-core path: candidate backward + dG_u (+ dG_r = 0 when Hprev is null), bf16 copies
+cudaError_t launch_cand_bwd_tc(int64_t RH, int H, const float *dHa, const float *dHb,
+                               const float *dy, const float *Wout, int F_out, const float *u,
+                               const float *c, const float *Hprev, float *dC, void *dCb,
+                               float *dHprev, float *dG, void *dGb, cudaStream_t s);
 cudaError_t launch_gate_bwd(int64_t RH, int H, const float *drH, const float *Hprev,
                             const float *r, const float *u, const float *dU, float *dHprev,
                             float *dG, cudaStream_t s, void *dG_bf16 = nullptr);

@@ -7,6 +7,8 @@
 // order (deterministic).  Consecutive threads cover consecutive columns of one row, so every
 // neighbour read of a warp is a contiguous 512-byte segment.  (A warp-per-row design that
 // broadcast the CSR with shuffles measured 1.3-2.3x slower: tests/cuda/spmm_microbench.cu.)
+// With a window plan (pgti_graph_windows) the launch switches to k_spmm_win below, which stages
+// the dense operand in shared memory (tests/cuda/spmm_tiled_mb.cu has the measurements).
 // Element type per launch: fp32 (parity path, backward adjoint) or bf16 (tensor-core path's
 // diffusion blocks, which are the GEMM A operands).
 #include <cuda_bf16.h>
@@ -36,6 +38,11 @@ struct Lane<float> {
     acc[0] = __ffma2_rn(ww, make_float2(a.x, a.y), acc[0]);
     acc[1] = __ffma2_rn(ww, make_float2(a.z, a.w), acc[1]);
   }
+  static __device__ __forceinline__ void fma_v(float2 *acc, float w, uint4 r) {
+    const float2 ww = make_float2(w, w);
+    acc[0] = __ffma2_rn(ww, make_float2(__uint_as_float(r.x), __uint_as_float(r.y)), acc[0]);
+    acc[1] = __ffma2_rn(ww, make_float2(__uint_as_float(r.z), __uint_as_float(r.w)), acc[1]);
+  }
   static __device__ __forceinline__ void add(float2 *acc, const float *p) {
     const float4 a = *reinterpret_cast<const float4 *>(p);
     acc[0] = __fadd2_rn(acc[0], make_float2(a.x, a.y));
@@ -53,6 +60,13 @@ struct Lane<__nv_bfloat16> {
   }
   static __device__ __forceinline__ void fma(float2 *acc, float w, const __nv_bfloat16 *p) {
     const uint4 a = __ldg(reinterpret_cast<const uint4 *>(p));
+    const float2 ww = make_float2(w, w);
+    acc[0] = __ffma2_rn(ww, unpack(a.x), acc[0]);
+    acc[1] = __ffma2_rn(ww, unpack(a.y), acc[1]);
+    acc[2] = __ffma2_rn(ww, unpack(a.z), acc[2]);
+    acc[3] = __ffma2_rn(ww, unpack(a.w), acc[3]);
+  }
+  static __device__ __forceinline__ void fma_v(float2 *acc, float w, uint4 a) {
     const float2 ww = make_float2(w, w);
     acc[0] = __ffma2_rn(ww, unpack(a.x), acc[0]);
     acc[1] = __ffma2_rn(ww, unpack(a.y), acc[1]);
@@ -122,6 +136,117 @@ __global__ void __launch_bounds__(256) k_spmm(const __grid_constant__ SpmmParams
   T *Y = reinterpret_cast<T *>(jb.Y) + o;
   if (jb.accumulate) L::add(acc, Y);
   L::store(Y, acc);
+}
+
+// Shared-memory staged variant (the plan of pgti_graph_windows): CTA = (window of win_rows
+// consecutive nodes, 512-byte column chunk).  The union of the window's neighbour rows is staged
+// once into shared memory with cp.async (16 bytes per lane, L1 bypassed), then warp w reduces rows
+// w, w+8, ... of the window with lane = one 16-byte vector, reading neighbours from shared memory
+// (a warp reads one contiguous 512-byte row: conflict-free).  L2->SM traffic for the dense
+// operand drops from nnz/N (~8.3) slices per output slice to the window's union/rows (~1.9 at 32
+// rows on the kNN sensor graphs).  Same terms, same CSR order, same FFMA2 sequence as k_spmm:
+// bit-identical results.
+constexpr int kWinMaxSmem = 192 * 1024;
+
+struct WinParams {
+  SpmmJob job[kMaxSpmmJobs];
+  int block_begin[kMaxSpmmJobs + 1];
+  int nchunk[kMaxSpmmJobs];
+  int vecs[kMaxSpmmJobs];
+  int njobs, N, nwin, win_rows, win_max;
+};
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *g) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(g) : "memory");
+}
+
+template <typename T, int RPW>
+__global__ void __launch_bounds__(256) k_spmm_win(const __grid_constant__ WinParams p) {
+  using L = Lane<T>;
+  constexpr int V = L::V, P = V / 2;
+  extern __shared__ uint4 stage[];  // [union][32]
+  const int bid = int(blockIdx.x);
+  int j = 0;
+#pragma unroll
+  for (int q = 1; q < kMaxSpmmJobs; ++q)
+    if (q < p.njobs && bid >= p.block_begin[q]) j = q;
+  const SpmmJob &jb = p.job[j];
+  int rem = bid - p.block_begin[j];
+  const int nchunk = p.nchunk[j];
+  const int chunk = rem % nchunk;
+  rem /= nchunk;
+  const int win = rem % p.nwin, g = rem / p.nwin;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int vec = chunk * 32 + lane;
+  const bool act = vec < p.vecs[j];
+  const int W = int(jb.W);
+  const int64_t goff = int64_t(g) * jb.gstride;
+  const int row0 = win * p.win_rows;
+
+  float2 acc[RPW][P];
+#pragma unroll
+  for (int i = 0; i < RPW; ++i)
+#pragma unroll
+    for (int q = 0; q < P; ++q) acc[i][q] = make_float2(0.f, 0.f);
+  int *s_nodes = reinterpret_cast<int *>(stage + p.win_max * 32);
+  for (int t = 0; t < jb.nterms; ++t) {
+    if (t) __syncthreads();  // every warp is done with the previous term's stage
+    const int ub = __ldg(jb.win_ptr[t] + win), nu = __ldg(jb.win_ptr[t] + win + 1) - ub;
+    // every index load is issued up front, lane-parallel: the union's node ids into shared
+    // memory, and each warp's rows' first 32 CSR entries into registers (one per lane)
+    for (int i = threadIdx.x; i < nu; i += blockDim.x) s_nodes[i] = __ldg(jb.win_nodes[t] + ub + i);
+    const uint16_t *lc = jb.lcol[t];
+    const float *val = jb.val[t];
+    int beg[RPW], cnt[RPW], cc[RPW];
+    float cv[RPW];
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      const int r = warp + 8 * i, n = row0 + r;
+      beg[i] = cnt[i] = cc[i] = 0, cv[i] = 0.f;
+      if (r >= p.win_rows || n >= p.N) continue;  // warp-uniform
+      beg[i] = __ldg(jb.rowptr[t] + n);
+      cnt[i] = __ldg(jb.rowptr[t] + n + 1) - beg[i];
+      if (lane < cnt[i]) cc[i] = __ldg(lc + beg[i] + lane), cv[i] = __ldg(val + beg[i] + lane);
+    }
+    __syncthreads();
+    const T *X = reinterpret_cast<const T *>(jb.X[t]) + goff + int64_t(vec) * V;
+    if (act)
+      for (int k = warp; k < nu; k += 8) cp_async16(stage + k * 32 + lane, X + int64_t(s_nodes[k]) * W);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      const int n0 = min(cnt[i], 32);
+      int u = 0;
+      for (; u + 4 <= n0; u += 4) {
+        const int c0 = __shfl_sync(0xffffffffu, cc[i], u), c1 = __shfl_sync(0xffffffffu, cc[i], u + 1),
+                  c2 = __shfl_sync(0xffffffffu, cc[i], u + 2), c3 = __shfl_sync(0xffffffffu, cc[i], u + 3);
+        const float w0 = __shfl_sync(0xffffffffu, cv[i], u), w1 = __shfl_sync(0xffffffffu, cv[i], u + 1),
+                    w2 = __shfl_sync(0xffffffffu, cv[i], u + 2), w3 = __shfl_sync(0xffffffffu, cv[i], u + 3);
+        L::fma_v(acc[i], w0, stage[c0 * 32 + lane]);
+        L::fma_v(acc[i], w1, stage[c1 * 32 + lane]);
+        L::fma_v(acc[i], w2, stage[c2 * 32 + lane]);
+        L::fma_v(acc[i], w3, stage[c3 * 32 + lane]);
+      }
+      for (; u < n0; ++u)
+        L::fma_v(acc[i], __shfl_sync(0xffffffffu, cv[i], u),
+                 stage[__shfl_sync(0xffffffffu, cc[i], u) * 32 + lane]);
+      for (int e = beg[i] + 32; e < beg[i] + cnt[i]; ++e)  // rows with > 32 entries
+        L::fma_v(acc[i], __ldg(val + e), stage[__ldg(lc + e) * 32 + lane]);
+    }
+  }
+  if (!act) return;
+#pragma unroll
+  for (int i = 0; i < RPW; ++i) {
+    const int r = warp + 8 * i, n = row0 + r;
+    if (r >= p.win_rows || n >= p.N) continue;
+    const int64_t o = goff + int64_t(n) * W + int64_t(vec) * V;
+    if (jb.add) L::add(acc[i], reinterpret_cast<const T *>(jb.add) + o);
+    T *Y = reinterpret_cast<T *>(jb.Y) + o;
+    if (jb.accumulate) L::add(acc[i], Y);
+    L::store(Y, acc[i]);
+  }
 }
 
 // Scalar fp32 fallback for widths that are not a multiple of 4 (test shapes only).
@@ -194,6 +319,46 @@ cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s) {
     }
   }
   ProfScope prof(kProfSpmm, s, bytes, flops);
+  // shared-memory staged kernel when every term carries a window plan of one size that fits
+  bool win = vec && jobs[0].win_rows > 0 && jobs[0].win_max > 0 &&
+             jobs[0].win_max * 516 <= kWinMaxSmem;
+  for (int i = 0; i < njobs && win; ++i) {
+    const SpmmJob &j = jobs[i];
+    win = j.nterms >= 1 && j.win_rows == jobs[0].win_rows && j.win_max == jobs[0].win_max;
+    for (int t = 0; t < j.nterms && win; ++t) win = j.win_ptr[t] && j.win_nodes[t] && j.lcol[t];
+  }
+  if (win) {
+    WinParams w{};
+    w.njobs = njobs, w.N = N, w.win_rows = jobs[0].win_rows, w.win_max = jobs[0].win_max;
+    w.nwin = int(ceil_div(N, w.win_rows));
+    int64_t nb = 0;
+    for (int i = 0; i < njobs; ++i) {
+      w.job[i] = jobs[i];
+      w.vecs[i] = int(jobs[i].W / V);
+      w.nchunk[i] = int(ceil_div(w.vecs[i], 32));
+      w.block_begin[i] = int(nb);
+      nb += int64_t(jobs[i].G) * w.nwin * w.nchunk[i];
+    }
+    w.block_begin[njobs] = int(nb);
+    const int smem = jobs[0].win_max * 516;  // staged rows + their node ids
+    const int rpw = (w.win_rows + 7) / 8;
+    auto go = [&](auto kernel) -> cudaError_t {
+      cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      kernel<<<unsigned(nb), 256, smem, s>>>(w);
+      return cudaGetLastError();
+    };
+    if (bf) {
+      if (rpw <= 1) return go(k_spmm_win<__nv_bfloat16, 1>);
+      if (rpw <= 2) return go(k_spmm_win<__nv_bfloat16, 2>);
+      if (rpw <= 4) return go(k_spmm_win<__nv_bfloat16, 4>);
+      return go(k_spmm_win<__nv_bfloat16, 8>);
+    }
+    if (rpw <= 1) return go(k_spmm_win<float, 1>);
+    if (rpw <= 2) return go(k_spmm_win<float, 2>);
+    if (rpw <= 4) return go(k_spmm_win<float, 4>);
+    return go(k_spmm_win<float, 8>);
+  }
   const unsigned blocks = unsigned(ceil_div(th, 256));
   if (bf)
     k_spmm<__nv_bfloat16><<<blocks, 256, 0, s>>>(p);

@@ -1,9 +1,11 @@
 // K3: tcgen05 gate GEMMs (bf16 operands staged by TMA into SWIZZLE_128B shared memory, fp32
 // accumulators in TMEM, one elected thread issuing tcgen05.mma) with the GRU math fused into
-// the TMEM -> register epilogue.
+// the epilogue.
 //   k_tc_fwd   : multi-block GEMM (forward gates, and the backward "diffuse-then-GEMM" dgrad)
 //                10 warps: warp 0 TMA producer, warp 1 TMEM alloc + MMA issuer, warps 2-9
-//                epilogue (thread = one accumulator row x 32 of the tile's 64 columns)
+//                epilogue.  Epilogue = TMEM -> registers -> shared-memory tile (the drained
+//                pipeline stages are reused) -> coalesced element-wise math and global I/O
+//                (consecutive threads touch consecutive columns of a row).
 //   k_tc_wgrad : split-K weight gradient, MN-major A (diffusion blocks) and B (gate gradients)
 // 4-stage mbarrier ring between TMA and MMA (full / empty), one commit barrier MMA -> epilogue.
 // Equations: Li et al. Eq. 2-3 [ext], PAPER.md P:168, P:222 (readings c1-c7).
@@ -61,11 +63,19 @@ __device__ __forceinline__ void teardown(Barriers *bar, uint32_t ncols) {
   }
 }
 
+__device__ __forceinline__ float4 ld4(const float *p) { return *reinterpret_cast<const float4 *>(p); }
+__device__ __forceinline__ void st4(float *p, float4 v) { *reinterpret_cast<float4 *>(p) = v; }
+__device__ __forceinline__ void st4_bf16(bf16 *p, float4 v) {
+  __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t *>(&a);
+  u.y = *reinterpret_cast<uint32_t *>(&b);
+  *reinterpret_cast<uint2 *>(p) = u;
+}
+
 // ================================================================== multi-block GEMM
-// One CTA = 128 rows x one 64-column tile.  Everything the epilogue needs that does not depend
-// on the accumulator (bias, layer-0 x part by FFMA, H_{t-1}, u, the bwd destination) is
-// gathered while the MMAs run; after the commit barrier only TMEM -> math -> stores remain.
 constexpr int kFwdThreads = 320, kEpiThreads = 256;
+constexpr int kTileLd = 68;  // shared epilogue tile pitch (floats): 16-byte rows, spread banks
 
 __device__ __forceinline__ void epi_bar() {
   asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
@@ -73,17 +83,21 @@ __device__ __forceinline__ void epi_bar() {
 
 // NSUB = 64-column sub-tiles per CTA: 1 (small R: more CTAs) or 2 (large R: A read once for
 // both the r and u halves of the gate / the input and hidden tiles of the backward GEMM).
-template <int NSUB>
-__global__ void __launch_bounds__(kFwdThreads, 3 - NSUB)
+// MODE (kEpiGate / kEpiCand / kEpiBwd) is compile-time so each epilogue gets its own registers.
+template <int NSUB, int MODE>
+__global__ void __launch_bounds__(kFwdThreads, NSUB == 1 ? 2 : 1)
     k_tc_fwd(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
              const __grid_constant__ CUtensorMap mB, const __grid_constant__ TcFwd p) {
   constexpr int NT = 64 * NSUB;
   constexpr int A_BYTES = kBM * kBK * 2, B_BYTES = NT * kBK * 2, STAGE = A_BYTES + B_BYTES;
+  static_assert(kStages * STAGE >= kBM * kTileLd * 4, "epilogue tile reuses the stage buffers");
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
   Barriers *bar = carve<A_BYTES, B_BYTES>(smem);
   float *wx_s = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(bar) + 256);  // [20][64]
-  float *y_s = wx_s + 20 * 64;                                                       // [128][4]
+  float *tile_s = reinterpret_cast<float *>(smem);                                  // [128][68]
+  float *xs_s = tile_s + kBM * kTileLd;                                             // [128][<=20]
+  static_assert(kStages * STAGE >= kBM * (kTileLd + 20) * 4, "x rows fit behind the tile");
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int row0 = blockIdx.x * kBM, ct0 = blockIdx.y * NSUB;
   if (threadIdx.x == 0) tma_prefetch(&mA0), tma_prefetch(&mA1), tma_prefetch(&mB);
@@ -120,145 +134,129 @@ __global__ void __launch_bounds__(kFwdThreads, 3 - NSUB)
     }
   } else {
     const int e = warp - 2, q = warp & 3, hh = e >> 2;
-    const int r = q * 32 + lane, row = row0 + r;
-    const bool valid = row < p.R;
+    const int et = e * 32 + lane;  // 0..255
     const int H = p.H;
+    const int nx = (MODE != kEpiBwd && p.Dx) ? p.F * p.M : 0;
+    mbar_wait(&bar->tfull, 0);  // MMAs done => every stage buffer is free for the tile
+    tc_fence_after();
 #pragma unroll 1
     for (int sub = 0; sub < NSUB; ++sub) {
-    if (sub > 0) epi_bar();                  // sub-tile 0 finished with wx_s / y_s
-    const int ct = ct0 + sub;
-    const int jc = hh * 32;                  // first tile column of this thread
-    const uint32_t tsub = uint32_t(sub * 64);  // TMEM column of this sub-tile
-    if (p.mode == kEpiBwd) {
-      float *dst = p.dst[ct];
-      const int64_t ro = int64_t(row) * 64 + jc;
-      float old[32];
+      const int ct = ct0 + sub;
+      // ---- phase 1: TMEM -> smem tile (thread = one accumulator row, 32 of the 64 columns)
+      if (sub > 0) epi_bar();  // previous sub-tile done reading tile_s / wx_s
+      {
+        const int r = q * 32 + lane;
+        float acc[32];
+        if (p.nkb) {
+          const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + sub * 64 + hh * 32;
+          tmem_ld16(taddr, acc);
+          tmem_ld16(taddr + 16, acc + 16);
+          tmem_wait_ld();
+        } else {
 #pragma unroll
-      for (int i = 0; i < 32; i += 4) {
-        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid && p.dst_acc[ct]) a = *reinterpret_cast<const float4 *>(dst + ro + i);
-        old[i] = a.x, old[i + 1] = a.y, old[i + 2] = a.z, old[i + 3] = a.w;
-      }
-      mbar_wait(&bar->tfull, 0);
-      tc_fence_after();
-      float acc[32];
-      const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + tsub + jc;
-      tmem_ld16(taddr, acc);
-      tmem_ld16(taddr + 16, acc + 16);
-      tmem_wait_ld();
-      if (valid) {
+          for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+        }
+        float *dst = tile_s + r * kTileLd + hh * 32;
 #pragma unroll
-        for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<float4 *>(dst + ro + i) =
-              make_float4(old[i] + acc[i], old[i + 1] + acc[i + 1], old[i + 2] + acc[i + 2],
-                          old[i + 3] + acc[i + 3]);
+        for (int i = 0; i < 32; i += 4) st4(dst + i, make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]));
       }
-    } else {
-      const int nx = p.Dx ? p.F * p.M : 0;
-      // stage this tile's x-part weight rows (fp32) in shared memory
-      for (int i = e * 32 + lane; i < nx * 64; i += kEpiThreads) {
+      for (int i = et; i < nx * 64; i += kEpiThreads) {  // x-part weight rows of this tile
         const int mf = i / 64, j = i % 64, m = mf / p.F, f = mf % p.F;
         wx_s[i] = __ldg(p.Wx + int64_t(m * p.C_in + f) * p.Nout + ct * 64 + j);
       }
+      if (sub == 0)  // x-part row values of the tile's 128 rows (diffused layer-0 input)
+        for (int i = et; i < nx * kBM; i += kEpiThreads) {
+          const int rl = i / nx, mf = i - rl * nx, m = mf / p.F, f = mf - m * p.F;
+          xs_s[i] = row0 + rl < p.R ? __ldg(p.Dx + m * p.dx_mstride + int64_t(row0 + rl) * p.F + f) : 0.f;
+        }
       epi_bar();
-      const int jg = ct * 64 + jc;  // first gate column
-      float pre[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) pre[i] = __ldg(p.bias + jg + i);
-      if (nx && valid) {
-        for (int mf = 0; mf < nx; ++mf) {
-          const int m = mf / p.F, f = mf % p.F;
-          const float xv = __ldg(p.Dx + m * p.dx_mstride + int64_t(row) * p.F + f);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) pre[i] = fmaf(xv, wx_s[mf * 64 + jc + i], pre[i]);
+      // ---- phase 2: coalesced element-wise epilogue: 16 threads per row, 4 columns each
+#pragma unroll 2
+      for (int it = 0; it < (kBM * 64 / 4) / kEpiThreads; ++it) {
+        const int idx = it * kEpiThreads + et;
+        const int rl = idx >> 4, c4 = (idx & 15) * 4;
+        const int row = row0 + rl;
+        const bool valid = row < p.R;
+        float4 a = ld4(tile_s + rl * kTileLd + c4);
+        if (MODE == kEpiBwd) {
+          if (!valid) continue;
+          if (ct == p.fuse_tile) {
+            // fused gate backward: a = d(r*H_{t-1}); dG_r = a H r (1-r); dH_{t-1} += a r
+            const int64_t ro = int64_t(row) * 64 + c4, rg = int64_t(row) * 128 + c4;
+            const float4 hp = ld4(p.Hprev + ro), rr = ld4(p.g_r + ro), dh = ld4(p.g_dHprev + ro);
+            const float4 g = make_float4(a.x * hp.x * rr.x * (1.f - rr.x), a.y * hp.y * rr.y * (1.f - rr.y),
+                                         a.z * hp.z * rr.z * (1.f - rr.z), a.w * hp.w * rr.w * (1.f - rr.w));
+            st4(p.g_dHprev + ro, make_float4(fmaf(a.x, rr.x, dh.x), fmaf(a.y, rr.y, dh.y),
+                                             fmaf(a.z, rr.z, dh.z), fmaf(a.w, rr.w, dh.w)));
+            st4(p.g_dG + rg, g);
+            st4_bf16(p.g_dGb + rg, g);
+          } else {
+            float *d = p.dst[ct] + int64_t(row) * 64 + c4;
+            if (p.dst_acc[ct]) {
+              const float4 o = ld4(d);
+              a.x += o.x, a.y += o.y, a.z += o.z, a.w += o.w;
+            }
+            st4(d, a);
+          }
+          continue;
         }
-      }
-      const int jh = (p.mode == kEpiGate ? 0 : ct * 64) + jc;  // hidden index of column 0
-      const int64_t ro = int64_t(row) * H + jh;
-      const bool need_h = p.mode == kEpiCand || ct == 0;
-      float hp[32], uu[32];
-#pragma unroll
-      for (int i = 0; i < 32; i += 4) {
-        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-        if (valid && need_h && p.Hprev) a = *reinterpret_cast<const float4 *>(p.Hprev + ro + i);
-        if (valid && p.mode == kEpiCand) b = *reinterpret_cast<const float4 *>(p.u_in + ro + i);
-        hp[i] = a.x, hp[i + 1] = a.y, hp[i + 2] = a.z, hp[i + 3] = a.w;
-        uu[i] = b.x, uu[i + 1] = b.y, uu[i + 2] = b.z, uu[i + 3] = b.w;
-      }
-      mbar_wait(&bar->tfull, 0);
-      tc_fence_after();
-      float acc[32];
-      if (p.nkb) {
-        const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + tsub + jc;
-        tmem_ld16(taddr, acc);
-        tmem_ld16(taddr + 16, acc + 16);
-        tmem_wait_ld();
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) acc[i] = 0.f;
-      }
-      if (p.mode == kEpiGate) {
-        float *out = ct == 0 ? p.out_r : p.out_u;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) acc[i] = sigmoid_f(acc[i] + pre[i]);
-        if (valid) {
-#pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            *reinterpret_cast<float4 *>(out + ro + i) =
-                make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
-          if (ct == 0) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) hp[i] *= acc[i];
-#pragma unroll
-            for (int i = 0; i < 32; i += 8)
-              *reinterpret_cast<uint4 *>(p.out_rH + ro + i) = pack8_bf16(hp + i);
+        // forward: pre-activation = acc + bias (+ layer-0 x part)
+        const int jg = ct * 64 + c4;
+        const float4 b = ld4(p.bias + jg);
+        a.x += b.x, a.y += b.y, a.z += b.z, a.w += b.w;
+        if (nx) {
+          const float *xr = xs_s + rl * nx;
+          for (int mf = 0; mf < nx; ++mf) {
+            const float xv = xr[mf];
+            const float4 w = ld4(wx_s + mf * 64 + c4);
+            a.x = fmaf(xv, w.x, a.x), a.y = fmaf(xv, w.y, a.y);
+            a.z = fmaf(xv, w.z, a.z), a.w = fmaf(xv, w.w, a.w);
           }
         }
-      } else {
-        float ys0 = 0.f, ys1 = 0.f, ys2 = 0.f, ys3 = 0.f;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float c = tanhf(acc[i] + pre[i]);
-          acc[i] = c;
-          pre[i] = uu[i] * hp[i] + (1.0f - uu[i]) * c;  // H_t
-        }
-        if (p.yhat) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float *w = p.Wout + (jh + i) * p.F_out;
-            ys0 = fmaf(pre[i], __ldg(w), ys0);
-            if (p.F_out > 1) ys1 = fmaf(pre[i], __ldg(w + 1), ys1);
-            if (p.F_out > 2) ys2 = fmaf(pre[i], __ldg(w + 2), ys2);
-            if (p.F_out > 3) ys3 = fmaf(pre[i], __ldg(w + 3), ys3);
+        const int jh = (MODE == kEpiGate ? 0 : ct * 64) + c4;  // hidden unit of column c4
+        const int64_t ro = int64_t(row) * H + jh;
+        if (MODE == kEpiGate) {
+          const float4 s = make_float4(sigmoid_f(a.x), sigmoid_f(a.y), sigmoid_f(a.z), sigmoid_f(a.w));
+          if (valid) {
+            if (ct == 0) {
+              st4(p.out_r + ro, s);
+              float4 hp = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (p.Hprev) hp = ld4(p.Hprev + ro);
+              st4_bf16(p.out_rH + ro, make_float4(s.x * hp.x, s.y * hp.y, s.z * hp.z, s.w * hp.w));
+            } else {
+              st4(p.out_u + ro, s);
+            }
           }
-        }
-        const float ys[4] = {ys0, ys1, ys2, ys3};
-        if (valid) {
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            *reinterpret_cast<float4 *>(p.out_c + ro + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
-            *reinterpret_cast<float4 *>(p.out_H + ro + i) = make_float4(pre[i], pre[i + 1], pre[i + 2], pre[i + 3]);
+        } else {  // kEpiCand
+          float4 hn = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (valid) {
+            const float4 c = make_float4(tanhf(a.x), tanhf(a.y), tanhf(a.z), tanhf(a.w));
+            const float4 u = ld4(p.u_in + ro);
+            float4 hp = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (p.Hprev) hp = ld4(p.Hprev + ro);
+            hn = make_float4(u.x * hp.x + (1.f - u.x) * c.x, u.y * hp.y + (1.f - u.y) * c.y,
+                             u.z * hp.z + (1.f - u.z) * c.z, u.w * hp.w + (1.f - u.w) * c.w);
+            st4(p.out_c + ro, c);
+            st4(p.out_H + ro, hn);
+            st4_bf16(p.out_Hb + ro, hn);
           }
+          if (p.yhat) {  // readout: 16 lanes of this row hold its 64 hidden units
 #pragma unroll
-          for (int i = 0; i < 32; i += 8)
-            *reinterpret_cast<uint4 *>(p.out_Hb + ro + i) = pack8_bf16(pre + i);
-        }
-        if (p.yhat) {
-          if (hh == 1) {
+            for (int o = 0; o < 4; ++o) {
+              if (o >= p.F_out) break;
+              float y = hn.x * __ldg(p.Wout + (jh + 0) * p.F_out + o) +
+                        hn.y * __ldg(p.Wout + (jh + 1) * p.F_out + o) +
+                        hn.z * __ldg(p.Wout + (jh + 2) * p.F_out + o) +
+                        hn.w * __ldg(p.Wout + (jh + 3) * p.F_out + o);
 #pragma unroll
-            for (int o = 0; o < 4; ++o) y_s[r * 4 + o] = ys[o];
-          }
-          epi_bar();
-          if (hh == 0 && valid) {
-#pragma unroll
-            for (int o = 0; o < 4; ++o)
-              if (o < p.F_out)
-                p.yhat[int64_t(row) * p.F_out + o] = (ys[o] + y_s[r * 4 + o]) + __ldg(p.bout + o);
+              for (int off = 8; off > 0; off >>= 1) y += __shfl_xor_sync(0xffffffffu, y, off);
+              if ((lane & 15) == 0 && valid)
+                p.yhat[int64_t(row) * p.F_out + o] = y + __ldg(p.bout + o);
+            }
           }
         }
       }
     }
-    }  // sub-tiles
   }
   teardown(bar, NT);
 }
@@ -395,7 +393,7 @@ cudaError_t set_smem(K kernel, int bytes) {
 
 constexpr int wg_smem_bytes(int b_rows) { return kStages * (kBM * kBK * 2 + b_rows * kBK * 2) + 1024 + 256; }
 constexpr int fwd_smem_bytes(int nsub) {
-  return kStages * (kBM * kBK * 2 + 64 * nsub * kBK * 2) + 1024 + 256 + (20 * 64 + 128 * 4) * 4;
+  return kStages * (kBM * kBK * 2 + 64 * nsub * kBK * 2) + 1024 + 256 + 20 * 64 * 4;
 }
 
 }  // namespace
@@ -427,16 +425,22 @@ cudaError_t launch_tc_fwd(const TcFwd &p, cudaStream_t s) {
                                  : 1.0 + (p.dst_acc[0] ? 1.0 : 0.0);
   const double bytes = 2.0 * p.R * 64 * p.nkb + 2.0 * p.nkb * 64 * N + 4.0 * p.R * N * io / 2 * 2;
   ProfScope prof(p.mode == kEpiBwd ? kProfGemmDgrad : kProfGemmFwd, s, bytes, 2.0 * p.R * Kt * N);
-  if (nsub == 2) {
-    static cudaError_t once = set_smem(k_tc_fwd<2>, fwd_smem_bytes(2));
-    if (once != cudaSuccess) return once;
-    k_tc_fwd<2><<<grid, kFwdThreads, fwd_smem_bytes(2), s>>>(ma0, ma1, mb, p);
-  } else {
-    static cudaError_t once = set_smem(k_tc_fwd<1>, fwd_smem_bytes(1));
-    if (once != cudaSuccess) return once;
-    k_tc_fwd<1><<<grid, kFwdThreads, fwd_smem_bytes(1), s>>>(ma0, ma1, mb, p);
+  auto go = [&](auto kernel, int smem) -> cudaError_t {
+    cudaError_t e = set_smem(kernel, smem);  // idempotent, cheap
+    if (e != cudaSuccess) return e;
+    kernel<<<grid, kFwdThreads, smem, s>>>(ma0, ma1, mb, p);
+    return cudaGetLastError();
+  };
+  const int sm1 = fwd_smem_bytes(1), sm2 = fwd_smem_bytes(2);
+  switch (p.mode * 2 + (nsub - 1)) {
+    case kEpiGate * 2: return go(k_tc_fwd<1, kEpiGate>, sm1);
+    case kEpiGate * 2 + 1: return go(k_tc_fwd<2, kEpiGate>, sm2);
+    case kEpiCand * 2: return go(k_tc_fwd<1, kEpiCand>, sm1);
+    case kEpiCand * 2 + 1: return go(k_tc_fwd<2, kEpiCand>, sm2);
+    case kEpiBwd * 2: return go(k_tc_fwd<1, kEpiBwd>, sm1);
+    case kEpiBwd * 2 + 1: return go(k_tc_fwd<2, kEpiBwd>, sm2);
+    default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 size_t tc_wgrad_partial_floats(int V, int Nout, int T, int R) {

@@ -41,7 +41,10 @@ class DcrnnDesc(C.Structure):
                 ("T_in", _i32), ("T_out", _i32), ("B", _i32), ("precision", _i32),
                 ("ld", _i64), ("nnz", _i64),
                 ("a_rowptr", _vp), ("a_col", _vp), ("Pf_val", _vp), ("PbT_val", _vp),
-                ("at_rowptr", _vp), ("at_col", _vp), ("Pb_val", _vp), ("PfT_val", _vp)]
+                ("at_rowptr", _vp), ("at_col", _vp), ("Pb_val", _vp), ("PfT_val", _vp),
+                ("win_rows", _i32), ("win_max", _i32),
+                ("a_win_ptr", _vp), ("a_win_nodes", _vp), ("a_lcol", _vp),
+                ("at_win_ptr", _vp), ("at_win_nodes", _vp), ("at_lcol", _vp)]
 
 
 def _sig(name, restype, *argtypes):
@@ -56,6 +59,8 @@ version = lambda: _sig("pgti_version", C.c_char_p)().decode()  # noqa: E731
 _check_dev = _sig("pgti_check_device_error", C.c_int, _vp)
 _graph_build = _sig("pgti_graph_build", C.c_int, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                     _vp, _vp, _vp, _vp)
+_graph_windows = _sig("pgti_graph_windows", C.c_int, _i32, _vp, _vp, _i32, _vp, _vp, _vp,
+                      C.POINTER(_i32))
 _load = _sig("pgti_load_series", C.c_int, C.POINTER(_vp), _vp, _i64, _i64, _i64, _i64, _vp, _i64,
              _vp)
 _stats = _sig("pgti_series_stats", C.c_int, _vp, _i64, C.c_int, _i64, _i64, _f64, _vp, _vp)
@@ -156,6 +161,46 @@ def graph_build(N: int, src, dst, w) -> dict:
     return out
 
 
+def default_win_rows(N: int) -> int:
+    """Rows per SpMM staging window (0 = gather straight from L2).  Measured on B200
+    (tests/cuda/spmm_tiled_mb.cu, one bf16 hop, W = 4096): staging pays once the operand is
+    far larger than what one wave re-reads from L2 -- full-PeMS N=11160: 66 us vs 96 us;
+    PeMS-All-LA N=2716: 18.5 vs 20.6 us alone but slower inside the step, where its shared
+    memory competes with the concurrently running tcgen05 GEMMs; METR-LA: equal."""
+    return 16 if N >= 4096 else 0
+
+
+def graph_windows(N: int, rowptr, col, rows: int) -> dict:
+    """pgti_graph_windows on one CSR pattern -> win_ptr, win_nodes, lcol (int16 bits), max."""
+    rowptr = np.ascontiguousarray(rowptr, np.int32)
+    col = np.ascontiguousarray(col, np.int32)
+    nnz = int(rowptr[N])
+    nwin = (N + rows - 1) // rows if rows > 0 else 0
+    win_ptr = np.zeros(nwin + 1, np.int32)
+    win_nodes = np.zeros(max(nnz, 1), np.int32)
+    lcol = np.zeros(max(nnz, 1), np.uint16)
+    mx = _i32(0)
+    _ok(_graph_windows(N, _ptr(rowptr), _ptr(col), rows, _ptr(win_ptr), _ptr(win_nodes),
+                       _ptr(lcol), C.byref(mx)))
+    return dict(win_ptr=win_ptr, win_nodes=win_nodes[:max(int(win_ptr[-1]), 1)].copy(),
+                lcol=lcol.view(np.int16), max_union=int(mx.value))
+
+
+def add_windows(csr: dict, N: int, rows: int | None = None) -> dict:
+    """Adds the SpMM staging plans of both patterns to a graph_build dict (rows=0: none)."""
+    rows = default_win_rows(N) if rows is None else rows
+    out = dict(csr)
+    if rows <= 0 or csr["a_col"].size == 0:
+        out["win_rows"], out["win_max"] = 0, 0
+        return out
+    a = graph_windows(N, csr["a_rowptr"], csr["a_col"], rows)
+    t = graph_windows(N, csr["at_rowptr"], csr["at_col"], rows)
+    out.update(a_win_ptr=a["win_ptr"], a_win_nodes=a["win_nodes"], a_lcol=a["lcol"],
+               at_win_ptr=t["win_ptr"], at_win_nodes=t["win_nodes"], at_lcol=t["lcol"],
+               win_rows=rows, win_max=max(a["max_union"], t["max_union"]))
+    return out
+
+
 # ------------------------------------------------------------------------------ series
 class Series:
     """Handle over a caller-owned device buffer [nrows][ld] (kept alive here)."""
@@ -215,7 +260,10 @@ class DCRNN:
         nnz = int(self.csr["a_col"].numel()) if csr_dev else 0
         self.desc = DcrnnDesc(N, F, F_out, L, H, K, T_in, T_out, B, precision, ld, nnz,
                               g("a_rowptr"), g("a_col"), g("Pf_val"), g("PbT_val"),
-                              g("at_rowptr"), g("at_col"), g("Pb_val"), g("PfT_val"))
+                              g("at_rowptr"), g("at_col"), g("Pb_val"), g("PfT_val"),
+                              int(self.csr.get("win_rows", 0)), int(self.csr.get("win_max", 0)),
+                              g("a_win_ptr"), g("a_win_nodes"), g("a_lcol"),
+                              g("at_win_ptr"), g("at_win_nodes"), g("at_lcol"))
         self.N, self.F, self.F_out, self.L, self.H, self.K = N, F, F_out, L, H, K
         self.T_in, self.T_out, self.B, self.ld = T_in, T_out, B, ld
 
@@ -253,7 +301,8 @@ class DCRNN:
 
 def csr_to_device(csr: dict, device):
     import torch
-    return {k: torch.from_numpy(v).to(device) for k, v in csr.items()}
+    return {k: torch.from_numpy(v).to(device) if isinstance(v, np.ndarray) else v
+            for k, v in csr.items()}
 
 
 # ------------------------------------------------------------------------------ comm / adam

@@ -88,7 +88,7 @@ class Trainer:
         self.mu, self.sigma = self._stats()
         self.series.normalize(self.mu, self.sigma)
 
-        csr = pgti.graph_build(cfg.N, *graph)
+        csr = pgti.add_windows(pgti.graph_build(cfg.N, *graph), cfg.N)
         self.csr = pgti.csr_to_device(csr, self.dev)
         self.model = pgti.DCRNN(cfg.N, cfg.F, cfg.F_out, cfg.L, cfg.H, cfg.K, cfg.T_in,
                                 cfg.T_out, cfg.B, self.ld, self.csr, precision)

@@ -29,8 +29,10 @@ def load_series(pgti, torch, v_rows, row0, cfg, mu=None, sigma=None):
     return s
 
 
-def model_for(pgti, torch, cfg, graph, precision=0):
-    csr = pgti.csr_to_device(pgti.graph_build(cfg.N, *graph), "cuda")
+def model_for(pgti, torch, cfg, graph, precision=0, win_rows=None):
+    """win_rows: SpMM staging window (None = the library default, 0 = no staging plan)."""
+    csr = pgti.add_windows(pgti.graph_build(cfg.N, *graph), cfg.N, win_rows)
+    csr = pgti.csr_to_device(csr, "cuda")
     return pgti.DCRNN(cfg.N, cfg.F, cfg.F_out, cfg.L, cfg.H, cfg.K, cfg.T_in, cfg.T_out, cfg.B,
                       ld_of(cfg), csr, precision)
 

@@ -69,6 +69,45 @@ def test_graph_build_errors(pgti):
         pgti.graph_build(3, [0], [1], [-1.0])
 
 
+@pytest.mark.parametrize("N,rows,graph", [(207, 16, "knn"), (37, 7, "er"), (100, 1, "knn"),
+                                           (45, 64, "ring"), (2716, 32, "knn")])
+def test_graph_windows_plan(pgti, N, rows, graph):
+    """SpMM staging plan (pgti_graph_windows): each window's list is exactly the sorted set of
+    its rows' columns and lcol maps every CSR entry back to its column (brute force)."""
+    g = {"er": lambda: synth.random_graph(N, 0.15, seed=N), "knn": lambda: synth.make_graph(N, 8),
+         "ring": lambda: synth.ring_graph(N)}[graph]()
+    csr = pgti.graph_build(N, *g)
+    full = pgti.add_windows(csr, N, rows)
+    mx = 0
+    for pat in ("a", "at"):
+        rp, col = csr[pat + "_rowptr"], csr[pat + "_col"]
+        wp, wn = full[pat + "_win_ptr"], full[pat + "_win_nodes"]
+        lc = full[pat + "_lcol"].view(np.uint16)
+        nwin = -(-N // rows)
+        assert wp.shape == (nwin + 1,) and wp[0] == 0
+        for w in range(nwin):
+            r0, r1 = w * rows, min(N, (w + 1) * rows)
+            u = wn[wp[w]:wp[w + 1]]
+            assert np.array_equal(u, np.unique(col[rp[r0]:rp[r1]]))
+            e = np.arange(rp[r0], rp[r1])
+            assert np.array_equal(u[lc[e]], col[e])
+            mx = max(mx, u.size)
+    assert full["win_max"] == mx and full["win_rows"] == rows
+    assert pgti.add_windows(csr, N, 0)["win_rows"] == 0
+
+
+def test_graph_windows_errors(pgti):
+    csr = pgti.graph_build(4, [0, 1], [1, 2], [1.0, 1.0])
+    for rows in (0, 65):
+        with pytest.raises(pgti.PgtiError) as e:
+            pgti.graph_windows(4, csr["a_rowptr"], csr["a_col"], rows)
+        assert e.value.name == "INVALID_ARG"
+    bad = csr["a_col"].copy()
+    bad[0] = 9
+    with pytest.raises(pgti.PgtiError):
+        pgti.graph_windows(4, csr["a_rowptr"], bad, 2)
+
+
 def test_desc_validation_without_gpu(pgti):
     m = pgti.DCRNN(207, 2, 1, 2, 64, 2, 12, 12, 64, 416, None)
     with pytest.raises(pgti.PgtiError):  # K > 0 needs CSR pointers

@@ -184,6 +184,65 @@ def test_diffusion_vs_oracle(env, N, W, K, graph):
     assert scale_rel(dZ.cpu().numpy().reshape(N, W), want) <= 1e-6
 
 
+@pytest.mark.parametrize("N,W,K,graph,rows", [(207, 4096, 2, "knn", 16), (37, 24, 3, "er", 7),
+                                               (300, 128, 2, "knn", 64), (100, 256, 1, "knn", 1),
+                                               (45, 1000, 2, "ring", 32)])
+def test_diffusion_staged_plan_bitexact(env, N, W, K, graph, rows):
+    """The shared-memory staged SpMM (pgti_graph_windows plan) only changes where neighbour rows
+    are read from: forward and adjoint diffusion are bit-identical to the unstaged kernel and
+    match the oracle.  Covers ragged last windows, rows not a multiple of 8, partial chunks."""
+    pgti, torch = env
+    g = {"er": lambda: synth.random_graph(N, 0.15, seed=N),
+         "knn": lambda: synth.make_graph(N, 8),
+         "ring": lambda: synth.ring_graph(N)}[graph]()
+    cfg = synth.Config("d", N=N, E=10, F=1, T_in=1, T_out=1, L=1, H=16, K=K, B=1)
+    staged = model_for(pgti, torch, cfg, g, win_rows=rows)
+    plain = model_for(pgti, torch, cfg, g, win_rows=0)
+    assert staged.desc.win_rows == rows and plain.desc.win_rows == 0
+    Pf, Pb = transitions.transition_matrices(N, *g)
+    rng = np.random.default_rng(1)
+    Z = torch.from_numpy(rng.normal(size=(N, W)).astype(np.float32)).cuda()
+    M = 2 * K + 1
+    outs = []
+    for m in (staged, plain):
+        out = torch.empty(M * N * W, device="cuda")
+        m.diffuse(Z, W, out)
+        outs.append(out.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+    want = dcgru.diffusion_features(Pf, Pb, Z.cpu().numpy().astype(np.float64), K)
+    assert scale_rel(outs[0].reshape(M, N, W), want) <= 1e-6
+    dT = torch.from_numpy(rng.normal(size=(M, N, W)).astype(np.float32)).cuda()
+    adj = []
+    for m in (staged, plain):
+        dZ = torch.empty(N * W, device="cuda")
+        m.diffuse_adjoint(dT, W, dZ)
+        adj.append(dZ.cpu().numpy())
+    assert np.array_equal(adj[0], adj[1])
+    want = dcgru.diffusion_adjoint(Pf, Pb, dT.cpu().numpy().astype(np.float64), K)
+    assert scale_rel(adj[0].reshape(N, W), want) <= 1e-6
+
+
+def test_step_staged_plan_bitexact_both_precisions(env):
+    """Whole training step with and without the SpMM staging plan: identical loss and grads in
+    fp32 and on the bf16 tcgen05 path (where the diffused blocks are bf16)."""
+    pgti, torch = env
+    for precision, cfg in ((0, SMALL_CONFIGS["odd"]), (1, TC_CONFIGS["tc_odd"])):
+        ref = ref_for(cfg)
+        s = load_series(pgti, torch, ref.v, 0, cfg, ref.mu, ref.sigma)
+        idx = torch.arange(cfg.B, dtype=torch.int32, device="cuda") * 3
+        ld = ld_of(cfg)
+        x = torch.empty(cfg.B * cfg.T_in * ld, device="cuda")
+        y = torch.empty(cfg.B * cfg.T_out * ld, device="cuda")
+        s.gather(idx, cfg.B, cfg.T_in, cfg.T_out, x, y)
+        theta = synth.make_params(cfg, kind="random")
+        res = []
+        for rows in (None, 5, 0):
+            model = model_for(pgti, torch, cfg, ref.graph, precision=precision, win_rows=rows)
+            res.append(run_step(pgti, torch, model, theta, x, y, dump=False))
+        for r in res[1:]:
+            assert r[0] == res[0][0] and np.array_equal(r[1], res[0][1]), precision
+
+
 # ------------------------------------------------------------------ full step (K1..K5)
 def _step_case(env, cfg, seed=0, B=None, scale=1.0):
     pgti, torch = env
