@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--profile-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--epoch", action="store_true",
+                    help="also train one full epoch (every rank's shard) and report its time")
     return ap.parse_args()
 
 
@@ -359,6 +361,28 @@ def main():
                        "gather+fwd+bwd+allreduce+Adam, D2H of the loss, host sync",
                "load_s": round(load_s, 3)}
 
+    # ---------------------------------------------------------------- one full epoch
+    epoch = None
+    if args.epoch:
+        tr.start_epoch(2)
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record()
+        for j in range(spe):
+            tr.step(j)
+        ev1.record()
+        torch.cuda.synchronize()
+        tr.check()
+        barrier()
+        ems = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        esec = float(ems.item()) / 1e3
+        epoch = {"steps_per_rank": spe, "samples": world * cfg.B * spe, "seconds": round(esec, 3),
+                 "samples_per_s": round(world * cfg.B * spe / esec, 2),
+                 "loss_last": float(tr.loss.item()),
+                 "what": "epoch 2 of the sharded index range, CUDA-graph steps, max over ranks"}
+
     # ---------------------------------------------------------------- memory + gather
     peak_alloc = torch.cuda.max_memory_allocated(dev) / 1e9
     try:
@@ -399,6 +423,8 @@ def main():
                 "launches_per_step": launches_per_step, "clocks": ck,
                 "kernels": kernels, "eager_ms_per_step": round(eager_ms, 4),
                 "loss_last": loss_last, "steps_per_epoch": spe}
+        if epoch is not None:
+            line["epoch"] = epoch
         emit(line)
     # tear down: drop the captured graph (it holds NCCL kernels) before the communicator
     tr.graph = None

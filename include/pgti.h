@@ -88,6 +88,20 @@ pgti_status pgti_graph_windows(int32_t N, const int32_t *rowptr, const int32_t *
                                int32_t rows_per_window, int32_t *win_ptr, int32_t *win_nodes,
                                uint16_t *lcol, int32_t *max_union);
 
+/* Two-hop operators for the single-launch K = 2 diffusion (reading c20): S = M M
+ * for a CSR M (host arrays) carrying two value arrays val_a, val_b on one
+ * pattern -- called on pattern(A) with (P_f, P_b^T) it yields pattern(A^2) with
+ * (P_f^2, (P_b^2)^T); on pattern(A^T) with (P_b, P_f^T) it yields (P_b^2,
+ * (P_f^2)^T).  Products summed in double, stored as float; the pattern is the
+ * boolean square (explicit zeros kept), columns ascending.  Two calls: with
+ * out_col = NULL only *out_nnz is computed; then out_rowptr [N+1], out_col,
+ * out_val_a, out_val_b [*out_nnz] are filled.  Errors: INVALID_ARG (null,
+ * non-monotone rowptr, column outside [0,N), nnz >= 2^31). */
+pgti_status pgti_graph_square(int32_t N, const int32_t *rowptr, const int32_t *col,
+                              const float *val_a, const float *val_b, int32_t *out_rowptr,
+                              int32_t *out_col, float *out_val_a, float *out_val_b,
+                              int64_t *out_nnz);
+
 /* ----------------------------------------------------------------- the series */
 typedef struct pgti_series pgti_series; /* opaque; BORROWS dev_buf */
 
@@ -184,6 +198,21 @@ typedef struct {
   const uint16_t *a_lcol;
   const int32_t *at_win_ptr, *at_win_nodes; /* pattern(A^T) plan                 */
   const uint16_t *at_lcol;
+  /* Optional two-hop matrices (pgti_graph_square; device CSR, nnz2 entries each):
+   * when set, K = 2 and precision = 1, each diffusion of the step runs as ONE
+   * launch [P_f Z, P_f^2 Z, P_b Z, P_b^2 Z] instead of the hop chain P_f (P_f Z)
+   * (reading c20: same operator, one fewer dependent launch; the bf16 rounding
+   * of the intermediate hop disappears).  Null -> the chain.  Window plans of the
+   * squared patterns are optional as above (win_max then covers all four). */
+  int64_t nnz2;
+  const int32_t *a2_rowptr, *a2_col;   /* pattern(A^2): values P_f^2, (P_b^2)^T   */
+  const float *Pf2_val, *Pb2T_val;
+  const int32_t *at2_rowptr, *at2_col; /* pattern((A^T)^2): P_b^2, (P_f^2)^T      */
+  const float *Pb2_val, *Pf2T_val;
+  const int32_t *a2_win_ptr, *a2_win_nodes;
+  const uint16_t *a2_lcol;
+  const int32_t *at2_win_ptr, *at2_win_nodes;
+  const uint16_t *at2_lcol;
 } pgti_dcrnn_desc;
 
 /* Number of float parameters of the layout above (0 if desc invalid). */

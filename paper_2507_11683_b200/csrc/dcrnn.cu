@@ -68,6 +68,11 @@ pgti_status check_desc(const pgti_dcrnn_desc *desc, Dims *out) {
     PGTI_REQUIRE(g.a_rowptr && g.a_col && g.Pf_val && g.PbT_val && g.at_rowptr && g.at_col &&
                      g.Pb_val && g.PfT_val && g.nnz >= 0,
                  PGTI_ERR_INVALID_ARG, "desc: CSR pointers must be set when K > 0");
+  if (g.a2_rowptr || g.at2_rowptr)
+    PGTI_REQUIRE(g.K == 2 && g.a2_rowptr && g.a2_col && g.Pf2_val && g.Pb2T_val && g.at2_rowptr &&
+                     g.at2_col && g.Pb2_val && g.Pf2T_val && g.nnz2 >= 0,
+                 PGTI_ERR_INVALID_ARG,
+                 "desc: two-hop matrices need K = 2 and all eight pointers (K=%d)", g.K);
   if (g.K > 0 && g.win_rows != 0)
     PGTI_REQUIRE(g.win_rows >= 1 && g.win_rows <= 64 && g.win_max >= 0 && g.a_win_ptr &&
                      g.a_win_nodes && g.a_lcol && g.at_win_ptr && g.at_win_nodes && g.at_lcol,
@@ -85,14 +90,20 @@ namespace {
 // term t of a job: pattern(A) (pat 0) or pattern(A^T) (pat 1) with values val, operand X
 void set_term(SpmmJob &j, int t, const pgti_dcrnn_desc &g, int pat, const float *val,
               const float *X) {
-  j.rowptr[t] = pat ? g.at_rowptr : g.a_rowptr;
-  j.col[t] = pat ? g.at_col : g.a_col;
+  // pat: 0 = pattern(A), 1 = pattern(A^T), 2 = pattern(A^2), 3 = pattern((A^T)^2)
+  const int32_t *rp[4] = {g.a_rowptr, g.at_rowptr, g.a2_rowptr, g.at2_rowptr};
+  const int32_t *cl[4] = {g.a_col, g.at_col, g.a2_col, g.at2_col};
+  const int32_t *wp[4] = {g.a_win_ptr, g.at_win_ptr, g.a2_win_ptr, g.at2_win_ptr};
+  const int32_t *wn[4] = {g.a_win_nodes, g.at_win_nodes, g.a2_win_nodes, g.at2_win_nodes};
+  const uint16_t *lc[4] = {g.a_lcol, g.at_lcol, g.a2_lcol, g.at2_lcol};
+  j.rowptr[t] = rp[pat];
+  j.col[t] = cl[pat];
   j.val[t] = val;
   j.X[t] = X;
-  j.nnz[t] = g.nnz;
-  j.win_ptr[t] = pat ? g.at_win_ptr : g.a_win_ptr;
-  j.win_nodes[t] = pat ? g.at_win_nodes : g.a_win_nodes;
-  j.lcol[t] = pat ? g.at_lcol : g.a_lcol;
+  j.nnz[t] = pat < 2 ? g.nnz : g.nnz2;
+  j.win_ptr[t] = wp[pat];
+  j.win_nodes[t] = wn[pat];
+  j.lcol[t] = lc[pat];
   j.win_rows = g.win_rows, j.win_max = g.win_max;
 }
 }  // namespace
@@ -104,6 +115,22 @@ cudaError_t diffuse_fwd(const pgti_dcrnn_desc &g, const Dims &d, float *base, in
   char *b = reinterpret_cast<char *>(base);
   const char *z = src0 ? static_cast<const char *>(src0) : b;
   auto blk = [&](int m) { return b + int64_t(m) * mstride * es; };
+  if (d.K == 2 && bf16 && g.a2_rowptr) {  // one launch: [P Z, P^2 Z] for both directions
+    SpmmJob j[4] = {};
+    const float *x0 = reinterpret_cast<const float *>(z);
+    if (!transposed) {
+      set_term(j[0], 0, g, 0, g.Pf_val, x0), set_term(j[1], 0, g, 2, g.Pf2_val, x0);
+      set_term(j[2], 0, g, 1, g.Pb_val, x0), set_term(j[3], 0, g, 3, g.Pb2_val, x0);
+    } else {
+      set_term(j[0], 0, g, 1, g.PfT_val, x0), set_term(j[1], 0, g, 3, g.Pf2T_val, x0);
+      set_term(j[2], 0, g, 0, g.PbT_val, x0), set_term(j[3], 0, g, 2, g.Pb2T_val, x0);
+    }
+    for (int q = 0; q < 4; ++q) {
+      j[q].Y = reinterpret_cast<float *>(blk(q + 1));
+      j[q].nterms = 1, j[q].W = W, j[q].G = G, j[q].gstride = gstride, j[q].bf16 = bf16;
+    }
+    return launch_spmm(j, 4, d.N, s);
+  }
   for (int k = 1; k <= d.K; ++k) {
     SpmmJob j[2] = {};
     const float *xf = reinterpret_cast<const float *>(k == 1 ? z : blk(k - 1));

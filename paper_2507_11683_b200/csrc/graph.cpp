@@ -109,3 +109,53 @@ extern "C" pgti_status pgti_graph_windows(int32_t N, const int32_t *rowptr, cons
   *max_union = mx;
   return PGTI_OK;
 }
+
+// Two-hop transition matrices for the single-launch K = 2 diffusion of the tensor-core path:
+// S = M M for a CSR M carrying two value arrays on one pattern (pattern(A): P_f, P_b^T ->
+// P_f^2, (P_b^2)^T; pattern(A^T): P_b, P_f^T -> P_b^2, (P_f^2)^T).  Products are summed in
+// double and stored as float; the structural pattern is that of the boolean square (entries
+// whose products are all zero are kept as explicit zeros), so both value arrays share it.
+extern "C" pgti_status pgti_graph_square(int32_t N, const int32_t *rowptr, const int32_t *col,
+                                         const float *val_a, const float *val_b,
+                                         int32_t *out_rowptr, int32_t *out_col,
+                                         float *out_val_a, float *out_val_b, int64_t *out_nnz) {
+  pgti::clear_error();
+  PGTI_REQUIRE(N > 0 && rowptr && out_nnz && (rowptr[N] == 0 || (col && val_a && val_b)),
+               PGTI_ERR_INVALID_ARG, "pgti_graph_square: null pointer or N=%d", N);
+  const bool fill = out_col != nullptr;
+  PGTI_REQUIRE(!fill || (out_rowptr && out_val_a && out_val_b), PGTI_ERR_INVALID_ARG,
+               "pgti_graph_square: out_col set but out_rowptr / out_val_* null");
+  for (int32_t i = 0; i < N; ++i)
+    PGTI_REQUIRE(rowptr[i + 1] >= rowptr[i], PGTI_ERR_INVALID_ARG, "rowptr not monotone at %d", i);
+  for (int64_t e = 0; e < rowptr[N]; ++e)
+    PGTI_REQUIRE(col[e] >= 0 && col[e] < N, PGTI_ERR_INVALID_ARG, "column %d outside [0, %d)",
+                 col[e], N);
+  std::vector<double> acc_a(N, 0.0), acc_b(N, 0.0);
+  std::vector<int32_t> mark(N, -1), cols;
+  int64_t nnz = 0;
+  if (fill) out_rowptr[0] = 0;
+  for (int32_t i = 0; i < N; ++i) {
+    cols.clear();
+    for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+      const int32_t j = col[e];
+      for (int64_t f = rowptr[j]; f < rowptr[j + 1]; ++f) {
+        const int32_t k = col[f];
+        if (mark[k] != i) mark[k] = i, cols.push_back(k), acc_a[k] = acc_b[k] = 0.0;
+        acc_a[k] += double(val_a[e]) * double(val_a[f]);
+        acc_b[k] += double(val_b[e]) * double(val_b[f]);
+      }
+    }
+    std::sort(cols.begin(), cols.end());
+    if (fill)
+      for (size_t q = 0; q < cols.size(); ++q) {
+        out_col[nnz + int64_t(q)] = cols[q];
+        out_val_a[nnz + int64_t(q)] = float(acc_a[cols[q]]);
+        out_val_b[nnz + int64_t(q)] = float(acc_b[cols[q]]);
+      }
+    nnz += int64_t(cols.size());
+    PGTI_REQUIRE(nnz < (int64_t(1) << 31), PGTI_ERR_INVALID_ARG, "squared nnz exceeds int32");
+    if (fill) out_rowptr[i + 1] = int32_t(nnz);
+  }
+  *out_nnz = nnz;
+  return PGTI_OK;
+}

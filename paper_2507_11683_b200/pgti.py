@@ -44,7 +44,12 @@ class DcrnnDesc(C.Structure):
                 ("at_rowptr", _vp), ("at_col", _vp), ("Pb_val", _vp), ("PfT_val", _vp),
                 ("win_rows", _i32), ("win_max", _i32),
                 ("a_win_ptr", _vp), ("a_win_nodes", _vp), ("a_lcol", _vp),
-                ("at_win_ptr", _vp), ("at_win_nodes", _vp), ("at_lcol", _vp)]
+                ("at_win_ptr", _vp), ("at_win_nodes", _vp), ("at_lcol", _vp),
+                ("nnz2", _i64),
+                ("a2_rowptr", _vp), ("a2_col", _vp), ("Pf2_val", _vp), ("Pb2T_val", _vp),
+                ("at2_rowptr", _vp), ("at2_col", _vp), ("Pb2_val", _vp), ("Pf2T_val", _vp),
+                ("a2_win_ptr", _vp), ("a2_win_nodes", _vp), ("a2_lcol", _vp),
+                ("at2_win_ptr", _vp), ("at2_win_nodes", _vp), ("at2_lcol", _vp)]
 
 
 def _sig(name, restype, *argtypes):
@@ -61,6 +66,8 @@ _graph_build = _sig("pgti_graph_build", C.c_int, _i32, _i64, _vp, _vp, _vp, _vp,
                     _vp, _vp, _vp, _vp)
 _graph_windows = _sig("pgti_graph_windows", C.c_int, _i32, _vp, _vp, _i32, _vp, _vp, _vp,
                       C.POINTER(_i32))
+_graph_square = _sig("pgti_graph_square", C.c_int, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                     C.POINTER(_i64))
 _load = _sig("pgti_load_series", C.c_int, C.POINTER(_vp), _vp, _i64, _i64, _i64, _i64, _vp, _i64,
              _vp)
 _stats = _sig("pgti_series_stats", C.c_int, _vp, _i64, C.c_int, _i64, _i64, _f64, _vp, _vp)
@@ -186,18 +193,52 @@ def graph_windows(N: int, rowptr, col, rows: int) -> dict:
                 lcol=lcol.view(np.int16), max_union=int(mx.value))
 
 
+def graph_square(N: int, rowptr, col, val_a, val_b) -> tuple:
+    """pgti_graph_square: (rowptr, col, val_a^2, val_b^2) of the two-hop operators."""
+    rowptr = np.ascontiguousarray(rowptr, np.int32)
+    col = np.ascontiguousarray(col, np.int32)
+    val_a = np.ascontiguousarray(val_a, np.float32)
+    val_b = np.ascontiguousarray(val_b, np.float32)
+    nnz = _i64(0)
+    _ok(_graph_square(N, _ptr(rowptr), _ptr(col), _ptr(val_a), _ptr(val_b), None, None, None,
+                      None, C.byref(nnz)))
+    n = int(nnz.value)
+    orp = np.zeros(N + 1, np.int32)
+    oc, oa, ob = np.zeros(max(n, 1), np.int32), np.zeros(max(n, 1), np.float32), \
+        np.zeros(max(n, 1), np.float32)
+    _ok(_graph_square(N, _ptr(rowptr), _ptr(col), _ptr(val_a), _ptr(val_b), _ptr(orp), _ptr(oc),
+                      _ptr(oa), _ptr(ob), C.byref(nnz)))
+    return orp, oc[:n], oa[:n], ob[:n]
+
+
+def add_squares(csr: dict, N: int) -> dict:
+    """Adds the two-hop operators (P_f^2, (P_b^2)^T on pattern(A^2); P_b^2, (P_f^2)^T on
+    pattern((A^T)^2)) that let the K = 2 tensor-core path diffuse in one launch."""
+    out = dict(csr)
+    out["a2_rowptr"], out["a2_col"], out["Pf2_val"], out["Pb2T_val"] = graph_square(
+        N, csr["a_rowptr"], csr["a_col"], csr["Pf_val"], csr["PbT_val"])
+    out["at2_rowptr"], out["at2_col"], out["Pb2_val"], out["Pf2T_val"] = graph_square(
+        N, csr["at_rowptr"], csr["at_col"], csr["Pb_val"], csr["PfT_val"])
+    return out
+
+
 def add_windows(csr: dict, N: int, rows: int | None = None) -> dict:
-    """Adds the SpMM staging plans of both patterns to a graph_build dict (rows=0: none)."""
+    """Adds the SpMM staging plans of every pattern present (one-hop, and two-hop if
+    add_squares ran) to a graph_build dict (rows=0: none)."""
     rows = default_win_rows(N) if rows is None else rows
     out = dict(csr)
     if rows <= 0 or csr["a_col"].size == 0:
         out["win_rows"], out["win_max"] = 0, 0
         return out
-    a = graph_windows(N, csr["a_rowptr"], csr["a_col"], rows)
-    t = graph_windows(N, csr["at_rowptr"], csr["at_col"], rows)
-    out.update(a_win_ptr=a["win_ptr"], a_win_nodes=a["win_nodes"], a_lcol=a["lcol"],
-               at_win_ptr=t["win_ptr"], at_win_nodes=t["win_nodes"], at_lcol=t["lcol"],
-               win_rows=rows, win_max=max(a["max_union"], t["max_union"]))
+    mx = 0
+    for pat in ("a", "at", "a2", "at2"):
+        if pat + "_rowptr" not in csr:
+            continue
+        w = graph_windows(N, csr[pat + "_rowptr"], csr[pat + "_col"], rows)
+        out[pat + "_win_ptr"], out[pat + "_win_nodes"] = w["win_ptr"], w["win_nodes"]
+        out[pat + "_lcol"] = w["lcol"]
+        mx = max(mx, w["max_union"])
+    out["win_rows"], out["win_max"] = rows, mx
     return out
 
 
@@ -263,7 +304,12 @@ class DCRNN:
                               g("at_rowptr"), g("at_col"), g("Pb_val"), g("PfT_val"),
                               int(self.csr.get("win_rows", 0)), int(self.csr.get("win_max", 0)),
                               g("a_win_ptr"), g("a_win_nodes"), g("a_lcol"),
-                              g("at_win_ptr"), g("at_win_nodes"), g("at_lcol"))
+                              g("at_win_ptr"), g("at_win_nodes"), g("at_lcol"),
+                              int(self.csr["a2_col"].numel()) if "a2_col" in self.csr else 0,
+                              g("a2_rowptr"), g("a2_col"), g("Pf2_val"), g("Pb2T_val"),
+                              g("at2_rowptr"), g("at2_col"), g("Pb2_val"), g("Pf2T_val"),
+                              g("a2_win_ptr"), g("a2_win_nodes"), g("a2_lcol"),
+                              g("at2_win_ptr"), g("at2_win_nodes"), g("at2_lcol"))
         self.N, self.F, self.F_out, self.L, self.H, self.K = N, F, F_out, L, H, K
         self.T_in, self.T_out, self.B, self.ld = T_in, T_out, B, ld
 

@@ -65,7 +65,8 @@ class Trainer:
     """
 
     def __init__(self, cfg, graph, series_fn, params0, rank=0, world=1, device=0, comm=None,
-                 seed=3, lr=1e-2, precision=0, shuffle=True, use_cuda_graph=True):
+                 seed=3, lr=1e-2, precision=0, shuffle=True, use_cuda_graph=True,
+                 two_hop=False):
         import torch
 
         self.torch = torch
@@ -88,7 +89,10 @@ class Trainer:
         self.mu, self.sigma = self._stats()
         self.series.normalize(self.mu, self.sigma)
 
-        csr = pgti.add_windows(pgti.graph_build(cfg.N, *graph), cfg.N)
+        csr = pgti.graph_build(cfg.N, *graph)
+        if two_hop and cfg.K == 2 and precision == 1:  # one-launch two-hop diffusion (c20)
+            csr = pgti.add_squares(csr, cfg.N)
+        csr = pgti.add_windows(csr, cfg.N)
         self.csr = pgti.csr_to_device(csr, self.dev)
         self.model = pgti.DCRNN(cfg.N, cfg.F, cfg.F_out, cfg.L, cfg.H, cfg.K, cfg.T_in,
                                 cfg.T_out, cfg.B, self.ld, self.csr, precision)

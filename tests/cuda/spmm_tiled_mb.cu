@@ -69,6 +69,36 @@ __global__ void __launch_bounds__(256) kOld(const int *rp, const int *ci, const 
   *reinterpret_cast<uint4 *>(Y + size_t(n) * W + col0) = pack(acc);
 }
 
+// global gather with all of a row's loads in flight: CSR entries first (predicated), then up to
+// U neighbour slices, then the FMAs in CSR order
+template <int U>
+__global__ void __launch_bounds__(256) kOldU(const int *rp, const int *ci, const float *va,
+                                             const bf16 *X, bf16 *Y, int N, int W) {
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, vecs = W / 8;
+  if (tid >= N * vecs) return;
+  const int n = tid / vecs, col0 = (tid % vecs) * 8;
+  const bf16 *Xc = X + col0;
+  float2 acc[4] = {};
+  const int beg = __ldg(rp + n), end = __ldg(rp + n + 1);
+  for (int e0 = beg; e0 < end; e0 += U) {
+    int c[U];
+    float w[U];
+    uint4 x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      c[u] = e0 + u < end ? __ldg(ci + e0 + u) : 0;
+      w[u] = e0 + u < end ? __ldg(va + e0 + u) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (e0 + u < end) x[u] = __ldg(reinterpret_cast<const uint4 *>(Xc + size_t(c[u]) * W));
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (e0 + u < end) fma8(acc, w[u], x[u]);
+  }
+  *reinterpret_cast<uint4 *>(Y + size_t(n) * W + col0) = pack(acc);
+}
+
 struct Plan {
   const int *rp;
   const float *va;
@@ -215,6 +245,12 @@ int main(int argc, char **argv) {
     kCopy<<<unsigned((nel / 8 + 255) / 256), 256>>>((const uint4 *)X, (uint4 *)Y, nel / 8);
   });
   time("global gather (old)", [&] { kOld<<<unsigned((N * vecs + 255) / 256), 256>>>(d_rp, d_ci, d_va, X, Y0, N, W); });
+  time("global gather U=8", [&] { kOldU<8><<<unsigned((N * vecs + 255) / 256), 256>>>(d_rp, d_ci, d_va, X, Y, N, W); });
+  check("U=8");
+  time("global gather U=12", [&] { kOldU<12><<<unsigned((N * vecs + 255) / 256), 256>>>(d_rp, d_ci, d_va, X, Y, N, W); });
+  check("U=12");
+  time("global gather U=16 128thr", [&] { kOldU<16><<<unsigned((N * vecs + 127) / 128), 128>>>(d_rp, d_ci, d_va, X, Y, N, W); });
+  check("U=16");
   const int nchunk = (vecs + 31) / 32;
   for (int rows : {16, 32, 64}) {
     const int nwin = (N + rows - 1) / rows;

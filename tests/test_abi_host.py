@@ -96,6 +96,42 @@ def test_graph_windows_plan(pgti, N, rows, graph):
     assert pgti.add_windows(csr, N, 0)["win_rows"] == 0
 
 
+@pytest.mark.parametrize("N,graph", [(207, "knn"), (37, "er"), (45, "ring"), (1, "er")])
+def test_graph_square_matches_oracle_powers(pgti, N, graph):
+    """Two-hop operators (reading c20) against the oracle's dense P_f, P_b squared in float64:
+    P_f^2 and (P_b^2)^T on pattern(A^2), P_b^2 and (P_f^2)^T on pattern((A^T)^2)."""
+    g = {"er": lambda: synth.random_graph(N, 0.15, seed=N), "knn": lambda: synth.make_graph(N, 8),
+         "ring": lambda: synth.ring_graph(N)}[graph]()
+    csr = pgti.add_squares(pgti.graph_build(N, *g), N)
+    Pf, Pb = transitions.transition_matrices(N, *g)
+    Pf, Pb = np.asarray(Pf.todense() if hasattr(Pf, "todense") else Pf), \
+        np.asarray(Pb.todense() if hasattr(Pb, "todense") else Pb)
+
+    def dense(rp, col, val):
+        D = np.zeros((N, N))
+        for i in range(N):
+            assert np.all(np.diff(col[rp[i]:rp[i + 1]]) > 0)  # ascending, no duplicates
+            D[i, col[rp[i]:rp[i + 1]]] = val[rp[i]:rp[i + 1]]
+        return D
+    for (pat, va, vb), (A, Bm) in ((("a2", "Pf2_val", "Pb2T_val"), (Pf @ Pf, (Pb @ Pb).T)),
+                                   (("at2", "Pb2_val", "Pf2T_val"), (Pb @ Pb, (Pf @ Pf).T))):
+        rp, col = csr[pat + "_rowptr"], csr[pat + "_col"]
+        assert rp[-1] == col.size
+        for name, want in ((va, A), (vb, Bm)):
+            got = dense(rp, col, csr[name])
+            assert np.abs(got - want).max() <= 1e-6 * max(1.0, np.abs(want).max()), name
+        # the pattern is the boolean square of the one-hop pattern (explicit zeros included)
+        one = pat[:-1]
+        S = np.zeros((N, N), bool)
+        for i in range(N):
+            S[i, csr[one + "_col"][csr[one + "_rowptr"][i]:csr[one + "_rowptr"][i + 1]]] = True
+        S2 = (S.astype(np.int64) @ S.astype(np.int64)) > 0
+        got = np.zeros((N, N), bool)
+        for i in range(N):
+            got[i, col[rp[i]:rp[i + 1]]] = True
+        assert np.array_equal(got, S2)
+
+
 def test_graph_windows_errors(pgti):
     csr = pgti.graph_build(4, [0, 1], [1, 2], [1.0, 1.0])
     for rows in (0, 65):

@@ -417,7 +417,7 @@ TC_CONFIGS = {
 }
 
 
-def _step_case_tc(env, cfg, B=None, seed=0):
+def _step_case_tc(env, cfg, B=None, seed=0, two_hop=False, win_rows=None):
     pgti, torch = env
     B = B or cfg.B
     cfg = cfg.replace(B=B)
@@ -429,7 +429,8 @@ def _step_case_tc(env, cfg, B=None, seed=0):
     x = torch.empty(B * cfg.T_in * ld, device="cuda")
     y = torch.empty(B * cfg.T_out * ld, device="cuda")
     s.gather(idx, B, cfg.T_in, cfg.T_out, x, y)
-    model = model_for(pgti, torch, cfg, ref.graph, precision=1)
+    model = model_for(pgti, torch, cfg, ref.graph, precision=1, two_hop=two_hop,
+                      win_rows=win_rows)
     theta = synth.make_params(cfg, seed=synth.SEED_PARAMS + seed, kind="random")
     loss, g, act = run_step(pgti, torch, model, theta, x, y)
     xo, yo = ref.batch(idx_np)
@@ -448,3 +449,16 @@ def test_step_parity_bf16_small(env, name):
 @pytest.mark.parametrize("name,B", [("metr_la", 64), ("pems_bay", 16)])
 def test_step_parity_bf16_traffic(env, name, B):
     _check_step(_step_case_tc(env, synth.CONFIGS[name], B=B), tol=TOL_BF16)
+
+
+@pytest.mark.parametrize("name,B,two_hop,win_rows", [("tc_tiny", None, True, 0),
+                                                      ("tc_big", None, True, None),
+                                                      ("tc_big", None, True, 16),
+                                                      ("tc_big", None, False, 16),
+                                                      ("metr_la", 64, True, 0),
+                                                      ("metr_la", 64, True, 32)])
+def test_step_parity_bf16_diffusion_variants(env, name, B, two_hop, win_rows):
+    """The bf16 path with the single-launch two-hop operators (P^2, reading c20) and with
+    staged SpMM (window plans, also of the squared patterns)."""
+    cfg = TC_CONFIGS.get(name) or synth.CONFIGS[name]
+    _check_step(_step_case_tc(env, cfg, B=B, two_hop=two_hop, win_rows=win_rows), tol=TOL_BF16)
