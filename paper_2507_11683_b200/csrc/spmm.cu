@@ -150,7 +150,7 @@ constexpr int kWinMaxSmem = 192 * 1024;
 
 struct WinParams {
   SpmmJob job[kMaxSpmmJobs];
-  int block_begin[kMaxSpmmJobs + 1];
+  int z_begin[kMaxSpmmJobs + 1];  // grid.z slots of job j: [z_begin[j], z_begin[j+1]) = groups
   int nchunk[kMaxSpmmJobs];
   int vecs[kMaxSpmmJobs];
   int njobs, N, nwin, win_rows, win_max;
@@ -161,22 +161,21 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(g) : "memory");
 }
 
+// grid = (512-byte column chunk, window, job x group): decoded without integer division
 template <typename T, int RPW>
 __global__ void __launch_bounds__(256) k_spmm_win(const __grid_constant__ WinParams p) {
   using L = Lane<T>;
   constexpr int V = L::V, P = V / 2;
   extern __shared__ uint4 stage[];  // [union][32]
-  const int bid = int(blockIdx.x);
+  const int z = int(blockIdx.z);
   int j = 0;
 #pragma unroll
   for (int q = 1; q < kMaxSpmmJobs; ++q)
-    if (q < p.njobs && bid >= p.block_begin[q]) j = q;
+    if (q < p.njobs && z >= p.z_begin[q]) j = q;
+  const int chunk = int(blockIdx.x);
+  if (chunk >= p.nchunk[j]) return;  // jobs narrower than the widest one
   const SpmmJob &jb = p.job[j];
-  int rem = bid - p.block_begin[j];
-  const int nchunk = p.nchunk[j];
-  const int chunk = rem % nchunk;
-  rem /= nchunk;
-  const int win = rem % p.nwin, g = rem / p.nwin;
+  const int g = z - p.z_begin[j], win = int(blockIdx.y);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int vec = chunk * 32 + lane;
   const bool act = vec < p.vecs[j];
@@ -327,25 +326,30 @@ cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s) {
     win = j.nterms >= 1 && j.win_rows == jobs[0].win_rows && j.win_max == jobs[0].win_max;
     for (int t = 0; t < j.nterms && win; ++t) win = j.win_ptr[t] && j.win_nodes[t] && j.lcol[t];
   }
+  WinParams w{};
+  int nz = 0, maxc = 0;
   if (win) {
-    WinParams w{};
     w.njobs = njobs, w.N = N, w.win_rows = jobs[0].win_rows, w.win_max = jobs[0].win_max;
     w.nwin = int(ceil_div(N, w.win_rows));
-    int64_t nb = 0;
     for (int i = 0; i < njobs; ++i) {
       w.job[i] = jobs[i];
       w.vecs[i] = int(jobs[i].W / V);
       w.nchunk[i] = int(ceil_div(w.vecs[i], 32));
-      w.block_begin[i] = int(nb);
-      nb += int64_t(jobs[i].G) * w.nwin * w.nchunk[i];
+      w.z_begin[i] = nz;
+      nz += jobs[i].G;
+      maxc = std::max(maxc, w.nchunk[i]);
     }
-    w.block_begin[njobs] = int(nb);
+    w.z_begin[njobs] = nz;
+    if (nz > 65535 || w.nwin > 65535) win = false;
+  }
+  if (win) {
+    const dim3 grid(unsigned(maxc), unsigned(w.nwin), unsigned(nz));
     const int smem = jobs[0].win_max * 516;  // staged rows + their node ids
     const int rpw = (w.win_rows + 7) / 8;
     auto go = [&](auto kernel) -> cudaError_t {
       cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return e;
-      kernel<<<unsigned(nb), 256, smem, s>>>(w);
+      kernel<<<grid, 256, smem, s>>>(w);
       return cudaGetLastError();
     };
     if (bf) {

@@ -7,7 +7,9 @@
 //                pipeline stages are reused) -> coalesced element-wise math and global I/O
 //                (consecutive threads touch consecutive columns of a row).
 //   k_tc_wgrad : split-K weight gradient, MN-major A (diffusion blocks) and B (gate gradients)
-// 4-stage mbarrier ring between TMA and MMA (full / empty), one commit barrier MMA -> epilogue.
+// mbarrier ring between TMA and MMA (full / empty; 4 stages, 3 for two-sub-tile CTAs so two
+// CTAs fit per SM and one's epilogue overlaps the other's main loop), one commit barrier
+// MMA -> epilogue.
 // Equations: Li et al. Eq. 2-3 [ext], PAPER.md P:168, P:222 (readings c1-c7).
 #include <cudaTypedefs.h>
 
@@ -32,9 +34,9 @@ struct Barriers {
   uint32_t tmem;
 };
 
-template <int A_BYTES, int B_BYTES>
+template <int A_BYTES, int B_BYTES, int NST = kStages>
 __device__ __forceinline__ Barriers *carve(uint8_t *smem) {
-  return reinterpret_cast<Barriers *>(smem + kStages * (A_BYTES + B_BYTES));
+  return reinterpret_cast<Barriers *>(smem + NST * (A_BYTES + B_BYTES));
 }
 
 __device__ __forceinline__ uint8_t *align1024(uint8_t *p) {
@@ -75,6 +77,7 @@ __device__ __forceinline__ void st4_bf16(bf16 *p, float4 v) {
 
 // ================================================================== multi-block GEMM
 constexpr int kFwdThreads = 320, kEpiThreads = 256;
+constexpr int fwd_stages(int nsub) { return nsub == 2 ? 3 : 4; }
 constexpr int kTileLd = 68;  // shared epilogue tile pitch (floats): 16-byte rows, spread banks
 
 __device__ __forceinline__ void epi_bar() {
@@ -85,15 +88,17 @@ __device__ __forceinline__ void epi_bar() {
 // both the r and u halves of the gate / the input and hidden tiles of the backward GEMM).
 // MODE (kEpiGate / kEpiCand / kEpiBwd) is compile-time so each epilogue gets its own registers.
 template <int NSUB, int MODE>
-__global__ void __launch_bounds__(kFwdThreads, NSUB == 1 ? 2 : 1)
+__global__ void __launch_bounds__(kFwdThreads, 2)
     k_tc_fwd(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
              const __grid_constant__ CUtensorMap mB, const __grid_constant__ TcFwd p) {
   constexpr int NT = 64 * NSUB;
   constexpr int A_BYTES = kBM * kBK * 2, B_BYTES = NT * kBK * 2, STAGE = A_BYTES + B_BYTES;
+  constexpr int kStages = fwd_stages(NSUB);  // two CTAs per SM: one's epilogue overlaps the
+                                             // other's main loop
   static_assert(kStages * STAGE >= kBM * kTileLd * 4, "epilogue tile reuses the stage buffers");
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
-  Barriers *bar = carve<A_BYTES, B_BYTES>(smem);
+  Barriers *bar = carve<A_BYTES, B_BYTES, kStages>(smem);
   float *wx_s = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(bar) + 256);  // [20][64]
   float *tile_s = reinterpret_cast<float *>(smem);                                  // [128][68]
   float *xs_s = tile_s + kBM * kTileLd;                                             // [128][<=20]
@@ -393,7 +398,7 @@ cudaError_t set_smem(K kernel, int bytes) {
 
 constexpr int wg_smem_bytes(int b_rows) { return kStages * (kBM * kBK * 2 + b_rows * kBK * 2) + 1024 + 256; }
 constexpr int fwd_smem_bytes(int nsub) {
-  return kStages * (kBM * kBK * 2 + 64 * nsub * kBK * 2) + 1024 + 256 + 20 * 64 * 4;
+  return fwd_stages(nsub) * (kBM * kBK * 2 + 64 * nsub * kBK * 2) + 1024 + 256 + 20 * 64 * 4;
 }
 
 }  // namespace

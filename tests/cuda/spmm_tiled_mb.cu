@@ -104,7 +104,7 @@ struct Plan {
   const float *va;
   const int *wptr, *wnodes;
   const uint16_t *lcol;
-  int N, W, rows, nwin, maxu;
+  int N, W, rows, nwin, maxu, maxe;
 };
 
 // staged, CPB chunks per CTA, NBUF stage buffers (NBUF = 2: chunk c+1 staged while c computes).
@@ -178,6 +178,58 @@ __global__ void __launch_bounds__(256) kWin(const Plan p, const bf16 *X, bf16 *Y
       if (vec < vecs) *reinterpret_cast<uint4 *>(Y + size_t(n) * p.W + size_t(vec) * 8) = pack(acc);
     }
     __syncthreads();  // buffer free before it is re-staged
+  }
+}
+
+// v3: 2-D grid (x = 512-byte chunk, y = window: no integer division), the window's CSR staged in
+// shared memory as (byte offset into the stage, value) pairs, read back with one broadcast LDS.64
+// per entry; one chunk per CTA.
+template <int RPW>
+__global__ void __launch_bounds__(256) kWin3(const Plan p, const bf16 *X, bf16 *Y) {
+  extern __shared__ uint4 sm[];
+  const int vecs = p.W / 8;
+  const int chunk = blockIdx.x, win = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row0 = win * p.rows, nrows = min(p.rows, p.N - row0);
+  const int ub = __ldg(p.wptr + win), nu = __ldg(p.wptr + win + 1) - ub;
+  const int e0 = __ldg(p.rp + row0), e1 = __ldg(p.rp + row0 + nrows);
+  uint4 *stage = sm;
+  int *s_nodes = reinterpret_cast<int *>(sm + p.maxu * 32);
+  int2 *s_ent = reinterpret_cast<int2 *>(s_nodes + p.maxu + (p.maxu & 1));
+  int *s_rp = reinterpret_cast<int *>(s_ent + p.maxe);
+  for (int i = threadIdx.x; i < nu; i += 256) s_nodes[i] = __ldg(p.wnodes + ub + i);
+  for (int i = threadIdx.x; i < e1 - e0; i += 256)
+    s_ent[i] = make_int2(int(__ldg(p.lcol + e0 + i)) * 512, __float_as_int(__ldg(p.va + e0 + i)));
+  for (int i = threadIdx.x; i <= nrows; i += 256) s_rp[i] = __ldg(p.rp + row0 + i) - e0;
+  __syncthreads();
+  const int vec = chunk * 32 + lane;
+  const bool act = vec < vecs;
+  if (act) {
+    const bf16 *Xc = X + size_t(vec) * 8;
+    for (int k = warp; k < nu; k += 8) cp_async16(stage + k * 32 + lane, Xc + size_t(s_nodes[k]) * p.W);
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  const char *sb = reinterpret_cast<const char *>(stage) + lane * 16;
+#pragma unroll
+  for (int i = 0; i < RPW; ++i) {
+    const int r = warp + 8 * i;
+    if (r >= nrows) break;
+    float2 acc[4] = {};
+    const int b = s_rp[r], e = s_rp[r + 1];
+    int q = b;
+    for (; q + 2 <= e; q += 2) {
+      const int2 a0 = s_ent[q], a1 = s_ent[q + 1];
+      const uint4 x0 = *reinterpret_cast<const uint4 *>(sb + a0.x);
+      const uint4 x1 = *reinterpret_cast<const uint4 *>(sb + a1.x);
+      fma8(acc, __int_as_float(a0.y), x0);
+      fma8(acc, __int_as_float(a1.y), x1);
+    }
+    if (q < e) {
+      const int2 a0 = s_ent[q];
+      fma8(acc, __int_as_float(a0.y), *reinterpret_cast<const uint4 *>(sb + a0.x));
+    }
+    if (act) *reinterpret_cast<uint4 *>(Y + size_t(row0 + r) * p.W + size_t(vec) * 8) = pack(acc);
   }
 }
 
@@ -276,7 +328,9 @@ int main(int argc, char **argv) {
     CK(cudaMemcpy(d_wp, wptr.data(), wptr.size() * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(d_wn, wn.data(), wn.size() * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(d_lc, lc.data(), lc.size() * 2, cudaMemcpyHostToDevice));
-    Plan p{d_rp, d_va, d_wp, d_wn, d_lc, N, W, rows, nwin, maxu};
+    int maxe = 0;
+    for (int w = 0; w < nwin; ++w) maxe = std::max(maxe, rp[std::min(N, (w + 1) * rows)] - rp[w * rows]);
+    Plan p{d_rp, d_va, d_wp, d_wn, d_lc, N, W, rows, nwin, maxu, maxe};
     printf("rows=%d maxu=%d union/rows=%.2f\n", rows, maxu, double(wn.size()) / N);
 #define RUN(RPW, CPB, NBUF)                                                                      \
   if ((rows + 7) / 8 == RPW) {                                                                   \
@@ -288,9 +342,17 @@ int main(int argc, char **argv) {
     time(nm, [&] { kWin<RPW, CPB, NBUF><<<grid, 256, smem>>>(p, X, Y); });                       \
     check(nm);                                                                                   \
   }
-    RUN(2, 1, 1) RUN(2, 2, 2) RUN(2, 4, 2) RUN(2, 16, 2) RUN(2, 4, 3)
-    RUN(4, 1, 1) RUN(4, 2, 2) RUN(4, 4, 2) RUN(4, 16, 2) RUN(4, 4, 3)
-    RUN(8, 1, 1) RUN(8, 2, 2) RUN(8, 4, 2) RUN(8, 16, 2)
+    RUN(2, 1, 1) RUN(4, 1, 1) RUN(8, 1, 1)
+#define RUN3(RPW)                                                                                \
+  if ((rows + 7) / 8 == RPW) {                                                                   \
+    const int smem = maxu * 512 + (maxu + 1) * 4 + maxe * 8 + (rows + 1) * 4 + 16;               \
+    CK(cudaFuncSetAttribute(kWin3<RPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));    \
+    char nm[64];                                                                                 \
+    snprintf(nm, 64, "  v3 RPW=%d (%d CTAs)", RPW, nwin * nchunk);                               \
+    time(nm, [&] { kWin3<RPW><<<dim3(nchunk, nwin), 256, smem>>>(p, X, Y); });                   \
+    check(nm);                                                                                   \
+  }
+    RUN3(2) RUN3(4) RUN3(8)
   }
   return 0;
 }
