@@ -331,6 +331,15 @@ def main():
                 "frac": round(ach / pk, 4), "traffic": None, "kernel": dom, "peak_source": src}
     roof["share_of_step"] = round(d["ms"] / P / eager_ms, 4)
     roof["per_launch_ms"] = round(d["ms"] / d["launches"], 5)
+    # traffic: DRAM bytes per launch of this kernel class from the committed ncu --set full
+    # capture of the same workload (profiles/traffic_<config>.json, cold cache per launch)
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{cfg.name}.json")
+    if os.path.exists(tpath):
+        tj = json.load(open(tpath))
+        tk = "gemm" if dom in ("gemm_fwd", "gemm_dgrad") else dom
+        if tk in tj:
+            roof["traffic"] = tj[tk]["dram_bytes_per_launch"]
+            roof["traffic_source"] = f"profiles/traffic_{cfg.name}.json ({tj[tk]['source']})"
     roof["algorithmic_per_launch"] = {"bytes": d["bytes"] / d["launches"],
                                       "flops": d["flops"] / d["launches"]}
 

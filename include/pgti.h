@@ -88,7 +88,7 @@ pgti_status pgti_graph_windows(int32_t N, const int32_t *rowptr, const int32_t *
                                int32_t rows_per_window, int32_t *win_ptr, int32_t *win_nodes,
                                uint16_t *lcol, int32_t *max_union);
 
-/* Two-hop operators for the single-launch K = 2 diffusion (reading c20): S = M M
+/* Two-hop operators for the single-launch K = 2 diffusion (reading c23): S = M M
  * for a CSR M (host arrays) carrying two value arrays val_a, val_b on one
  * pattern -- called on pattern(A) with (P_f, P_b^T) it yields pattern(A^2) with
  * (P_f^2, (P_b^2)^T); on pattern(A^T) with (P_b, P_f^T) it yields (P_b^2,
@@ -201,7 +201,7 @@ typedef struct {
   /* Optional two-hop matrices (pgti_graph_square; device CSR, nnz2 entries each):
    * when set, K = 2 and precision = 1, each diffusion of the step runs as ONE
    * launch [P_f Z, P_f^2 Z, P_b Z, P_b^2 Z] instead of the hop chain P_f (P_f Z)
-   * (reading c20: same operator, one fewer dependent launch; the bf16 rounding
+   * (reading c23: same operator, one fewer dependent launch; the bf16 rounding
    * of the intermediate hop disappears).  Null -> the chain.  Window plans of the
    * squared patterns are optional as above (win_max then covers all four). */
   int64_t nnz2;

@@ -90,7 +90,7 @@ class Trainer:
         self.series.normalize(self.mu, self.sigma)
 
         csr = pgti.graph_build(cfg.N, *graph)
-        if two_hop and cfg.K == 2 and precision == 1:  # one-launch two-hop diffusion (c20)
+        if two_hop and cfg.K == 2 and precision == 1:  # one-launch two-hop diffusion (c23)
             csr = pgti.add_squares(csr, cfg.N)
         csr = pgti.add_windows(csr, cfg.N)
         self.csr = pgti.csr_to_device(csr, self.dev)

@@ -53,8 +53,8 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
 
 
 def full(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv", "--print-units", "base"],
+                         capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     if not rows:
         print("no data")
@@ -63,7 +63,9 @@ def full(path):
     idx = {m: hdr.index(m) for m in METRICS if m in hdr}
     kcol = hdr.index("Kernel Name")
     print(f"# ncu --set full: {path}\n")
-    print("| kernel | " + " | ".join(idx) + " |")
+    units = rows[1]
+    print("| kernel | " + " | ".join(f"{m} [{units[i]}]" if units[i] else m
+                                     for m, i in idx.items()) + " |")
     print("|---|" + "---|" * len(idx))
     for r in rows[2:]:
         if len(r) <= kcol:
@@ -71,7 +73,29 @@ def full(path):
         print(f"| `{short(r[kcol])}` | " + " | ".join(r[i] for i in idx.values()) + " |")
 
 
+def traffic(path):
+    """Mean DRAM bytes (read + write) per launch of each kernel class in an ncu --set full report
+    (cold cache: ncu flushes caches before every replayed kernel) -> JSON for bench.py."""
+    import json
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv", "--print-units", "base"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr = rows[0]
+    k, rd, wr = (hdr.index(c) for c in ("Kernel Name", "dram__bytes_read.sum",
+                                         "dram__bytes_write.sum"))
+    per = collections.defaultdict(list)
+    for r in rows[2:]:
+        if len(r) > max(k, rd, wr):
+            name = short(r[k])
+            cls = ("spmm" if "spmm" in name else "gemm_wgrad" if "wgrad" in name
+                   else "gemm" if "tc_fwd" in name else name)
+            per[cls].append(float(r[rd]) + float(r[wr]))
+    print(json.dumps({c: {"dram_bytes_per_launch": sum(v) / len(v), "launches": len(v),
+                          "source": path.rsplit("/", 1)[-1]} for c, v in per.items()}, indent=1))
+
+
 if __name__ == "__main__":
     mode, path = sys.argv[1], sys.argv[2]
     skip = int(sys.argv[sys.argv.index("--skip") + 1]) if "--skip" in sys.argv else 0
-    launches(path, skip) if mode == "launches" else full(path)
+    {"launches": lambda: launches(path, skip), "full": lambda: full(path),
+     "traffic": lambda: traffic(path)}[mode]()

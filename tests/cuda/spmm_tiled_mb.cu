@@ -233,6 +233,58 @@ __global__ void __launch_bounds__(256) kWin3(const Plan p, const bf16 *X, bf16 *
   }
 }
 
+// v4: v3 with VPL 16-byte vectors per lane (chunk = VPL * 512 bytes) and NW warps per CTA
+template <int RPW, int VPL, int NWARP>
+__global__ void __launch_bounds__(NWARP * 32) kWin4(const Plan p, const bf16 *X, bf16 *Y) {
+  extern __shared__ uint4 sm[];
+  constexpr int CV = 32 * VPL;  // vectors per chunk
+  const int vecs = p.W / 8;
+  const int chunk = blockIdx.x, win = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row0 = win * p.rows, nrows = min(p.rows, p.N - row0);
+  const int ub = __ldg(p.wptr + win), nu = __ldg(p.wptr + win + 1) - ub;
+  const int e0 = __ldg(p.rp + row0), e1 = __ldg(p.rp + row0 + nrows);
+  uint4 *stage = sm;
+  int *s_nodes = reinterpret_cast<int *>(sm + p.maxu * CV);
+  int2 *s_ent = reinterpret_cast<int2 *>(s_nodes + p.maxu + (p.maxu & 1));
+  int *s_rp = reinterpret_cast<int *>(s_ent + p.maxe);
+  for (int i = threadIdx.x; i < nu; i += NWARP * 32) s_nodes[i] = __ldg(p.wnodes + ub + i);
+  for (int i = threadIdx.x; i < e1 - e0; i += NWARP * 32)
+    s_ent[i] = make_int2(int(__ldg(p.lcol + e0 + i)) * CV * 16, __float_as_int(__ldg(p.va + e0 + i)));
+  for (int i = threadIdx.x; i <= nrows; i += NWARP * 32) s_rp[i] = __ldg(p.rp + row0 + i) - e0;
+  __syncthreads();
+  const int vbase = chunk * CV;
+  for (int k = warp; k < nu; k += NWARP) {
+    const bf16 *Xr = X + size_t(s_nodes[k]) * p.W;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      const int vec = vbase + v * 32 + lane;
+      if (vec < vecs) cp_async16(stage + k * CV + v * 32 + lane, Xr + size_t(vec) * 8);
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  const char *sb = reinterpret_cast<const char *>(stage) + lane * 16;
+#pragma unroll
+  for (int i = 0; i < RPW; ++i) {
+    const int r = warp + NWARP * i;
+    if (r >= nrows) break;
+    float2 acc[VPL][4] = {};
+    const int b = s_rp[r], e = s_rp[r + 1];
+    for (int q = b; q < e; ++q) {
+      const int2 a0 = s_ent[q];
+      const float w = __int_as_float(a0.y);
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) fma8(acc[v], w, *reinterpret_cast<const uint4 *>(sb + a0.x + v * 512));
+    }
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      const int vec = vbase + v * 32 + lane;
+      if (vec < vecs) *reinterpret_cast<uint4 *>(Y + size_t(row0 + r) * p.W + size_t(vec) * 8) = pack(acc[v]);
+    }
+  }
+}
+
 __global__ void kCopy(const uint4 *X, uint4 *Y, size_t n) {
   const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (i < n) Y[i] = X[i];
@@ -353,6 +405,19 @@ int main(int argc, char **argv) {
     check(nm);                                                                                   \
   }
     RUN3(2) RUN3(4) RUN3(8)
+#define RUN4(RPW, VPL, NWARP)                                                                    \
+  if ((rows + NWARP - 1) / NWARP == RPW) {                                                       \
+    const int smem = maxu * 512 * VPL + (maxu + 1) * 4 + maxe * 8 + (rows + 1) * 4 + 16;         \
+    CK(cudaFuncSetAttribute(kWin4<RPW, VPL, NWARP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
+    char nm[64];                                                                                 \
+    const int nch = (vecs + 32 * VPL - 1) / (32 * VPL);                                          \
+    snprintf(nm, 64, "  v4 RPW=%d VPL=%d NW=%d (%d CTAs)", RPW, VPL, NWARP, nwin * nch);         \
+    time(nm, [&] { kWin4<RPW, VPL, NWARP><<<dim3(nch, nwin), NWARP * 32, smem>>>(p, X, Y); });  \
+    check(nm);                                                                                   \
+  }
+    RUN4(2, 1, 8) RUN4(2, 2, 8) RUN4(1, 1, 16) RUN4(1, 2, 16)
+    RUN4(4, 1, 8) RUN4(4, 2, 8) RUN4(2, 1, 16) RUN4(2, 2, 16)
+    RUN4(8, 1, 8) RUN4(4, 1, 16) RUN4(4, 2, 16)
   }
   return 0;
 }

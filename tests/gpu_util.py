@@ -31,7 +31,7 @@ def load_series(pgti, torch, v_rows, row0, cfg, mu=None, sigma=None):
 
 def model_for(pgti, torch, cfg, graph, precision=0, win_rows=None, two_hop=False):
     """win_rows: SpMM staging window (None = the library default, 0 = no staging plan);
-    two_hop: pass the P^2 operators (opt-in single-launch K = 2 diffusion, reading c20)."""
+    two_hop: pass the P^2 operators (opt-in single-launch K = 2 diffusion, reading c23)."""
     csr = pgti.graph_build(cfg.N, *graph)
     if two_hop and cfg.K == 2 and precision == 1:
         csr = pgti.add_squares(csr, cfg.N)

@@ -98,7 +98,7 @@ def test_graph_windows_plan(pgti, N, rows, graph):
 
 @pytest.mark.parametrize("N,graph", [(207, "knn"), (37, "er"), (45, "ring"), (1, "er")])
 def test_graph_square_matches_oracle_powers(pgti, N, graph):
-    """Two-hop operators (reading c20) against the oracle's dense P_f, P_b squared in float64:
+    """Two-hop operators (reading c23) against the oracle's dense P_f, P_b squared in float64:
     P_f^2 and (P_b^2)^T on pattern(A^2), P_b^2 and (P_f^2)^T on pattern((A^T)^2)."""
     g = {"er": lambda: synth.random_graph(N, 0.15, seed=N), "knn": lambda: synth.make_graph(N, 8),
          "ring": lambda: synth.ring_graph(N)}[graph]()

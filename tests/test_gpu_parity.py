@@ -458,7 +458,7 @@ def test_step_parity_bf16_traffic(env, name, B):
                                                       ("metr_la", 64, True, 0),
                                                       ("metr_la", 64, True, 32)])
 def test_step_parity_bf16_diffusion_variants(env, name, B, two_hop, win_rows):
-    """The bf16 path with the single-launch two-hop operators (P^2, reading c20) and with
+    """The bf16 path with the single-launch two-hop operators (P^2, reading c23) and with
     staged SpMM (window plans, also of the squared patterns)."""
     cfg = TC_CONFIGS.get(name) or synth.CONFIGS[name]
     _check_step(_step_case_tc(env, cfg, B=B, two_hop=two_hop, win_rows=win_rows), tol=TOL_BF16)
