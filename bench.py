@@ -44,6 +44,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--epoch", action="store_true",
                     help="also train one full epoch (every rank's shard) and report its time")
+    ap.add_argument("--placement", default="halo", choices=["halo", "replicated"],
+                    help="halo shard (BASELINE north star) or the paper's replicated copy with a "
+                         "global shuffle and per-epoch validation all-reduce (P:325, P:424)")
+    ap.add_argument("--shuffle", default="window", choices=["window", "batch", "none"],
+                    help="per-epoch window shuffle, batch-order shuffle (P:454), or none")
     return ap.parse_args()
 
 
@@ -197,7 +202,8 @@ def config_dict(cfg, world, args):
     return {"workload": cfg.name, "N": cfg.N, "E": cfg.E, "F": cfg.F, "T_in": cfg.T_in,
             "T_out": cfg.T_out, "layers": cfg.L, "hidden": cfg.H, "K_hops": cfg.K,
             "per_gpu_batch": cfg.B, "global_batch": cfg.B * world,
-            "parallelism": f"dp{world} (halo-sharded distributed-index-batching)",
+            "parallelism": f"dp{world} ({args.placement} distributed-index-batching, "
+                           f"{args.shuffle} shuffle)",
             "precision": "fp32" if args.precision == 0 else "bf16",
             "l2": "no flush: each step writes >= 1 GB of fresh activations (>> 126 MB L2)",
             "cuda_graph": not args.no_graph}
@@ -241,13 +247,17 @@ def main():
     graph = synth.make_graph(cfg.N, cfg.knn)
     params0 = synth.make_params(cfg, kind="train")
     from paper_2507_11683_b200.trainer import shard_plan, train_windows, window_count
-    p = shard_plan(train_windows(window_count(cfg.E, cfg.T_in, cfg.T_out)), world, rank,
-                   cfg.T_in, cfg.T_out)
+    from paper_2507_11683_b200.trainer import replicated_plan
+    S_tr = train_windows(window_count(cfg.E, cfg.T_in, cfg.T_out))
+    p = (shard_plan(S_tr, world, rank, cfg.T_in, cfg.T_out) if args.placement == "halo"
+         else replicated_plan(S_tr, cfg.E, cfg.T_in))
     rows = synth.make_series(cfg, row_lo=p.row_lo, row_hi=p.row_hi)
     barrier()
     t0 = time.perf_counter()
     tr = Trainer(cfg, graph, lambda a, b: rows, params0, rank, world, local, comm,
-                 precision=args.precision, use_cuda_graph=not args.no_graph)
+                 precision=args.precision, use_cuda_graph=not args.no_graph,
+                 placement=args.placement,
+                 shuffle={"window": True, "batch": "batch", "none": False}[args.shuffle])
     torch.cuda.synchronize()
     load_s = time.perf_counter() - t0
     spe = tr.start_epoch(0)
@@ -330,6 +340,13 @@ def main():
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": pk, "unit": "GB/s",
                 "frac": round(ach / pk, 4), "traffic": None, "kernel": dom, "peak_source": src}
     roof["share_of_step"] = round(d["ms"] / P / eager_ms, 4)
+    # whole step against the HBM roofline: the algorithmic bytes of every libpgti launch of one
+    # step (the per-kernel models of DESIGN.md section 5) over the timed step time
+    step_bytes = sum(v["bytes"] for k, v in ours.items()) / P
+    step_ach = step_bytes / (t_ms / args.steps / 1e3) / 1e9
+    step_roof = {"bytes_per_step": step_bytes, "bytes_per_sample": step_bytes / cfg.B,
+                 "achieved": round(step_ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                 "frac": round(step_ach / peaks["hbm_gbs"], 4)}
     roof["per_launch_ms"] = round(d["ms"] / d["launches"], 5)
     # traffic: DRAM bytes per launch of this kernel class from the committed ncu --set full
     # capture of the same workload (profiles/traffic_<config>.json, cold cache per launch)
@@ -348,7 +365,7 @@ def main():
     if not args.no_e2e:
         B = cfg.B
         tr.start_epoch(1)
-        plan_host = tr.idx[:tr.n_used].cpu().pin_memory()
+        plan_host = tr.epoch_plan().cpu().pin_memory()
         loss_host = torch.zeros(1, dtype=torch.float32).pin_memory()
         n_e2e = min(args.steps, tr.n_used // B)
         for j in range(min(3, n_e2e)):
@@ -387,10 +404,19 @@ def main():
         if world > 1:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         esec = float(ems.item()) / 1e3
+        val = None
+        if args.placement == "replicated":  # the paper's per-epoch validation all-reduce
+            barrier()
+            torch.cuda.synchronize()
+            tv = time.perf_counter()
+            mae = tr.validate()
+            torch.cuda.synchronize()
+            val = {"mae_normalised": mae, "seconds": round(time.perf_counter() - tv, 3)}
         epoch = {"steps_per_rank": spe, "samples": world * cfg.B * spe, "seconds": round(esec, 3),
+                 "validation": val,
                  "samples_per_s": round(world * cfg.B * spe / esec, 2),
                  "loss_last": float(tr.loss.item()),
-                 "what": "epoch 2 of the sharded index range, CUDA-graph steps, max over ranks"}
+                 "what": "epoch 2 of this placement's plan, CUDA-graph steps, max over ranks"}
 
     # ---------------------------------------------------------------- memory + gather
     peak_alloc = torch.cuda.max_memory_allocated(dev) / 1e9
@@ -430,6 +456,7 @@ def main():
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps,
                 "launches_per_step": launches_per_step, "clocks": ck,
+                "step_roofline": step_roof,
                 "kernels": kernels, "eager_ms_per_step": round(eager_ms, 4),
                 "loss_last": loss_last, "steps_per_epoch": spe}
         if epoch is not None:

@@ -150,7 +150,14 @@ pgti_status pgti_series_destroy(pgti_series *s);
  * argsort of the Philox4x32-10 keys
  *   key_i = (w0 << 32) | w1,  (w0,w1,..) = Philox4x32-10(ctr = (i, epoch_lo,
  *           epoch_hi, rank), key = (seed_lo, seed_hi))
- * (shuffle = 1), or the identity (shuffle = 0).  *n_used (host) =
+ * (shuffle = 1), or the identity (shuffle = 0).  shuffle = 2 is the generalized
+ * variant's local batch shuffle: batch membership
+ * is frozen to consecutive windows and only the batch ORDER is permuted --
+ * dev_idx[jB + u] = win_lo + rho(j) B + u with rho the stable argsort of the
+ * same Philox keys over batch indices j < floor(n/B) (entries past n_used are
+ * left untouched).  The replicated placement's global shuffle (SURVEY
+ * f1) is this call with [win_lo, win_hi) = all training windows and rank = 0 on
+ * every rank, each rank then visiting its slice of the one plan.  *n_used (host) =
  * floor((win_hi-win_lo)/B)*B: batch j is dev_idx[jB, (j+1)B).  Every window must
  * lie inside the series' rows: win_lo >= row0, win_hi-1+T_in+T_out <= row0+nrows.
  * Errors: INVALID_ARG, OUT_OF_RANGE, TOO_FEW_WINDOWS (fewer than B), CUDA. */
@@ -232,6 +239,14 @@ size_t pgti_dcrnn_workspace_bytes(const pgti_dcrnn_desc *d);
 pgti_status pgti_dcrnn_step(const pgti_dcrnn_desc *d, const float *params, float *grads,
                             const float *x, const float *y, float *loss_dev, void *workspace,
                             size_t ws_bytes, float *act_dump, void *stream);
+
+/* Forward pass and loss only (the validation MAE of distributed-index-batching,
+ * P:424): the same forward as pgti_dcrnn_step -- same kernels, same
+ * workspace (workspace_bytes), same *loss_dev -- with no backward and no
+ * gradients.  Errors: INVALID_ARG, SHAPE, ALIGNMENT, WORKSPACE, UNSUPPORTED, CUDA. */
+pgti_status pgti_dcrnn_loss(const pgti_dcrnn_desc *d, const float *params, const float *x,
+                            const float *y, float *loss_dev, void *workspace, size_t ws_bytes,
+                            void *stream);
 
 /* Diffusion features alone (test / profiling hook for the SpMM kernel):
  * X [N][W] -> out [M][N][W] = T(X) (block order as above). */

@@ -81,3 +81,28 @@ def shard_rows(S_tr: int, R: int, r: int, T_in: int, T_out: int) -> tuple[int, i
     read, i.e. S_r starts plus a halo of T_in + T_out - 1 rows."""
     a_r, S_r = shard(S_tr, R, r)
     return a_r, a_r + S_r + T_in + T_out - 1
+
+
+def batch_plan(S_tr: int, R: int, r: int, B: int, seed: int, epoch: int) -> np.ndarray:
+    """Generalized-distributed-index-batching's local shuffle (SURVEY A10/A11,
+    NEXT f4): the partition (rank r's shard, as in `index_plan`) is fixed and so is every batch's
+    MEMBERSHIP -- batch j holds the consecutive windows a_r + [jB, (j+1)B) -- while the ORDER of
+    the floor(S_r/B) batches is shuffled each epoch by the same Philox key construction applied to
+    batch indices (ctr = (j, epoch_lo, epoch_hi, r)).  Returns the window starts in visiting
+    order (n_used = floor(S_r/B) B entries)."""
+    a_r, S_r = shard(S_tr, R, r)
+    nb = S_r // B
+    order = epoch_permutation(seed, epoch, r, nb)
+    return (a_r + (order[:, None] * B + np.arange(B)[None, :]).reshape(-1)).astype(np.int64)
+
+
+def global_plan(S_tr: int, R: int, r: int, B: int, seed: int, epoch: int) -> np.ndarray:
+    """Distributed-index-batching with replicated data and communication-free GLOBAL shuffling
+    (SURVEY A6/A7, NEXT f1): every rank holds the whole series and derives the same
+    permutation of all S_tr training windows (Philox ctr rank word fixed to 0); rank r visits
+    slice [r S_r, (r+1) S_r) of it, truncated to whole batches.  The R slices are disjoint and
+    together cover R S_r windows of the one global order."""
+    S_r = S_tr // R
+    perm = epoch_permutation(seed, epoch, 0, S_tr)
+    mine = perm[r * S_r:(r + 1) * S_r]
+    return mine[:(S_r // B) * B].astype(np.int64)

@@ -295,6 +295,7 @@ pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *param
   }
   CU(launch_loss(Fp(Ly.yhat), y, d.T_out, d.N, d.B, d.F, d.F_out, d.ld, Fp(Ly.dyhat),
                  reinterpret_cast<double *>(ws + Ly.lossp), loss_dev, err, s));
+  if (!grads) return PGTI_OK;  // pgti_dcrnn_loss: forward and loss only
 
   // ------------------------------------------------------------------ backward (BPTT)
   std::vector<float *> dHcur(L), dHprev(L);
@@ -415,6 +416,26 @@ extern "C" size_t pgti_dcrnn_workspace_bytes(const pgti_dcrnn_desc *desc) {
   Dims d;
   if (check_desc(desc, &d) != PGTI_OK) return 0;
   return workspace_for(d);
+}
+
+extern "C" pgti_status pgti_dcrnn_loss(const pgti_dcrnn_desc *desc, const float *params,
+                                       const float *x, const float *y, float *loss_dev,
+                                       void *workspace, size_t ws_bytes, void *stream) {
+  clear_error();
+  Dims d;
+  PGTI_STATUS_TRY(check_desc(desc, &d));
+  PGTI_REQUIRE(params && x && y && loss_dev && workspace, PGTI_ERR_INVALID_ARG,
+               "pgti_dcrnn_loss: null pointer");
+  PGTI_REQUIRE(aligned16(params) && aligned16(workspace), PGTI_ERR_ALIGNMENT,
+               "pgti_dcrnn_loss: params / workspace must be 16-byte aligned");
+  const size_t need = workspace_for(d);
+  PGTI_REQUIRE(ws_bytes >= need, PGTI_ERR_WORKSPACE,
+               "pgti_dcrnn_loss: workspace %zu bytes < %zu needed", ws_bytes, need);
+  if (d.precision == 1)
+    return run_step_tc(*desc, d, params, nullptr, x, y, loss_dev, static_cast<char *>(workspace),
+                       nullptr, as_stream(stream));
+  return run_step(*desc, d, params, nullptr, x, y, loss_dev, static_cast<char *>(workspace),
+                  nullptr, as_stream(stream));
 }
 
 extern "C" pgti_status pgti_dcrnn_step(const pgti_dcrnn_desc *desc, const float *params,

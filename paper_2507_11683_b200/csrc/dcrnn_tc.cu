@@ -228,6 +228,10 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
   cudaStream_t top = st[L - 1];
   CU(launch_loss(Fp(Ly.yhat), y, d.T_out, d.N, d.B, d.F, d.F_out, d.ld, Fp(Ly.dyhat),
                  reinterpret_cast<double *>(ws + Ly.lossp), loss_dev, err, top));
+  if (!grads) {  // pgti_dcrnn_loss: forward and loss only
+    for (int l = 1; l < L; ++l) CU(depend(sp, st[l], s));  // join
+    return PGTI_OK;
+  }
 
   // ------------------------------------------------------------------ backward (BPTT)
   // dZ = sum_m Q_m W_m^T, Q_0 = gradient itself (map A0), Q_{m>0} = (P^m)^T grad (map A1)

@@ -126,6 +126,14 @@ __global__ void k_keys(int64_t n, int32_t win_lo, uint64_t seed, uint64_t epoch,
   }
 }
 
+// batch-level shuffle (shuffle = 2): window t of the plan = win_lo + order[t / B] * B + t % B
+__global__ void k_expand_batches(int64_t n_used, int B, int32_t win_lo,
+                                 const int32_t *__restrict__ order, int32_t *__restrict__ idx) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n_used;
+       t += int64_t(gridDim.x) * blockDim.x)
+    idx[t] = win_lo + order[t / B] * B + int32_t(t % B);
+}
+
 // ------------------------------------------------------------------ K1 window gather
 // LDG.128/STG.128 variant: block (chunk, b); each thread moves kUnroll float4 with all loads
 // issued before the stores (bytes in flight).
@@ -331,7 +339,7 @@ extern "C" pgti_status pgti_make_index(const pgti_series *sr, int64_t win_lo, in
                                        void *stream) {
   pgti::clear_error();
   PGTI_REQUIRE(sr && dev_idx && n_used, PGTI_ERR_INVALID_ARG, "pgti_make_index: null pointer");
-  PGTI_REQUIRE(T_in >= 1 && T_out >= 1 && B >= 1 && rank >= 0 && (shuffle == 0 || shuffle == 1),
+  PGTI_REQUIRE(T_in >= 1 && T_out >= 1 && B >= 1 && rank >= 0 && shuffle >= 0 && shuffle <= 2,
                PGTI_ERR_INVALID_ARG, "pgti_make_index: T_in=%d T_out=%d B=%d rank=%d shuffle=%d",
                T_in, T_out, B, rank, shuffle);
   PGTI_REQUIRE(win_lo >= 0 && win_hi >= win_lo && win_hi < (int64_t(1) << 31),
@@ -351,7 +359,34 @@ extern "C" pgti_status pgti_make_index(const pgti_series *sr, int64_t win_lo, in
   const int grid = int(std::min<int64_t>(pgti::ceil_div(n, 256), 148 * 8));
   pgti::ProfScope prof(pgti::kProfIndex, s, double(n) * (shuffle ? 48.0 : 4.0), 0.0,
                        shuffle ? 5 : 1);
-  if (!shuffle) {
+  if (shuffle == 2) {  // membership frozen, batch order permuted
+    const int64_t nb = n / B;
+    size_t temp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, (unsigned long long *)nullptr,
+                                    (unsigned long long *)nullptr, (int32_t *)nullptr,
+                                    (int32_t *)nullptr, int(nb), 0, 64, s);
+    const size_t kb = pgti::round_up(nb * 8, 256), vb = pgti::round_up(nb * 4, 256);
+    char *scratch = nullptr;
+    PGTI_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&scratch), 2 * kb + 2 * vb + temp_bytes,
+                                  s));
+    auto *keys_in = reinterpret_cast<unsigned long long *>(scratch);
+    auto *keys_out = reinterpret_cast<unsigned long long *>(scratch + kb);
+    auto *vals_in = reinterpret_cast<int32_t *>(scratch + 2 * kb);
+    auto *vals_out = reinterpret_cast<int32_t *>(scratch + 2 * kb + vb);
+    void *temp = scratch + 2 * kb + 2 * vb;
+    const int gb = int(std::min<int64_t>(pgti::ceil_div(nb, 256), 148 * 8));
+    k_keys<<<gb, 256, 0, s>>>(nb, 0, seed, epoch, uint32_t(rank), 1, keys_in, vals_in);
+    cudaError_t e1 = cudaGetLastError();
+    cudaError_t e2 = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in,
+                                                     vals_out, int(nb), 0, 64, s);
+    k_expand_batches<<<grid, 256, 0, s>>>(nb * B, B, int32_t(win_lo), vals_out, dev_idx);
+    cudaError_t e3 = cudaGetLastError();
+    cudaError_t e4 = cudaFreeAsync(scratch, s);
+    PGTI_CUDA_TRY(e1);
+    PGTI_CUDA_TRY(e2);
+    PGTI_CUDA_TRY(e3);
+    PGTI_CUDA_TRY(e4);
+  } else if (!shuffle) {
     k_keys<<<grid, 256, 0, s>>>(n, int32_t(win_lo), seed, epoch, uint32_t(rank), 0, nullptr,
                                 dev_idx);
     PGTI_LAUNCH_TRY();

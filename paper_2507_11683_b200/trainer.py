@@ -7,9 +7,15 @@ every value the model sees is produced by libpgti kernels:
    -> per-epoch index plan -> per step: gather -> DCGRU
   forward/backward -> NCCL all-reduce -> Adam.
 
-Halo sharding (BASELINE.json north_star): rank r of R owns window starts
+Halo sharding (BASELINE.json north_star, the default): rank r of R owns window starts
 [r S_r, (r+1) S_r), S_r = floor(S_tr / R), and holds series rows [r S_r, (r+1) S_r + T_in +
 T_out - 1).  The last rank additionally holds the rows the statistics need up to S_tr + T_in - 1.
+
+Replicated placement (the paper's distributed-index-batching): every rank
+holds the whole series, derives the same global permutation of all training windows with no
+exchange and visits its slice of it; validation MAE is all-reduced each epoch.
+Batch-level shuffle (generalized variant): shuffle="batch" keeps each batch's
+membership and permutes the batch order.
 """
 from __future__ import annotations
 
@@ -51,6 +57,18 @@ def shard_plan(S_tr: int, R: int, r: int, T_in: int, T_out: int) -> ShardPlan:
     return ShardPlan(win_lo, win_hi, row_lo, row_hi, stat_lo, stat_hi)
 
 
+def replicated_plan(S_tr: int, E: int, T_in: int) -> ShardPlan:
+    """Replicated placement: all rows [0, E) held, all training windows in the (global) plan,
+    statistics computed locally over the rows training windows read (no exchange)."""
+    return ShardPlan(0, S_tr, 0, E, 0, S_tr + T_in - 1)
+
+
+def val_windows(S: int) -> int:
+    """Validation windows after the training ones: S - round(0.7 S) - round(0.2 S) (the 70/10/20
+    split of P:243, Alg. 1 line 200 with Python round)."""
+    return S - round(S * 0.70) - round(S * 0.20)
+
+
 def row_pitch(N: int, F: int) -> int:
     """ld = roundup(N F, 4) floats: 16-byte aligned time rows (SURVEY decision 5)."""
     return (N * F + 3) // 4 * 4
@@ -66,7 +84,7 @@ class Trainer:
 
     def __init__(self, cfg, graph, series_fn, params0, rank=0, world=1, device=0, comm=None,
                  seed=3, lr=1e-2, precision=0, shuffle=True, use_cuda_graph=True,
-                 two_hop=False):
+                 two_hop=False, placement="halo"):
         import torch
 
         self.torch = torch
@@ -76,7 +94,14 @@ class Trainer:
         self.seed, self.lr, self.shuffle = seed, lr, shuffle
         self.S = window_count(cfg.E, cfg.T_in, cfg.T_out)
         self.S_tr = train_windows(self.S)
-        self.plan = shard_plan(self.S_tr, world, rank, cfg.T_in, cfg.T_out)
+        assert placement in ("halo", "replicated"), placement
+        assert shuffle in (True, False, "batch"), shuffle
+        assert not (placement == "replicated" and shuffle == "batch"), "batch shuffle is per shard"
+        self.placement = placement
+        self.S_r = self.S_tr // world
+        self.idx_off = 0
+        self.plan = (shard_plan(self.S_tr, world, rank, cfg.T_in, cfg.T_out)
+                     if placement == "halo" else replicated_plan(self.S_tr, cfg.E, cfg.T_in))
         self.ld = row_pitch(cfg.N, cfg.F)
         p = self.plan
         rows = np.ascontiguousarray(series_fn(p.row_lo, p.row_hi), dtype=np.float32)
@@ -124,7 +149,7 @@ class Trainer:
         for _ in range(2):   # pass 1: mean; pass 2: variance about the mean (no cancellation)
             sums = torch.zeros(3, dtype=torch.float64, device=self.dev)
             self.series.stats(self.S_tr, cfg.T_in, p.stat_lo, p.stat_hi, shift, sums)
-            if self.comm is not None and self.world > 1:
+            if self.comm is not None and self.world > 1 and self.placement == "halo":
                 self.comm.allreduce_f64(sums)
             s0, s1, s2 = sums.cpu().tolist()
             mean_d = s1 / s0
@@ -135,13 +160,50 @@ class Trainer:
         return mu, math.sqrt(max(var, 0.0))
 
     def steps_per_epoch(self) -> int:
-        return (self.plan.win_hi - self.plan.win_lo) // self.cfg.B
+        return self.S_r // self.cfg.B
 
     def start_epoch(self, epoch: int) -> int:
         p, cfg = self.plan, self.cfg
-        self.n_used = self.series.make_index(p.win_lo, p.win_hi, cfg.T_in, cfg.T_out, cfg.B,
-                                             self.seed, epoch, self.rank, self.shuffle, self.idx)
+        code = {False: 0, True: 1, "batch": 2}[self.shuffle]
+        if self.placement == "halo":
+            self.n_used = self.series.make_index(p.win_lo, p.win_hi, cfg.T_in, cfg.T_out, cfg.B,
+                                                 self.seed, epoch, self.rank, code, self.idx)
+            return self.n_used // cfg.B
+        # one global plan, identical on every rank (Philox rank word 0); this rank's slice
+        self.series.make_index(0, self.S_tr, cfg.T_in, cfg.T_out, cfg.B, self.seed, epoch, 0,
+                               code, self.idx)
+        self.idx_off = self.rank * self.S_r
+        self.n_used = (self.S_r // cfg.B) * cfg.B
         return self.n_used // cfg.B
+
+    def epoch_plan(self):
+        """This rank's window starts of the current epoch, in visiting order (device int32)."""
+        return self.idx[self.idx_off:self.idx_off + self.n_used]
+
+    def validate(self) -> float:
+        """Validation MAE (normalised units) over the validation windows [S_tr, S_tr + S_val),
+        split evenly over the ranks (whole batches), forward + loss only (pgti_dcrnn_loss),
+        per-rank sums all-reduced.  Needs the replicated placement (every rank holds the
+        validation rows)."""
+        assert self.placement == "replicated", "validation rows are held by the replicated placement"
+        torch, cfg = self.torch, self.cfg
+        B = cfg.B
+        V_r = val_windows(self.S) // self.world
+        nb = V_r // B
+        lo = self.S_tr + self.rank * V_r
+        vidx = torch.empty(max(1, V_r), dtype=torch.int32, device=self.dev)
+        losses = torch.zeros(max(1, nb), dtype=torch.float32, device=self.dev)
+        if nb:
+            self.series.make_index(lo, lo + V_r, cfg.T_in, cfg.T_out, B, self.seed, 0, 0, 0, vidx)
+        for j in range(nb):
+            self.series.gather(vidx[j * B:(j + 1) * B], B, cfg.T_in, cfg.T_out, self.x, self.y)
+            self.model.loss(self.params, self.x, self.y, losses[j:j + 1], self.ws)
+        host = losses[:nb].cpu().numpy().astype(np.float64)
+        sums = torch.tensor([host.sum(), float(nb)], dtype=torch.float64, device=self.dev)
+        if self.comm is not None and self.world > 1:
+            self.comm.allreduce_f64(sums)
+        total, count = sums.cpu().tolist()
+        return total / count if count else float("nan")
 
     # ------------------------------------------------------------------ one step
     def _body(self, idx):
@@ -156,7 +218,7 @@ class Trainer:
     def step(self, j: int):
         """Batch j of the current epoch (gather -> fwd/bwd -> all-reduce -> Adam)."""
         B = self.cfg.B
-        sl = self.idx[j * B:(j + 1) * B]
+        sl = self.idx[self.idx_off + j * B:self.idx_off + (j + 1) * B]
         if not self.use_cuda_graph:
             self._body(sl)
             return

@@ -163,6 +163,7 @@ def test_shard_plan_vs_oracle(pgti, name):
     assert trainer.window_count(cfg.E, cfg.T_in, cfg.T_out) == S
     S_tr = windows.split_counts(S)[0]
     assert trainer.train_windows(S) == S_tr
+    assert trainer.val_windows(S) == windows.split_counts(S)[1]
     for R in (1, 2, 4, 8):
         covered = []
         for r in range(R):

@@ -462,3 +462,75 @@ def test_step_parity_bf16_diffusion_variants(env, name, B, two_hop, win_rows):
     staged SpMM (window plans, also of the squared patterns)."""
     cfg = TC_CONFIGS.get(name) or synth.CONFIGS[name]
     _check_step(_step_case_tc(env, cfg, B=B, two_hop=two_hop, win_rows=win_rows), tol=TOL_BF16)
+
+
+# ------------------------------------------------------------------ NEXT f4 / f1 index plans
+@pytest.mark.parametrize("name", ["cp", "metr_la", "pems_bay"])
+@pytest.mark.parametrize("R", [1, 2, 4, 8])
+def test_batch_shuffle_plan_bitexact(env, name, R):
+    """shuffle = 2 (generalized variant's batch-level shuffle) against
+    oracle.philox.batch_plan, first and last rank, three epochs."""
+    pgti, torch = env
+    from paper_2507_11683_b200 import trainer
+    cfg = SMALL_CONFIGS.get(name) or synth.CONFIGS[name]
+    ref = ref_for(cfg)
+    for r in sorted({0, R - 1}):
+        p = trainer.shard_plan(ref.n_train, R, r, cfg.T_in, cfg.T_out)
+        s = load_series(pgti, torch, ref.v[p.row_lo:p.row_hi], p.row_lo, cfg, ref.mu, ref.sigma)
+        idx = torch.full((p.win_hi - p.win_lo,), -1, dtype=torch.int32, device="cuda")
+        for epoch in (0, 1, 7):
+            n_used = s.make_index(p.win_lo, p.win_hi, cfg.T_in, cfg.T_out, cfg.B, 3, epoch, r, 2,
+                                  idx)
+            want = philox.batch_plan(ref.n_train, R, r, cfg.B, 3, epoch)
+            assert n_used == want.size
+            assert np.array_equal(idx.cpu().numpy()[:n_used], want)
+
+
+@pytest.mark.parametrize("name", ["cp", "metr_la"])
+@pytest.mark.parametrize("R", [1, 2, 4, 8])
+def test_replicated_global_plan_bitexact(env, name, R):
+    """Replicated placement (f1): every rank derives the one global plan and visits its
+    slice -- against oracle.philox.global_plan; the Trainer's slices are disjoint."""
+    pgti, torch = env
+    from paper_2507_11683_b200.trainer import Trainer
+    cfg = SMALL_CONFIGS.get(name) or synth.CONFIGS[name]
+    ref = ref_for(cfg)
+    theta = synth.make_params(cfg, kind="random")
+    seen = []
+    for r in range(R):
+        tr = Trainer(cfg, ref.graph, lambda a, b: ref.v[a:b], theta, rank=r, world=R,
+                     precision=0, use_cuda_graph=False, placement="replicated")
+        assert (tr.mu, tr.sigma) == pytest.approx((ref.mu, ref.sigma), rel=1e-12)
+        for epoch in (0, 5):
+            steps = tr.start_epoch(epoch)
+            got = tr.epoch_plan().cpu().numpy()
+            want = philox.global_plan(ref.n_train, R, r, cfg.B, 3, epoch)
+            assert steps * cfg.B == want.size and np.array_equal(got, want)
+        seen.append(got)
+        del tr
+    allw = np.concatenate(seen)
+    assert np.unique(allw).size == allw.size
+
+
+@pytest.mark.parametrize("precision,tol", [(0, 1e-5), (1, TOL_BF16)])
+def test_validation_mae_vs_oracle(env, precision, tol):
+    """pgti_dcrnn_loss (forward + loss only) over the validation windows, as Trainer.validate
+    aggregates it, against the float64 oracle's MAE of the same batches; the training
+    step still matches after a validation pass (shared workspace)."""
+    pgti, torch = env
+    from paper_2507_11683_b200.trainer import Trainer, val_windows
+    cfg = synth.Config("val", N=40, E=150, F=2, T_in=4, T_out=3, L=2, H=64, K=2, B=6)
+    ref = ref_for(cfg)
+    theta = synth.make_params(cfg, kind="random")
+    tr = Trainer(cfg, ref.graph, lambda a, b: ref.v[a:b], theta, precision=precision,
+                 use_cuda_graph=False, placement="replicated")
+    mae = tr.validate()
+    nb = val_windows(ref.S) // cfg.B
+    assert nb >= 2
+    losses = []
+    for j in range(nb):
+        x, y = ref.batch(np.arange(ref.n_train + j * cfg.B, ref.n_train + (j + 1) * cfg.B))
+        losses.append(dcgru.forward(theta.astype(np.float64), ref.d, ref.Pf, ref.Pb,
+                                    x.astype(np.float64), y.astype(np.float64))["loss"])
+    want = float(np.mean(losses))
+    assert abs(mae - want) <= tol * abs(want), (mae, want)

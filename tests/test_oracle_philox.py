@@ -3,6 +3,7 @@ import itertools
 import os
 
 import numpy as np
+import pytest
 
 from oracle import philox
 
@@ -59,3 +60,47 @@ def test_index_plan_shards():
         assert len(set(seen)) == len(seen)
     ident = philox.index_plan(S_tr, 1, 0, B, 3, 2, shuffle=False)
     assert ident.tolist() == list(range(100))
+
+
+@pytest.mark.parametrize("S_tr,R,B", [(1000, 1, 8), (1000, 4, 16), (37, 2, 5)])
+def test_batch_plan_membership_frozen_order_shuffled(S_tr, R, B):
+    """f4: each batch is a consecutive block of the rank's shard, the blocks are a
+    permutation of the shard's whole batches, and the order changes between epochs."""
+    orders = []
+    for r in range(R):
+        a_r, S_r = philox.shard(S_tr, R, r)
+        nb = S_r // B
+        for epoch in (0, 1):
+            p = philox.batch_plan(S_tr, R, r, B, 3, epoch)
+            assert p.size == nb * B
+            blocks = p.reshape(nb, B)
+            assert np.all(np.diff(blocks, axis=1) == 1)          # membership: consecutive
+            starts = (blocks[:, 0] - a_r) // B
+            assert np.all((blocks[:, 0] - a_r) % B == 0)
+            assert sorted(starts.tolist()) == list(range(nb))   # every whole batch once
+            orders.append(tuple(starts))
+    if S_tr // R // B > 3:
+        assert orders[0] != orders[1]
+    assert np.array_equal(philox.batch_plan(S_tr, R, 0, B, 3, 1),
+                          philox.batch_plan(S_tr, R, 0, B, 3, 1))
+
+
+@pytest.mark.parametrize("S_tr,R,B", [(1000, 1, 8), (1000, 4, 16), (1003, 8, 4)])
+def test_global_plan_slices_one_permutation(S_tr, R, B):
+    """f1: the ranks' slices are disjoint, each lies in [0, S_tr), and their
+    concatenation (before batch truncation) is a prefix of one global permutation that every
+    rank derives identically (no exchange)."""
+    S_r = S_tr // R
+    seen = []
+    for r in range(R):
+        p = philox.global_plan(S_tr, R, r, B, 3, 2)
+        assert p.size == (S_r // B) * B and p.min() >= 0 and p.max() < S_tr
+        seen.append(p)
+    allw = np.concatenate(seen)
+    assert np.unique(allw).size == allw.size
+    perm = philox.epoch_permutation(3, 2, 0, S_tr)
+    for r in range(R):
+        assert np.array_equal(seen[r], perm[r * S_r:r * S_r + (S_r // B) * B])
+    # a global shuffle mixes the time axis across ranks (unlike the halo shard)
+    if R > 1:
+        assert seen[0].max() >= S_r
