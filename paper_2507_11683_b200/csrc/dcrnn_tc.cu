@@ -71,7 +71,7 @@ cudaError_t record(StreamPool *p, cudaStream_t st, cudaEvent_t *out) {
 // ------------------------------------------------------------------ workspace
 struct LayoutTC {
   size_t Dx, yhat, dyhat, lossp, total;
-  std::vector<size_t> DHb, DrHb, H32, Rg, Ug, Cg, dG, dGb, dC, dCb, Wf_ru, Wf_c, Wd_ru, Wd_c;
+  std::vector<size_t> DHb, DrHb, H32, Rg, Ug, Cg, dGb, dCb, Wf_ru, Wf_c, Wd_ru, Wd_c;
   std::vector<size_t> Q, wpart, dHrec0, dHrec1, dHup0, dHup1;
   size_t wpart_floats;
 };
@@ -100,10 +100,8 @@ LayoutTC make_layout_tc(const Dims &d) {
     L.Rg.push_back(take(T * R * H * 4));
     L.Ug.push_back(take(T * R * H * 4));
     L.Cg.push_back(take(T * R * H * 4));
-    L.dG.push_back(take(T * R * 2 * H * 4));
-    L.dGb.push_back(take(T * R * 2 * H * 2));
-    L.dC.push_back(take(T * R * H * 4));
-    L.dCb.push_back(take(T * R * H * 2));
+    L.dGb.push_back(take(T * R * 2 * H * 2));  // bf16 only: dgrad / wgrad operands and the
+    L.dCb.push_back(take(T * R * H * 2));      // skinny bias / input-row reductions
     L.Wf_ru.push_back(take(size_t(nkb_total(d, l)) * 2 * H * 64 * 2));
     L.Wf_c.push_back(take(size_t(nkb_total(d, l)) * H * 64 * 2));
     L.Wd_ru.push_back(take(size_t(vrows(d, l)) * 2 * H * 2));
@@ -285,7 +283,7 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
       const bool need_in = l > 0, need_h = t > 0;
       const float *Hprev = t > 0 ? Fp(Ly.H32[l]) + (t - 1) * RH : nullptr;
       const float *r = Fp(Ly.Rg[l]) + t * RH, *u = Fp(Ly.Ug[l]) + t * RH, *c = Fp(Ly.Cg[l]) + t * RH;
-      float *dC = Fp(Ly.dC[l]) + t * RH, *dG = Fp(Ly.dG[l]) + t * 2 * RH;
+      float *dC = nullptr, *dG = nullptr;
       bf16 *dCb = Bp(Ly.dCb[l]) + t * RH, *dGb = Bp(Ly.dGb[l]) + t * 2 * RH;
       const float *dy = (l == L - 1 && t >= T - d.T_out)
                             ? Fp(Ly.dyhat) + int64_t(t - (T - d.T_out)) * R * d.F_out
@@ -335,9 +333,9 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
     if (l == 0) sw.Dx = Dx, sw.dx_mstride = int64_t(T) * RF, sw.dx_tstride = RF;
     sw.M = d.M, sw.F = d.F, sw.C_in = C;
     sw.partial = wpart, sw.partial_cap = int64_t(Ly.wpart_floats);
-    sw.G = Fp(Ly.dG[l]), sw.g_tstride = 2 * RH, sw.NG = 2 * d.H, sw.out = grads + P.Wru[l];
+    sw.Gb = Bp(Ly.dGb[l]), sw.g_tstride = 2 * RH, sw.NG = 2 * d.H, sw.out = grads + P.Wru[l];
     CU(launch_small_wgrad(sw, ss));
-    sw.G = Fp(Ly.dC[l]), sw.g_tstride = RH, sw.NG = d.H, sw.out = grads + P.Wc[l];
+    sw.Gb = Bp(Ly.dCb[l]), sw.g_tstride = RH, sw.NG = d.H, sw.out = grads + P.Wc[l];
     CU(launch_small_wgrad(sw, ss));
   }
   SmallWgrad rw{};

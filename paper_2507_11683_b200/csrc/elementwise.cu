@@ -103,6 +103,16 @@ __global__ void k_cand_bwd(int64_t RH, int H, const float *__restrict__ dHcur,
 // Tensor-core path candidate backward: as k_cand_bwd, plus the update-gate half of the gate
 // gradient dG_u = dU u (1-u) (dU never leaves registers) and, when H_{t-1} = 0, dG_r = 0; the
 // reset half dG_r is finished by the candidate dgrad GEMM's epilogue (TcFwd::fuse_tile).
+// Thread = 4 consecutive hidden units of one row (16-byte loads / stores, 8-byte bf16 stores).
+// The fp32 copies dC / dG are optional (the tensor-core path keeps only the bf16 ones).
+__device__ __forceinline__ void st4bf(__nv_bfloat16 *p, float a, float b, float c, float d) {
+  __nv_bfloat162 x = __floats2bfloat162_rn(a, b), y = __floats2bfloat162_rn(c, d);
+  uint2 v;
+  v.x = *reinterpret_cast<uint32_t *>(&x);
+  v.y = *reinterpret_cast<uint32_t *>(&y);
+  *reinterpret_cast<uint2 *>(p) = v;
+}
+
 __global__ void k_cand_bwd_tc(int64_t RH, int H, const float *__restrict__ dHa,
                               const float *__restrict__ dHb, const float *__restrict__ dy,
                               const float *__restrict__ Wout, int F_out,
@@ -110,25 +120,46 @@ __global__ void k_cand_bwd_tc(int64_t RH, int H, const float *__restrict__ dHa,
                               const float *__restrict__ Hprev, float *__restrict__ dC,
                               __nv_bfloat16 *__restrict__ dCb, float *__restrict__ dHprev,
                               float *__restrict__ dG, __nv_bfloat16 *__restrict__ dGb) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < RH;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t row = i / H;
+  const int64_t n4 = RH / 4;
+  auto ld = [](const float *p, int64_t q) { return reinterpret_cast<const float4 *>(p)[q]; };
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n4;
+       q += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = q * 4, row = i / H;
     const int j = int(i - row * H);
-    float dh = dHa ? dHa[i] : 0.f;
-    if (dHb) dh += dHb[i];
+    float4 dh = dHa ? ld(dHa, q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (dHb) {
+      const float4 b = ld(dHb, q);
+      dh.x += b.x, dh.y += b.y, dh.z += b.z, dh.w += b.w;
+    }
     if (dy)
-      for (int o = 0; o < F_out; ++o) dh = fmaf(dy[row * F_out + o], Wout[j * F_out + o], dh);
-    const float uu = u[i], cc = c[i], hp = Hprev ? Hprev[i] : 0.f;
-    const float dc = dh * (1.0f - uu) * (1.0f - cc * cc);
-    dC[i] = dc;
-    dCb[i] = __float2bfloat16_rn(dc);
-    if (dHprev) dHprev[i] = dh * uu;
-    const float gu = dh * (hp - cc) * uu * (1.0f - uu);
-    dG[row * 2 * H + H + j] = gu;
-    dGb[row * 2 * H + H + j] = __float2bfloat16_rn(gu);
+      for (int o = 0; o < F_out; ++o) {
+        const float e = dy[row * F_out + o];
+        dh.x = fmaf(e, Wout[(j + 0) * F_out + o], dh.x);
+        dh.y = fmaf(e, Wout[(j + 1) * F_out + o], dh.y);
+        dh.z = fmaf(e, Wout[(j + 2) * F_out + o], dh.z);
+        dh.w = fmaf(e, Wout[(j + 3) * F_out + o], dh.w);
+      }
+    const float4 uu = ld(u, q), cc = ld(c, q);
+    const float4 hp = Hprev ? ld(Hprev, q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 dc = make_float4(dh.x * (1.0f - uu.x) * (1.0f - cc.x * cc.x),
+                                  dh.y * (1.0f - uu.y) * (1.0f - cc.y * cc.y),
+                                  dh.z * (1.0f - uu.z) * (1.0f - cc.z * cc.z),
+                                  dh.w * (1.0f - uu.w) * (1.0f - cc.w * cc.w));
+    if (dC) reinterpret_cast<float4 *>(dC)[q] = dc;
+    st4bf(dCb + i, dc.x, dc.y, dc.z, dc.w);
+    if (dHprev)
+      reinterpret_cast<float4 *>(dHprev)[q] =
+          make_float4(dh.x * uu.x, dh.y * uu.y, dh.z * uu.z, dh.w * uu.w);
+    const float4 gu = make_float4(dh.x * (hp.x - cc.x) * uu.x * (1.0f - uu.x),
+                                  dh.y * (hp.y - cc.y) * uu.y * (1.0f - uu.y),
+                                  dh.z * (hp.z - cc.z) * uu.z * (1.0f - uu.z),
+                                  dh.w * (hp.w - cc.w) * uu.w * (1.0f - uu.w));
+    const int64_t gi = row * 2 * H + H + j;
+    if (dG) *reinterpret_cast<float4 *>(dG + gi) = gu;
+    st4bf(dGb + gi, gu.x, gu.y, gu.z, gu.w);
     if (!Hprev) {
-      dG[row * 2 * H + j] = 0.f;
-      dGb[row * 2 * H + j] = __float2bfloat16_rn(0.f);
+      if (dG) *reinterpret_cast<float4 *>(dG + gi - H) = make_float4(0.f, 0.f, 0.f, 0.f);
+      st4bf(dGb + gi - H, 0.f, 0.f, 0.f, 0.f);
     }
   }
 }
@@ -233,12 +264,14 @@ cudaError_t launch_cand_bwd_tc(int64_t RH, int H, const float *dHa, const float 
                                const float *dy, const float *Wout, int F_out, const float *u,
                                const float *c, const float *Hprev, float *dC, void *dCb,
                                float *dHprev, float *dG, void *dGb, cudaStream_t s) {
+  if (H % 4) return cudaErrorInvalidValue;
   ProfScope prof(kProfElementwise, s,
-                 double(RH) * (4.0 * ((dHa ? 1 : 0) + (dHb ? 1 : 0) + 2 + (Hprev ? 1 : 0) + 1 +
-                                      (dHprev ? 1 : 0) + (Hprev ? 1 : 2)) +
+                 double(RH) * (4.0 * ((dHa ? 1 : 0) + (dHb ? 1 : 0) + 2 + (Hprev ? 1 : 0) +
+                                      (dC ? 1 : 0) + (dHprev ? 1 : 0) +
+                                      (dG ? (Hprev ? 1 : 2) : 0)) +
                                2.0 * (1 + (Hprev ? 1 : 2))),
                  0.0);
-  k_cand_bwd_tc<<<grid_for(RH), kT, 0, s>>>(RH, H, dHa, dHb, dy, Wout, F_out, u, c, Hprev, dC,
+  k_cand_bwd_tc<<<grid_for(RH / 4), kT, 0, s>>>(RH, H, dHa, dHb, dy, Wout, F_out, u, c, Hprev, dC,
                                             static_cast<__nv_bfloat16 *>(dCb), dHprev, dG,
                                             static_cast<__nv_bfloat16 *>(dGb));
   return cudaGetLastError();

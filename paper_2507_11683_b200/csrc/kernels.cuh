@@ -1,6 +1,8 @@
 // Internal launch interfaces shared by the step orchestration (dcrnn.cu) and the kernels.
 #pragma once
 
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 
 namespace pgti {
@@ -136,6 +138,7 @@ struct SmallWgrad {
   const float *dy;        // kSmallReadout: [T][R][F_out]
   int F_out;
   const float *G;         // + t*g_tstride, [R][NG]
+  const __nv_bfloat16 *Gb;  // same layout in bf16 (used instead of G when set)
   int64_t g_tstride;
   int NG;
   float *partial;

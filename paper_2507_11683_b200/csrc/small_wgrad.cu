@@ -72,6 +72,68 @@ __global__ void __launch_bounds__(kThr) k_small_wgrad(const __grid_constant__ Sm
       p.partial[(int64_t(chunk) * q.ns + s) * q.ngt + j] = red[0][s][j] + red[1][s][j];
 }
 
+// bf16 G (the tensor-core path's gate gradients): thread = 2 adjacent columns (one 4-byte load),
+// NG/2 threads per row, kThr/(NG/2) row groups, folded in shared memory in group order (fixed,
+// deterministic).  No ones column (bias rows use S = 1 instead).
+__global__ void __launch_bounds__(kThr) k_small_wgrad_bf(const __grid_constant__ SmallWgrad p,
+                                                         Plan q) {
+  __shared__ float S[kTile][kSmallMax];
+  __shared__ float2 red[kSmallMax][64];
+  const int chunk = blockIdx.x, t = chunk / q.cpt;
+  const int r0 = (chunk - t * q.cpt) * q.RC, r1 = min(p.R, r0 + q.RC);
+  const int cpr = p.NG / 2, ng = kThr / cpr;
+  const int jj = threadIdx.x % cpr, lg = threadIdx.x / cpr;
+  float2 acc[kSmallMax];
+#pragma unroll
+  for (int s = 0; s < kSmallMax; ++s) acc[s] = make_float2(0.f, 0.f);
+  const __nv_bfloat162 *G =
+      reinterpret_cast<const __nv_bfloat162 *>(p.Gb + t * p.g_tstride) + jj;
+  for (int rb = r0; rb < r1; rb += kTile) {
+    const int nr = min(kTile, r1 - rb);
+    for (int i = threadIdx.x; i < nr * q.ns; i += kThr) {
+      const int rr = i / q.ns, s = i % q.ns, row = rb + rr;
+      float v;
+      if (s == q.ns - 1) {
+        v = 1.0f;
+      } else {
+        const int m = s / p.F, f = s % p.F;
+        v = __ldg(p.Dx + m * p.dx_mstride + t * p.dx_tstride + int64_t(row) * p.F + f);
+      }
+      S[rr][s] = v;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int rr = lg; rr < nr; rr += ng) {
+      const float2 g = __bfloat1622float2(G[int64_t(rb + rr) * cpr]);
+#pragma unroll
+      for (int s = 0; s < kSmallMax; ++s)
+        if (s < q.ns) {
+          const float v = S[rr][s];
+          acc[s].x = fmaf(v, g.x, acc[s].x), acc[s].y = fmaf(v, g.y, acc[s].y);
+        }
+    }
+    __syncthreads();
+  }
+  for (int g = 0; g < ng; ++g) {  // fold the row groups in order
+    if (lg == g)
+#pragma unroll
+      for (int s = 0; s < kSmallMax; ++s) {
+        if (g == 0) {
+          red[s][jj] = acc[s];
+        } else {
+          const float2 o = red[s][jj];
+          red[s][jj] = make_float2(o.x + acc[s].x, o.y + acc[s].y);
+        }
+      }
+    __syncthreads();
+  }
+  float *out = p.partial + int64_t(chunk) * q.ns * q.ngt;
+  for (int i = threadIdx.x; i < q.ns * cpr; i += kThr) {
+    const int s = i / cpr, c = i % cpr;
+    *reinterpret_cast<float2 *>(out + s * q.ngt + 2 * c) = red[s][c];
+  }
+}
+
 // One warp per output: lane l sums chunks l, l+32, ... (fixed order), then a fixed xor-tree.
 __global__ void k_small_reduce(const __grid_constant__ SmallWgrad p, Plan q) {
   const int n = q.ns * q.ngt;
@@ -105,11 +167,16 @@ size_t small_wgrad_partial_floats(int T, int R, int NG) {
 cudaError_t launch_small_wgrad(const SmallWgrad &p, cudaStream_t s) {
   const Plan q = plan_for(p);
   if (q.ns > kSmallMax || q.ngt > 128 || p.NG > 128) return cudaErrorInvalidValue;
+  if (p.Gb && (p.mode != kSmallBiasX || p.NG % 64)) return cudaErrorInvalidValue;
   if (int64_t(q.nchunks) * q.ns * q.ngt > p.partial_cap) return cudaErrorInvalidValue;
   {
     const double tr = double(p.T) * p.R;
-    ProfScope prof(kProfGemmWgrad, s, 4.0 * tr * (p.NG + q.ns), 2.0 * tr * q.ns * q.ngt);
-    k_small_wgrad<<<unsigned(q.nchunks), kThr, 0, s>>>(p, q);
+    ProfScope prof(kProfGemmWgrad, s, tr * ((p.Gb ? 2.0 : 4.0) * p.NG + 4.0 * q.ns),
+                   2.0 * tr * q.ns * q.ngt);
+    if (p.Gb)
+      k_small_wgrad_bf<<<unsigned(q.nchunks), kThr, 0, s>>>(p, q);
+    else
+      k_small_wgrad<<<unsigned(q.nchunks), kThr, 0, s>>>(p, q);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;

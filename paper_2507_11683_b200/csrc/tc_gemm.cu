@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
                                          a.z * hp.z * rr.z * (1.f - rr.z), a.w * hp.w * rr.w * (1.f - rr.w));
             st4(p.g_dHprev + ro, make_float4(fmaf(a.x, rr.x, dh.x), fmaf(a.y, rr.y, dh.y),
                                              fmaf(a.z, rr.z, dh.z), fmaf(a.w, rr.w, dh.w)));
-            st4(p.g_dG + rg, g);
+            if (p.g_dG) st4(p.g_dG + rg, g);
             st4_bf16(p.g_dGb + rg, g);
           } else {
             float *d = p.dst[ct] + int64_t(row) * 64 + c4;

@@ -51,7 +51,7 @@ struct TcFwd {
   int dst_acc[2];
   // bwd, candidate GEMM: column tile `fuse_tile` is d(r*H_{t-1}); instead of storing it, run the
   // gate backward there: dG_r = acc H_{t-1} r (1-r) (fp32 g_dG + bf16 g_dGb, [R][2H], columns
-  // [0,H)), g_dHprev += acc r.  Uses Hprev.  -1 = off.
+  // [0,H)), g_dHprev += acc r.  Uses Hprev.  -1 = off.  g_dG may be null (bf16 copy only).
   int fuse_tile = -1;
   const float *g_r;
   float *g_dG;
