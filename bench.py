@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--placement", default="halo", choices=["halo", "replicated"],
                     help="halo shard (BASELINE north star) or the paper's replicated copy with a "
                          "global shuffle and per-epoch validation all-reduce (P:325, P:424)")
+    ap.add_argument("--zero-copy", action="store_true",
+                    help="read windows straight from the series by index (no x/y gather, f2)")
     ap.add_argument("--shuffle", default="window", choices=["window", "batch", "none"],
                     help="per-epoch window shuffle, batch-order shuffle (P:454), or none")
     return ap.parse_args()
@@ -206,7 +208,7 @@ def config_dict(cfg, world, args):
                            f"{args.shuffle} shuffle)",
             "precision": "fp32" if args.precision == 0 else "bf16",
             "l2": "no flush: each step writes >= 1 GB of fresh activations (>> 126 MB L2)",
-            "cuda_graph": not args.no_graph}
+            "cuda_graph": not args.no_graph, "zero_copy": bool(args.zero_copy)}
 
 
 # ------------------------------------------------------------------------------ our arm
@@ -256,7 +258,7 @@ def main():
     t0 = time.perf_counter()
     tr = Trainer(cfg, graph, lambda a, b: rows, params0, rank, world, local, comm,
                  precision=args.precision, use_cuda_graph=not args.no_graph,
-                 placement=args.placement,
+                 placement=args.placement, zero_copy=args.zero_copy,
                  shuffle={"window": True, "batch": "batch", "none": False}[args.shuffle])
     torch.cuda.synchronize()
     load_s = time.perf_counter() - t0

@@ -240,6 +240,20 @@ pgti_status pgti_dcrnn_step(const pgti_dcrnn_desc *d, const float *params, float
                             const float *x, const float *y, float *loss_dev, void *workspace,
                             size_t ws_bytes, float *act_dump, void *stream);
 
+/* Zero-copy index-batched step ("views, not copies"):
+ * the same forward + BPTT as pgti_dcrnn_step, but the first layer's inputs and
+ * the loss targets are read straight from the resident series by window start
+ * -- sample b's x_t is series row dev_idx[b] + t and its y_t row dev_idx[b] +
+ * T_in + t -- so no x / y batch buffers and no gather launch.  dev_idx: B device
+ * int32 window starts (global rows; windows must be held by `series`, else the
+ * sample reads zeros and the OUT_OF_RANGE device flag is raised).  series N, F,
+ * ld must equal the desc's.  Results are bit-identical to pgti_gather_batch +
+ * pgti_dcrnn_step.  Errors: as pgti_dcrnn_step, plus SHAPE (series vs desc). */
+pgti_status pgti_dcrnn_step_indexed(const pgti_dcrnn_desc *d, const float *params, float *grads,
+                                    const pgti_series *series, const int32_t *dev_idx,
+                                    float *loss_dev, void *workspace, size_t ws_bytes,
+                                    float *act_dump, void *stream);
+
 /* Forward pass and loss only (the validation MAE of distributed-index-batching,
  * P:424): the same forward as pgti_dcrnn_step -- same kernels, same
  * workspace (workspace_bytes), same *loss_dev -- with no backward and no

@@ -16,6 +16,9 @@ pgti_status fail(pgti_status st, const char *fmt, ...);
 void clear_error();
 // Device address of the sticky error-flag word (bit 1: out of range, bit 2: non-finite).
 unsigned *device_error_flag();
+// internal view of a series handle (series.cu)
+void series_view(const pgti_series *sr, const float **buf, int64_t *row0, int64_t *nrows,
+                 int64_t *N, int64_t *F, int64_t *ld);
 
 enum : unsigned { kDevErrRange = 1u, kDevErrNonfinite = 2u };
 

@@ -247,7 +247,8 @@ Layout make_layout(const Dims &d) {
 }
 
 pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *params, float *grads,
-                     const float *x, const float *y, float *loss_dev, char *ws, float *act_dump,
+                     const WindowSrc &x, const WindowSrc &y, float *loss_dev, char *ws,
+                     float *act_dump,
                      cudaStream_t s) {
   const Layout Ly = make_layout(d);
   const ParamOffsets P = param_offsets(d);
@@ -260,7 +261,7 @@ pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *param
   PGTI_REQUIRE(err, PGTI_ERR_CUDA, "device error flag unavailable");
 
   // ------------------------------------------------------------------ forward
-  CU(launch_x_prep(x, d.B, T, d.ld, d.N, d.F, Dx, s));
+  CU(launch_x_prep(x, d.B, T, d.ld, d.N, d.F, Dx, err, s));
   CU(diffuse_fwd(g, d, Dx, int64_t(T) * RF, T, RF, int64_t(d.B) * d.F, s));
   for (int t = 0; t < T; ++t) {
     for (int l = 0; l < L; ++l) {
@@ -431,10 +432,11 @@ extern "C" pgti_status pgti_dcrnn_loss(const pgti_dcrnn_desc *desc, const float 
   const size_t need = workspace_for(d);
   PGTI_REQUIRE(ws_bytes >= need, PGTI_ERR_WORKSPACE,
                "pgti_dcrnn_loss: workspace %zu bytes < %zu needed", ws_bytes, need);
+  const WindowSrc xs{x, nullptr, 0, 0, 0, 0}, ys{y, nullptr, 0, 0, 0, 0};
   if (d.precision == 1)
-    return run_step_tc(*desc, d, params, nullptr, x, y, loss_dev, static_cast<char *>(workspace),
+    return run_step_tc(*desc, d, params, nullptr, xs, ys, loss_dev, static_cast<char *>(workspace),
                        nullptr, as_stream(stream));
-  return run_step(*desc, d, params, nullptr, x, y, loss_dev, static_cast<char *>(workspace),
+  return run_step(*desc, d, params, nullptr, xs, ys, loss_dev, static_cast<char *>(workspace),
                   nullptr, as_stream(stream));
 }
 
@@ -452,10 +454,41 @@ extern "C" pgti_status pgti_dcrnn_step(const pgti_dcrnn_desc *desc, const float 
   const size_t need = workspace_for(d);
   PGTI_REQUIRE(ws_bytes >= need, PGTI_ERR_WORKSPACE,
                "pgti_dcrnn_step: workspace %zu bytes < %zu needed", ws_bytes, need);
+  const WindowSrc xs{x, nullptr, 0, 0, 0, 0}, ys{y, nullptr, 0, 0, 0, 0};
   if (d.precision == 1)
-    return run_step_tc(*desc, d, params, grads, x, y, loss_dev, static_cast<char *>(workspace),
+    return run_step_tc(*desc, d, params, grads, xs, ys, loss_dev, static_cast<char *>(workspace),
                        act_dump, as_stream(stream));
-  return run_step(*desc, d, params, grads, x, y, loss_dev, static_cast<char *>(workspace),
+  return run_step(*desc, d, params, grads, xs, ys, loss_dev, static_cast<char *>(workspace),
+                  act_dump, as_stream(stream));
+}
+
+extern "C" pgti_status pgti_dcrnn_step_indexed(const pgti_dcrnn_desc *desc, const float *params,
+                                               float *grads, const pgti_series *series,
+                                               const int32_t *dev_idx, float *loss_dev,
+                                               void *workspace, size_t ws_bytes, float *act_dump,
+                                               void *stream) {
+  clear_error();
+  Dims d;
+  PGTI_STATUS_TRY(check_desc(desc, &d));
+  PGTI_REQUIRE(params && grads && series && dev_idx && loss_dev && workspace,
+               PGTI_ERR_INVALID_ARG, "pgti_dcrnn_step_indexed: null pointer");
+  PGTI_REQUIRE(aligned16(params) && aligned16(grads) && aligned16(workspace), PGTI_ERR_ALIGNMENT,
+               "pgti_dcrnn_step_indexed: params / grads / workspace must be 16-byte aligned");
+  const float *buf = nullptr;
+  int64_t row0 = 0, nrows = 0, N = 0, F = 0, ld = 0;
+  series_view(series, &buf, &row0, &nrows, &N, &F, &ld);
+  PGTI_REQUIRE(N == d.N && F == d.F && ld == d.ld, PGTI_ERR_SHAPE,
+               "pgti_dcrnn_step_indexed: series N=%lld F=%lld ld=%lld vs desc N=%d F=%d ld=%lld",
+               (long long)N, (long long)F, (long long)ld, d.N, d.F, (long long)d.ld);
+  const size_t need = workspace_for(d);
+  PGTI_REQUIRE(ws_bytes >= need, PGTI_ERR_WORKSPACE,
+               "pgti_dcrnn_step_indexed: workspace %zu bytes < %zu needed", ws_bytes, need);
+  const int span = d.T_in + d.T_out;
+  const WindowSrc xs{buf, dev_idx, row0, nrows, 0, span}, ys{buf, dev_idx, row0, nrows, d.T_in, span};
+  if (d.precision == 1)
+    return run_step_tc(*desc, d, params, grads, xs, ys, loss_dev, static_cast<char *>(workspace),
+                       act_dump, as_stream(stream));
+  return run_step(*desc, d, params, grads, xs, ys, loss_dev, static_cast<char *>(workspace),
                   act_dump, as_stream(stream));
 }
 

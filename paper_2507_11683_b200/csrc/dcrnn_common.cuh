@@ -45,8 +45,8 @@ cudaError_t diffuse_adj(const pgti_dcrnn_desc &g, const Dims &d, AdjChain *ch, i
 // precision = 1 (dcrnn_tc.cu)
 size_t workspace_tc(const Dims &d);
 pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *params,
-                        float *grads, const float *x, const float *y, float *loss_dev, char *ws,
-                        float *act_dump, cudaStream_t s);
+                        float *grads, const WindowSrc &x, const WindowSrc &y, float *loss_dev,
+                        char *ws, float *act_dump, cudaStream_t s);
 
 }  // namespace detail
 }  // namespace pgti

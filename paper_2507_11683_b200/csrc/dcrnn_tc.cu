@@ -126,8 +126,8 @@ LayoutTC make_layout_tc(const Dims &d) {
 size_t workspace_tc(const Dims &d) { return make_layout_tc(d).total; }
 
 pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *params,
-                        float *grads, const float *x, const float *y, float *loss_dev, char *ws,
-                        float *act_dump, cudaStream_t s) {
+                        float *grads, const WindowSrc &x, const WindowSrc &y, float *loss_dev,
+                        char *ws, float *act_dump, cudaStream_t s) {
   const LayoutTC Ly = make_layout_tc(d);
   const ParamOffsets P = param_offsets(d);
   auto Fp = [&](size_t off) { return reinterpret_cast<float *>(ws + off); };
@@ -158,7 +158,7 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
     }
     for (int i = 0; i < nj; i += 8) CU(launch_convert_weights(jobs + i, std::min(8, nj - i), s));
   }
-  CU(launch_x_prep(x, d.B, T, d.ld, d.N, d.F, Dx, s));
+  CU(launch_x_prep(x, d.B, T, d.ld, d.N, d.F, Dx, err, s));
   CU(diffuse_fwd(g, d, Dx, int64_t(T) * RF, T, RF, int64_t(d.B) * d.F, s));
   for (int l = 1; l < L; ++l) CU(depend(sp, s, st[l]));  // fork
 

@@ -15,8 +15,17 @@ inline unsigned grid_for(int64_t n, int cap = 148 * 16) {
 
 // x[b][t][ld] (gathered batch, sample-major) -> X0[t][n][b][f] (node-major rows = n*B + b,
 // the dense-operand layout of the diffusion SpMM and the row order of the gate GEMMs).
-__global__ void k_x_prep(const float *__restrict__ x, int B, int T_in, int64_t ld, int N, int F,
-                         float *__restrict__ X0) {
+// Row t of sample b's slice (nullptr if the window is not held: caller reads zeros).
+__device__ __forceinline__ const float *win_row(const WindowSrc &w, int b, int t, int T,
+                                                int64_t ld) {
+  if (!w.idx) return w.base + (int64_t(b) * T + t) * ld;
+  const int64_t s = int64_t(w.idx[b]) - w.row0;
+  if (s < 0 || s + w.span > w.nrows) return nullptr;
+  return w.base + (s + w.toff + t) * ld;
+}
+
+__global__ void k_x_prep(const __grid_constant__ WindowSrc xs, int B, int T_in, int64_t ld,
+                         int N, int F, float *__restrict__ X0, unsigned *__restrict__ err) {
   const int64_t total = int64_t(T_in) * N * B * F;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
        i += int64_t(gridDim.x) * blockDim.x) {
@@ -27,13 +36,15 @@ __global__ void k_x_prep(const float *__restrict__ x, int B, int T_in, int64_t l
     q /= B;
     const int n = int(q % N);
     const int t = int(q / N);
-    X0[i] = x[(int64_t(b) * T_in + t) * ld + int64_t(n) * F + f];
+    const float *row = win_row(xs, b, t, T_in, ld);
+    if (!row && n == 0 && f == 0 && t == 0) atomicOr(err, kDevErrRange);
+    X0[i] = row ? row[int64_t(n) * F + f] : 0.f;
   }
 }
 
 // loss = mean |yhat - y[..., :F_out]|; dyhat = sign(resid) / count (0 at ties).
 // yhat/dyhat [T_out][N*B][F_out] (row n*B + b); y [B][T_out][ld].
-__global__ void k_loss_partial(const float *__restrict__ yhat, const float *__restrict__ y,
+__global__ void k_loss_partial(const float *__restrict__ yhat, const __grid_constant__ WindowSrc ys,
                                int T_out, int N, int B, int F, int F_out, int64_t ld,
                                float *__restrict__ dyhat, double *__restrict__ partials) {
   const int64_t R = int64_t(N) * B, total = int64_t(T_out) * R * F_out;
@@ -46,7 +57,8 @@ __global__ void k_loss_partial(const float *__restrict__ yhat, const float *__re
     const int64_t row = rt % R;
     const int tt = int(rt / R);
     const int n = int(row / B), b = int(row % B);
-    const float yv = y[(int64_t(b) * T_out + tt) * ld + int64_t(n) * F + o];
+    const float *yr = win_row(ys, b, tt, T_out, ld);
+    const float yv = yr ? yr[int64_t(n) * F + o] : 0.f;
     const float r = yhat[i] - yv;
     dyhat[i] = r > 0.f ? inv : (r < 0.f ? -inv : 0.f);
     acc += double(fabsf(r));
@@ -228,15 +240,15 @@ __global__ void k_convert_weights(const __grid_constant__ WeightParams p) {
 
 }  // namespace
 
-cudaError_t launch_x_prep(const float *x, int B, int T_in, int64_t ld, int N, int F, float *X0,
-                          cudaStream_t s) {
+cudaError_t launch_x_prep(const WindowSrc &xs, int B, int T_in, int64_t ld, int N, int F,
+                          float *X0, unsigned *err, cudaStream_t s) {
   const int64_t n = int64_t(T_in) * N * B * F;
   ProfScope prof(kProfElementwise, s, 8.0 * double(n), 0.0);
-  k_x_prep<<<grid_for(n), kT, 0, s>>>(x, B, T_in, ld, N, F, X0);
+  k_x_prep<<<grid_for(n), kT, 0, s>>>(xs, B, T_in, ld, N, F, X0, err);
   return cudaGetLastError();
 }
 
-cudaError_t launch_loss(const float *yhat, const float *y, int T_out, int N, int B, int F,
+cudaError_t launch_loss(const float *yhat, const WindowSrc &y, int T_out, int N, int B, int F,
                         int F_out, int64_t ld, float *dyhat, double *partials, float *loss,
                         unsigned *err, cudaStream_t s) {
   ProfScope prof(kProfLoss, s, 12.0 * double(T_out) * N * B * F_out, 0.0, 2);

@@ -149,9 +149,19 @@ cudaError_t launch_small_wgrad(const SmallWgrad &p, cudaStream_t s);
 size_t small_wgrad_partial_floats(int T, int R, int NG);
 
 // ------------------------------------------------------------------ elementwise
-cudaError_t launch_x_prep(const float *x, int B, int T_in, int64_t ld, int N, int F, float *X0,
-                          cudaStream_t s);
-cudaError_t launch_loss(const float *yhat, const float *y, int T_out, int N, int B, int F,
+// Where the step reads its windows: a gathered batch ([B][T][ld], idx == nullptr) or, zero-copy
+// (SURVEY f2), the resident series itself by window start: sample b's row t of the slice is
+// series row idx[b] - row0 + toff + t (toff = 0 for x, T_in for y).  A start whose window
+// [idx[b], idx[b] + span) is not held reads zeros and raises the OUT_OF_RANGE device flag.
+struct WindowSrc {
+  const float *base;
+  const int32_t *idx;   // nullable: gathered batch
+  int64_t row0, nrows;  // series rows held (idx != nullptr)
+  int toff, span;
+};
+cudaError_t launch_x_prep(const WindowSrc &xs, int B, int T_in, int64_t ld, int N, int F,
+                          float *X0, unsigned *err, cudaStream_t s);
+cudaError_t launch_loss(const float *yhat, const WindowSrc &ys, int T_out, int N, int B, int F,
                         int F_out, int64_t ld, float *dyhat, double *partials, float *loss,
                         unsigned *err, cudaStream_t s);
 constexpr int kLossBlocks = 296;

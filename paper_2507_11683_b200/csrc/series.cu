@@ -315,6 +315,13 @@ extern "C" pgti_status pgti_series_normalize(pgti_series *sr, double mu, double 
   return PGTI_OK;
 }
 
+namespace pgti {
+void series_view(const pgti_series *sr, const float **buf, int64_t *row0, int64_t *nrows,
+                 int64_t *N, int64_t *F, int64_t *ld) {
+  *buf = sr->buf, *row0 = sr->row0, *nrows = sr->nrows, *N = sr->N, *F = sr->F, *ld = sr->ld;
+}
+}  // namespace pgti
+
 extern "C" pgti_status pgti_series_info(const pgti_series *sr, int64_t *row0, int64_t *nrows,
                                         int64_t *N, int64_t *F, int64_t *ld) {
   pgti::clear_error();

@@ -82,6 +82,8 @@ _num_params = _sig("pgti_dcrnn_num_params", _sz, C.POINTER(DcrnnDesc))
 _ws_bytes = _sig("pgti_dcrnn_workspace_bytes", _sz, C.POINTER(DcrnnDesc))
 _step = _sig("pgti_dcrnn_step", C.c_int, C.POINTER(DcrnnDesc), _vp, _vp, _vp, _vp, _vp, _vp, _sz,
              _vp, _vp)
+_step_idx = _sig("pgti_dcrnn_step_indexed", C.c_int, C.POINTER(DcrnnDesc), _vp, _vp, _vp, _vp,
+                 _vp, _vp, _sz, _vp, _vp)
 _loss = _sig("pgti_dcrnn_loss", C.c_int, C.POINTER(DcrnnDesc), _vp, _vp, _vp, _vp, _vp, _sz, _vp)
 _diffuse = _sig("pgti_diffuse", C.c_int, C.POINTER(DcrnnDesc), _vp, _i64, _vp, _vp)
 _diffuse_adj = _sig("pgti_diffuse_adjoint", C.c_int, C.POINTER(DcrnnDesc), _vp, _i64, _vp, _vp)
@@ -338,6 +340,14 @@ class DCRNN:
         _ok(_step(C.byref(self.desc), _ptr(params), _ptr(grads), _ptr(x), _ptr(y),
                   _ptr(loss_dev), _ptr(workspace), workspace.numel() * workspace.element_size(),
                   _ptr(act_dump), _stream(stream)))
+
+    def step_indexed(self, params, grads, series, dev_idx, loss_dev, workspace, act_dump=None,
+                     stream=None):
+        """pgti_dcrnn_step_indexed: zero-copy step reading windows from `series` (a Series)."""
+        _ok(_step_idx(C.byref(self.desc), _ptr(params), _ptr(grads), series.h, _ptr(dev_idx),
+                      _ptr(loss_dev), _ptr(workspace),
+                      workspace.numel() * workspace.element_size(), _ptr(act_dump),
+                      _stream(stream)))
 
     def loss(self, params, x, y, loss_dev, workspace, stream=None):
         """pgti_dcrnn_loss: forward + loss only (validation)."""

@@ -84,7 +84,7 @@ class Trainer:
 
     def __init__(self, cfg, graph, series_fn, params0, rank=0, world=1, device=0, comm=None,
                  seed=3, lr=1e-2, precision=0, shuffle=True, use_cuda_graph=True,
-                 two_hop=False, placement="halo"):
+                 two_hop=False, placement="halo", zero_copy=False):
         import torch
 
         self.torch = torch
@@ -98,6 +98,7 @@ class Trainer:
         assert shuffle in (True, False, "batch"), shuffle
         assert not (placement == "replicated" and shuffle == "batch"), "batch shuffle is per shard"
         self.placement = placement
+        self.zero_copy = zero_copy  # f2: windows read from the series by index, no x/y gather
         self.S_r = self.S_tr // world
         self.idx_off = 0
         self.plan = (shard_plan(self.S_tr, world, rank, cfg.T_in, cfg.T_out)
@@ -208,8 +209,11 @@ class Trainer:
     # ------------------------------------------------------------------ one step
     def _body(self, idx):
         cfg = self.cfg
-        self.series.gather(idx, cfg.B, cfg.T_in, cfg.T_out, self.x, self.y)
-        self.model.step(self.params, self.grads, self.x, self.y, self.loss, self.ws)
+        if self.zero_copy:
+            self.model.step_indexed(self.params, self.grads, self.series, idx, self.loss, self.ws)
+        else:
+            self.series.gather(idx, cfg.B, cfg.T_in, cfg.T_out, self.x, self.y)
+            self.model.step(self.params, self.grads, self.x, self.y, self.loss, self.ws)
         if self.comm is not None and self.world > 1:
             self.comm.allreduce_grads(self.grads)
         pgti.adam_step(self.params, self.grads, self.m, self.v, 0, self.lr,

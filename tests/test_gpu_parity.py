@@ -534,3 +534,70 @@ def test_validation_mae_vs_oracle(env, precision, tol):
                                     x.astype(np.float64), y.astype(np.float64))["loss"])
     want = float(np.mean(losses))
     assert abs(mae - want) <= tol * abs(want), (mae, want)
+
+
+# ------------------------------------------------------------------ NEXT f2: zero-copy step
+@pytest.mark.parametrize("name,precision,B", [("odd", 0, None), ("tc_tiny", 1, None),
+                                              ("metr_la", 1, 64), ("metr_la", 0, 8)])
+def test_step_indexed_bitexact_vs_gather(env, name, precision, B):
+    """pgti_dcrnn_step_indexed reads x / y straight from the resident series by window start
+    (SURVEY f2): loss, activations and gradients are bit-identical to gather + step, on a shard
+    whose rows start past 0 (global row indices)."""
+    pgti, torch = env
+    from paper_2507_11683_b200 import trainer
+    cfg = TC_CONFIGS.get(name) or SMALL_CONFIGS.get(name) or synth.CONFIGS[name]
+    cfg = cfg.replace(B=B or cfg.B)
+    ref = ref_for(cfg)
+    p = trainer.shard_plan(ref.n_train, 2, 1, cfg.T_in, cfg.T_out)
+    s = load_series(pgti, torch, ref.v[p.row_lo:p.row_hi], p.row_lo, cfg, ref.mu, ref.sigma)
+    idx = torch.empty(p.win_hi - p.win_lo, dtype=torch.int32, device="cuda")
+    s.make_index(p.win_lo, p.win_hi, cfg.T_in, cfg.T_out, cfg.B, 3, 4, 1, 1, idx)
+    bidx = idx[:cfg.B].clone()
+    ld = ld_of(cfg)
+    x = torch.empty(cfg.B * cfg.T_in * ld, device="cuda")
+    y = torch.empty(cfg.B * cfg.T_out * ld, device="cuda")
+    s.gather(bidx, cfg.B, cfg.T_in, cfg.T_out, x, y)
+    model = model_for(pgti, torch, cfg, ref.graph, precision=precision)
+    theta = torch.from_numpy(synth.make_params(cfg, kind="random")).cuda()
+    n = model.num_params()
+    ws = torch.empty(model.workspace_bytes(), dtype=torch.uint8, device="cuda")
+    out = []
+    for indexed in (False, True):
+        grads = torch.full((n,), float("nan"), device="cuda")
+        loss = torch.zeros(1, device="cuda")
+        act = torch.empty(model.act_dump_floats(), device="cuda")
+        if indexed:
+            model.step_indexed(theta, grads, s, bidx, loss, ws, act)
+        else:
+            model.step(theta, grads, x, y, loss, ws, act)
+        pgti.check_device_error()
+        out.append((loss.item(), grads.cpu().numpy(), act.cpu().numpy()))
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1]) and np.array_equal(out[0][2], out[1][2])
+    # a window start outside the held rows raises the device flag
+    bad = bidx.clone()
+    bad[0] = p.row_lo - 1
+    model.step_indexed(theta, torch.empty(n, device="cuda"), s, bad, loss, ws)
+    with pytest.raises(pgti.PgtiError) as e:
+        pgti.check_device_error()
+    assert e.value.name == "OUT_OF_RANGE"
+
+
+def test_trainer_zero_copy_graph_matches_gather(env):
+    """Trainer(zero_copy=True) under CUDA-graph replay: the same parameters after 3 steps as the
+    gather path (bitwise)."""
+    pgti, torch = env
+    from paper_2507_11683_b200.trainer import Trainer
+    cfg = SMALL_CONFIGS["cp"]
+    ref = ref_for(cfg)
+    theta = synth.make_params(cfg, kind="random")
+    res = []
+    for zc in (False, True):
+        tr = Trainer(cfg, ref.graph, lambda a, b: ref.v[a:b], theta, precision=0,
+                     use_cuda_graph=True, zero_copy=zc)
+        tr.start_epoch(0)
+        for j in range(3):
+            tr.step(j)
+        tr.check()
+        res.append(tr.params.cpu().numpy())
+    assert np.array_equal(res[0], res[1])
