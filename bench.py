@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--placement", default="halo", choices=["halo", "replicated"],
                     help="halo shard (BASELINE north star) or the paper's replicated copy with a "
                          "global shuffle and per-epoch validation all-reduce (P:325, P:424)")
+    ap.add_argument("--model", default="stepwise", choices=["stepwise", "encdec"],
+                    help="stepwise PGT-DCRNN (default) or Li et al.'s encoder-decoder (f3, "
+                         "runs on the fp32 path: use with --precision 0)")
     ap.add_argument("--zero-copy", action="store_true",
                     help="read windows straight from the series by index (no x/y gather, f2)")
     ap.add_argument("--shuffle", default="window", choices=["window", "batch", "none"],
@@ -122,18 +125,19 @@ def blas_threads():
         return 1
 
 
-def oracle_samples_per_s(cfg, n_windows: int, repeats: int, warm: int = 1):
+def oracle_samples_per_s(cfg, n_windows: int, repeats: int, warm: int = 1,
+                         model: str = "stepwise"):
     """Time the float64 oracle (Alg. 1 materialisation of the sampled windows + DCGRU forward/
     backward + Adam) on a bounded sample of the workload.  Returns (samples/s, details)."""
     import numpy as np
 
     import synth
-    from oracle import adam, dcgru, pipeline
+    from oracle import adam, dcgru, encdec, pipeline
 
     t0 = time.perf_counter()
     ref = pipeline.Reference(cfg, materialize_all=False)
     setup_s = time.perf_counter() - t0
-    theta = synth.make_params(cfg, kind="train").astype(np.float64)
+    theta = synth.make_params(cfg, kind="train", model=model).astype(np.float64)
     m = np.zeros_like(theta)
     v = np.zeros_like(theta)
     plan = ref.plan(1, 0)
@@ -143,8 +147,12 @@ def oracle_samples_per_s(cfg, n_windows: int, repeats: int, warm: int = 1):
         j += n_windows
         t1 = time.perf_counter()
         x, y = ref.batch(idx)
-        _, g, _ = dcgru.backward(theta, ref.d, ref.Pf, ref.Pb, x.astype(np.float64),
-                                 y.astype(np.float64))
+        if model == "encdec":
+            _, g, _ = encdec.loss_and_grad(theta, ref.d, ref.Pf, ref.Pb, x.astype(np.float64),
+                                           y.astype(np.float64))
+        else:
+            _, g, _ = dcgru.backward(theta, ref.d, ref.Pf, ref.Pb, x.astype(np.float64),
+                                     y.astype(np.float64))
         theta, m, v = adam.adam_step(theta, g, m, v, it + 1, 1e-2)
         if it >= warm:
             t_run += time.perf_counter() - t1
@@ -161,10 +169,10 @@ def run_reference(args, cfg):
     import numpy as np  # noqa: F401
     K, W = args.steps, args.warmup
     # calibrate the per-window cost, then size each step so the whole run ends in ~3 min
-    sps1, _ = oracle_samples_per_s(cfg, 1, 1, warm=0)
+    sps1, _ = oracle_samples_per_s(cfg, 1, 1, warm=0, model=args.model)
     per_step_budget = 150.0 / max(1, K + W)
     b = int(max(1, min(cfg.B, math.floor(per_step_budget * sps1))))
-    sps, det = oracle_samples_per_s(cfg, b, K, warm=W)
+    sps, det = oracle_samples_per_s(cfg, b, K, warm=W, model=args.model)
     cores = blas_threads()
     line = {"metric": METRIC, "value": round(sps, 4), "unit": "samples/s", "n_gpus": args.gpus,
             "steps": K, "warmup": W, "ms_per_step": round(1000.0 * b / sps, 3),
@@ -208,7 +216,8 @@ def config_dict(cfg, world, args):
                            f"{args.shuffle} shuffle)",
             "precision": "fp32" if args.precision == 0 else "bf16",
             "l2": "no flush: each step writes >= 1 GB of fresh activations (>> 126 MB L2)",
-            "cuda_graph": not args.no_graph, "zero_copy": bool(args.zero_copy)}
+            "cuda_graph": not args.no_graph, "zero_copy": bool(args.zero_copy),
+            "model": args.model}
 
 
 # ------------------------------------------------------------------------------ our arm
@@ -247,7 +256,7 @@ def main():
 
     # ---------------------------------------------------------------- setup (untimed)
     graph = synth.make_graph(cfg.N, cfg.knn)
-    params0 = synth.make_params(cfg, kind="train")
+    params0 = synth.make_params(cfg, kind="train", model=args.model)
     from paper_2507_11683_b200.trainer import shard_plan, train_windows, window_count
     from paper_2507_11683_b200.trainer import replicated_plan
     S_tr = train_windows(window_count(cfg.E, cfg.T_in, cfg.T_out))
@@ -259,6 +268,7 @@ def main():
     tr = Trainer(cfg, graph, lambda a, b: rows, params0, rank, world, local, comm,
                  precision=args.precision, use_cuda_graph=not args.no_graph,
                  placement=args.placement, zero_copy=args.zero_copy,
+                 model=1 if args.model == "encdec" else 0,
                  shuffle={"window": True, "batch": "batch", "none": False}[args.shuffle])
     torch.cuda.synchronize()
     load_s = time.perf_counter() - t0
@@ -438,7 +448,7 @@ def main():
         ck["reasons"] = reasons
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sps, det = oracle_samples_per_s(cfg, 8, 3)
+        sps, det = oracle_samples_per_s(cfg, 8, 3, model=args.model)
         cpu = {"value": round(sps, 4), "unit": "samples/s", "cores": blas_threads(),
                "kind": "oracle",
                "sample": f"3 batches x 8 windows of {cfg.name} (+1 warm-up), float64 Alg. 1 "

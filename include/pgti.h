@@ -220,6 +220,19 @@ typedef struct {
   const uint16_t *a2_lcol;
   const int32_t *at2_win_ptr, *at2_win_nodes;
   const uint16_t *at2_lcol;
+  /* Model family.  0 = the stepwise stacked PGT-DCRNN above.  1 = Li et al.'s
+   * DCRNN encoder-decoder (reading c24): the L-layer
+   * stack above run as the encoder over x_0..x_{T_in-1} (no readout), then a
+   * second L-layer stack (the decoder, own parameters, layer-0 C_in = F_out + H)
+   * for T_out steps starting from the encoder's final states; its layer-0 input
+   * is the GO symbol (zeros) at step 0, then the previous prediction
+   * (teacher_forcing = 0) or the previous target y[..., :F_out]
+   * (teacher_forcing = 1); yhat_s = H^L_s W_out + b_out on every decoder step.
+   * Parameters: encoder layers, decoder layers, W_out, b_out.  T_out may exceed
+   * T_in.  act_dump covers the T_in + T_out steps.  precision 0 only in this
+   * build (UNSUPPORTED otherwise). */
+  int32_t model;
+  int32_t teacher_forcing;
 } pgti_dcrnn_desc;
 
 /* Number of float parameters of the layout above (0 if desc invalid). */

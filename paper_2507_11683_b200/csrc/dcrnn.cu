@@ -26,8 +26,9 @@ namespace detail {
 ParamOffsets param_offsets(const Dims &d) {
   ParamOffsets o;
   size_t off = 0;
-  for (int l = 0; l < d.L; ++l) {
-    const size_t C = size_t((l == 0 ? d.F : d.H) + d.H);
+  for (int ll = 0; ll < d.L * (d.model ? 2 : 1); ++ll) {
+    const int l = ll % d.L, f0 = ll < d.L ? d.F : d.F_out;
+    const size_t C = size_t((l == 0 ? f0 : d.H) + d.H);
     o.Wru.push_back(off), off += size_t(d.M) * C * 2 * d.H;
     o.bru.push_back(off), off += 2 * d.H;
     o.Wc.push_back(off), off += size_t(d.M) * C * d.H;
@@ -45,7 +46,14 @@ pgti_status check_desc(const pgti_dcrnn_desc *desc, Dims *out) {
   PGTI_REQUIRE(g.N > 0 && g.F > 0 && g.L > 0 && g.K >= 0 && g.T_in > 0 && g.B > 0,
                PGTI_ERR_SHAPE, "desc: N=%d F=%d L=%d K=%d T_in=%d B=%d", g.N, g.F, g.L, g.K,
                g.T_in, g.B);
-  PGTI_REQUIRE(g.T_out >= 1 && g.T_out <= g.T_in, PGTI_ERR_SHAPE,
+  PGTI_REQUIRE(g.model == 0 || g.model == 1, PGTI_ERR_INVALID_ARG,
+               "desc: model=%d (0 = stepwise, 1 = encoder-decoder)", g.model);
+  PGTI_REQUIRE(g.teacher_forcing == 0 || (g.model == 1 && g.teacher_forcing == 1),
+               PGTI_ERR_INVALID_ARG, "desc: teacher_forcing=%d needs model 1",
+               g.teacher_forcing);
+  PGTI_REQUIRE(g.model == 0 || g.precision == 0, PGTI_ERR_UNSUPPORTED,
+               "desc: the encoder-decoder (model 1) runs on the fp32 path (precision 0) only");
+  PGTI_REQUIRE(g.T_out >= 1 && (g.model == 1 || g.T_out <= g.T_in), PGTI_ERR_SHAPE,
                "desc: need 1 <= T_out=%d <= T_in=%d (stepwise readout, reading c6)", g.T_out,
                g.T_in);
   PGTI_REQUIRE(g.F_out >= 1 && g.F_out <= g.F && g.F_out <= 4, PGTI_ERR_SHAPE,
@@ -81,7 +89,7 @@ pgti_status check_desc(const pgti_dcrnn_desc *desc, Dims *out) {
                  "plan pointers (win_rows=%d)",
                  g.win_rows);
   Dims d{g.N, g.F, g.F_out, g.L, g.H, g.K, g.T_in, g.T_out, g.B, 2 * g.K + 1,
-         int64_t(g.N) * g.B, g.ld, g.precision};
+         int64_t(g.N) * g.B, g.ld, g.precision, g.model, g.teacher_forcing};
   *out = d;
   return PGTI_OK;
 }
@@ -198,7 +206,7 @@ cudaError_t diffuse_adj(const pgti_dcrnn_desc &g, const Dims &d, AdjChain *ch, i
 namespace {
 
 struct Layout {
-  size_t Dx, yhat, dyhat, lossp, dU, drH, dTin, dTH, wpart, total;
+  size_t Dx, Dy, yhat, dyhat, lossp, dU, drH, dTin, dTH, wpart, total;
   size_t tmp[8];
   std::vector<size_t> DH, DrH, Rg, Ug, Cg, dG, dC, dHa, dHb;
   size_t tmp_floats, wpart_floats;
@@ -213,15 +221,18 @@ Layout make_layout(const Dims &d) {
     return o;
   };
   const size_t R = size_t(d.R), H = size_t(d.H), M = size_t(d.M), T = size_t(d.T_in);
+  const size_t TT = size_t(d.steps());
   L.Dx = take(M * T * R * d.F * 4);
+  // model 1: diffusion blocks of every decoder step's layer-0 input [T_out][M][R*F_out]
+  L.Dy = take(d.model ? size_t(d.T_out) * M * R * d.F_out * 4 : 0);
   for (int l = 0; l < d.L; ++l) {
-    L.DH.push_back(take(T * M * R * H * 4));
-    L.DrH.push_back(take(T * M * R * H * 4));
-    L.Rg.push_back(take(T * R * H * 4));
-    L.Ug.push_back(take(T * R * H * 4));
-    L.Cg.push_back(take(T * R * H * 4));
-    L.dG.push_back(take(T * R * 2 * H * 4));
-    L.dC.push_back(take(T * R * H * 4));
+    L.DH.push_back(take(TT * M * R * H * 4));
+    L.DrH.push_back(take(TT * M * R * H * 4));
+    L.Rg.push_back(take(TT * R * H * 4));
+    L.Ug.push_back(take(TT * R * H * 4));
+    L.Cg.push_back(take(TT * R * H * 4));
+    L.dG.push_back(take(TT * R * 2 * H * 4));
+    L.dC.push_back(take(TT * R * H * 4));
     L.dHa.push_back(take(R * H * 4));
     L.dHb.push_back(take(R * H * 4));
   }
@@ -230,15 +241,16 @@ Layout make_layout(const Dims &d) {
   L.lossp = take(size_t(kLossBlocks) * 8);
   L.dU = take(R * H * 4);
   L.drH = take(R * H * 4);
-  const size_t fin_max = d.L > 1 ? H : size_t(d.F);
+  const size_t fin_max = std::max(d.L > 1 ? H : size_t(d.F), size_t(d.model ? d.F_out : 0));
   L.dTin = take(M * R * fin_max * 4);
   L.dTH = take(M * R * H * 4);
   L.tmp_floats = R * std::max(H, fin_max);
   for (int i = 0; i < 8; ++i) L.tmp[i] = take(L.tmp_floats * 4);
   size_t wp = small_wgrad_partial_floats(d.T_out, int(d.R), d.H);
-  for (int l = 0; l < d.L; ++l) {
-    const int C = (l == 0 ? d.F : d.H) + d.H;
-    wp = std::max(wp, wgrad_partial_floats(d.M, C, 2 * d.H, d.T_in, int(d.R)));
+  for (int ll = 0; ll < d.L * (d.model ? 2 : 1); ++ll) {
+    const int l = ll % d.L, f0 = ll < d.L ? d.F : d.F_out;
+    const int C = (l == 0 ? f0 : d.H) + d.H, T_set = ll < d.L ? d.T_in : d.T_out;
+    wp = std::max(wp, wgrad_partial_floats(d.M, C, 2 * d.H, T_set, int(d.R)));
   }
   L.wpart_floats = wp;
   L.wpart = take(wp * 4);
@@ -246,6 +258,11 @@ Layout make_layout(const Dims &d) {
   return L;
 }
 
+// The fp32 step.  Stepwise model (model 0): hidden-state steps t < T_in, readout on the last
+// T_out.  Encoder-decoder (model 1, reading c24): steps t < T_in run the encoder stack (layer
+// set l), steps T_in <= t < T_in + T_out the decoder stack (layer set L + l) on the same hidden
+// chains, with a readout on every decoder step and the decoder's layer-0 input diffused per step
+// from the GO symbol / the previous prediction / the previous target.
 pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *params, float *grads,
                      const WindowSrc &x, const WindowSrc &y, float *loss_dev, char *ws,
                      float *act_dump,
@@ -254,20 +271,43 @@ pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *param
   const ParamOffsets P = param_offsets(d);
   auto Fp = [&](size_t off) { return reinterpret_cast<float *>(ws + off); };
   const int64_t R = d.R, H = d.H, M = d.M, RH = R * H, MRH = M * RH;
-  const int T = d.T_in, L = d.L;
-  float *Dx = Fp(Ly.Dx);
-  const int64_t RF = R * d.F;
+  const int T = d.T_in, L = d.L, TT = d.steps();
+  float *Dx = Fp(Ly.Dx), *Dy = Fp(Ly.Dy);
+  const int64_t RF = R * d.F, RFo = R * d.F_out;
   unsigned *err = device_error_flag();
   PGTI_REQUIRE(err, PGTI_ERR_CUDA, "device error flag unavailable");
+  // step t: decoder?  parameter set of layer l; readout slot (-1: none) of the top layer
+  auto is_dec = [&](int t) { return d.model == 1 && t >= T; };
+  auto pset = [&](int t, int l) { return is_dec(t) ? L + l : l; };
+  auto out_slot = [&](int t) {
+    return d.model == 1 ? (t >= T ? t - T : -1) : (t >= T - d.T_out ? t - (T - d.T_out) : -1);
+  };
+  auto fin_of = [&](int t, int l) { return l > 0 ? d.H : (is_dec(t) ? d.F_out : d.F); };
+  // layer-0 input blocks of step t and their block stride
+  auto in0 = [&](int t) { return is_dec(t) ? Dy + int64_t(t - T) * M * RFo : Dx + t * RF; };
+  auto in0_ms = [&](int t) { return is_dec(t) ? RFo : int64_t(T) * RF; };
 
   // ------------------------------------------------------------------ forward
   CU(launch_x_prep(x, d.B, T, d.ld, d.N, d.F, Dx, err, s));
   CU(diffuse_fwd(g, d, Dx, int64_t(T) * RF, T, RF, int64_t(d.B) * d.F, s));
-  for (int t = 0; t < T; ++t) {
+  for (int t = 0; t < TT; ++t) {
+    if (is_dec(t)) {  // decoder layer-0 input: GO, previous prediction or previous target
+      float *blk = Dy + int64_t(t - T) * M * RFo;
+      if (t == T) {
+        CU(cudaMemsetAsync(blk, 0, size_t(M * RFo) * 4, s));
+      } else {
+        if (d.teacher)
+          CU(launch_dec_input(y, t - T - 1, d.B, d.T_out, d.ld, d.N, d.F, d.F_out, blk, s));
+        else
+          CU(cudaMemcpyAsync(blk, Fp(Ly.yhat) + int64_t(t - T - 1) * RFo, size_t(RFo) * 4,
+                             cudaMemcpyDeviceToDevice, s));
+        CU(diffuse_fwd(g, d, blk, RFo, 1, 0, int64_t(d.B) * d.F_out, s));
+      }
+    }
     for (int l = 0; l < L; ++l) {
-      const int Fin = l == 0 ? d.F : d.H;
-      const float *Din = l == 0 ? Dx + t * RF : Fp(Ly.DH[l - 1]) + t * MRH;
-      const int64_t din_ms = l == 0 ? int64_t(T) * RF : RH;
+      const int Fin = fin_of(t, l), ps = pset(t, l);
+      const float *Din = l == 0 ? in0(t) : Fp(Ly.DH[l - 1]) + t * MRH;
+      const int64_t din_ms = l == 0 ? in0_ms(t) : RH;
       float *DHt = Fp(Ly.DH[l]) + t * MRH;
       const float *DHp = t > 0 ? Fp(Ly.DH[l]) + (t - 1) * MRH : nullptr;
       float *DrHt = Fp(Ly.DrH[l]) + t * MRH;
@@ -275,7 +315,7 @@ pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *param
 
       GconvFwd gate{};
       gate.a = GconvA{Din, din_ms, DHp, RH, Fin, d.H, d.M};
-      gate.R = int(R), gate.W = params + P.Wru[l], gate.bias = params + P.bru[l];
+      gate.R = int(R), gate.W = params + P.Wru[ps], gate.bias = params + P.bru[ps];
       gate.Nout = 2 * d.H, gate.mode = kEpiGate, gate.Hprev = DHp;
       gate.out_r = r, gate.out_u = u, gate.out_rH = DrHt;
       CU(launch_gconv_fwd(gate, s));
@@ -283,15 +323,15 @@ pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *param
 
       GconvFwd cand{};
       cand.a = GconvA{Din, din_ms, DrHt, RH, Fin, d.H, d.M};
-      cand.R = int(R), cand.W = params + P.Wc[l], cand.bias = params + P.bc[l];
+      cand.R = int(R), cand.W = params + P.Wc[ps], cand.bias = params + P.bc[ps];
       cand.Nout = d.H, cand.mode = kEpiCand, cand.Hprev = DHp;
       cand.u_in = u, cand.out_c = c, cand.out_H = DHt;
-      if (l == L - 1 && t >= T - d.T_out) {
+      if (l == L - 1 && out_slot(t) >= 0) {
         cand.Wout = params + P.Wout, cand.bout = params + P.bout, cand.F_out = d.F_out;
-        cand.yhat = Fp(Ly.yhat) + int64_t(t - (T - d.T_out)) * R * d.F_out;
+        cand.yhat = Fp(Ly.yhat) + int64_t(out_slot(t)) * RFo;
       }
       CU(launch_gconv_fwd(cand, s));
-      if (!(l == L - 1 && t == T - 1)) CU(diffuse_fwd(g, d, DHt, RH, 1, 0, int64_t(d.B) * d.H, s));
+      if (!(l == L - 1 && t == TT - 1)) CU(diffuse_fwd(g, d, DHt, RH, 1, 0, int64_t(d.B) * d.H, s));
     }
   }
   CU(launch_loss(Fp(Ly.yhat), y, d.T_out, d.N, d.B, d.F, d.F_out, d.ld, Fp(Ly.dyhat),
@@ -307,22 +347,24 @@ pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *param
   float *dU = Fp(Ly.dU), *drH = Fp(Ly.drH), *dTin = Fp(Ly.dTin), *dTH = Fp(Ly.dTH);
   float *tmp[8];
   for (int i = 0; i < 8; ++i) tmp[i] = Fp(Ly.tmp[i]);
-  for (int t = T - 1; t >= 0; --t) {
+  for (int t = TT - 1; t >= 0; --t) {
     for (int l = L - 1; l >= 0; --l) {
-      const int Fin = l == 0 ? d.F : d.H, C = Fin + d.H;
-      const bool need_in = l > 0, need_h = t > 0;
+      const int Fin = fin_of(t, l), C = Fin + d.H, ps = pset(t, l);
+      // the decoder's layer-0 input is the previous prediction: its gradient joins dyhat
+      const bool feed = l == 0 && is_dec(t) && t > T && !d.teacher;
+      const bool need_in = l > 0 || feed, need_h = t > 0;
       const float *Hprev = t > 0 ? Fp(Ly.DH[l]) + (t - 1) * MRH : nullptr;
       const float *r = Fp(Ly.Rg[l]) + t * RH, *u = Fp(Ly.Ug[l]) + t * RH, *c = Fp(Ly.Cg[l]) + t * RH;
       float *dC = Fp(Ly.dC[l]) + t * RH, *dG = Fp(Ly.dG[l]) + t * 2 * RH;
-      const float *dy = (l == L - 1 && t >= T - d.T_out)
-                            ? Fp(Ly.dyhat) + int64_t(t - (T - d.T_out)) * R * d.F_out
+      const float *dy = (l == L - 1 && out_slot(t) >= 0)
+                            ? Fp(Ly.dyhat) + int64_t(out_slot(t)) * RFo
                             : nullptr;
       CU(launch_cand_bwd(RH, d.H, dHcur[l], nullptr, dy, params + P.Wout, d.F_out, u, c, Hprev,
                          dU, dC, need_h ? dHprev[l] : nullptr, s));
       const int64_t tin_ms = R * Fin;
       if (need_in || need_h) {
         GconvDgrad dg{};
-        dg.G = dC, dg.R = int(R), dg.Nout = d.H, dg.W = params + P.Wc[l];
+        dg.G = dC, dg.R = int(R), dg.Nout = d.H, dg.W = params + P.Wc[ps];
         dg.M = d.M, dg.Fin = Fin, dg.Hd = d.H;
         dg.c_lo = need_in ? 0 : Fin, dg.c_hi = need_h ? C : Fin;
         dg.Tin = dTin, dg.tin_mstride = tin_ms, dg.acc_in = 0, dg.Th = dTH, dg.th_mstride = RH;
@@ -336,7 +378,7 @@ pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *param
                          need_h ? dHprev[l] : nullptr, dG, s));
       if (need_in || need_h) {
         GconvDgrad dg{};
-        dg.G = dG, dg.R = int(R), dg.Nout = 2 * d.H, dg.W = params + P.Wru[l];
+        dg.G = dG, dg.R = int(R), dg.Nout = 2 * d.H, dg.W = params + P.Wru[ps];
         dg.M = d.M, dg.Fin = Fin, dg.Hd = d.H;
         dg.c_lo = need_in ? 0 : Fin, dg.c_hi = need_h ? C : Fin;
         dg.Tin = dTin, dg.tin_mstride = tin_ms, dg.acc_in = 1, dg.Th = dTH, dg.th_mstride = RH;
@@ -346,9 +388,10 @@ pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *param
         if (need_h)
           ch[nch++] = AdjChain{dTH, RH, int64_t(d.B) * d.H, dHprev[l], 1, {tmp[0], tmp[1]},
                                {tmp[2], tmp[3]}};
-        if (need_in)
-          ch[nch++] = AdjChain{dTin, tin_ms, int64_t(d.B) * Fin, dHcur[l - 1], 1,
-                               {tmp[4], tmp[5]}, {tmp[6], tmp[7]}};
+        if (need_in)  // to the layer below, or (decoder layer 0) to the previous prediction
+          ch[nch++] = AdjChain{dTin, tin_ms, int64_t(d.B) * Fin,
+                               l > 0 ? dHcur[l - 1] : Fp(Ly.dyhat) + int64_t(out_slot(t) - 1) * RFo,
+                               1, {tmp[4], tmp[5]}, {tmp[6], tmp[7]}};
         CU(diffuse_adj(g, d, ch, nch, s));
       }
       std::swap(dHcur[l], dHprev[l]);
@@ -356,33 +399,44 @@ pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *param
   }
 
   // ------------------------------------------------------------------ weight gradients
-  for (int l = 0; l < L; ++l) {
-    const int Fin = l == 0 ? d.F : d.H;
+  for (int ll = 0; ll < L * (d.model ? 2 : 1); ++ll) {
+    const int l = ll % L, dec = ll >= L;
+    const int t0 = dec ? T : 0, nt = dec ? d.T_out : T;
+    const int Fin = l > 0 ? d.H : (dec ? d.F_out : d.F);
     GconvWgrad w{};
-    w.in = l == 0 ? Dx : Fp(Ly.DH[l - 1]);
-    w.in_tstride = l == 0 ? RF : MRH;
-    w.in_mstride = l == 0 ? int64_t(T) * RF : RH;
-    w.Fin = Fin, w.Hd = d.H, w.M = d.M, w.T = T, w.R = int(R);
+    if (l == 0) {
+      w.in = dec ? Dy : Dx;
+      w.in_tstride = dec ? M * RFo : RF;
+      w.in_mstride = dec ? RFo : int64_t(T) * RF;
+    } else {
+      w.in = Fp(Ly.DH[l - 1]) + t0 * MRH, w.in_tstride = MRH, w.in_mstride = RH;
+    }
+    w.Fin = Fin, w.Hd = d.H, w.M = d.M, w.T = nt, w.R = int(R);
     w.partial = Fp(Ly.wpart), w.partial_cap = int64_t(Ly.wpart_floats);
-    // r|u gate: Z_t = [in_t, H_{t-1}]
-    w.h = Fp(Ly.DH[l]), w.h_tstride = MRH, w.h_mstride = RH, w.h_toff = -1;
-    w.G = Fp(Ly.dG[l]), w.g_tstride = 2 * RH, w.Nout = 2 * d.H, w.out = grads + P.Wru[l];
+    // r|u gate: Z_t = [in_t, H_{t-1}] (the decoder's first step reads the encoder's last state)
+    if (dec)
+      w.h = Fp(Ly.DH[l]) + (t0 - 1) * MRH, w.h_toff = 0;
+    else
+      w.h = Fp(Ly.DH[l]), w.h_toff = -1;
+    w.h_tstride = MRH, w.h_mstride = RH;
+    w.G = Fp(Ly.dG[l]) + t0 * 2 * RH, w.g_tstride = 2 * RH, w.Nout = 2 * d.H;
+    w.out = grads + P.Wru[ll];
     CU(launch_gconv_wgrad(w, s));
     // candidate: Z'_t = [in_t, r*H_{t-1}]
-    w.h = Fp(Ly.DrH[l]), w.h_toff = 0;
-    w.G = Fp(Ly.dC[l]), w.g_tstride = RH, w.Nout = d.H, w.out = grads + P.Wc[l];
+    w.h = Fp(Ly.DrH[l]) + t0 * MRH, w.h_toff = 0;
+    w.G = Fp(Ly.dC[l]) + t0 * RH, w.g_tstride = RH, w.Nout = d.H, w.out = grads + P.Wc[ll];
     CU(launch_gconv_wgrad(w, s));
   }
   SmallWgrad rw{};
   rw.mode = kSmallReadout, rw.T = d.T_out, rw.R = int(R);
   rw.dy = Fp(Ly.dyhat), rw.F_out = d.F_out;
-  rw.G = Fp(Ly.DH[L - 1]) + int64_t(T - d.T_out) * MRH, rw.g_tstride = MRH, rw.NG = d.H;
+  rw.G = Fp(Ly.DH[L - 1]) + int64_t(TT - d.T_out) * MRH, rw.g_tstride = MRH, rw.NG = d.H;
   rw.partial = Fp(Ly.wpart), rw.partial_cap = int64_t(Ly.wpart_floats), rw.out = grads + P.Wout;
   CU(launch_small_wgrad(rw, s));
 
   // ------------------------------------------------------------------ test-only dump
   if (act_dump) {
-    for (int t = 0; t < T; ++t)
+    for (int t = 0; t < TT; ++t)
       for (int l = 0; l < L; ++l) {
         float *dst = act_dump + (int64_t(t) * L + l) * 4 * RH;
         const float *src[4] = {Fp(Ly.DH[l]) + t * MRH, Fp(Ly.Rg[l]) + t * RH,
@@ -390,7 +444,7 @@ pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *param
         for (int q = 0; q < 4; ++q)
           CU(cudaMemcpyAsync(dst + q * RH, src[q], size_t(RH) * 4, cudaMemcpyDeviceToDevice, s));
       }
-    CU(cudaMemcpyAsync(act_dump + int64_t(T) * L * 4 * RH, Fp(Ly.yhat),
+    CU(cudaMemcpyAsync(act_dump + int64_t(TT) * L * 4 * RH, Fp(Ly.yhat),
                        size_t(d.T_out) * R * d.F_out * 4, cudaMemcpyDeviceToDevice, s));
   }
   return PGTI_OK;

@@ -13,9 +13,14 @@ struct Dims {
   int N, F, F_out, L, H, K, T_in, T_out, B, M;
   int64_t R, ld;
   int precision;
+  int model;    // 0 stepwise stack, 1 encoder-decoder (pgti.h)
+  int teacher;  // encoder-decoder: 1 = decoder fed the previous target, 0 = its own prediction
+  // hidden-state steps: T_in (stepwise) or T_in + T_out (encoder then decoder)
+  int steps() const { return T_in + (model ? T_out : 0); }
 };
 
-// parameter offsets (floats) in the flat layout of pgti.h
+// parameter offsets (floats) in the flat layout of pgti.h; layer sets: [0, L) the (encoder)
+// stack, [L, 2L) the decoder of model 1
 struct ParamOffsets {
   std::vector<size_t> Wru, bru, Wc, bc;
   size_t Wout, bout, total;

@@ -42,6 +42,19 @@ __global__ void k_x_prep(const __grid_constant__ WindowSrc xs, int B, int T_in, 
   }
 }
 
+__global__ void k_dec_input(const __grid_constant__ WindowSrc ys, int tt, int B, int64_t ld,
+                            int N, int F, int F_out, int T_out, float *__restrict__ out) {
+  const int64_t total = int64_t(N) * B * F_out;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int o = int(i % F_out);
+    const int64_t row = i / F_out;
+    const int n = int(row / B), b = int(row % B);
+    const float *yr = win_row(ys, b, tt, T_out, ld);
+    out[i] = yr ? yr[int64_t(n) * F + o] : 0.f;
+  }
+}
+
 // loss = mean |yhat - y[..., :F_out]|; dyhat = sign(resid) / count (0 at ties).
 // yhat/dyhat [T_out][N*B][F_out] (row n*B + b); y [B][T_out][ld].
 __global__ void k_loss_partial(const float *__restrict__ yhat, const __grid_constant__ WindowSrc ys,
@@ -245,6 +258,14 @@ cudaError_t launch_x_prep(const WindowSrc &xs, int B, int T_in, int64_t ld, int 
   const int64_t n = int64_t(T_in) * N * B * F;
   ProfScope prof(kProfElementwise, s, 8.0 * double(n), 0.0);
   k_x_prep<<<grid_for(n), kT, 0, s>>>(xs, B, T_in, ld, N, F, X0, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dec_input(const WindowSrc &ys, int tt, int B, int T_out, int64_t ld, int N,
+                             int F, int F_out, float *out, cudaStream_t s) {
+  const int64_t n = int64_t(N) * B * F_out;
+  ProfScope prof(kProfElementwise, s, 8.0 * double(n), 0.0);
+  k_dec_input<<<grid_for(n), kT, 0, s>>>(ys, tt, B, ld, N, F, F_out, T_out, out);
   return cudaGetLastError();
 }
 

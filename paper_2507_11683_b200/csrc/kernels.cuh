@@ -161,6 +161,10 @@ struct WindowSrc {
 };
 cudaError_t launch_x_prep(const WindowSrc &xs, int B, int T_in, int64_t ld, int N, int F,
                           float *X0, unsigned *err, cudaStream_t s);
+// encoder-decoder teacher forcing: out[n*B + b][o] = y_tt[b][n][o] for o < F_out (row tt of the
+// target slice), the decoder's layer-0 input block 0
+cudaError_t launch_dec_input(const WindowSrc &ys, int tt, int B, int T_out, int64_t ld, int N,
+                             int F, int F_out, float *out, cudaStream_t s);
 cudaError_t launch_loss(const float *yhat, const WindowSrc &ys, int T_out, int N, int B, int F,
                         int F_out, int64_t ld, float *dyhat, double *partials, float *loss,
                         unsigned *err, cudaStream_t s);

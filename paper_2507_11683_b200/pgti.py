@@ -49,7 +49,8 @@ class DcrnnDesc(C.Structure):
                 ("a2_rowptr", _vp), ("a2_col", _vp), ("Pf2_val", _vp), ("Pb2T_val", _vp),
                 ("at2_rowptr", _vp), ("at2_col", _vp), ("Pb2_val", _vp), ("Pf2T_val", _vp),
                 ("a2_win_ptr", _vp), ("a2_win_nodes", _vp), ("a2_lcol", _vp),
-                ("at2_win_ptr", _vp), ("at2_win_nodes", _vp), ("at2_lcol", _vp)]
+                ("at2_win_ptr", _vp), ("at2_win_nodes", _vp), ("at2_lcol", _vp),
+                ("model", _i32), ("teacher_forcing", _i32)]
 
 
 def _sig(name, restype, *argtypes):
@@ -298,7 +299,9 @@ class DCRNN:
     """pgti_dcrnn_desc + the device CSR arrays it points to."""
 
     def __init__(self, N, F, F_out, L, H, K, T_in, T_out, B, ld, csr_dev: dict | None,
-                 precision: int = 0):
+                 precision: int = 0, model: int = 0, teacher_forcing: int = 0):
+        """model 0: stepwise stacked PGT-DCRNN; 1: Li et al. encoder-decoder (teacher_forcing:
+        decoder fed the previous target instead of its own prediction)."""
         self.csr = csr_dev or {}
         g = lambda k: _ptr(self.csr.get(k))  # noqa: E731
         nnz = int(self.csr["a_col"].numel()) if csr_dev else 0
@@ -312,7 +315,9 @@ class DCRNN:
                               g("a2_rowptr"), g("a2_col"), g("Pf2_val"), g("Pb2T_val"),
                               g("at2_rowptr"), g("at2_col"), g("Pb2_val"), g("Pf2T_val"),
                               g("a2_win_ptr"), g("a2_win_nodes"), g("a2_lcol"),
-                              g("at2_win_ptr"), g("at2_win_nodes"), g("at2_lcol"))
+                              g("at2_win_ptr"), g("at2_win_nodes"), g("at2_lcol"),
+                              int(model), int(teacher_forcing))
+        self.model = int(model)
         self.N, self.F, self.F_out, self.L, self.H, self.K = N, F, F_out, L, H, K
         self.T_in, self.T_out, self.B, self.ld = T_in, T_out, B, ld
 
@@ -334,7 +339,8 @@ class DCRNN:
 
     def act_dump_floats(self) -> int:
         R = self.N * self.B
-        return self.T_in * self.L * 4 * R * self.H + self.T_out * R * self.F_out
+        steps = self.T_in + (self.T_out if self.model else 0)
+        return steps * self.L * 4 * R * self.H + self.T_out * R * self.F_out
 
     def step(self, params, grads, x, y, loss_dev, workspace, act_dump=None, stream=None):
         _ok(_step(C.byref(self.desc), _ptr(params), _ptr(grads), _ptr(x), _ptr(y),

@@ -84,7 +84,7 @@ class Trainer:
 
     def __init__(self, cfg, graph, series_fn, params0, rank=0, world=1, device=0, comm=None,
                  seed=3, lr=1e-2, precision=0, shuffle=True, use_cuda_graph=True,
-                 two_hop=False, placement="halo", zero_copy=False):
+                 two_hop=False, placement="halo", zero_copy=False, model=0, teacher_forcing=0):
         import torch
 
         self.torch = torch
@@ -121,7 +121,8 @@ class Trainer:
         csr = pgti.add_windows(csr, cfg.N)
         self.csr = pgti.csr_to_device(csr, self.dev)
         self.model = pgti.DCRNN(cfg.N, cfg.F, cfg.F_out, cfg.L, cfg.H, cfg.K, cfg.T_in,
-                                cfg.T_out, cfg.B, self.ld, self.csr, precision)
+                                cfg.T_out, cfg.B, self.ld, self.csr, precision, model=model,
+                                teacher_forcing=teacher_forcing)
         n = self.model.num_params()
         assert params0.size == n, (params0.size, n)
         f32 = dict(dtype=torch.float32, device=self.dev)

@@ -214,31 +214,34 @@ def make_series(cfg: Config, seed: int = SEED_DATA, row_lo: int = 0, row_hi: int
 
 
 # --------------------------------------------------------------------------- params
-def param_shapes(cfg: Config):
-    """Parameter blocks in flat order."""
+def param_shapes(cfg: Config, model: str = "stepwise"):
+    """Parameter blocks in flat order; model "encdec": the encoder
+    layers, then the decoder layers (layer-0 input F_out channels), then the readout."""
     M = 2 * cfg.K + 1
     shapes = []
-    for l in range(cfg.L):
-        c_in = (cfg.F if l == 0 else cfg.H) + cfg.H
-        shapes += [(f"W_ru{l}", (M, c_in, 2 * cfg.H)), (f"b_ru{l}", (2 * cfg.H,)),
-                   (f"W_c{l}", (M, c_in, cfg.H)), (f"b_c{l}", (cfg.H,))]
+    stacks = [("", cfg.F)] + ([("dec", cfg.F_out)] if model == "encdec" else [])
+    for pre, f0 in stacks:
+        for l in range(cfg.L):
+            c_in = (f0 if l == 0 else cfg.H) + cfg.H
+            shapes += [(f"W_ru{pre}{l}", (M, c_in, 2 * cfg.H)), (f"b_ru{pre}{l}", (2 * cfg.H,)),
+                       (f"W_c{pre}{l}", (M, c_in, cfg.H)), (f"b_c{pre}{l}", (cfg.H,))]
     shapes += [("W_out", (cfg.H, cfg.F_out)), ("b_out", (cfg.F_out,))]
     return shapes
 
 
-def num_params(cfg: Config) -> int:
-    return sum(int(np.prod(s)) for _, s in param_shapes(cfg))
+def num_params(cfg: Config, model: str = "stepwise") -> int:
+    return sum(int(np.prod(s)) for _, s in param_shapes(cfg, model))
 
 
 def make_params(cfg: Config, seed: int = SEED_PARAMS, kind: str = "random",
-                scale: float = 1.0) -> np.ndarray:
+                scale: float = 1.0, model: str = "stepwise") -> np.ndarray:
     """Flat float32 parameters.  ``kind="random"``: every entry (biases too)
     uniform in +-scale/sqrt(fan_in), to exercise every path in parity tests;
     ``kind="train"``: weights as above, b_ru = 1, other biases 0 (Li et al.'s
     bias_start, [ext])."""
     rng = np.random.default_rng(seed)
     parts = []
-    for name, shp in param_shapes(cfg):
+    for name, shp in param_shapes(cfg, model):
         fan_in = shp[0] * shp[1] if len(shp) == 3 else (shp[0] if name == "W_out" else cfg.H)
         bound = scale / math.sqrt(fan_in)
         p = rng.uniform(-bound, bound, size=shp)

@@ -1,0 +1,118 @@
+"""Li et al. DCRNN encoder-decoder (desc.model = 1, reading c24) through the C ABI
+against oracle.encdec (float64): loss, predictions, every gradient tensor (1e-5 scale-relative,
+reading c19), in both decoder feedback modes; and the bit-exact zero-copy variant."""
+import numpy as np
+import pytest
+
+import synth
+from gpu_util import ld_of, load_series, scale_rel
+from oracle import dcgru, encdec, pipeline
+
+pytestmark = pytest.mark.gpu
+TOL32 = 1e-5
+
+CFGS = {
+    "ed_small": synth.Config("ed_small", N=12, E=60, F=2, T_in=3, T_out=4, L=2, H=16, K=2, B=3),
+    "ed_odd": synth.Config("ed_odd", N=33, E=70, F=3, F_out=2, T_in=4, T_out=2, L=1, H=32, K=1,
+                           B=5),
+    "ed_k0": synth.Config("ed_k0", N=9, E=50, F=2, T_in=2, T_out=3, L=3, H=16, K=0, B=2),
+}
+_REFS = {}
+
+
+def _ref(cfg):
+    if cfg.name not in _REFS:
+        _REFS[cfg.name] = pipeline.Reference(cfg)
+    return _REFS[cfg.name]
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2507_11683_b200 import build
+    build.build()
+    from paper_2507_11683_b200 import pgti
+    return pgti, torch
+
+
+def _model(pgti, torch, cfg, graph, tf):
+    csr = pgti.csr_to_device(pgti.graph_build(cfg.N, *graph), "cuda")
+    return pgti.DCRNN(cfg.N, cfg.F, cfg.F_out, cfg.L, cfg.H, cfg.K, cfg.T_in, cfg.T_out, cfg.B,
+                      ld_of(cfg), csr, 0, model=1, teacher_forcing=tf)
+
+
+def _case(env, cfg, tf, seed=0):
+    pgti, torch = env
+    ref = _ref(cfg)
+    s = load_series(pgti, torch, ref.v, 0, cfg, ref.mu, ref.sigma)
+    idx_np = ref.plan(1, 0, epoch=seed)[:cfg.B]
+    idx = torch.from_numpy(idx_np.astype(np.int32)).cuda()
+    ld = ld_of(cfg)
+    x = torch.empty(cfg.B * cfg.T_in * ld, device="cuda")
+    y = torch.empty(cfg.B * cfg.T_out * ld, device="cuda")
+    s.gather(idx, cfg.B, cfg.T_in, cfg.T_out, x, y)
+    model = _model(pgti, torch, cfg, ref.graph, tf)
+    d = dcgru.Dims.of(cfg)
+    n = model.num_params()
+    assert n == encdec.num_params(d)
+    theta = np.random.default_rng(seed + 11).uniform(-0.4, 0.4, n).astype(np.float32)
+    params = torch.from_numpy(theta).cuda()
+    grads = torch.full((n,), float("nan"), device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    ws = torch.empty(model.workspace_bytes(), dtype=torch.uint8, device="cuda")
+    act = torch.empty(model.act_dump_floats(), device="cuda")
+    model.step(params, grads, x, y, loss, ws, act)
+    pgti.check_device_error()
+    xo, yo = ref.batch(idx_np)
+    loss_ref, g_ref, yhat_ref = encdec.loss_and_grad(theta.astype(np.float64), d, ref.Pf, ref.Pb,
+                                                     xo.astype(np.float64),
+                                                     yo.astype(np.float64), teacher_forcing=tf)
+    margin = np.min(np.abs(yhat_ref - yo[..., :cfg.F_out].astype(np.float64)))
+    return dict(loss=loss.item(), g=grads.cpu().numpy(), act=act.cpu().numpy(), loss_ref=loss_ref,
+                g_ref=g_ref, yhat_ref=yhat_ref, margin=margin, d=d, model=model, s=s, idx=idx,
+                params=params, ws=ws)
+
+
+@pytest.mark.parametrize("tf", [0, 1])
+@pytest.mark.parametrize("name", list(CFGS))
+def test_encdec_step_vs_oracle(env, name, tf):
+    cfg = CFGS[name]
+    c = _case(env, cfg, tf)
+    assert c["margin"] > 1e-5, "a residual sits at an |.| kink; pick another seed"
+    assert abs(c["loss"] - c["loss_ref"]) <= TOL32 * abs(c["loss_ref"])
+    R = cfg.N * cfg.B
+    steps = cfg.T_in + cfg.T_out
+    yhat = c["act"][steps * cfg.L * 4 * R * cfg.H:].reshape(cfg.T_out, cfg.N, cfg.B, cfg.F_out)
+    assert scale_rel(yhat, c["yhat_ref"].transpose(1, 2, 0, 3)) <= TOL32
+    gscale = np.max(np.abs(c["g_ref"]))
+    off = 0
+    for nm, shp in encdec.layer_shapes(c["d"]):
+        n = int(np.prod(shp))
+        g, gr = c["g"][off:off + n].astype(np.float64), c["g_ref"][off:off + n]
+        den = max(np.max(np.abs(gr)), 1e-2 * gscale)
+        assert np.max(np.abs(g - gr)) / den <= TOL32, (nm, np.max(np.abs(g - gr)) / den)
+        off += n
+    assert off == c["g"].size
+
+
+def test_encdec_zero_copy_bitexact(env):
+    pgti, torch = env
+    cfg = CFGS["ed_small"]
+    c = _case(env, cfg, 0)
+    grads = torch.full_like(c["params"], float("nan"))
+    loss = torch.zeros(1, device="cuda")
+    c["model"].step_indexed(c["params"], grads, c["s"], c["idx"], loss, c["ws"])
+    pgti.check_device_error()
+    assert loss.item() == c["loss"] and np.array_equal(grads.cpu().numpy(), c["g"])
+
+
+def test_encdec_metr_la_shape(env):
+    """METR-LA-shaped encoder-decoder (372,353 parameters, 12 + 12 steps) at B = 8."""
+    cfg = synth.CONFIGS["metr_la"].replace(B=8)
+    c = _case(env, cfg, 0)
+    assert c["model"].num_params() == 372353
+    assert c["margin"] > 1e-5
+    assert abs(c["loss"] - c["loss_ref"]) <= TOL32 * abs(c["loss_ref"])
+    assert scale_rel(c["g"], c["g_ref"]) <= TOL32
