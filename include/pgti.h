@@ -322,6 +322,13 @@ const char *pgti_profile_class_name(int c);
 pgti_status pgti_profile_read(double *ms, double *bytes, double *flops, int64_t *launches, int n);
 /* Number of kernel launches libpgti has issued (captured launches included) since load. */
 uint64_t pgti_launch_count(void);
+/* Per-launch timeline of the recorded (not yet read) eager launches, in launch order:
+ * class, start / end in ms relative to the first record's start, and the stream handle
+ * (as an integer).  *count = the number recorded; at most cap entries are written (cap 0:
+ * count only).  Call before pgti_profile_read, which clears the records.  Errors:
+ * INVALID_ARG, CUDA. */
+pgti_status pgti_profile_timeline(int *cls, double *start_ms, double *end_ms, int64_t *stream,
+                                  int cap, int *count);
 
 #ifdef __cplusplus
 }

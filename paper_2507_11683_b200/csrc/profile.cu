@@ -12,6 +12,7 @@ struct Rec {
   int cls;
   cudaEvent_t a, b;
   double bytes, flops;
+  cudaStream_t s;
 };
 
 std::mutex g_mu;
@@ -48,7 +49,7 @@ ProfScope::ProfScope(int cls, cudaStream_t s, double bytes, double flops, int la
   g_launches.fetch_add(static_cast<unsigned long long>(launches));
   std::lock_guard<std::mutex> lk(g_mu);
   if (!g_enabled || capturing(s)) return;
-  Rec r{cls, get_event(), get_event(), bytes, flops};
+  Rec r{cls, get_event(), get_event(), bytes, flops, s};
   cudaEventRecord(r.a, s);
   g_recs.push_back(r);
   slot_ = int(g_recs.size()) - 1;
@@ -100,6 +101,29 @@ extern "C" pgti_status pgti_profile_read(double *ms, double *bytes, double *flop
   }
   g_recs.clear();
   return st;
+}
+
+extern "C" pgti_status pgti_profile_timeline(int *cls, double *start_ms, double *end_ms,
+                                             int64_t *stream, int cap, int *count) {
+  clear_error();
+  PGTI_REQUIRE(count && (cap == 0 || (cls && start_ms && end_ms && stream)), PGTI_ERR_INVALID_ARG,
+               "pgti_profile_timeline: null pointer");
+  std::lock_guard<std::mutex> lk(g_mu);
+  *count = int(g_recs.size());
+  if (g_recs.empty() || cap == 0) return PGTI_OK;
+  const cudaEvent_t t0 = g_recs.front().a;
+  for (int i = 0; i < int(g_recs.size()) && i < cap; ++i) {
+    const Rec &r = g_recs[i];
+    float a = 0.f, b = 0.f;
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&a, t0, r.a);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&b, t0, r.b);
+    PGTI_REQUIRE(e == cudaSuccess, PGTI_ERR_CUDA, "pgti_profile_timeline: %s",
+                 cudaGetErrorString(e));
+    cls[i] = r.cls, start_ms[i] = a, end_ms[i] = b;
+    stream[i] = int64_t(reinterpret_cast<intptr_t>(r.s));
+  }
+  return PGTI_OK;
 }
 
 extern "C" uint64_t pgti_launch_count(void) { return g_launches.load(); }

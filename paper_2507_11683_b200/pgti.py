@@ -102,6 +102,22 @@ _prof_n = _sig("pgti_profile_num_classes", C.c_int)
 _prof_name = _sig("pgti_profile_class_name", C.c_char_p, C.c_int)
 _prof_read = _sig("pgti_profile_read", C.c_int, _vp, _vp, _vp, _vp, C.c_int)
 _launch_count = _sig("pgti_launch_count", C.c_uint64)
+_prof_timeline = _sig("pgti_profile_timeline", C.c_int, _vp, _vp, _vp, _vp, C.c_int,
+                      C.POINTER(C.c_int))
+
+
+def profile_timeline() -> list:
+    """[(class, start_ms, end_ms, stream)] of the recorded eager launches (before profile_read)."""
+    cnt = C.c_int(0)
+    _ok(_prof_timeline(None, None, None, None, 0, C.byref(cnt)))
+    n = cnt.value
+    cls, st, en = np.zeros(n, np.int32), np.zeros(n), np.zeros(n)
+    sid = np.zeros(n, np.int64)
+    if n:
+        _ok(_prof_timeline(cls.ctypes.data, st.ctypes.data, en.ctypes.data, sid.ctypes.data, n,
+                           C.byref(cnt)))
+    names = [_prof_name(i).decode() for i in range(_prof_n())]
+    return [(names[c], float(a), float(b), int(s)) for c, a, b, s in zip(cls, st, en, sid)]
 
 
 def profile_enable(on: bool = True):
