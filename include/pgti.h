@@ -229,8 +229,7 @@ typedef struct {
    * (teacher_forcing = 0) or the previous target y[..., :F_out]
    * (teacher_forcing = 1); yhat_s = H^L_s W_out + b_out on every decoder step.
    * Parameters: encoder layers, decoder layers, W_out, b_out.  T_out may exceed
-   * T_in.  act_dump covers the T_in + T_out steps.  precision 0 only in this
-   * build (UNSUPPORTED otherwise). */
+   * T_in.  act_dump covers the T_in + T_out steps.  Both precisions. */
   int32_t model;
   int32_t teacher_forcing;
 } pgti_dcrnn_desc;

@@ -51,8 +51,6 @@ pgti_status check_desc(const pgti_dcrnn_desc *desc, Dims *out) {
   PGTI_REQUIRE(g.teacher_forcing == 0 || (g.model == 1 && g.teacher_forcing == 1),
                PGTI_ERR_INVALID_ARG, "desc: teacher_forcing=%d needs model 1",
                g.teacher_forcing);
-  PGTI_REQUIRE(g.model == 0 || g.precision == 0, PGTI_ERR_UNSUPPORTED,
-               "desc: the encoder-decoder (model 1) runs on the fp32 path (precision 0) only");
   PGTI_REQUIRE(g.T_out >= 1 && (g.model == 1 || g.T_out <= g.T_in), PGTI_ERR_SHAPE,
                "desc: need 1 <= T_out=%d <= T_in=%d (stepwise readout, reading c6)", g.T_out,
                g.T_in);

@@ -70,7 +70,7 @@ cudaError_t record(StreamPool *p, cudaStream_t st, cudaEvent_t *out) {
 
 // ------------------------------------------------------------------ workspace
 struct LayoutTC {
-  size_t Dx, yhat, dyhat, lossp, total;
+  size_t Dx, Dy, yhat, dyhat, lossp, total;
   std::vector<size_t> DHb, DrHb, H32, Rg, Ug, Cg, dGb, dCb, Wf_ru, Wf_c, Wd_ru, Wd_c;
   std::vector<size_t> Q, wpart, dHrec0, dHrec1, dHup0, dHup1;
   size_t wpart_floats;
@@ -88,24 +88,31 @@ LayoutTC make_layout_tc(const Dims &d) {
     return o;
   };
   const size_t R = size_t(d.R), H = size_t(d.H), M = size_t(d.M), T = size_t(d.T_in);
+  const size_t TT = size_t(d.steps());  // hidden-state steps (encoder + decoder for model 1)
   L.Dx = take(M * T * R * d.F * 4);
-  size_t wp = small_wgrad_partial_floats(d.T_in, int(d.R), 2 * d.H);
+  L.Dy = take(d.model ? size_t(d.T_out) * M * R * d.F_out * 4 : 0);
+  const int Tmax = std::max(d.T_in, d.model ? d.T_out : 0);
+  size_t wp = std::max(small_wgrad_partial_floats(Tmax, int(d.R), 2 * d.H),
+                       small_wgrad_partial_floats(d.T_out, int(d.R), d.H));
   for (int l = 0; l < d.L; ++l)
-    wp = std::max(wp, tc_wgrad_partial_floats(vrows(d, l), 2 * d.H, d.T_in, int(d.R)));
+    wp = std::max(wp, tc_wgrad_partial_floats(vrows(d, l), 2 * d.H, Tmax, int(d.R)));
   L.wpart_floats = wp;
-  for (int l = 0; l < d.L; ++l) {
-    L.DHb.push_back(take(T * M * R * H * 2));
-    L.DrHb.push_back(take(T * M * R * H * 2));
-    L.H32.push_back(take(T * R * H * 4));
-    L.Rg.push_back(take(T * R * H * 4));
-    L.Ug.push_back(take(T * R * H * 4));
-    L.Cg.push_back(take(T * R * H * 4));
-    L.dGb.push_back(take(T * R * 2 * H * 2));  // bf16 only: dgrad / wgrad operands and the
-    L.dCb.push_back(take(T * R * H * 2));      // skinny bias / input-row reductions
+  for (int ll = 0; ll < d.L * (d.model ? 2 : 1); ++ll) {  // bf16 weight tiles per layer set
+    const int l = ll % d.L;
     L.Wf_ru.push_back(take(size_t(nkb_total(d, l)) * 2 * H * 64 * 2));
     L.Wf_c.push_back(take(size_t(nkb_total(d, l)) * H * 64 * 2));
     L.Wd_ru.push_back(take(size_t(vrows(d, l)) * 2 * H * 2));
     L.Wd_c.push_back(take(size_t(vrows(d, l)) * H * 2));
+  }
+  for (int l = 0; l < d.L; ++l) {
+    L.DHb.push_back(take(TT * M * R * H * 2));
+    L.DrHb.push_back(take(TT * M * R * H * 2));
+    L.H32.push_back(take(TT * R * H * 4));
+    L.Rg.push_back(take(TT * R * H * 4));
+    L.Ug.push_back(take(TT * R * H * 4));
+    L.Cg.push_back(take(TT * R * H * 4));
+    L.dGb.push_back(take(TT * R * 2 * H * 2));  // bf16 only: dgrad / wgrad operands and the
+    L.dCb.push_back(take(TT * R * H * 2));      // skinny bias / input-row reductions
     // per-layer (= per-stream) scratch
     L.Q.push_back(take(M * R * 2 * H * 2));
     L.wpart.push_back(take(wp * 4));
@@ -133,9 +140,16 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
   auto Fp = [&](size_t off) { return reinterpret_cast<float *>(ws + off); };
   auto Bp = [&](size_t off) { return reinterpret_cast<bf16 *>(ws + off); };
   const int64_t R = d.R, H = d.H, M = d.M, RH = R * H, MRH = M * RH;
-  const int T = d.T_in, L = d.L;
-  float *Dx = Fp(Ly.Dx);
-  const int64_t RF = R * d.F;
+  const int T = d.T_in, L = d.L, TT = d.steps();
+  float *Dx = Fp(Ly.Dx), *Dy = Fp(Ly.Dy);
+  const int64_t RF = R * d.F, RFo = R * d.F_out;
+  // encoder-decoder bookkeeping (model 1, reading c24): decoder steps t >= T use layer set L + l,
+  // a readout every decoder step, and a layer-0 input diffused per step (Dy)
+  auto is_dec = [&](int t) { return d.model == 1 && t >= T; };
+  auto pset = [&](int t, int l) { return is_dec(t) ? L + l : l; };
+  auto out_slot = [&](int t) {
+    return d.model == 1 ? (t >= T ? t - T : -1) : (t >= T - d.T_out ? t - (T - d.T_out) : -1);
+  };
   unsigned *err = device_error_flag();
   PGTI_REQUIRE(err, PGTI_ERR_CUDA, "device error flag unavailable");
   cudaError_t perr = cudaSuccess;
@@ -147,14 +161,14 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
 
   // ------------------------------------------------------------------ prologue on s
   {
-    WeightJob jobs[16];
+    WeightJob jobs[32];
     int nj = 0;
-    for (int l = 0; l < L; ++l) {
-      const int Fin = l == 0 ? d.F : d.H, C = Fin + d.H;
-      jobs[nj++] = WeightJob{params + P.Wru[l], 2 * d.H, C, d.M, Fin, l == 0, Bp(Ly.Wf_ru[l]),
-                             Bp(Ly.Wd_ru[l])};
-      jobs[nj++] = WeightJob{params + P.Wc[l], d.H, C, d.M, Fin, l == 0, Bp(Ly.Wf_c[l]),
-                             Bp(Ly.Wd_c[l])};
+    for (int ll = 0; ll < L * (d.model ? 2 : 1); ++ll) {
+      const int l = ll % L, Fin = l > 0 ? d.H : (ll < L ? d.F : d.F_out), C = Fin + d.H;
+      jobs[nj++] = WeightJob{params + P.Wru[ll], 2 * d.H, C, d.M, Fin, l == 0, Bp(Ly.Wf_ru[ll]),
+                             Bp(Ly.Wd_ru[ll])};
+      jobs[nj++] = WeightJob{params + P.Wc[ll], d.H, C, d.M, Fin, l == 0, Bp(Ly.Wf_c[ll]),
+                             Bp(Ly.Wd_c[ll])};
     }
     for (int i = 0; i < nj; i += 8) CU(launch_convert_weights(jobs + i, std::min(8, nj - i), s));
   }
@@ -163,12 +177,29 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
   for (int l = 1; l < L; ++l) CU(depend(sp, s, st[l]));  // fork
 
   // ------------------------------------------------------------------ forward
-  std::vector<std::vector<cudaEvent_t>> fdone(L, std::vector<cudaEvent_t>(T));
-  for (int t = 0; t < T; ++t) {
+  std::vector<std::vector<cudaEvent_t>> fdone(L, std::vector<cudaEvent_t>(TT));
+  for (int t = 0; t < TT; ++t) {
+    if (is_dec(t)) {  // decoder layer-0 input on layer 0's stream: GO, previous prediction/target
+      float *blk = Dy + int64_t(t - T) * M * RFo;
+      if (t == T) {
+        CU(cudaMemsetAsync(blk, 0, size_t(M * RFo) * 4, st[0]));
+      } else {
+        if (d.teacher) {
+          CU(launch_dec_input(y, t - T - 1, d.B, d.T_out, d.ld, d.N, d.F, d.F_out, blk, st[0]));
+        } else {
+          if (L > 1) CU(cudaStreamWaitEvent(st[0], fdone[L - 1][t - 1], 0));
+          CU(cudaMemcpyAsync(blk, Fp(Ly.yhat) + int64_t(t - T - 1) * RFo, size_t(RFo) * 4,
+                             cudaMemcpyDeviceToDevice, st[0]));
+        }
+        CU(diffuse_fwd(g, d, blk, RFo, 1, 0, int64_t(d.B) * d.F_out, st[0]));
+      }
+    }
     for (int l = 0; l < L; ++l) {
       cudaStream_t ss = st[l];
       if (l > 0) CU(cudaStreamWaitEvent(ss, fdone[l - 1][t], 0));
-      const int Fin = l == 0 ? d.F : d.H, C = Fin + d.H;
+      const int Fin = l > 0 ? d.H : (is_dec(t) ? d.F_out : d.F), C = Fin + d.H, ps = pset(t, l);
+      float *Xin = is_dec(t) ? Dy + int64_t(t - T) * M * RFo : Dx + t * RF;
+      const int64_t x_ms = is_dec(t) ? RFo : int64_t(T) * RF;
       const bf16 *Ain = l == 0 ? nullptr : Bp(Ly.DHb[l - 1]) + t * MRH;
       const bf16 *DHp = t > 0 ? Bp(Ly.DHb[l]) + (t - 1) * MRH : nullptr;
       bf16 *DHt = Bp(Ly.DHb[l]) + t * MRH, *DrHt = Bp(Ly.DrHb[l]) + t * MRH;
@@ -193,11 +224,11 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
       TcFwd gate{};
       gate.R = int(R), gate.H = d.H, gate.Nout = 2 * d.H, gate.mode = kEpiGate, gate.ntiles = 2;
       fill_kb(gate, DHp, 2 * d.H);
-      gate.Bw = Bp(Ly.Wf_ru[l]);
-      gate.bias = params + P.bru[l];
+      gate.Bw = Bp(Ly.Wf_ru[ps]);
+      gate.bias = params + P.bru[ps];
       if (l == 0)
-        gate.Dx = Dx + t * RF, gate.dx_mstride = int64_t(T) * RF, gate.F = d.F, gate.C_in = C,
-        gate.M = d.M, gate.Wx = params + P.Wru[l];
+        gate.Dx = Xin, gate.dx_mstride = x_ms, gate.F = Fin, gate.C_in = C, gate.M = d.M,
+        gate.Wx = params + P.Wru[ps];
       gate.Hprev = Hp32;
       gate.out_r = r, gate.out_u = u, gate.out_rH = DrHt;
       CU(launch_tc_fwd(gate, ss));
@@ -206,21 +237,21 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
       TcFwd cand{};
       cand.R = int(R), cand.H = d.H, cand.Nout = d.H, cand.mode = kEpiCand, cand.ntiles = 1;
       fill_kb(cand, t > 0 ? DrHt : nullptr, d.H);
-      cand.Bw = Bp(Ly.Wf_c[l]);
-      cand.bias = params + P.bc[l];
+      cand.Bw = Bp(Ly.Wf_c[ps]);
+      cand.bias = params + P.bc[ps];
       if (l == 0)
-        cand.Dx = Dx + t * RF, cand.dx_mstride = int64_t(T) * RF, cand.F = d.F, cand.C_in = C,
-        cand.M = d.M, cand.Wx = params + P.Wc[l];
+        cand.Dx = Xin, cand.dx_mstride = x_ms, cand.F = Fin, cand.C_in = C, cand.M = d.M,
+        cand.Wx = params + P.Wc[ps];
       cand.Hprev = Hp32, cand.u_in = u, cand.out_c = c;
       cand.out_H = Fp(Ly.H32[l]) + t * RH, cand.out_Hb = DHt;
-      if (l == L - 1 && t >= T - d.T_out) {
+      if (l == L - 1 && out_slot(t) >= 0) {
         cand.Wout = params + P.Wout, cand.bout = params + P.bout, cand.F_out = d.F_out;
-        cand.yhat = Fp(Ly.yhat) + int64_t(t - (T - d.T_out)) * R * d.F_out;
+        cand.yhat = Fp(Ly.yhat) + int64_t(out_slot(t)) * RFo;
       }
       CU(launch_tc_fwd(cand, ss));
-      if (!(l == L - 1 && t == T - 1))
+      if (!(l == L - 1 && t == TT - 1))
         CU(diffuse_fwd(g, d, reinterpret_cast<float *>(DHt), RH, 1, 0, int64_t(d.B) * d.H, ss, 1));
-      if (l + 1 < L) CU(record(sp, ss, &fdone[l][t]));
+      if (l + 1 < L || d.model == 1) CU(record(sp, ss, &fdone[l][t]));
     }
   }
   cudaStream_t top = st[L - 1];
@@ -270,25 +301,32 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
     CU(launch_tc_fwd(b, ss));
     return PGTI_OK;
   };
-  std::vector<std::vector<cudaEvent_t>> bdone(L, std::vector<cudaEvent_t>(T));
+  std::vector<std::vector<cudaEvent_t>> bdone(L, std::vector<cudaEvent_t>(TT));
   auto rec_buf = [&](int l, int t) { return Fp((t & 1) ? Ly.dHrec1[l] : Ly.dHrec0[l]); };
   auto up_buf = [&](int l, int t) { return Fp((t & 1) ? Ly.dHup1[l] : Ly.dHup0[l]); };
-  for (int t = T - 1; t >= 0; --t) {
+  for (int t = TT - 1; t >= 0; --t) {
     for (int l = L - 1; l >= 0; --l) {
       cudaStream_t ss = st[l];
       // d(H^l_t) from above is ready; the parity buffer this step writes (for layer l-1) was
       // last read by (l-1, t+2)
       if (l + 1 < L) CU(cudaStreamWaitEvent(ss, bdone[l + 1][t], 0));
-      if (l > 0 && t + 2 < T) CU(cudaStreamWaitEvent(ss, bdone[l - 1][t + 2], 0));
+      if (l > 0 && t + 2 < TT) CU(cudaStreamWaitEvent(ss, bdone[l - 1][t + 2], 0));
+      // own-prediction decoder: the next step's layer 0 added its input gradient to this step's
+      // dyhat
+      const bool fed_back = d.model == 1 && !d.teacher && t + 1 < TT && t + 1 > T;
+      if (l == L - 1 && fed_back && L > 1) CU(cudaStreamWaitEvent(ss, bdone[0][t + 1], 0));
+      const bool feed = l == 0 && d.model == 1 && !d.teacher && t > T;  // input = yhat_{t-1}
       const bool need_in = l > 0, need_h = t > 0;
+      const int ps = pset(t, l), C0 = (is_dec(t) ? d.F_out : d.F) + d.H;
       const float *Hprev = t > 0 ? Fp(Ly.H32[l]) + (t - 1) * RH : nullptr;
       const float *r = Fp(Ly.Rg[l]) + t * RH, *u = Fp(Ly.Ug[l]) + t * RH, *c = Fp(Ly.Cg[l]) + t * RH;
       float *dC = nullptr, *dG = nullptr;
       bf16 *dCb = Bp(Ly.dCb[l]) + t * RH, *dGb = Bp(Ly.dGb[l]) + t * 2 * RH;
-      const float *dy = (l == L - 1 && t >= T - d.T_out)
-                            ? Fp(Ly.dyhat) + int64_t(t - (T - d.T_out)) * R * d.F_out
+      const float *dy = (l == L - 1 && out_slot(t) >= 0)
+                            ? Fp(Ly.dyhat) + int64_t(out_slot(t)) * RFo
                             : nullptr;
-      const float *dH_rec = t + 1 < T ? rec_buf(l, t) : nullptr;   // from (l, t+1)
+      float *dfeed = feed ? Fp(Ly.dyhat) + int64_t(out_slot(t) - 1) * RFo : nullptr;
+      const float *dH_rec = t + 1 < TT ? rec_buf(l, t) : nullptr;  // from (l, t+1)
       const float *dH_up = l + 1 < L ? up_buf(l, t) : nullptr;     // from (l+1, t)
       float *dH_prev = need_h ? rec_buf(l, t - 1) : nullptr;       // to (l, t-1)
       float *dIn = need_in ? up_buf(l - 1, t) : nullptr;           // to (l-1, t)
@@ -296,59 +334,71 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
       // candidate backward (+ dG_u, and dG_r = 0 at t = 0)
       CU(launch_cand_bwd_tc(RH, d.H, dH_rec, dH_up, dy, params + P.Wout, d.F_out, u, c, Hprev,
                             dC, dCb, dH_prev, dG, dGb, ss));
-      if (need_in || need_h) {
+      if (need_in || need_h || feed) {
         // d[in, r*H] = sum_m ((P^m)^T dC) W_c[m]^T; the hidden tile's epilogue runs the gate
         // backward (dG_r, dH_{t-1} += d(rH) r) in place of storing d(rH)
         CU(diffuse_fwd(g, d, reinterpret_cast<float *>(Q), RH, 1, 0, int64_t(d.B) * d.H, ss, 1, 1,
                        dCb));
         const GateFuse fz{Hprev, r, dG, dGb, dH_prev};
-        PGTI_STATUS_TRY(bwd_gemm(l, dCb, d.H, Bp(Ly.Wd_c[l]), Q, need_in, need_h, dIn, 0, nullptr,
-                                 0, &fz, ss));
+        PGTI_STATUS_TRY(bwd_gemm(l, dCb, d.H, Bp(Ly.Wd_c[ps]), Q, need_in, need_h, dIn, 0,
+                                 nullptr, 0, &fz, ss));
+        if (feed)  // the decoder input's F_out channels: into the previous prediction's dyhat
+          CU(launch_xpart_dgrad(dCb, Q, RH, d.M, d.H, params + P.Wc[ps], C0, d.F_out, R, dfeed,
+                                ss));
         // d[in, H] += sum_m ((P^m)^T dG) W_ru[m]^T
         CU(diffuse_fwd(g, d, reinterpret_cast<float *>(Q), 2 * RH, 1, 0, int64_t(d.B) * 2 * d.H,
                        ss, 1, 1, dGb));
-        PGTI_STATUS_TRY(bwd_gemm(l, dGb, 2 * d.H, Bp(Ly.Wd_ru[l]), Q, need_in, need_h, dIn, 1,
+        PGTI_STATUS_TRY(bwd_gemm(l, dGb, 2 * d.H, Bp(Ly.Wd_ru[ps]), Q, need_in, need_h, dIn, 1,
                                  dH_prev, 1, nullptr, ss));
+        if (feed)
+          CU(launch_xpart_dgrad(dGb, Q, 2 * RH, d.M, 2 * d.H, params + P.Wru[ps], C0, d.F_out, R,
+                                dfeed, ss));
       }
       CU(record(sp, ss, &bdone[l][t]));
     }
   }
 
   // ------------------------------------------------------------------ weight gradients
-  for (int l = 0; l < L; ++l) {
+  for (int ll = 0; ll < L * (d.model ? 2 : 1); ++ll) {  // (encoder) stack, then the decoder
+    const int l = ll % L, dec = ll >= L, t0 = dec ? T : 0, nt = dec ? d.T_out : T;
     cudaStream_t ss = st[l];  // layer l's backward is complete in stream order
-    const int Fin = l == 0 ? d.F : d.H, C = Fin + d.H;
-    const int V = vrows(d, l), vseg = l == 0 ? 64 : 2 * d.H, coff = l == 0 ? d.F : 0;
-    const bf16 *Ain = l == 0 ? nullptr : Bp(Ly.DHb[l - 1]);
+    const int Fin = l > 0 ? d.H : (dec ? d.F_out : d.F), C = Fin + d.H;
+    const int V = vrows(d, l), vseg = l == 0 ? 64 : 2 * d.H, coff = l == 0 ? Fin : 0;
+    const bf16 *Ain = l == 0 ? nullptr : Bp(Ly.DHb[l - 1]) + t0 * MRH;
     float *wpart = Fp(Ly.wpart[l]);
-    TcWgrad tw{Ain, Bp(Ly.DHb[l]), -1, T, d.M, int(R), Bp(Ly.dGb[l]), 2 * d.H,
-               V, vseg, coff, C, wpart, int64_t(Ly.wpart_floats), grads + P.Wru[l]};
+    // gate: Z_t = [in_t, H_{t-1}] (the decoder's first step reads the encoder's last state)
+    TcWgrad tw{Ain, dec ? Bp(Ly.DHb[l]) + (t0 - 1) * MRH : Bp(Ly.DHb[l]), dec ? 0 : -1, nt,
+               d.M, int(R), Bp(Ly.dGb[l]) + int64_t(t0) * 2 * RH, 2 * d.H, V, vseg, coff, C,
+               wpart, int64_t(Ly.wpart_floats), grads + P.Wru[ll]};
     CU(launch_tc_wgrad(tw, ss));
-    tw.A_h = Bp(Ly.DrHb[l]), tw.h_toff = 0, tw.G = Bp(Ly.dCb[l]), tw.Nout = d.H;
-    tw.out = grads + P.Wc[l];
+    tw.A_h = Bp(Ly.DrHb[l]) + t0 * MRH, tw.h_toff = 0, tw.G = Bp(Ly.dCb[l]) + int64_t(t0) * RH;
+    tw.Nout = d.H, tw.out = grads + P.Wc[ll];
     CU(launch_tc_wgrad(tw, ss));
-    // input rows of layer 0 (fp32 x part) and the bias rows: skinny reduction over T*R rows
+    // input rows of layer 0 (fp32 x part) and the bias rows: skinny reduction over nt*R rows
     SmallWgrad sw{};
-    sw.mode = kSmallBiasX, sw.T = T, sw.R = int(R);
-    if (l == 0) sw.Dx = Dx, sw.dx_mstride = int64_t(T) * RF, sw.dx_tstride = RF;
-    sw.M = d.M, sw.F = d.F, sw.C_in = C;
+    sw.mode = kSmallBiasX, sw.T = nt, sw.R = int(R);
+    if (l == 0 && !dec) sw.Dx = Dx, sw.dx_mstride = int64_t(T) * RF, sw.dx_tstride = RF;
+    if (l == 0 && dec) sw.Dx = Dy, sw.dx_mstride = RFo, sw.dx_tstride = M * RFo;
+    sw.M = d.M, sw.F = Fin, sw.C_in = C;
     sw.partial = wpart, sw.partial_cap = int64_t(Ly.wpart_floats);
-    sw.Gb = Bp(Ly.dGb[l]), sw.g_tstride = 2 * RH, sw.NG = 2 * d.H, sw.out = grads + P.Wru[l];
+    sw.Gb = Bp(Ly.dGb[l]) + int64_t(t0) * 2 * RH, sw.g_tstride = 2 * RH, sw.NG = 2 * d.H;
+    sw.out = grads + P.Wru[ll];
     CU(launch_small_wgrad(sw, ss));
-    sw.Gb = Bp(Ly.dCb[l]), sw.g_tstride = RH, sw.NG = d.H, sw.out = grads + P.Wc[l];
+    sw.Gb = Bp(Ly.dCb[l]) + int64_t(t0) * RH, sw.g_tstride = RH, sw.NG = d.H;
+    sw.out = grads + P.Wc[ll];
     CU(launch_small_wgrad(sw, ss));
   }
   SmallWgrad rw{};
   rw.mode = kSmallReadout, rw.T = d.T_out, rw.R = int(R);
   rw.dy = Fp(Ly.dyhat), rw.F_out = d.F_out;
-  rw.G = Fp(Ly.H32[L - 1]) + int64_t(T - d.T_out) * RH, rw.g_tstride = RH, rw.NG = d.H;
+  rw.G = Fp(Ly.H32[L - 1]) + int64_t(TT - d.T_out) * RH, rw.g_tstride = RH, rw.NG = d.H;
   rw.partial = Fp(Ly.wpart[L - 1]), rw.partial_cap = int64_t(Ly.wpart_floats);
   rw.out = grads + P.Wout;
   CU(launch_small_wgrad(rw, top));
   for (int l = 1; l < L; ++l) CU(depend(sp, st[l], s));  // join
 
   if (act_dump) {
-    for (int t = 0; t < T; ++t)
+    for (int t = 0; t < TT; ++t)
       for (int l = 0; l < L; ++l) {
         float *dst = act_dump + (int64_t(t) * L + l) * 4 * RH;
         const float *src[4] = {Fp(Ly.H32[l]) + t * RH, Fp(Ly.Rg[l]) + t * RH,
@@ -356,7 +406,7 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
         for (int q = 0; q < 4; ++q)
           CU(cudaMemcpyAsync(dst + q * RH, src[q], size_t(RH) * 4, cudaMemcpyDeviceToDevice, s));
       }
-    CU(cudaMemcpyAsync(act_dump + int64_t(T) * L * 4 * RH, Fp(Ly.yhat),
+    CU(cudaMemcpyAsync(act_dump + int64_t(TT) * L * 4 * RH, Fp(Ly.yhat),
                        size_t(d.T_out) * R * d.F_out * 4, cudaMemcpyDeviceToDevice, s));
   }
   return PGTI_OK;

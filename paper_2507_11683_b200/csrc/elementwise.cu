@@ -261,6 +261,49 @@ cudaError_t launch_x_prep(const WindowSrc &xs, int B, int T_in, int64_t ld, int 
   return cudaGetLastError();
 }
 
+// thread = one row r: F_out accumulators over the M blocks x NG columns (bf16 pairs), the x-part
+// weight rows staged in shared memory
+__global__ void k_xpart_dgrad(const __nv_bfloat16 *__restrict__ grad,
+                              const __nv_bfloat16 *__restrict__ Q, int64_t mstride, int M, int NG,
+                              const float *__restrict__ W, int C_in, int F_out, int64_t R,
+                              float *__restrict__ out) {
+  extern __shared__ float wsm[];  // [M][F_out][NG]
+  for (int i = threadIdx.x; i < M * F_out * NG; i += blockDim.x) {
+    const int m = i / (F_out * NG), o = (i / NG) % F_out, j = i % NG;
+    wsm[i] = W[int64_t(m * C_in + o) * NG + j];
+  }
+  __syncthreads();
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < R;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int m = 0; m < M; ++m) {
+      const __nv_bfloat162 *src = reinterpret_cast<const __nv_bfloat162 *>(
+          (m == 0 ? grad : Q + m * mstride) + r * NG);
+      const float *wm = wsm + m * F_out * NG;
+      for (int j2 = 0; j2 < NG / 2; ++j2) {
+        const float2 v = __bfloat1622float2(src[j2]);
+#pragma unroll
+        for (int o = 0; o < 4; ++o)
+          if (o < F_out)
+            acc[o] = fmaf(v.x, wm[o * NG + 2 * j2], fmaf(v.y, wm[o * NG + 2 * j2 + 1], acc[o]));
+      }
+    }
+    for (int o = 0; o < F_out; ++o) out[r * F_out + o] += acc[o];
+  }
+}
+
+cudaError_t launch_xpart_dgrad(const void *grad, const void *Q, int64_t mstride, int M, int NG,
+                               const float *W, int C_in, int F_out, int64_t R, float *out,
+                               cudaStream_t s) {
+  if (F_out > 4 || NG % 2) return cudaErrorInvalidValue;
+  ProfScope prof(kProfElementwise, s, double(R) * (2.0 * M * NG + 8.0 * F_out), 2.0 * R * M * NG * F_out);
+  const int smem = M * F_out * NG * 4;
+  k_xpart_dgrad<<<grid_for(R), kT, smem, s>>>(static_cast<const __nv_bfloat16 *>(grad),
+                                             static_cast<const __nv_bfloat16 *>(Q), mstride, M,
+                                             NG, W, C_in, F_out, R, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_dec_input(const WindowSrc &ys, int tt, int B, int T_out, int64_t ld, int N,
                              int F, int F_out, float *out, cudaStream_t s) {
   const int64_t n = int64_t(N) * B * F_out;

@@ -184,6 +184,13 @@ cudaError_t launch_gate_bwd(int64_t RH, int H, const float *drH, const float *Hp
                             const float *r, const float *u, const float *dU, float *dHprev,
                             float *dG, cudaStream_t s, void *dG_bf16 = nullptr);
 
+// Encoder-decoder (tensor-core path): the decoder layer-0 input gradient, i.e. the F_out input
+// channels of dZ = sum_m Q_m W_m^T with Q_0 = grad (bf16 [R][NG]) and Q_m = Q + m * mstride:
+//   out[r][o] += sum_m sum_j Q_m[r][j] W[m*C_in + o][j]      (W fp32 [M*C_in][NG])
+cudaError_t launch_xpart_dgrad(const void *grad, const void *Q, int64_t mstride, int M, int NG,
+                               const float *W, int C_in, int F_out, int64_t R, float *out,
+                               cudaStream_t s);
+
 // bf16 weight tiles of the tensor-core path, rebuilt from the fp32 parameters every step:
 //   fwd  (K-major B):  Wf[kb][j][c]  = W[row_kb + c][j]           c < 64, j < Nout
 //   dgrad(K-major B):  Wd[v][j]      = W[(v/vseg)*C_in + coff + v%vseg][j]

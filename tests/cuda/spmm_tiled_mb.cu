@@ -285,6 +285,31 @@ __global__ void __launch_bounds__(NWARP * 32) kWin4(const Plan p, const bf16 *X,
   }
 }
 
+// global gather, persistent grid-stride: G CTAs per SM, each thread loops over (node, vector)
+// work items (fewer CTAs to launch than one thread per item)
+__global__ void __launch_bounds__(256) kOldGS(const int *rp, const int *ci, const float *va,
+                                              const bf16 *X, bf16 *Y, int N, int W) {
+  const int vecs = W / 8;
+  const int total = N * vecs;
+  for (int tid = blockIdx.x * blockDim.x + threadIdx.x; tid < total; tid += gridDim.x * blockDim.x) {
+    const int n = tid / vecs, col0 = (tid % vecs) * 8;
+    const bf16 *Xc = X + col0;
+    float2 acc[4] = {};
+    const int beg = __ldg(rp + n), end = __ldg(rp + n + 1);
+    int e = beg;
+    for (; e + 4 <= end; e += 4) {
+      const int c0 = __ldg(ci + e), c1 = __ldg(ci + e + 1), c2 = __ldg(ci + e + 2), c3 = __ldg(ci + e + 3);
+      const float w0 = __ldg(va + e), w1 = __ldg(va + e + 1), w2 = __ldg(va + e + 2), w3 = __ldg(va + e + 3);
+      fma8(acc, w0, __ldg(reinterpret_cast<const uint4 *>(Xc + size_t(c0) * W)));
+      fma8(acc, w1, __ldg(reinterpret_cast<const uint4 *>(Xc + size_t(c1) * W)));
+      fma8(acc, w2, __ldg(reinterpret_cast<const uint4 *>(Xc + size_t(c2) * W)));
+      fma8(acc, w3, __ldg(reinterpret_cast<const uint4 *>(Xc + size_t(c3) * W)));
+    }
+    for (; e < end; ++e) fma8(acc, __ldg(va + e), __ldg(reinterpret_cast<const uint4 *>(Xc + size_t(__ldg(ci + e)) * W)));
+    *reinterpret_cast<uint4 *>(Y + size_t(n) * W + col0) = pack(acc);
+  }
+}
+
 __global__ void kCopy(const uint4 *X, uint4 *Y, size_t n) {
   const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (i < n) Y[i] = X[i];
@@ -349,6 +374,12 @@ int main(int argc, char **argv) {
     kCopy<<<unsigned((nel / 8 + 255) / 256), 256>>>((const uint4 *)X, (uint4 *)Y, nel / 8);
   });
   time("global gather (old)", [&] { kOld<<<unsigned((N * vecs + 255) / 256), 256>>>(d_rp, d_ci, d_va, X, Y0, N, W); });
+  for (int g : {1, 2, 4, 8}) {
+    char nm[48];
+    snprintf(nm, 48, "gather grid-stride %d CTA/SM", g);
+    time(nm, [&] { kOldGS<<<148 * g, 256>>>(d_rp, d_ci, d_va, X, Y, N, W); });
+    check(nm);
+  }
   time("global gather U=8", [&] { kOldU<8><<<unsigned((N * vecs + 255) / 256), 256>>>(d_rp, d_ci, d_va, X, Y, N, W); });
   check("U=8");
   time("global gather U=12", [&] { kOldU<12><<<unsigned((N * vecs + 255) / 256), 256>>>(d_rp, d_ci, d_va, X, Y, N, W); });

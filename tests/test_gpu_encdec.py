@@ -37,13 +37,13 @@ def env():
     return pgti, torch
 
 
-def _model(pgti, torch, cfg, graph, tf):
+def _model(pgti, torch, cfg, graph, tf, precision=0):
     csr = pgti.csr_to_device(pgti.graph_build(cfg.N, *graph), "cuda")
     return pgti.DCRNN(cfg.N, cfg.F, cfg.F_out, cfg.L, cfg.H, cfg.K, cfg.T_in, cfg.T_out, cfg.B,
-                      ld_of(cfg), csr, 0, model=1, teacher_forcing=tf)
+                      ld_of(cfg), csr, precision, model=1, teacher_forcing=tf)
 
 
-def _case(env, cfg, tf, seed=0):
+def _case(env, cfg, tf, seed=0, precision=0):
     pgti, torch = env
     ref = _ref(cfg)
     s = load_series(pgti, torch, ref.v, 0, cfg, ref.mu, ref.sigma)
@@ -53,11 +53,15 @@ def _case(env, cfg, tf, seed=0):
     x = torch.empty(cfg.B * cfg.T_in * ld, device="cuda")
     y = torch.empty(cfg.B * cfg.T_out * ld, device="cuda")
     s.gather(idx, cfg.B, cfg.T_in, cfg.T_out, x, y)
-    model = _model(pgti, torch, cfg, ref.graph, tf)
+    model = _model(pgti, torch, cfg, ref.graph, tf, precision)
     d = dcgru.Dims.of(cfg)
     n = model.num_params()
     assert n == encdec.num_params(d)
-    theta = np.random.default_rng(seed + 11).uniform(-0.4, 0.4, n).astype(np.float32)
+    if precision == 0:
+        theta = np.random.default_rng(seed + 11).uniform(-0.4, 0.4, n).astype(np.float32)
+    else:  # the bf16 path at the fan-in scaled init (as the stepwise bf16 parity tests)
+        theta = synth.make_params(cfg, seed=synth.SEED_PARAMS + seed, kind="random",
+                                  model="encdec")
     params = torch.from_numpy(theta).cuda()
     grads = torch.full((n,), float("nan"), device="cuda")
     loss = torch.zeros(1, device="cuda")
@@ -116,3 +120,39 @@ def test_encdec_metr_la_shape(env):
     assert c["margin"] > 1e-5
     assert abs(c["loss"] - c["loss_ref"]) <= TOL32 * abs(c["loss_ref"])
     assert scale_rel(c["g"], c["g_ref"]) <= TOL32
+
+
+TOL_BF16 = 2e-2
+TC_CFGS = {
+    "ed_tc": synth.Config("ed_tc", N=12, E=60, F=2, T_in=3, T_out=4, L=2, H=64, K=2, B=3),
+    "ed_tc_odd": synth.Config("ed_tc_odd", N=33, E=70, F=3, F_out=2, T_in=4, T_out=2, L=1,
+                              H=64, K=1, B=5),
+    "ed_tc_l3": synth.Config("ed_tc_l3", N=20, E=60, F=2, T_in=2, T_out=3, L=3, H=64, K=2, B=4),
+}
+
+
+def _check(c, tol):
+    assert c["margin"] > 1e-5, "a residual sits at an |.| kink; pick another seed"
+    assert abs(c["loss"] - c["loss_ref"]) <= tol * abs(c["loss_ref"])
+    gscale = np.max(np.abs(c["g_ref"]))
+    off = 0
+    for nm, shp in encdec.layer_shapes(c["d"]):
+        n = int(np.prod(shp))
+        g, gr = c["g"][off:off + n].astype(np.float64), c["g_ref"][off:off + n]
+        den = max(np.max(np.abs(gr)), 1e-2 * gscale)
+        assert np.max(np.abs(g - gr)) / den <= tol, (nm, np.max(np.abs(g - gr)) / den)
+        off += n
+
+
+@pytest.mark.parametrize("tf", [0, 1])
+@pytest.mark.parametrize("name", list(TC_CFGS))
+def test_encdec_bf16_vs_oracle(env, name, tf):
+    """The encoder-decoder on the bf16 tcgen05 path (decoder input diffused per step, its layer-0
+    input gradient by the skinny x-part dgrad) at the 2e-2 bf16 tolerance."""
+    _check(_case(env, TC_CFGS[name], tf, precision=1), TOL_BF16)
+
+
+@pytest.mark.parametrize("tf", [0, 1])
+def test_encdec_bf16_metr_la(env, tf):
+    cfg = synth.CONFIGS["metr_la"].replace(B=16)
+    _check(_case(env, cfg, tf, precision=1), TOL_BF16)
