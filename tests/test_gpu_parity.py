@@ -601,3 +601,48 @@ def test_trainer_zero_copy_graph_matches_gather(env):
         tr.check()
         res.append(tr.params.cpu().numpy())
     assert np.array_equal(res[0], res[1])
+
+
+def test_new_entry_point_errors(env):
+    """Argument errors of the later entry points: step_indexed against a series of another
+    shape, forward-only loss with a short workspace, invalid model / feedback flags."""
+    pgti, torch = env
+    cfg = SMALL_CONFIGS["tiny2"]
+    ref = ref_for(cfg)
+    model = model_for(pgti, torch, cfg, ref.graph)
+    n = model.num_params()
+    p = torch.zeros(n, device="cuda")
+    ws = torch.empty(model.workspace_bytes(), dtype=torch.uint8, device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    other = cfg.replace(N=cfg.N + 1)
+    v2 = synth.make_series(other)
+    s2 = load_series(pgti, torch, v2, 0, other, 0.0, 1.0)
+    idx = torch.zeros(cfg.B, dtype=torch.int32, device="cuda")
+    with pytest.raises(pgti.PgtiError) as e:
+        model.step_indexed(p, p.clone(), s2, idx, loss, ws)
+    assert e.value.name == "SHAPE"
+    x = torch.zeros(cfg.B * cfg.T_in * ld_of(cfg), device="cuda")
+    y = torch.zeros(cfg.B * cfg.T_out * ld_of(cfg), device="cuda")
+    with pytest.raises(pgti.PgtiError) as e:
+        model.loss(p, x, y, loss, ws[:-512])
+    assert e.value.name == "WORKSPACE"
+    csr = pgti.csr_to_device(pgti.graph_build(cfg.N, *ref.graph), "cuda")
+    for kw, want in ((dict(model=2), "INVALID_ARG"), (dict(teacher_forcing=1), "INVALID_ARG")):
+        bad = pgti.DCRNN(cfg.N, cfg.F, cfg.F_out, cfg.L, cfg.H, cfg.K, cfg.T_in, cfg.T_out, cfg.B,
+                         ld_of(cfg), csr, 0, **kw)
+        with pytest.raises(pgti.PgtiError) as e:   # the desc check runs before anything else
+            bad.step(p, p.clone(), x, y, loss, ws)
+        assert e.value.name == want, str(e.value)
+
+
+@pytest.mark.parametrize("name,precision", [("cp", 0), ("tc_tiny", 1), ("tc_k3", 1),
+                                            ("metr_la", 1)])
+def test_step_parity_batch_of_one(env, name, precision):
+    """B = 1 (one window per rank: R = N rows, ragged GEMM tiles), and the bf16 path at K = 3
+    (seven diffusion blocks)."""
+    cfg = (TC_CONFIGS.get(name) or SMALL_CONFIGS.get(name) or synth.CONFIGS.get(name)
+           or synth.Config("tc_k3", N=20, E=60, F=1, T_in=3, T_out=2, L=2, H=64, K=3, B=4))
+    if precision == 0:
+        _check_step(_step_case(env, cfg, B=1))
+    else:
+        _check_step(_step_case_tc(env, cfg, B=1 if name != "tc_k3" else None), tol=TOL_BF16)
