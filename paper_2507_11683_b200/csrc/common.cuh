@@ -29,6 +29,32 @@ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
 constexpr int kNumSMs = 148;  // B200
 
+// Programmatic dependent launch (PDL).  Kernels launched with pdl_launch may start while their
+// stream predecessor is still finishing: they run their data-independent prologue, then
+// griddep_wait() (griddepcontrol.wait: every prerequisite grid has completed and its writes are
+// visible) before touching any input; griddep_launch_dependents() lets the successor's CTAs be
+// scheduled once every CTA of this grid has started.  Both are no-ops for normal launches.
+// PGTI_PDL=0 turns PDL off (A/B measurements).
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+bool pdl_enabled();
+template <typename K, typename... Args>
+cudaError_t pdl_launch(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid, cfg.blockDim = block, cfg.dynamicSmemBytes = smem, cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at, cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args...);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 }  // namespace pgti
 
 #define PGTI_REQUIRE(cond, status, ...)                     \

@@ -145,6 +145,8 @@ __global__ void k_cand_bwd_tc(int64_t RH, int H, const float *__restrict__ dHa,
                               const float *__restrict__ Hprev, float *__restrict__ dC,
                               __nv_bfloat16 *__restrict__ dCb, float *__restrict__ dHprev,
                               float *__restrict__ dG, __nv_bfloat16 *__restrict__ dGb) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int64_t n4 = RH / 4;
   auto ld = [](const float *p, int64_t q) { return reinterpret_cast<const float4 *>(p)[q]; };
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n4;
@@ -347,10 +349,9 @@ cudaError_t launch_cand_bwd_tc(int64_t RH, int H, const float *dHa, const float 
                                       (dG ? (Hprev ? 1 : 2) : 0)) +
                                2.0 * (1 + (Hprev ? 1 : 2))),
                  0.0);
-  k_cand_bwd_tc<<<grid_for(RH / 4), kT, 0, s>>>(RH, H, dHa, dHb, dy, Wout, F_out, u, c, Hprev, dC,
-                                            static_cast<__nv_bfloat16 *>(dCb), dHprev, dG,
-                                            static_cast<__nv_bfloat16 *>(dGb));
-  return cudaGetLastError();
+  return pdl_launch(k_cand_bwd_tc, dim3(grid_for(RH / 4)), dim3(kT), 0, s, RH, H, dHa, dHb, dy,
+                    Wout, F_out, u, c, Hprev, dC, static_cast<__nv_bfloat16 *>(dCb), dHprev, dG,
+                    static_cast<__nv_bfloat16 *>(dGb));
 }
 
 cudaError_t launch_gate_bwd(int64_t RH, int H, const float *drH, const float *Hprev,

@@ -1,5 +1,6 @@
 // Thread-local error text, the sticky device error flag, pgti_check_device_error.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -10,6 +11,14 @@ __device__ unsigned g_dev_err = 0;
 }  // namespace
 
 namespace pgti {
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char *v = std::getenv("PGTI_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
 
 pgti_status fail(pgti_status st, const char *fmt, ...) {
   va_list ap;

@@ -95,6 +95,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_spmm(const __grid_constant__ SpmmParams p) {
   using L = Lane<T>;
   constexpr int V = L::V, P = V / 2;
+  griddep_launch_dependents();
+  griddep_wait();
   const int tid = int(blockIdx.x * blockDim.x + threadIdx.x);
   if (tid >= p.thread_begin[p.njobs]) return;
   int j = 0;
@@ -167,6 +169,8 @@ __global__ void __launch_bounds__(256) k_spmm_win(const __grid_constant__ WinPar
   using L = Lane<T>;
   constexpr int V = L::V, P = V / 2;
   extern __shared__ uint4 stage[];  // [union][32]
+  griddep_launch_dependents();
+  griddep_wait();
   const int z = int(blockIdx.z);
   int j = 0;
 #pragma unroll
@@ -250,6 +254,8 @@ __global__ void __launch_bounds__(256) k_spmm_win(const __grid_constant__ WinPar
 
 // Scalar fp32 fallback for widths that are not a multiple of 4 (test shapes only).
 __global__ void __launch_bounds__(256) k_spmm_scalar(const __grid_constant__ SpmmParams p) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int tid = int(blockIdx.x * blockDim.x + threadIdx.x);
   if (tid >= p.thread_begin[p.njobs]) return;
   int j = 0;
@@ -349,8 +355,7 @@ cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s) {
     auto go = [&](auto kernel) -> cudaError_t {
       cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return e;
-      kernel<<<grid, 256, smem, s>>>(w);
-      return cudaGetLastError();
+      return pdl_launch(kernel, grid, dim3(256), smem, s, w);
     };
     if (bf) {
       if (rpw <= 1) return go(k_spmm_win<__nv_bfloat16, 1>);
@@ -364,13 +369,9 @@ cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s) {
     return go(k_spmm_win<float, 8>);
   }
   const unsigned blocks = unsigned(ceil_div(th, 256));
-  if (bf)
-    k_spmm<__nv_bfloat16><<<blocks, 256, 0, s>>>(p);
-  else if (vec)
-    k_spmm<float><<<blocks, 256, 0, s>>>(p);
-  else
-    k_spmm_scalar<<<blocks, 256, 0, s>>>(p);
-  return cudaGetLastError();
+  if (bf) return pdl_launch(k_spmm<__nv_bfloat16>, dim3(blocks), dim3(256), 0, s, p);
+  if (vec) return pdl_launch(k_spmm<float>, dim3(blocks), dim3(256), 0, s, p);
+  return pdl_launch(k_spmm_scalar, dim3(blocks), dim3(256), 0, s, p);
 }
 
 }  // namespace pgti

@@ -105,20 +105,33 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
   static_assert(kStages * STAGE >= kBM * (kTileLd + 20) * 4, "x rows fit behind the tile");
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int row0 = blockIdx.x * kBM, ct0 = blockIdx.y * NSUB;
+  griddep_launch_dependents();
   if (threadIdx.x == 0) tma_prefetch(&mA0), tma_prefetch(&mA1), tma_prefetch(&mB);
-  setup(bar, NT);
+  setup(bar, NT);  // barriers + TMEM: the prologue that may overlap the predecessor's tail
   const uint32_t tmem = bar->tmem;
 
   if (warp == 0) {
     if (lane == 0) {
+      // The weight tiles (B) were written by a plain (non-PDL) launch at the start of the step,
+      // which completed before any later kernel started: the first ring's B loads go out before
+      // griddepcontrol.wait, the A loads (the predecessor's outputs) after it.
+      const int pre = min(p.nkb, kStages);
+      for (int kb = 0; kb < pre; ++kb) {
+        mbar_expect_tx(&bar->full[kb], STAGE);
+        tma_load_3d(smem + kb * STAGE + A_BYTES, &mB, &bar->full[kb], p.kb_bx[kb],
+                    p.kb_by[kb] + ct0 * 64, p.kb_bz[kb]);
+      }
+      griddep_wait();
       for (int kb = 0; kb < p.nkb; ++kb) {
         const int s = kb % kStages;
-        mbar_wait(&bar->empty[s], ((kb / kStages) & 1) ^ 1);
-        mbar_expect_tx(&bar->full[s], STAGE);
         uint8_t *a = smem + s * STAGE;
+        if (kb >= pre) {
+          mbar_wait(&bar->empty[s], ((kb / kStages) & 1) ^ 1);
+          mbar_expect_tx(&bar->full[s], STAGE);
+          tma_load_3d(a + A_BYTES, &mB, &bar->full[s], p.kb_bx[kb], p.kb_by[kb] + ct0 * 64,
+                      p.kb_bz[kb]);
+        }
         tma_load_3d(a, p.kb_as[kb] ? &mA1 : &mA0, &bar->full[s], p.kb_ac[kb], row0, p.kb_am[kb]);
-        tma_load_3d(a + A_BYTES, &mB, &bar->full[s], p.kb_bx[kb], p.kb_by[kb] + ct0 * 64,
-                    p.kb_bz[kb]);
       }
     }
   } else if (warp == 1) {
@@ -138,6 +151,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       mma_commit(&bar->tfull);
     }
   } else {
+    griddep_wait();  // the epilogue reads the predecessor's outputs (H_{t-1}, u, r, dH, ...)
     const int e = warp - 2, q = warp & 3, hh = e >> 2;
     const int et = e * 32 + lane;  // 0..255
     const int H = p.H;
@@ -433,8 +447,7 @@ cudaError_t launch_tc_fwd(const TcFwd &p, cudaStream_t s) {
   auto go = [&](auto kernel, int smem) -> cudaError_t {
     cudaError_t e = set_smem(kernel, smem);  // idempotent, cheap
     if (e != cudaSuccess) return e;
-    kernel<<<grid, kFwdThreads, smem, s>>>(ma0, ma1, mb, p);
-    return cudaGetLastError();
+    return pdl_launch(kernel, grid, dim3(kFwdThreads), smem, s, ma0, ma1, mb, p);
   };
   const int sm1 = fwd_smem_bytes(1), sm2 = fwd_smem_bytes(2);
   switch (p.mode * 2 + (nsub - 1)) {
