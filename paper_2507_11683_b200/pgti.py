@@ -189,12 +189,14 @@ def graph_build(N: int, src, dst, w) -> dict:
 
 
 def default_win_rows(N: int) -> int:
-    """Rows per SpMM staging window (0 = gather straight from L2).  Measured on B200
-    (tests/cuda/spmm_tiled_mb.cu, one bf16 hop, W = 4096): staging pays once the operand is
-    far larger than what one wave re-reads from L2 -- full-PeMS N=11160: 66 us vs 96 us;
-    PeMS-All-LA N=2716: 18.5 vs 20.6 us alone but slower inside the step, where its shared
-    memory competes with the concurrently running tcgen05 GEMMs; METR-LA: equal."""
-    return 16 if N >= 4096 else 0
+    """Rows per SpMM staging window (0 = gather neighbour rows straight from L2).  Measured in
+    the bf16 training step on B200 (samples/s, no plan / 16 / 32 / 64 rows): METR-LA 30.8 K /
+    31.2 K / 31.7 K; PeMS-Bay 22.0 K / 22.6 K / 22.6 K; PeMS-All-LA 2.74 K / 2.96 K / 3.01 K /
+    2.11 K; full PeMS 662 / 725 / 740 / 515.  PGTI_WIN_ROWS overrides (A/B measurements)."""
+    env = os.environ.get("PGTI_WIN_ROWS")
+    if env is not None:
+        return int(env)
+    return 32
 
 
 def graph_windows(N: int, rowptr, col, rows: int) -> dict:
