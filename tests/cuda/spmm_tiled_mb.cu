@@ -11,6 +11,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <cstring>
+#include <cmath>
 
 #define CK(x)                                                                    \
   do {                                                                           \
@@ -310,6 +312,70 @@ __global__ void __launch_bounds__(256) kOldGS(const int *rp, const int *ci, cons
   }
 }
 
+// v3 with bf16 weights and mixed-precision FMA (fma.rn.f32.bf16 -> FHFMA.BF16): each bf16 of the
+// neighbour slice is multiplied in place (no unpack), fp32 accumulation
+__device__ __forceinline__ float fhfma_lo(uint32_t x, uint32_t w2, float acc) {
+  float r;
+  asm("fma.rn.f32.bf16 %0, %1, %2, %3;" : "=f"(r) : "h"((unsigned short)(x & 0xffff)),
+      "h"((unsigned short)(w2 & 0xffff)), "f"(acc));
+  return r;
+}
+__device__ __forceinline__ float fhfma_hi(uint32_t x, uint32_t w2, float acc) {
+  float r;
+  asm("fma.rn.f32.bf16 %0, %1, %2, %3;" : "=f"(r) : "h"((unsigned short)(x >> 16)),
+      "h"((unsigned short)(w2 & 0xffff)), "f"(acc));
+  return r;
+}
+template <int RPW>
+__global__ void __launch_bounds__(256) kWin3h(const Plan p, const bf16 *X, bf16 *Y) {
+  extern __shared__ uint4 sm[];
+  const int vecs = p.W / 8;
+  const int chunk = blockIdx.x, win = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row0 = win * p.rows, nrows = min(p.rows, p.N - row0);
+  const int ub = __ldg(p.wptr + win), nu = __ldg(p.wptr + win + 1) - ub;
+  const int e0 = __ldg(p.rp + row0), e1 = __ldg(p.rp + row0 + nrows);
+  uint4 *stage = sm;
+  int *s_nodes = reinterpret_cast<int *>(sm + p.maxu * 32);
+  int2 *s_ent = reinterpret_cast<int2 *>(s_nodes + p.maxu + (p.maxu & 1));
+  int *s_rp = reinterpret_cast<int *>(s_ent + p.maxe);
+  for (int i = threadIdx.x; i < nu; i += 256) s_nodes[i] = __ldg(p.wnodes + ub + i);
+  for (int i = threadIdx.x; i < e1 - e0; i += 256) {
+    const __nv_bfloat16 wb = __float2bfloat16_rn(__ldg(p.va + e0 + i));
+    s_ent[i] = make_int2(int(__ldg(p.lcol + e0 + i)) * 512, int(*reinterpret_cast<const unsigned short *>(&wb)));
+  }
+  for (int i = threadIdx.x; i <= nrows; i += 256) s_rp[i] = __ldg(p.rp + row0 + i) - e0;
+  __syncthreads();
+  const int vec = chunk * 32 + lane;
+  const bool act = vec < vecs;
+  if (act) {
+    const bf16 *Xc = X + size_t(vec) * 8;
+    for (int k = warp; k < nu; k += 8) cp_async16(stage + k * 32 + lane, Xc + size_t(s_nodes[k]) * p.W);
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  const char *sb = reinterpret_cast<const char *>(stage) + lane * 16;
+#pragma unroll
+  for (int i = 0; i < RPW; ++i) {
+    const int r = warp + 8 * i;
+    if (r >= nrows) break;
+    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const int b = s_rp[r], e = s_rp[r + 1];
+    for (int q = b; q < e; ++q) {
+      const int2 en = s_ent[q];
+      const uint4 x = *reinterpret_cast<const uint4 *>(sb + en.x);
+      const uint32_t w2 = uint32_t(en.y);
+      a[0] = fhfma_lo(x.x, w2, a[0]), a[1] = fhfma_hi(x.x, w2, a[1]);
+      a[2] = fhfma_lo(x.y, w2, a[2]), a[3] = fhfma_hi(x.y, w2, a[3]);
+      a[4] = fhfma_lo(x.z, w2, a[4]), a[5] = fhfma_hi(x.z, w2, a[5]);
+      a[6] = fhfma_lo(x.w, w2, a[6]), a[7] = fhfma_hi(x.w, w2, a[7]);
+    }
+    float2 acc[4] = {make_float2(a[0], a[1]), make_float2(a[2], a[3]), make_float2(a[4], a[5]),
+                     make_float2(a[6], a[7])};
+    if (act) *reinterpret_cast<uint4 *>(Y + size_t(row0 + r) * p.W + size_t(vec) * 8) = pack(acc);
+  }
+}
+
 __global__ void kCopy(const uint4 *X, uint4 *Y, size_t n) {
   const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (i < n) Y[i] = X[i];
@@ -436,6 +502,22 @@ int main(int argc, char **argv) {
     check(nm);                                                                                   \
   }
     RUN3(2) RUN3(4) RUN3(8)
+#define RUN3H(RPW)                                                                               \
+  if ((rows + 7) / 8 == RPW) {                                                                   \
+    const int smem = maxu * 512 + (maxu + 1) * 4 + maxe * 8 + (rows + 1) * 4 + 16;               \
+    CK(cudaFuncSetAttribute(kWin3h<RPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));   \
+    char nm[64];                                                                                 \
+    snprintf(nm, 64, "  v3 bf16-w FHFMA RPW=%d", RPW);                                           \
+    time(nm, [&] { kWin3h<RPW><<<dim3(nchunk, nwin), 256, smem>>>(p, X, Y); });                  \
+    { std::vector<uint16_t> h0(nel), h1(nel);                                                    \
+      CK(cudaMemcpy(h0.data(), Y0, nel * 2, cudaMemcpyDeviceToHost));                            \
+      CK(cudaMemcpy(h1.data(), Y, nel * 2, cudaMemcpyDeviceToHost));                             \
+      double mx = 0; for (size_t i = 0; i < nel; ++i) { uint32_t u0 = uint32_t(h0[i]) << 16,    \
+        u1 = uint32_t(h1[i]) << 16; float f0, f1; memcpy(&f0, &u0, 4); memcpy(&f1, &u1, 4);      \
+        mx = std::max(mx, double(fabsf(f0 - f1))); }                                             \
+      printf("    max |diff| vs fp32-weight result: %.3g\n", mx); }                               \
+  }
+    RUN3H(2) RUN3H(4)
 #define RUN4(RPW, VPL, NWARP)                                                                    \
   if ((rows + NWARP - 1) / NWARP == RPW) {                                                       \
     const int smem = maxu * 512 * VPL + (maxu + 1) * 4 + maxe * 8 + (rows + 1) * 4 + 16;         \
