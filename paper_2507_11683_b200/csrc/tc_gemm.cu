@@ -156,6 +156,24 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
     const int et = e * 32 + lane;  // 0..255
     const int H = p.H;
     const int nx = (MODE != kEpiBwd && p.Dx) ? p.F * p.M : 0;
+    {  // while the MMAs run: pull the epilogue's [128 rows][64 fp32] input tiles into L2
+      const int rl = et >> 1, row = row0 + rl;
+      auto pf = [&](const float *base, int64_t pitch) {
+        if (base && row < p.R)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(base + row * pitch + (et & 1) * 32));
+      };
+      if (MODE == kEpiGate && ct0 == 0) pf(p.Hprev, H);
+      if (MODE == kEpiCand) pf(p.u_in + ct0 * 64, H), pf(p.Hprev ? p.Hprev + ct0 * 64 : nullptr, H);
+      if (MODE == kEpiBwd)
+        for (int sub = 0; sub < NSUB; ++sub) {
+          const int ct = ct0 + sub;
+          if (ct == p.fuse_tile) {
+            pf(p.Hprev, 64), pf(p.g_r, 64), pf(p.g_dHprev, 64);
+          } else if (p.dst_acc[ct]) {
+            pf(p.dst[ct], 64);
+          }
+        }
+    }
     mbar_wait(&bar->tfull, 0);  // MMAs done => every stage buffer is free for the tile
     tc_fence_after();
 #pragma unroll 1
