@@ -108,9 +108,9 @@ LayoutTC make_layout_tc(const Dims &d) {
     L.DHb.push_back(take(TT * M * R * H * 2));
     L.DrHb.push_back(take(TT * M * R * H * 2));
     L.H32.push_back(take(TT * R * H * 4));
-    L.Rg.push_back(take(TT * R * H * 4));
+    L.Rg.push_back(take(TT * R * H * 2));  // r, c: bf16 (backward-only operands)
     L.Ug.push_back(take(TT * R * H * 4));
-    L.Cg.push_back(take(TT * R * H * 4));
+    L.Cg.push_back(take(TT * R * H * 2));
     L.dGb.push_back(take(TT * R * 2 * H * 2));  // bf16 only: dgrad / wgrad operands and the
     L.dCb.push_back(take(TT * R * H * 2));      // skinny bias / input-row reductions
     // per-layer (= per-stream) scratch
@@ -204,7 +204,8 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
       const bf16 *DHp = t > 0 ? Bp(Ly.DHb[l]) + (t - 1) * MRH : nullptr;
       bf16 *DHt = Bp(Ly.DHb[l]) + t * MRH, *DrHt = Bp(Ly.DrHb[l]) + t * MRH;
       const float *Hp32 = t > 0 ? Fp(Ly.H32[l]) + (t - 1) * RH : nullptr;
-      float *r = Fp(Ly.Rg[l]) + t * RH, *u = Fp(Ly.Ug[l]) + t * RH, *c = Fp(Ly.Cg[l]) + t * RH;
+      bf16 *r = Bp(Ly.Rg[l]) + t * RH, *c = Bp(Ly.Cg[l]) + t * RH;
+      float *u = Fp(Ly.Ug[l]) + t * RH;
       // k-blocks: (input block m: map A0) and (hidden block m: map A1), B = Wf[kb] tiles
       auto fill_kb = [&](TcFwd &f, const bf16 *Ah, int Nout) {
         f.A0 = Ain, f.A1 = Ah, f.CA = 64, f.M0 = d.M, f.M1 = d.M;
@@ -265,7 +266,8 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
   // ------------------------------------------------------------------ backward (BPTT)
   // dZ = sum_m Q_m W_m^T, Q_0 = gradient itself (map A0), Q_{m>0} = (P^m)^T grad (map A1)
   struct GateFuse {
-    const float *Hprev, *r;
+    const float *Hprev;
+    const bf16 *r;
     float *dG;
     bf16 *dGb;
     float *dHprev;
@@ -319,7 +321,8 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
       const bool need_in = l > 0, need_h = t > 0;
       const int ps = pset(t, l), C0 = (is_dec(t) ? d.F_out : d.F) + d.H;
       const float *Hprev = t > 0 ? Fp(Ly.H32[l]) + (t - 1) * RH : nullptr;
-      const float *r = Fp(Ly.Rg[l]) + t * RH, *u = Fp(Ly.Ug[l]) + t * RH, *c = Fp(Ly.Cg[l]) + t * RH;
+      const bf16 *r = Bp(Ly.Rg[l]) + t * RH, *c = Bp(Ly.Cg[l]) + t * RH;
+      const float *u = Fp(Ly.Ug[l]) + t * RH;
       float *dC = nullptr, *dG = nullptr;
       bf16 *dCb = Bp(Ly.dCb[l]) + t * RH, *dGb = Bp(Ly.dGb[l]) + t * 2 * RH;
       const float *dy = (l == L - 1 && out_slot(t) >= 0)
@@ -401,10 +404,12 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
     for (int t = 0; t < TT; ++t)
       for (int l = 0; l < L; ++l) {
         float *dst = act_dump + (int64_t(t) * L + l) * 4 * RH;
-        const float *src[4] = {Fp(Ly.H32[l]) + t * RH, Fp(Ly.Rg[l]) + t * RH,
-                               Fp(Ly.Ug[l]) + t * RH, Fp(Ly.Cg[l]) + t * RH};
-        for (int q = 0; q < 4; ++q)
-          CU(cudaMemcpyAsync(dst + q * RH, src[q], size_t(RH) * 4, cudaMemcpyDeviceToDevice, s));
+        CU(cudaMemcpyAsync(dst, Fp(Ly.H32[l]) + t * RH, size_t(RH) * 4, cudaMemcpyDeviceToDevice,
+                           s));
+        CU(launch_bf16_to_f32(Bp(Ly.Rg[l]) + t * RH, dst + RH, RH, s));
+        CU(cudaMemcpyAsync(dst + 2 * RH, Fp(Ly.Ug[l]) + t * RH, size_t(RH) * 4,
+                           cudaMemcpyDeviceToDevice, s));
+        CU(launch_bf16_to_f32(Bp(Ly.Cg[l]) + t * RH, dst + 3 * RH, RH, s));
       }
     CU(cudaMemcpyAsync(act_dump + int64_t(TT) * L * 4 * RH, Fp(Ly.yhat),
                        size_t(d.T_out) * R * d.F_out * 4, cudaMemcpyDeviceToDevice, s));

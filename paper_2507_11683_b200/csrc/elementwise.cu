@@ -141,7 +141,7 @@ __device__ __forceinline__ void st4bf(__nv_bfloat16 *p, float a, float b, float 
 __global__ void k_cand_bwd_tc(int64_t RH, int H, const float *__restrict__ dHa,
                               const float *__restrict__ dHb, const float *__restrict__ dy,
                               const float *__restrict__ Wout, int F_out,
-                              const float *__restrict__ u, const float *__restrict__ c,
+                              const float *__restrict__ u, const __nv_bfloat16 *__restrict__ c,
                               const float *__restrict__ Hprev, float *__restrict__ dC,
                               __nv_bfloat16 *__restrict__ dCb, float *__restrict__ dHprev,
                               float *__restrict__ dG, __nv_bfloat16 *__restrict__ dGb) {
@@ -166,7 +166,14 @@ __global__ void k_cand_bwd_tc(int64_t RH, int H, const float *__restrict__ dHa,
         dh.z = fmaf(e, Wout[(j + 2) * F_out + o], dh.z);
         dh.w = fmaf(e, Wout[(j + 3) * F_out + o], dh.w);
       }
-    const float4 uu = ld(u, q), cc = ld(c, q);
+    const float4 uu = ld(u, q);
+    float4 cc;
+    {
+      const uint2 cw = reinterpret_cast<const uint2 *>(c)[q];
+      const float2 c0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&cw.x));
+      const float2 c1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&cw.y));
+      cc = make_float4(c0.x, c0.y, c1.x, c1.y);
+    }
     const float4 hp = Hprev ? ld(Hprev, q) : make_float4(0.f, 0.f, 0.f, 0.f);
     const float4 dc = make_float4(dh.x * (1.0f - uu.x) * (1.0f - cc.x * cc.x),
                                   dh.y * (1.0f - uu.y) * (1.0f - cc.y * cc.y),
@@ -306,6 +313,18 @@ cudaError_t launch_xpart_dgrad(const void *grad, const void *Q, int64_t mstride,
   return cudaGetLastError();
 }
 
+__global__ void k_bf16_to_f32(const __nv_bfloat16 *__restrict__ src, float *__restrict__ dst,
+                              int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = __bfloat162float(src[i]);
+}
+
+cudaError_t launch_bf16_to_f32(const void *src, float *dst, int64_t n, cudaStream_t s) {
+  k_bf16_to_f32<<<grid_for(n), kT, 0, s>>>(static_cast<const __nv_bfloat16 *>(src), dst, n);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_dec_input(const WindowSrc &ys, int tt, int B, int T_out, int64_t ld, int N,
                              int F, int F_out, float *out, cudaStream_t s) {
   const int64_t n = int64_t(N) * B * F_out;
@@ -340,7 +359,7 @@ cudaError_t launch_cand_bwd(int64_t RH, int H, const float *dHcur, const float *
 
 cudaError_t launch_cand_bwd_tc(int64_t RH, int H, const float *dHa, const float *dHb,
                                const float *dy, const float *Wout, int F_out, const float *u,
-                               const float *c, const float *Hprev, float *dC, void *dCb,
+                               const void *c, const float *Hprev, float *dC, void *dCb,
                                float *dHprev, float *dG, void *dGb, cudaStream_t s) {
   if (H % 4) return cudaErrorInvalidValue;
   ProfScope prof(kProfElementwise, s,
@@ -350,7 +369,8 @@ cudaError_t launch_cand_bwd_tc(int64_t RH, int H, const float *dHa, const float 
                                2.0 * (1 + (Hprev ? 1 : 2))),
                  0.0);
   return pdl_launch(k_cand_bwd_tc, dim3(grid_for(RH / 4)), dim3(kT), 0, s, RH, H, dHa, dHb, dy,
-                    Wout, F_out, u, c, Hprev, dC, static_cast<__nv_bfloat16 *>(dCb), dHprev, dG,
+                    Wout, F_out, u, static_cast<const __nv_bfloat16 *>(c), Hprev, dC,
+                    static_cast<__nv_bfloat16 *>(dCb), dHprev, dG,
                     static_cast<__nv_bfloat16 *>(dGb));
 }
 

@@ -176,10 +176,13 @@ cudaError_t launch_cand_bwd(int64_t RH, int H, const float *dHcur, const float *
                             const float *Hprev, float *dU, float *dC, float *dHprev_out,
                             cudaStream_t s, void *dC_bf16 = nullptr);
 // tensor-core path: candidate backward + dG_u (+ dG_r = 0 when Hprev is null), bf16 copies
+// (c is bf16 on the tensor-core path)
 cudaError_t launch_cand_bwd_tc(int64_t RH, int H, const float *dHa, const float *dHb,
                                const float *dy, const float *Wout, int F_out, const float *u,
-                               const float *c, const float *Hprev, float *dC, void *dCb,
+                               const void *c, const float *Hprev, float *dC, void *dCb,
                                float *dHprev, float *dG, void *dGb, cudaStream_t s);
+// act_dump helper: dst[i] = float(src[i]) for bf16 src
+cudaError_t launch_bf16_to_f32(const void *src, float *dst, int64_t n, cudaStream_t s);
 cudaError_t launch_gate_bwd(int64_t RH, int H, const float *drH, const float *Hprev,
                             const float *r, const float *u, const float *dU, float *dHprev,
                             float *dG, cudaStream_t s, void *dG_bf16 = nullptr);

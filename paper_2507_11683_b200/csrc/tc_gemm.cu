@@ -66,6 +66,12 @@ __device__ __forceinline__ void teardown(Barriers *bar, uint32_t ncols) {
 }
 
 __device__ __forceinline__ float4 ld4(const float *p) { return *reinterpret_cast<const float4 *>(p); }
+__device__ __forceinline__ float4 ld4_bf16(const bf16 *p) {
+  const uint2 u = *reinterpret_cast<const uint2 *>(p);
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
 __device__ __forceinline__ void st4(float *p, float4 v) { *reinterpret_cast<float4 *>(p) = v; }
 __device__ __forceinline__ void st4_bf16(bf16 *p, float4 v) {
   __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
@@ -168,7 +174,9 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
         for (int sub = 0; sub < NSUB; ++sub) {
           const int ct = ct0 + sub;
           if (ct == p.fuse_tile) {
-            pf(p.Hprev, 64), pf(p.g_r, 64), pf(p.g_dHprev, 64);
+            pf(p.Hprev, 64), pf(p.g_dHprev, 64);
+            if (row < p.R && !(et & 1))  // r is bf16: one 128-byte line per row
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(p.g_r + int64_t(row) * 64));
           } else if (p.dst_acc[ct]) {
             pf(p.dst[ct], 64);
           }
@@ -220,7 +228,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
           if (ct == p.fuse_tile) {
             // fused gate backward: a = d(r*H_{t-1}); dG_r = a H r (1-r); dH_{t-1} += a r
             const int64_t ro = int64_t(row) * 64 + c4, rg = int64_t(row) * 128 + c4;
-            const float4 hp = ld4(p.Hprev + ro), rr = ld4(p.g_r + ro), dh = ld4(p.g_dHprev + ro);
+            const float4 hp = ld4(p.Hprev + ro), rr = ld4_bf16(p.g_r + ro), dh = ld4(p.g_dHprev + ro);
             const float4 g = make_float4(a.x * hp.x * rr.x * (1.f - rr.x), a.y * hp.y * rr.y * (1.f - rr.y),
                                          a.z * hp.z * rr.z * (1.f - rr.z), a.w * hp.w * rr.w * (1.f - rr.w));
             st4(p.g_dHprev + ro, make_float4(fmaf(a.x, rr.x, dh.x), fmaf(a.y, rr.y, dh.y),
@@ -256,7 +264,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
           const float4 s = make_float4(sigmoid_f(a.x), sigmoid_f(a.y), sigmoid_f(a.z), sigmoid_f(a.w));
           if (valid) {
             if (ct == 0) {
-              st4(p.out_r + ro, s);
+              st4_bf16(p.out_r + ro, s);
               float4 hp = make_float4(0.f, 0.f, 0.f, 0.f);
               if (p.Hprev) hp = ld4(p.Hprev + ro);
               st4_bf16(p.out_rH + ro, make_float4(s.x * hp.x, s.y * hp.y, s.z * hp.z, s.w * hp.w));
@@ -273,7 +281,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
             if (p.Hprev) hp = ld4(p.Hprev + ro);
             hn = make_float4(u.x * hp.x + (1.f - u.x) * c.x, u.y * hp.y + (1.f - u.y) * c.y,
                              u.z * hp.z + (1.f - u.z) * c.z, u.w * hp.w + (1.f - u.w) * c.w);
-            st4(p.out_c + ro, c);
+            st4_bf16(p.out_c + ro, c);
             st4(p.out_H + ro, hn);
             st4_bf16(p.out_Hb + ro, hn);
           }

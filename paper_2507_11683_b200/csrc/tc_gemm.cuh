@@ -39,10 +39,12 @@ struct TcFwd {
   int F, C_in, M;
   const float *Wx;
   const float *Hprev;               // fp32 [R][H] or null
-  float *out_r, *out_u;             // gate
+  __nv_bfloat16 *out_r;             // gate: r (bf16: read only by the backward)
+  float *out_u;                     // gate: u (fp32: the forward recurrence reads it)
   __nv_bfloat16 *out_rH;            // gate: r*Hprev in bf16 (block 0 of the r*H diffusion)
   const float *u_in;                // cand
-  float *out_c, *out_H;
+  __nv_bfloat16 *out_c;             // cand: c (bf16: read only by the backward)
+  float *out_H;
   __nv_bfloat16 *out_Hb;
   const float *Wout, *bout;
   int F_out;
@@ -53,7 +55,7 @@ struct TcFwd {
   // gate backward there: dG_r = acc H_{t-1} r (1-r) (fp32 g_dG + bf16 g_dGb, [R][2H], columns
   // [0,H)), g_dHprev += acc r.  Uses Hprev.  -1 = off.  g_dG may be null (bf16 copy only).
   int fuse_tile = -1;
-  const float *g_r;
+  const __nv_bfloat16 *g_r;
   float *g_dG;
   __nv_bfloat16 *g_dGb;
   float *g_dHprev;
