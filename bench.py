@@ -232,6 +232,12 @@ def main():
     args = parse()
     import synth
     cfg = synth.CONFIGS[args.config]
+    if args.precision == 1 and cfg.H != 64:
+        # the tcgen05 path is built for 64 hidden units (one 128-byte SWIZZLE_128B row per
+        # diffusion block); Chickenpox's 32-unit model runs on the fp32 SIMT path
+        print(f"bench: {cfg.name} has H={cfg.H}: running the fp32 path (precision 0)",
+              file=sys.stderr)
+        args.precision = 0
     if args.impl == "reference":
         run_reference(args, cfg)
         return
