@@ -16,6 +16,7 @@
 // "Only new columns are diffused": T(Z) = [T(in), T(H)] is column-separable,
 // so each H^l_t is diffused once when produced and reused by layer l+1 at t and layer l at t+1.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "dcrnn_common.cuh"
@@ -121,6 +122,23 @@ cudaError_t diffuse_fwd(const pgti_dcrnn_desc &g, const Dims &d, float *base, in
   char *b = reinterpret_cast<char *>(base);
   const char *z = src0 ? static_cast<const char *>(src0) : b;
   auto blk = [&](int m) { return b + int64_t(m) * mstride * es; };
+  // opt-in (PGTI_RESIDENT=1): one launch per diffusion, but only W/64 CTAs -- measured slower
+  // inside the step (METR-LA 26.0 K vs 32.3 K samples/s) than one wide launch per hop
+  const char *res_env = std::getenv("PGTI_RESIDENT");
+  const bool resident_on = res_env && res_env[0] == '1';
+  if (bf16 && G == 1 && !g.a2_rowptr && resident_on && spmm_resident_fits(d.N, d.K, W)) {
+    // small graph: both directions' hop chain in one launch, the chunk resident in smem
+    ResidentJob r{};
+    const int pf = transposed ? 1 : 0, pb = transposed ? 0 : 1;  // 0: pattern(A), 1: A^T
+    const int32_t *rp[2] = {g.a_rowptr, g.at_rowptr};
+    const int32_t *cl[2] = {g.a_col, g.at_col};
+    r.rowptr[0] = rp[pf], r.col[0] = cl[pf], r.val[0] = transposed ? g.PfT_val : g.Pf_val;
+    r.rowptr[1] = rp[pb], r.col[1] = cl[pb], r.val[1] = transposed ? g.PbT_val : g.Pb_val;
+    r.nnz[0] = r.nnz[1] = g.nnz;
+    r.X = z, r.N = d.N, r.K = d.K, r.W = W;
+    for (int k = 1; k <= d.K; ++k) r.Y[0][k - 1] = blk(k), r.Y[1][k - 1] = blk(d.K + k);
+    return launch_spmm_resident(r, s);
+  }
   if (d.K == 2 && bf16 && g.a2_rowptr) {  // one launch: [P Z, P^2 Z] for both directions
     SpmmJob j[4] = {};
     const float *x0 = reinterpret_cast<const float *>(z);

@@ -37,6 +37,23 @@ struct SpmmJob {
 constexpr int kMaxSpmmJobs = 4;
 cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s);
 
+// Small-graph diffusion in one launch (bf16, K <= 2): each CTA keeps one 128-byte column chunk of
+// X for ALL N nodes in shared memory and computes both directions' hops 1..K from it (hop 2 from
+// the bf16 hop-1 rows it keeps), so the hop chain needs no second launch.  Y[d][k-1] = hop k of
+// direction d ([N][W] bf16).  Same CSR order and arithmetic as launch_spmm: bit-identical.
+// Opt-in (PGTI_RESIDENT=1): with only W/64 CTAs per launch it measured slower in the step.
+struct ResidentJob {
+  const int32_t *rowptr[2], *col[2];
+  const float *val[2];
+  int64_t nnz[2];
+  const void *X;
+  void *Y[2][2];
+  int N, K;
+  int64_t W;
+};
+bool spmm_resident_fits(int N, int K, int64_t W);
+cudaError_t launch_spmm_resident(const ResidentJob &p, cudaStream_t s);
+
 // ------------------------------------------------------------------ K3' fp32 SIMT GEMMs
 // Virtual A operand of the diffusion convolution: row r, column k = m*C_in + c reads
 //   c <  Fin : in[m*in_mstride + r*Fin + c]

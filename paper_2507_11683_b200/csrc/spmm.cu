@@ -252,6 +252,64 @@ __global__ void __launch_bounds__(256) k_spmm_win(const __grid_constant__ WinPar
   }
 }
 
+// ------------------------------------------------------------------ resident small-graph diffusion
+constexpr int kResThreads = 512, kResMaxSmem = 200 * 1024;
+
+template <int K>
+__global__ void __launch_bounds__(kResThreads) k_spmm_resident(const __grid_constant__ ResidentJob p) {
+  using L = Lane<__nv_bfloat16>;
+  extern __shared__ uint4 rs[];  // X chunk [N][8], then (K == 2) hop 1 [2][N][8]
+  griddep_launch_dependents();
+  griddep_wait();
+  const int N = p.N;
+  const int64_t W = p.W;
+  const int vecs = int(W / 8), vbase = int(blockIdx.x) * 8;
+  const int grp = threadIdx.x >> 3, l8 = threadIdx.x & 7, ngrp = kResThreads / 8;
+  const bool act = vbase + l8 < vecs;
+  const __nv_bfloat16 *X = static_cast<const __nv_bfloat16 *>(p.X) + int64_t(vbase + l8) * 8;
+  if (act)
+    for (int n = grp; n < N; n += ngrp) cp_async16(rs + n * 8 + l8, X + int64_t(n) * W);
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  uint4 *h1 = rs + N * 8;
+#pragma unroll
+  for (int hop = 0; hop < K; ++hop) {
+    if (hop) __syncthreads();  // hop-1 rows complete
+    for (int it = grp; it < 2 * N; it += ngrp) {
+      const int dir = it >= N, n = it - dir * N;
+      const uint4 *src = hop == 0 ? rs : h1 + dir * N * 8;
+      const int32_t *col = p.col[dir];
+      const float *val = p.val[dir];
+      float2 acc[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = make_float2(0.f, 0.f);
+      const int beg = __ldg(p.rowptr[dir] + n), end = __ldg(p.rowptr[dir] + n + 1);
+      int e = beg;
+      for (; e + 4 <= end; e += 4) {
+        const int c0 = __ldg(col + e), c1 = __ldg(col + e + 1), c2 = __ldg(col + e + 2),
+                  c3 = __ldg(col + e + 3);
+        const float w0 = __ldg(val + e), w1 = __ldg(val + e + 1), w2 = __ldg(val + e + 2),
+                    w3 = __ldg(val + e + 3);
+        L::fma_v(acc, w0, src[c0 * 8 + l8]);
+        L::fma_v(acc, w1, src[c1 * 8 + l8]);
+        L::fma_v(acc, w2, src[c2 * 8 + l8]);
+        L::fma_v(acc, w3, src[c3 * 8 + l8]);
+      }
+      for (; e < end; ++e) L::fma_v(acc, __ldg(val + e), src[__ldg(col + e) * 8 + l8]);
+      if (!act) continue;
+      uint4 o;
+      __nv_bfloat162 h;
+      h = __floats2bfloat162_rn(acc[0].x, acc[0].y), o.x = *reinterpret_cast<uint32_t *>(&h);
+      h = __floats2bfloat162_rn(acc[1].x, acc[1].y), o.y = *reinterpret_cast<uint32_t *>(&h);
+      h = __floats2bfloat162_rn(acc[2].x, acc[2].y), o.z = *reinterpret_cast<uint32_t *>(&h);
+      h = __floats2bfloat162_rn(acc[3].x, acc[3].y), o.w = *reinterpret_cast<uint32_t *>(&h);
+      *reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.Y[dir][hop]) + int64_t(n) * W +
+                                 int64_t(vbase + l8) * 8) = o;
+      if (hop + 1 < K) h1[(dir * N + n) * 8 + l8] = o;
+    }
+  }
+}
+
 // Scalar fp32 fallback for widths that are not a multiple of 4 (test shapes only).
 __global__ void __launch_bounds__(256) k_spmm_scalar(const __grid_constant__ SpmmParams p) {
   griddep_launch_dependents();
@@ -372,6 +430,30 @@ cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s) {
   if (bf) return pdl_launch(k_spmm<__nv_bfloat16>, dim3(blocks), dim3(256), 0, s, p);
   if (vec) return pdl_launch(k_spmm<float>, dim3(blocks), dim3(256), 0, s, p);
   return pdl_launch(k_spmm_scalar, dim3(blocks), dim3(256), 0, s, p);
+}
+
+bool spmm_resident_fits(int N, int K, int64_t W) {
+  return K >= 1 && K <= 2 && W % 8 == 0 && int64_t(N) * 128 * (K == 2 ? 3 : 1) <= kResMaxSmem;
+}
+
+cudaError_t launch_spmm_resident(const ResidentJob &p, cudaStream_t s) {
+  if (!spmm_resident_fits(p.N, p.K, p.W)) return cudaErrorInvalidValue;
+  const int smem = p.N * 128 * (p.K == 2 ? 3 : 1);
+  const unsigned grid = unsigned(ceil_div(p.W * 2, 128));
+  // algorithmic bytes as launch_spmm's 2 x K single-term jobs
+  double bytes = 0.0, flops = 0.0;
+  for (int d = 0; d < 2; ++d) {
+    bytes += 2.0 * double(p.N) * double(p.W) * 2.0 * p.K;
+    bytes += (double(p.nnz[d]) * 8.0 + double(p.N + 1) * 4.0) * p.K;
+    flops += 2.0 * double(p.nnz[d]) * double(p.W) * p.K;
+  }
+  ProfScope prof(kProfSpmm, s, bytes, flops);
+  auto go = [&](auto kernel) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    return pdl_launch(kernel, dim3(grid), dim3(kResThreads), smem, s, p);
+  };
+  return p.K == 2 ? go(k_spmm_resident<2>) : go(k_spmm_resident<1>);
 }
 
 }  // namespace pgti

@@ -376,6 +376,62 @@ __global__ void __launch_bounds__(256) kWin3h(const Plan p, const bf16 *X, bf16 
   }
 }
 
+// v5: v3 with CPB column chunks per CTA processed one after the other through one stage buffer
+// (the window's index prologue amortised over CPB chunks)
+template <int RPW, int CPB>
+__global__ void __launch_bounds__(256) kWin5(const Plan p, const bf16 *X, bf16 *Y) {
+  extern __shared__ uint4 sm[];
+  const int vecs = p.W / 8, nchunk = (vecs + 31) / 32;
+  const int win = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row0 = win * p.rows, nrows = min(p.rows, p.N - row0);
+  const int ub = __ldg(p.wptr + win), nu = __ldg(p.wptr + win + 1) - ub;
+  const int e0 = __ldg(p.rp + row0), e1 = __ldg(p.rp + row0 + nrows);
+  uint4 *stage = sm;
+  int *s_nodes = reinterpret_cast<int *>(sm + p.maxu * 32);
+  int2 *s_ent = reinterpret_cast<int2 *>(s_nodes + p.maxu + (p.maxu & 1));
+  int *s_rp = reinterpret_cast<int *>(s_ent + p.maxe);
+  for (int i = threadIdx.x; i < nu; i += 256) s_nodes[i] = __ldg(p.wnodes + ub + i);
+  for (int i = threadIdx.x; i < e1 - e0; i += 256)
+    s_ent[i] = make_int2(int(__ldg(p.lcol + e0 + i)) * 512, __float_as_int(__ldg(p.va + e0 + i)));
+  for (int i = threadIdx.x; i <= nrows; i += 256) s_rp[i] = __ldg(p.rp + row0 + i) - e0;
+  __syncthreads();
+  const char *sb = reinterpret_cast<const char *>(stage) + lane * 16;
+  for (int cc = 0; cc < CPB; ++cc) {
+    const int chunk = blockIdx.x * CPB + cc;
+    if (chunk >= nchunk) break;
+    const int vec = chunk * 32 + lane;
+    const bool act = vec < vecs;
+    if (cc) __syncthreads();
+    if (act) {
+      const bf16 *Xc = X + size_t(vec) * 8;
+      for (int k = warp; k < nu; k += 8) cp_async16(stage + k * 32 + lane, Xc + size_t(s_nodes[k]) * p.W);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      const int r = warp + 8 * i;
+      if (r >= nrows) break;
+      float2 acc[4] = {};
+      const int b = s_rp[r], e = s_rp[r + 1];
+      int q = b;
+      for (; q + 2 <= e; q += 2) {
+        const int2 a0 = s_ent[q], a1 = s_ent[q + 1];
+        const uint4 x0 = *reinterpret_cast<const uint4 *>(sb + a0.x);
+        const uint4 x1 = *reinterpret_cast<const uint4 *>(sb + a1.x);
+        fma8(acc, __int_as_float(a0.y), x0);
+        fma8(acc, __int_as_float(a1.y), x1);
+      }
+      if (q < e) {
+        const int2 a0 = s_ent[q];
+        fma8(acc, __int_as_float(a0.y), *reinterpret_cast<const uint4 *>(sb + a0.x));
+      }
+      if (act) *reinterpret_cast<uint4 *>(Y + size_t(row0 + r) * p.W + size_t(vec) * 8) = pack(acc);
+    }
+  }
+}
+
 __global__ void kCopy(const uint4 *X, uint4 *Y, size_t n) {
   const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (i < n) Y[i] = X[i];
@@ -518,6 +574,16 @@ int main(int argc, char **argv) {
       printf("    max |diff| vs fp32-weight result: %.3g\n", mx); }                               \
   }
     RUN3H(2) RUN3H(4)
+#define RUN5(RPW, CPB)                                                                           \
+  if ((rows + 7) / 8 == RPW) {                                                                   \
+    const int smem = maxu * 512 + (maxu + 1) * 4 + maxe * 8 + (rows + 1) * 4 + 16;               \
+    CK(cudaFuncSetAttribute(kWin5<RPW, CPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
+    char nm[64];                                                                                 \
+    snprintf(nm, 64, "  v5 RPW=%d CPB=%d (%d CTAs)", RPW, CPB, nwin * ((nchunk + CPB - 1) / CPB)); \
+    time(nm, [&] { kWin5<RPW, CPB><<<dim3((nchunk + CPB - 1) / CPB, nwin), 256, smem>>>(p, X, Y); }); \
+    check(nm);                                                                                   \
+  }
+    RUN5(2, 1) RUN5(2, 2) RUN5(2, 4) RUN5(4, 1) RUN5(4, 2) RUN5(4, 4)
 #define RUN4(RPW, VPL, NWARP)                                                                    \
   if ((rows + NWARP - 1) / NWARP == RPW) {                                                       \
     const int smem = maxu * 512 * VPL + (maxu + 1) * 4 + maxe * 8 + (rows + 1) * 4 + 16;         \

@@ -646,3 +646,21 @@ def test_step_parity_batch_of_one(env, name, precision):
         _check_step(_step_case(env, cfg, B=1))
     else:
         _check_step(_step_case_tc(env, cfg, B=1 if name != "tc_k3" else None), tol=TOL_BF16)
+
+
+@pytest.mark.parametrize("name,B,transposed", [("tc_tiny", None, 0), ("tc_odd", None, 0),
+                                               ("metr_la", 64, 0), ("pems_bay", 16, 0)])
+def test_step_resident_diffusion_bitexact(env, name, B, transposed, monkeypatch):
+    """The small-graph one-launch diffusion (column chunk of every node resident in shared memory,
+    hop 2 from the bf16 hop-1 rows) gives the bf16 step bit-identical results to the launch-per-hop
+    SpMM path (the default; the resident kernel is opt-in, PGTI_RESIDENT=1)."""
+    pgti, torch = env
+    cfg = TC_CONFIGS.get(name) or synth.CONFIGS[name]
+    cfg = cfg.replace(B=B or cfg.B)
+    res = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("PGTI_RESIDENT", flag)
+        c = _step_case_tc(env, cfg)
+        res.append((c["loss"], c["g"], c["act"]))
+    assert res[0][0] == res[1][0]
+    assert np.array_equal(res[0][1], res[1][1]) and np.array_equal(res[0][2], res[1][2])
