@@ -8,8 +8,10 @@ Model (reading c24; Li et al. 2018 [ext]):
 * Decoder: a second L-layer DCGRU stack (own parameters; layer 0 has C_in = F_out + H) that
   starts from the encoder's final hidden states and runs T_out steps.  Its layer-0 input is the
   GO symbol (zeros, F_out channels) at step 0 and the previous step's prediction at step s > 0
-  ("fed its own predictions"); with teacher_forcing it is the previous ground truth
-  y_{s-1}[..., :F_out] instead.  No scheduled sampling.
+  ("fed its own predictions"); with teacher forcing it is the previous ground truth
+  y_{s-1}[..., :F_out] instead.  teacher_forcing is per step (reading c24): True = every step,
+  False = none, an int = a bit mask (bit s-1 set: step s >= 1 is fed the target) -- the per-step
+  coin flips of Li et al.'s scheduled sampling, drawn by the caller.
 * Output projection on every decoder step: yhat_s = H^L_s W_out + b_out (F_out channels).
 * Loss = mean |yhat - y[..., :F_out]|, subgradient 0 at ties (reading c20).
 * Flat parameter layout: encoder layers (W_ru[M][C_in][2H], b_ru, W_c[M][C_in][H], b_c), then
@@ -67,7 +69,14 @@ def _cell(p: dict, pre: str, d: Dims, Pf, Pb, inp, Hprev):
     return u * Hprev + (1.0 - u) * c
 
 
-def forward(theta, d: Dims, Pf, Pb, x, y=None, teacher_forcing: bool = False) -> dict:
+def fed_truth(teacher_forcing, s: int) -> bool:
+    """Whether decoder step s (>= 1) is fed the previous target (see the module docstring)."""
+    if isinstance(teacher_forcing, (bool, np.bool_)):
+        return bool(teacher_forcing)
+    return bool((int(teacher_forcing) >> (s - 1)) & 1)
+
+
+def forward(theta, d: Dims, Pf, Pb, x, y=None, teacher_forcing=False) -> dict:
     """x[B][T_in][N][F], y[B][T_out][N][F].  Returns dict(yhat[B][T_out][N][F_out], loss,
     H_enc = the encoder's final hidden states [L][B][N][H])."""
     p = unpack(theta, d)
@@ -88,7 +97,8 @@ def forward(theta, d: Dims, Pf, Pb, x, y=None, teacher_forcing: bool = False) ->
             H[l] = _cell(p, f"dec{l}", d, Pf, Pb, inp, H[l])
             inp = H[l]
         yhat[:, s] = H[d.L - 1] @ p["W_out"] + p["b_out"]
-        prev = (np.asarray(y, np.float64)[:, s, :, :d.F_out] if teacher_forcing else yhat[:, s])
+        prev = (np.asarray(y, np.float64)[:, s, :, :d.F_out] if fed_truth(teacher_forcing, s + 1)
+                else yhat[:, s])
     out = dict(yhat=yhat, H_enc=H_enc)
     if y is not None:
         y = np.asarray(y, np.float64)
@@ -96,7 +106,7 @@ def forward(theta, d: Dims, Pf, Pb, x, y=None, teacher_forcing: bool = False) ->
     return out
 
 
-def loss_and_grad(theta, d: Dims, Pf, Pb, x, y, teacher_forcing: bool = False):
+def loss_and_grad(theta, d: Dims, Pf, Pb, x, y, teacher_forcing=False):
     """(loss, d loss / d theta) by torch float64 autograd of the same forward."""
     import torch
     th = torch.tensor(np.asarray(theta, np.float64), requires_grad=True)
@@ -143,7 +153,7 @@ def loss_and_grad(theta, d: Dims, Pf, Pb, x, y, teacher_forcing: bool = False):
             inp = H[l]
         yh = H[d.L - 1] @ p["W_out"] + p["b_out"]
         outs.append(yh)
-        prev = yt[:, s, :, :d.F_out] if teacher_forcing else yh
+        prev = yt[:, s, :, :d.F_out] if fed_truth(teacher_forcing, s + 1) else yh
     yhat = torch.stack(outs, 1)
     loss = torch.mean(torch.abs(yhat - yt[..., :d.F_out]))
     (g,) = torch.autograd.grad(loss, th)

@@ -73,7 +73,27 @@ def test_teacher_forcing_feeds_the_truth():
     assert np.allclose(tf, own, rtol=0, atol=1e-14)
 
 
-@pytest.mark.parametrize("tf,L,K", [(False, 2, 2), (True, 1, 1), (False, 1, 0)])
+def test_step_mask_selects_the_fed_inputs():
+    """A per-step mask (scheduled sampling's coin flips): mask 0 == own predictions, the full mask
+    == teacher forcing, and any mask is exact when y equals the model's own predictions."""
+    d = _dims(T_out=4)
+    theta, Pf, Pb, x, y = _problem(d, seed=6)
+    own = encdec.forward(theta, d, Pf, Pb, x, y)["yhat"]
+    assert np.array_equal(encdec.forward(theta, d, Pf, Pb, x, y, teacher_forcing=0)["yhat"], own)
+    full = encdec.forward(theta, d, Pf, Pb, x, y, teacher_forcing=True)["yhat"]
+    assert np.array_equal(encdec.forward(theta, d, Pf, Pb, x, y, teacher_forcing=0b111)["yhat"],
+                          full)
+    mixed = encdec.forward(theta, d, Pf, Pb, x, y, teacher_forcing=0b010)["yhat"]
+    assert np.array_equal(mixed[:, :2], own[:, :2])        # steps 0, 1 fed GO / own prediction
+    assert not np.allclose(mixed[:, 2], own[:, 2])          # step 2 fed the target y_1
+    y2 = y.copy()
+    y2[..., :d.F_out] = own
+    for m in (0b001, 0b010, 0b101):
+        assert np.allclose(encdec.forward(theta, d, Pf, Pb, x, y2, teacher_forcing=m)["yhat"], own,
+                           rtol=0, atol=1e-14)
+
+
+@pytest.mark.parametrize("tf,L,K", [(False, 2, 2), (True, 1, 1), (False, 1, 0), (0b10, 2, 1)])
 def test_gradient_finite_differences(tf, L, K):
     d = _dims(N=4, H=2, L=L, K=K, T_in=2, T_out=3)
     theta, Pf, Pb, x, y = _problem(d, seed=L * 7 + K)
