@@ -225,13 +225,15 @@ typedef struct {
    * stack above run as the encoder over x_0..x_{T_in-1} (no readout), then a
    * second L-layer stack (the decoder, own parameters, layer-0 C_in = F_out + H)
    * for T_out steps starting from the encoder's final states; its layer-0 input
-   * is the GO symbol (zeros) at step 0, then the previous prediction
-   * (teacher_forcing = 0) or the previous target y[..., :F_out]
-   * (teacher_forcing = 1); yhat_s = H^L_s W_out + b_out on every decoder step.
+   * is the GO symbol (zeros) at step 0, then for step s >= 1 the previous
+   * prediction, or the previous target y[..., :F_out] when bit s-1 of the
+   * teacher_forcing mask is set (all bits: teacher forcing; the caller's
+   * per-step coin flips: Li et al.'s scheduled sampling); yhat_s = H^L_s W_out +
+   * b_out on every decoder step.
    * Parameters: encoder layers, decoder layers, W_out, b_out.  T_out may exceed
    * T_in.  act_dump covers the T_in + T_out steps.  Both precisions. */
   int32_t model;
-  int32_t teacher_forcing;
+  int32_t teacher_forcing;  /* bit mask over decoder steps 1..T_out-1 (model 1) */
 } pgti_dcrnn_desc;
 
 /* Number of float parameters of the layout above (0 if desc invalid). */

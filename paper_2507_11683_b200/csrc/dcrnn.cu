@@ -49,9 +49,12 @@ pgti_status check_desc(const pgti_dcrnn_desc *desc, Dims *out) {
                g.T_in, g.B);
   PGTI_REQUIRE(g.model == 0 || g.model == 1, PGTI_ERR_INVALID_ARG,
                "desc: model=%d (0 = stepwise, 1 = encoder-decoder)", g.model);
-  PGTI_REQUIRE(g.teacher_forcing == 0 || (g.model == 1 && g.teacher_forcing == 1),
-               PGTI_ERR_INVALID_ARG, "desc: teacher_forcing=%d needs model 1",
-               g.teacher_forcing);
+  PGTI_REQUIRE(g.teacher_forcing == 0 ||
+                   (g.model == 1 && g.teacher_forcing > 0 && g.T_out <= 31 &&
+                    (g.teacher_forcing >> (g.T_out > 1 ? g.T_out - 1 : 0)) == 0),
+               PGTI_ERR_INVALID_ARG,
+               "desc: teacher_forcing=0x%x must be a mask of decoder steps 1..T_out-1 (model 1)",
+               unsigned(g.teacher_forcing));
   PGTI_REQUIRE(g.T_out >= 1 && (g.model == 1 || g.T_out <= g.T_in), PGTI_ERR_SHAPE,
                "desc: need 1 <= T_out=%d <= T_in=%d (stepwise readout, reading c6)", g.T_out,
                g.T_in);
@@ -312,7 +315,7 @@ pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *param
       if (t == T) {
         CU(cudaMemsetAsync(blk, 0, size_t(M * RFo) * 4, s));
       } else {
-        if (d.teacher)
+        if (d.fed_truth(t - T))
           CU(launch_dec_input(y, t - T - 1, d.B, d.T_out, d.ld, d.N, d.F, d.F_out, blk, s));
         else
           CU(cudaMemcpyAsync(blk, Fp(Ly.yhat) + int64_t(t - T - 1) * RFo, size_t(RFo) * 4,
@@ -367,7 +370,7 @@ pgti_status run_step(const pgti_dcrnn_desc &g, const Dims &d, const float *param
     for (int l = L - 1; l >= 0; --l) {
       const int Fin = fin_of(t, l), C = Fin + d.H, ps = pset(t, l);
       // the decoder's layer-0 input is the previous prediction: its gradient joins dyhat
-      const bool feed = l == 0 && is_dec(t) && t > T && !d.teacher;
+      const bool feed = l == 0 && is_dec(t) && t > T && !d.fed_truth(t - T);
       const bool need_in = l > 0 || feed, need_h = t > 0;
       const float *Hprev = t > 0 ? Fp(Ly.DH[l]) + (t - 1) * MRH : nullptr;
       const float *r = Fp(Ly.Rg[l]) + t * RH, *u = Fp(Ly.Ug[l]) + t * RH, *c = Fp(Ly.Cg[l]) + t * RH;

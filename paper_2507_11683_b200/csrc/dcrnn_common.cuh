@@ -14,7 +14,9 @@ struct Dims {
   int64_t R, ld;
   int precision;
   int model;    // 0 stepwise stack, 1 encoder-decoder (pgti.h)
-  int teacher;  // encoder-decoder: 1 = decoder fed the previous target, 0 = its own prediction
+  int teacher;  // encoder-decoder: bit s-1 set = decoder step s is fed the previous target
+  // decoder step s >= 1 fed the target y_{s-1} (else its own prediction yhat_{s-1})
+  bool fed_truth(int s) const { return s >= 1 && ((teacher >> (s - 1)) & 1); }
   // hidden-state steps: T_in (stepwise) or T_in + T_out (encoder then decoder)
   int steps() const { return T_in + (model ? T_out : 0); }
 };

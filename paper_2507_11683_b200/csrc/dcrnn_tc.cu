@@ -184,7 +184,7 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
       if (t == T) {
         CU(cudaMemsetAsync(blk, 0, size_t(M * RFo) * 4, st[0]));
       } else {
-        if (d.teacher) {
+        if (d.fed_truth(t - T)) {
           CU(launch_dec_input(y, t - T - 1, d.B, d.T_out, d.ld, d.N, d.F, d.F_out, blk, st[0]));
         } else {
           if (L > 1) CU(cudaStreamWaitEvent(st[0], fdone[L - 1][t - 1], 0));
@@ -315,9 +315,9 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
       if (l > 0 && t + 2 < TT) CU(cudaStreamWaitEvent(ss, bdone[l - 1][t + 2], 0));
       // own-prediction decoder: the next step's layer 0 added its input gradient to this step's
       // dyhat
-      const bool fed_back = d.model == 1 && !d.teacher && t + 1 < TT && t + 1 > T;
+      const bool fed_back = d.model == 1 && t + 1 < TT && t + 1 > T && !d.fed_truth(t + 1 - T);
       if (l == L - 1 && fed_back && L > 1) CU(cudaStreamWaitEvent(ss, bdone[0][t + 1], 0));
-      const bool feed = l == 0 && d.model == 1 && !d.teacher && t > T;  // input = yhat_{t-1}
+      const bool feed = l == 0 && d.model == 1 && t > T && !d.fed_truth(t - T);  // yhat_{t-1}
       const bool need_in = l > 0, need_h = t > 0;
       const int ps = pset(t, l), C0 = (is_dec(t) ? d.F_out : d.F) + d.H;
       const float *Hprev = t > 0 ? Fp(Ly.H32[l]) + (t - 1) * RH : nullptr;

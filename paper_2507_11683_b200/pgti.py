@@ -334,10 +334,21 @@ class DCRNN:
                               g("at2_rowptr"), g("at2_col"), g("Pb2_val"), g("Pf2T_val"),
                               g("a2_win_ptr"), g("a2_win_nodes"), g("a2_lcol"),
                               g("at2_win_ptr"), g("at2_win_nodes"), g("at2_lcol"),
-                              int(model), int(teacher_forcing))
+                              int(model), self._tf_mask(teacher_forcing, T_out))
         self.model = int(model)
         self.N, self.F, self.F_out, self.L, self.H, self.K = N, F, F_out, L, H, K
         self.T_in, self.T_out, self.B, self.ld = T_in, T_out, B, ld
+
+    @staticmethod
+    def _tf_mask(tf, T_out: int) -> int:
+        """True: every decoder step fed the target; False: none; an int: the step bit mask."""
+        if tf is True:
+            return (1 << max(T_out - 1, 0)) - 1
+        return int(tf)
+
+    def set_teacher_forcing(self, tf):
+        """Per-step mask for the next steps (scheduled sampling draws one per training step)."""
+        self.desc.teacher_forcing = self._tf_mask(tf, self.T_out)
 
     @property
     def M(self):

@@ -84,7 +84,8 @@ class Trainer:
 
     def __init__(self, cfg, graph, series_fn, params0, rank=0, world=1, device=0, comm=None,
                  seed=3, lr=1e-2, precision=0, shuffle=True, use_cuda_graph=True,
-                 two_hop=False, placement="halo", zero_copy=False, model=0, teacher_forcing=0):
+                 two_hop=False, placement="halo", zero_copy=False, model=0, teacher_forcing=0,
+                 scheduled_sampling=None):
         import torch
 
         self.torch = torch
@@ -99,6 +100,14 @@ class Trainer:
         assert not (placement == "replicated" and shuffle == "batch"), "batch shuffle is per shard"
         self.placement = placement
         self.zero_copy = zero_copy  # f2: windows read from the series by index, no x/y gather
+        # Li et al.'s curriculum (encoder-decoder): decoder step s >= 1 is fed the target with
+        # probability k / (k + exp(step / k)), one coin per step and batch; the mask lives in the
+        # descriptor, so this runs eager (no captured graph)
+        assert scheduled_sampling is None or (model == 1 and not use_cuda_graph), \
+            "scheduled sampling needs the encoder-decoder and eager steps"
+        self.ss_k = scheduled_sampling
+        self.ss_rng = np.random.default_rng(seed * 1000003 + rank)
+        self.steps_done = 0
         self.S_r = self.S_tr // world
         self.idx_off = 0
         self.plan = (shard_plan(self.S_tr, world, rank, cfg.T_in, cfg.T_out)
@@ -210,6 +219,12 @@ class Trainer:
     # ------------------------------------------------------------------ one step
     def _body(self, idx):
         cfg = self.cfg
+        if self.ss_k:
+            k = float(self.ss_k)
+            p = k / (k + math.exp(min(self.steps_done / k, 700.0)))
+            coins = self.ss_rng.uniform(size=max(cfg.T_out - 1, 0)) < p
+            self.model.set_teacher_forcing(sum(1 << i for i, c in enumerate(coins) if c))
+            self.steps_done += 1
         if self.zero_copy:
             self.model.step_indexed(self.params, self.grads, self.series, idx, self.loss, self.ws)
         else:

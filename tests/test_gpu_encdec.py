@@ -43,8 +43,12 @@ def _model(pgti, torch, cfg, graph, tf, precision=0):
                       ld_of(cfg), csr, precision, model=1, teacher_forcing=tf)
 
 
+MODES = {"own": 0, "tf": True, "mixed": 0b1}  # mixed: only decoder step 1 fed the target
+
+
 def _case(env, cfg, tf, seed=0, precision=0):
     pgti, torch = env
+    tf = MODES.get(tf, tf)
     ref = _ref(cfg)
     s = load_series(pgti, torch, ref.v, 0, cfg, ref.mu, ref.sigma)
     idx_np = ref.plan(1, 0, epoch=seed)[:cfg.B]
@@ -79,7 +83,7 @@ def _case(env, cfg, tf, seed=0, precision=0):
                 params=params, ws=ws)
 
 
-@pytest.mark.parametrize("tf", [0, 1])
+@pytest.mark.parametrize("tf", list(MODES))
 @pytest.mark.parametrize("name", list(CFGS))
 def test_encdec_step_vs_oracle(env, name, tf):
     cfg = CFGS[name]
@@ -104,7 +108,7 @@ def test_encdec_step_vs_oracle(env, name, tf):
 def test_encdec_zero_copy_bitexact(env):
     pgti, torch = env
     cfg = CFGS["ed_small"]
-    c = _case(env, cfg, 0)
+    c = _case(env, cfg, "own")
     grads = torch.full_like(c["params"], float("nan"))
     loss = torch.zeros(1, device="cuda")
     c["model"].step_indexed(c["params"], grads, c["s"], c["idx"], loss, c["ws"])
@@ -115,7 +119,7 @@ def test_encdec_zero_copy_bitexact(env):
 def test_encdec_metr_la_shape(env):
     """METR-LA-shaped encoder-decoder (372,353 parameters, 12 + 12 steps) at B = 8."""
     cfg = synth.CONFIGS["metr_la"].replace(B=8)
-    c = _case(env, cfg, 0)
+    c = _case(env, cfg, "mixed")
     assert c["model"].num_params() == 372353
     assert c["margin"] > 1e-5
     assert abs(c["loss"] - c["loss_ref"]) <= TOL32 * abs(c["loss_ref"])
@@ -144,7 +148,7 @@ def _check(c, tol):
         off += n
 
 
-@pytest.mark.parametrize("tf", [0, 1])
+@pytest.mark.parametrize("tf", list(MODES))
 @pytest.mark.parametrize("name", list(TC_CFGS))
 def test_encdec_bf16_vs_oracle(env, name, tf):
     """The encoder-decoder on the bf16 tcgen05 path (decoder input diffused per step, its layer-0
@@ -152,7 +156,32 @@ def test_encdec_bf16_vs_oracle(env, name, tf):
     _check(_case(env, TC_CFGS[name], tf, precision=1), TOL_BF16)
 
 
-@pytest.mark.parametrize("tf", [0, 1])
+@pytest.mark.parametrize("tf", list(MODES))
 def test_encdec_bf16_metr_la(env, tf):
     cfg = synth.CONFIGS["metr_la"].replace(B=16)
     _check(_case(env, cfg, tf, precision=1), TOL_BF16)
+
+
+def test_scheduled_sampling_trainer_matches_oracle_masks(env):
+    """Trainer(scheduled_sampling=k): each step draws the decoder's per-step feeding mask; the
+    step's loss equals the oracle's for that mask (fp32, 1e-5)."""
+    pgti, torch = env
+    from paper_2507_11683_b200.trainer import Trainer
+    cfg = CFGS["ed_small"]
+    ref = _ref(cfg)
+    d = dcgru.Dims.of(cfg)
+    theta = np.random.default_rng(3).uniform(-0.4, 0.4, encdec.num_params(d)).astype(np.float32)
+    tr = Trainer(cfg, ref.graph, lambda a, b: ref.v[a:b], theta, precision=0, use_cuda_graph=False,
+                 model=1, scheduled_sampling=2.0, lr=0.0)
+    tr.start_epoch(0)
+    masks = set()
+    for j in range(6):
+        tr.step(j)
+        mask = tr.model.desc.teacher_forcing
+        masks.add(mask)
+        idx = tr.epoch_plan()[j * cfg.B:(j + 1) * cfg.B].cpu().numpy()
+        xo, yo = ref.batch(idx)
+        want = encdec.forward(theta.astype(np.float64), d, ref.Pf, ref.Pb, xo.astype(np.float64),
+                              yo.astype(np.float64), teacher_forcing=mask)["loss"]
+        assert abs(tr.loss.item() - want) <= TOL32 * abs(want), (j, mask)
+    assert len(masks) > 1  # the curriculum actually varies the feeding
