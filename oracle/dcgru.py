@@ -39,6 +39,7 @@ class Dims:
     K: int
     T_in: int
     T_out: int
+    cheb: bool = False  # reading c25: blocks by the Chebyshev recurrence instead of powers
 
     @property
     def M(self) -> int:
@@ -52,7 +53,8 @@ class Dims:
 
     @staticmethod
     def of(cfg) -> "Dims":
-        return Dims(cfg.N, cfg.F, cfg.F_out, cfg.L, cfg.H, cfg.K, cfg.T_in, cfg.T_out)
+        return Dims(cfg.N, cfg.F, cfg.F_out, cfg.L, cfg.H, cfg.K, cfg.T_in, cfg.T_out,
+                    bool(getattr(cfg, "cheb", False)))
 
 
 def unpack(theta: np.ndarray, d: Dims):
@@ -84,25 +86,40 @@ def num_params(d: Dims) -> int:
     return n + d.H * d.F_out + d.F_out
 
 
-def diffusion_features(Pf, Pb, Z: np.ndarray, K: int) -> np.ndarray:
+def diffusion_features(Pf, Pb, Z: np.ndarray, K: int, cheb: bool = False) -> np.ndarray:
     """T(Z) for Z[N][W]: [Z, P_f Z, ..., P_f^K Z, P_b Z, ..., P_b^K Z] -> [M][N][W].
-    P^k Z is evaluated as k successive products (the definition of the power)."""
+    P^k Z is evaluated as k successive products (the definition of the power).
+    cheb (reading c25, Li et al.'s DCRNN code [ext]): block k of each direction is instead the
+    Chebyshev recurrence T_0 = Z, T_1 = P Z, T_k = 2 P T_{k-1} - T_{k-2}, restarted from Z for
+    each direction."""
     out = [Z]
-    T = Z
-    for _ in range(K):
-        T = Pf @ T
-        out.append(np.asarray(T))
-    T = Z
-    for _ in range(K):
-        T = Pb @ T
-        out.append(np.asarray(T))
+    for P in (Pf, Pb):
+        prev, T = Z, Z
+        for k in range(K):
+            if cheb and k >= 1:
+                T, prev = 2.0 * np.asarray(P @ T) - prev, T
+            else:
+                T, prev = np.asarray(P @ T), T
+            out.append(np.asarray(T))
     return np.stack(out)
 
 
-def diffusion_adjoint(Pf, Pb, dT: np.ndarray, K: int) -> np.ndarray:
+def diffusion_adjoint(Pf, Pb, dT: np.ndarray, K: int, cheb: bool = False) -> np.ndarray:
     """Transpose of diffusion_features: dZ = dT_0 + sum_k (P_f^k)^T dT_k
-    + sum_k (P_b^k)^T dT_{K+k}, with (P^k)^T = (P^T)^k applied k times."""
+    + sum_k (P_b^k)^T dT_{K+k}, with (P^k)^T = (P^T)^k applied k times.
+    cheb: dZ = dT_0 + sum_k C_k(P_f^T) dT_k + sum_k C_k(P_b^T) dT_{K+k}, the transpose of a
+    polynomial in P being the same polynomial in P^T; C_k(A) X is evaluated by the forward
+    recurrence C_0 X = X, C_1 X = A X, C_k X = 2 A C_{k-1} X - C_{k-2} X."""
     PfT, PbT = Pf.T, Pb.T
+    if cheb:
+        dZ = np.array(dT[0], dtype=np.float64, copy=True)
+        for A, base in ((PfT, 0), (PbT, K)):
+            for k in range(1, K + 1):
+                prev, cur = np.asarray(dT[base + k]), np.asarray(A @ dT[base + k])
+                for _ in range(k - 1):
+                    cur, prev = 2.0 * np.asarray(A @ cur) - prev, cur
+                dZ += cur
+        return dZ
     dZ = np.array(dT[0], dtype=np.float64, copy=True)
     for k in range(1, K + 1):
         a = dT[k]
@@ -116,20 +133,20 @@ def diffusion_adjoint(Pf, Pb, dT: np.ndarray, K: int) -> np.ndarray:
     return dZ
 
 
-def _feats_batched(Pf, Pb, Z: np.ndarray, K: int) -> np.ndarray:
+def _feats_batched(Pf, Pb, Z: np.ndarray, K: int, cheb: bool = False) -> np.ndarray:
     """T(Z) for a batch Z[B][N][C] -> [B][N][M*C] (column m*C + c = block m, channel c)."""
     B, N, C = Z.shape
-    T = diffusion_features(Pf, Pb, Z.transpose(1, 0, 2).reshape(N, B * C), K)  # [M][N][B*C]
+    T = diffusion_features(Pf, Pb, Z.transpose(1, 0, 2).reshape(N, B * C), K, cheb)
     M = T.shape[0]
     return T.reshape(M, N, B, C).transpose(2, 1, 0, 3).reshape(B, N, M * C)
 
 
-def _adjoint_batched(Pf, Pb, dT: np.ndarray, K: int, C: int) -> np.ndarray:
+def _adjoint_batched(Pf, Pb, dT: np.ndarray, K: int, C: int, cheb: bool = False) -> np.ndarray:
     """Transpose of _feats_batched: dT[B][N][M*C] -> dZ[B][N][C]."""
     B, N, MC = dT.shape
     M = MC // C
     d = dT.reshape(B, N, M, C).transpose(2, 1, 0, 3).reshape(M, N, B * C)
-    return diffusion_adjoint(Pf, Pb, d, K).reshape(N, B, C).transpose(1, 0, 2)
+    return diffusion_adjoint(Pf, Pb, d, K, cheb).reshape(N, B, C).transpose(1, 0, 2)
 
 
 def _sigmoid(a):
@@ -153,10 +170,10 @@ def forward(theta, d: Dims, Pf, Pb, x: np.ndarray, y: np.ndarray | None = None):
             p = layers[l]
             c_in = d.c_in(l)
             Hprev = H[l]
-            TZ = _feats_batched(Pf, Pb, np.concatenate([inp, Hprev], axis=-1), d.K)
+            TZ = _feats_batched(Pf, Pb, np.concatenate([inp, Hprev], axis=-1), d.K, d.cheb)
             G = TZ @ p["W_ru"].reshape(d.M * c_in, 2 * d.H) + p["b_ru"]
             r, u = _sigmoid(G[..., :d.H]), _sigmoid(G[..., d.H:])
-            TZ2 = _feats_batched(Pf, Pb, np.concatenate([inp, r * Hprev], axis=-1), d.K)
+            TZ2 = _feats_batched(Pf, Pb, np.concatenate([inp, r * Hprev], axis=-1), d.K, d.cheb)
             c = np.tanh(TZ2 @ p["W_c"].reshape(d.M * c_in, d.H) + p["b_c"])
             Hn = u * Hprev + (1.0 - u) * c
             step.append(dict(Hprev=Hprev, TZ=TZ, TZ2=TZ2, r=r, u=u, c=c, H=Hn))
@@ -207,7 +224,7 @@ def backward(theta, d: Dims, Pf, Pb, x, y, fwd=None):
             g["W_c"] += np.einsum("bnk,bnj->kj", cc["TZ2"], dCpre).reshape(g["W_c"].shape)
             g["b_c"] += dCpre.sum(axis=(0, 1))
             dTZ2 = dCpre @ p["W_c"].reshape(d.M * c_in, d.H).T
-            dZ2 = _adjoint_batched(Pf, Pb, dTZ2, d.K, c_in)
+            dZ2 = _adjoint_batched(Pf, Pb, dTZ2, d.K, c_in, d.cheb)
             dinp = dZ2[..., :f_in].copy()
             drH = dZ2[..., f_in:]
             dHprev += drH * r
@@ -215,7 +232,7 @@ def backward(theta, d: Dims, Pf, Pb, x, y, fwd=None):
             g["W_ru"] += np.einsum("bnk,bnj->kj", cc["TZ"], dG).reshape(g["W_ru"].shape)
             g["b_ru"] += dG.sum(axis=(0, 1))
             dTZ = dG @ p["W_ru"].reshape(d.M * c_in, 2 * d.H).T
-            dZ = _adjoint_batched(Pf, Pb, dTZ, d.K, c_in)
+            dZ = _adjoint_batched(Pf, Pb, dTZ, d.K, c_in, d.cheb)
             dinp += dZ[..., :f_in]
             dHprev += dZ[..., f_in:]
             dH[l] = dHprev

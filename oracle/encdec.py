@@ -61,10 +61,10 @@ def unpack(theta, d: Dims) -> dict:
 def _cell(p: dict, pre: str, d: Dims, Pf, Pb, inp, Hprev):
     """One DCGRU cell (Li et al. Eq. 2-3 [ext]; oracle.dcgru's reading c1)."""
     c_in = inp.shape[-1] + d.H
-    TZ = _feats_batched(Pf, Pb, np.concatenate([inp, Hprev], axis=-1), d.K)
+    TZ = _feats_batched(Pf, Pb, np.concatenate([inp, Hprev], axis=-1), d.K, d.cheb)
     G = TZ @ p[pre + ".W_ru"].reshape(d.M * c_in, 2 * d.H) + p[pre + ".b_ru"]
     r, u = _sigmoid(G[..., :d.H]), _sigmoid(G[..., d.H:])
-    TZ2 = _feats_batched(Pf, Pb, np.concatenate([inp, r * Hprev], axis=-1), d.K)
+    TZ2 = _feats_batched(Pf, Pb, np.concatenate([inp, r * Hprev], axis=-1), d.K, d.cheb)
     c = np.tanh(TZ2 @ p[pre + ".W_c"].reshape(d.M * c_in, d.H) + p[pre + ".b_c"])
     return u * Hprev + (1.0 - u) * c
 
@@ -123,9 +123,10 @@ def loss_and_grad(theta, d: Dims, Pf, Pb, x, y, teacher_forcing=False):
     def feats(Z):                                       # [B][N][C] -> [B][N][M][C]
         out = [Z]
         for P in (Pft, Pbt):
-            T = Z
-            for _ in range(d.K):
-                T = torch.einsum("ij,bjc->bic", P, T)
+            prev, T = Z, Z
+            for k in range(d.K):
+                PT = torch.einsum("ij,bjc->bic", P, T)
+                T, prev = (2.0 * PT - prev if d.cheb and k >= 1 else PT), T
                 out.append(T)
         return torch.stack(out, 2)
 

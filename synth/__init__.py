@@ -42,6 +42,7 @@ class Config:
     F_out: int = 1  # predicted channels (channel 0)
     knn: int = 8    # out-neighbours per node before thresholding
     period: int = 288  # samples per day (5-min data) / 52 weeks for CP
+    cheb: bool = False  # diffusion blocks by the Chebyshev recurrence (Li et al.'s code, c25)
 
     def replace(self, **kw) -> "Config":
         return dataclasses.replace(self, **kw)

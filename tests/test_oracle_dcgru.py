@@ -338,3 +338,50 @@ def test_adam_hand_step_and_torch():
         opt.step()
         th, m, v = adam.adam_step(th, g, m, v, step, 1e-2, grad_scale=0.5)
         assert np.allclose(p.detach().numpy(), th, rtol=1e-14, atol=1e-15)
+
+
+# --------------------------------------------------------- Chebyshev variant (reading c25)
+@pytest.mark.parametrize("a", [0.3, -0.7, 1.0])
+def test_chebyshev_blocks_on_scaled_identity(a):
+    """With P = a I the recurrence gives the Chebyshev polynomials of the first kind:
+    T_0 = 1, T_1 = a, T_2 = 2a^2 - 1, T_3 = 4a^3 - 3a."""
+    N, W, K = 4, 3, 3
+    P = a * np.eye(N)
+    Z = np.random.default_rng(0).normal(size=(N, W))
+    T = dcgru.diffusion_features(P, P, Z, K, cheb=True)
+    want = [1.0, a, 2 * a * a - 1, 4 * a ** 3 - 3 * a]
+    for k in range(K + 1):
+        assert np.allclose(T[k], want[k] * Z, rtol=0, atol=1e-14)
+        if k:
+            assert np.allclose(T[K + k], want[k] * Z, rtol=0, atol=1e-14)
+
+
+def test_chebyshev_k1_equals_powers_and_adjoint_identity():
+    src, dst, w = synth.random_graph(9, 0.3, seed=8)
+    Pf, Pb = transitions.transition_matrices(9, src, dst, w, dense=True)
+    rng = np.random.default_rng(1)
+    Z = rng.normal(size=(9, 5))
+    assert np.array_equal(dcgru.diffusion_features(Pf, Pb, Z, 1, cheb=True),
+                          dcgru.diffusion_features(Pf, Pb, Z, 1))
+    for K in (2, 3):
+        T = dcgru.diffusion_features(Pf, Pb, Z, K, cheb=True)
+        dT = rng.normal(size=T.shape)
+        lhs = np.sum(T * dT)
+        rhs = np.sum(Z * dcgru.diffusion_adjoint(Pf, Pb, dT, K, cheb=True))
+        assert abs(lhs - rhs) <= 1e-12 * max(1.0, abs(lhs))
+
+
+def test_chebyshev_backward_finite_differences():
+    d = dcgru.Dims(N=4, F=2, F_out=1, L=2, H=2, K=2, T_in=3, T_out=2, cheb=True)
+    theta, Pf, Pb, x, y, _ = _rand_problem(d, seed=9)
+    loss, grad, fwd = dcgru.backward(theta, d, Pf, Pb, x, y)
+    assert np.min(np.abs(fwd["yhat"] - y[..., :1])) > 1e-4
+    h = 1e-6
+    for i in range(theta.size):
+        tp, tm = theta.copy(), theta.copy()
+        tp[i] += h
+        tm[i] -= h
+        fd = (dcgru.forward(tp, d, Pf, Pb, x, y)["loss"] -
+              dcgru.forward(tm, d, Pf, Pb, x, y)["loss"]) / (2 * h)
+        if abs(grad[i]) > 1e-8 or abs(fd) > 1e-8:
+            assert abs(fd - grad[i]) <= 1e-5 * max(abs(grad[i]), abs(fd)) + 1e-9, (i, fd, grad[i])

@@ -108,3 +108,21 @@ def test_gradient_finite_differences(tf, L, K):
               encdec.forward(tm, d, Pf, Pb, x, y, teacher_forcing=tf)["loss"]) / (2 * h)
         if abs(grad[i]) > 1e-8 or abs(fd) > 1e-8:
             assert abs(fd - grad[i]) <= 1e-5 * max(abs(grad[i]), abs(fd)) + 1e-9, (i, fd, grad[i])
+
+
+def test_chebyshev_encdec_transcriptions_and_gradient():
+    d = _dims(N=4, H=2, L=2, K=2, T_in=2, T_out=3, cheb=True)
+    theta, Pf, Pb, x, y = _problem(d, seed=12)
+    out = encdec.forward(theta, d, Pf, Pb, x, y)
+    loss, grad, yhat = encdec.loss_and_grad(theta, d, Pf, Pb, x, y)
+    assert np.allclose(yhat, out["yhat"], rtol=0, atol=1e-13)
+    assert np.min(np.abs(yhat - y[..., :1])) > 1e-4
+    h = 1e-6
+    for i in range(0, theta.size, 7):
+        tp, tm = theta.copy(), theta.copy()
+        tp[i] += h
+        tm[i] -= h
+        fd = (encdec.forward(tp, d, Pf, Pb, x, y)["loss"] -
+              encdec.forward(tm, d, Pf, Pb, x, y)["loss"]) / (2 * h)
+        if abs(grad[i]) > 1e-8 or abs(fd) > 1e-8:
+            assert abs(fd - grad[i]) <= 1e-5 * max(abs(grad[i]), abs(fd)) + 1e-9, (i, fd, grad[i])
