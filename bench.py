@@ -48,8 +48,9 @@ def parse():
                     help="halo shard (BASELINE north star) or the paper's replicated copy with a "
                          "global shuffle and per-epoch validation all-reduce (P:325, P:424)")
     ap.add_argument("--model", default="stepwise", choices=["stepwise", "encdec"],
-                    help="stepwise PGT-DCRNN (default) or Li et al.'s encoder-decoder (f3, "
-                         "runs on the fp32 path: use with --precision 0)")
+                    help="stepwise PGT-DCRNN (default) or Li et al.'s encoder-decoder (f3)")
+    ap.add_argument("--cheb", action="store_true",
+                    help="diffusion blocks by the Chebyshev recurrence (f3, reading c25)")
     ap.add_argument("--zero-copy", action="store_true",
                     help="read windows straight from the series by index (no x/y gather, f2)")
     ap.add_argument("--shuffle", default="window", choices=["window", "batch", "none"],
@@ -223,7 +224,7 @@ def config_dict(cfg, world, args):
             "precision": "fp32" if args.precision == 0 else "bf16",
             "l2": "no flush: each step writes >= 1 GB of fresh activations (>> 126 MB L2)",
             "cuda_graph": not args.no_graph, "zero_copy": bool(args.zero_copy),
-            "model": args.model}
+            "model": args.model, "diffusion_basis": "chebyshev" if cfg.cheb else "powers"}
 
 
 # ------------------------------------------------------------------------------ our arm
@@ -232,6 +233,8 @@ def main():
     args = parse()
     import synth
     cfg = synth.CONFIGS[args.config]
+    if args.cheb:
+        cfg = cfg.replace(cheb=True)
     if args.precision == 1 and cfg.H != 64:
         # the tcgen05 path is built for 64 hidden units (one 128-byte SWIZZLE_128B row per
         # diffusion block); Chickenpox's 32-unit model runs on the fp32 SIMT path

@@ -234,7 +234,15 @@ typedef struct {
    * T_in.  act_dump covers the T_in + T_out steps.  Both precisions. */
   int32_t model;
   int32_t teacher_forcing;  /* bit mask over decoder steps 1..T_out-1 (model 1) */
+  /* Diffusion blocks (reading c25; Li et al.'s DCRNN code [ext]): 0 = plain powers
+   * P^k Z; 1 = the Chebyshev recurrence T_1 = P Z, T_k = 2 P T_{k-1} - T_{k-2}
+   * per direction (T_0 = Z); the adjoint is the same polynomial in P^T. */
+  int32_t cheb;
 } pgti_dcrnn_desc;
+
+/* sizeof(pgti_dcrnn_desc) as this build lays it out: bindings check their mirror of the
+ * struct against it before the first call (fields are only ever appended). */
+size_t pgti_dcrnn_desc_size(void);
 
 /* Number of float parameters of the layout above (0 if desc invalid). */
 size_t pgti_dcrnn_num_params(const pgti_dcrnn_desc *d);

@@ -47,6 +47,9 @@ pgti_status check_desc(const pgti_dcrnn_desc *desc, Dims *out) {
   PGTI_REQUIRE(g.N > 0 && g.F > 0 && g.L > 0 && g.K >= 0 && g.T_in > 0 && g.B > 0,
                PGTI_ERR_SHAPE, "desc: N=%d F=%d L=%d K=%d T_in=%d B=%d", g.N, g.F, g.L, g.K,
                g.T_in, g.B);
+  PGTI_REQUIRE(g.cheb == 0 || g.cheb == 1, PGTI_ERR_INVALID_ARG, "desc: cheb=%d", g.cheb);
+  PGTI_REQUIRE(!g.cheb || !g.a2_rowptr, PGTI_ERR_INVALID_ARG,
+               "desc: the two-hop operators are powers of P, not Chebyshev blocks");
   PGTI_REQUIRE(g.model == 0 || g.model == 1, PGTI_ERR_INVALID_ARG,
                "desc: model=%d (0 = stepwise, 1 = encoder-decoder)", g.model);
   PGTI_REQUIRE(g.teacher_forcing == 0 ||
@@ -91,7 +94,7 @@ pgti_status check_desc(const pgti_dcrnn_desc *desc, Dims *out) {
                  "plan pointers (win_rows=%d)",
                  g.win_rows);
   Dims d{g.N, g.F, g.F_out, g.L, g.H, g.K, g.T_in, g.T_out, g.B, 2 * g.K + 1,
-         int64_t(g.N) * g.B, g.ld, g.precision, g.model, g.teacher_forcing};
+         int64_t(g.N) * g.B, g.ld, g.precision, g.model, g.teacher_forcing, g.cheb};
   *out = d;
   return PGTI_OK;
 }
@@ -129,7 +132,8 @@ cudaError_t diffuse_fwd(const pgti_dcrnn_desc &g, const Dims &d, float *base, in
   // inside the step (METR-LA 26.0 K vs 32.3 K samples/s) than one wide launch per hop
   const char *res_env = std::getenv("PGTI_RESIDENT");
   const bool resident_on = res_env && res_env[0] == '1';
-  if (bf16 && G == 1 && !g.a2_rowptr && resident_on && spmm_resident_fits(d.N, d.K, W)) {
+  if (bf16 && G == 1 && !g.a2_rowptr && !d.cheb && resident_on &&
+      spmm_resident_fits(d.N, d.K, W)) {
     // small graph: both directions' hop chain in one launch, the chunk resident in smem
     ResidentJob r{};
     const int pf = transposed ? 1 : 0, pb = transposed ? 0 : 1;  // 0: pattern(A), 1: A^T
@@ -172,6 +176,11 @@ cudaError_t diffuse_fwd(const pgti_dcrnn_desc &g, const Dims &d, float *base, in
     j[0].Y = reinterpret_cast<float *>(blk(k));
     j[1].Y = reinterpret_cast<float *>(blk(d.K + k));
     for (auto &jb : j) jb.nterms = 1, jb.W = W, jb.G = G, jb.gstride = gstride, jb.bf16 = bf16;
+    if (d.cheb && k >= 2) {  // T_k = 2 P T_{k-1} - T_{k-2}
+      j[0].alpha = j[1].alpha = 2.f, j[0].beta = j[1].beta = -1.f;
+      j[0].add = reinterpret_cast<const float *>(k == 2 ? z : blk(k - 2));
+      j[1].add = reinterpret_cast<const float *>(k == 2 ? z : blk(d.K + k - 2));
+    }
     cudaError_t e = launch_spmm(j, 2, d.N, s);
     if (e != cudaSuccess) return e;
   }
@@ -190,6 +199,48 @@ cudaError_t diffuse_adj(const pgti_dcrnn_desc &g, const Dims &d, AdjChain *ch, i
       jobs[c].accumulate = ch[c].accumulate, jobs[c].W = ch[c].W, jobs[c].G = 1;
     }
     return launch_spmm(jobs, nch, d.N, s);
+  }
+  if (d.cheb && K >= 2) {
+    // Chebyshev blocks (reading c25): dZ = d_0 + sum_dir sum_k T_k(A) d_k with A = P^T of the
+    // direction, by Clenshaw's recurrence b_K = d_K, b_k = d_k + 2 A b_{k+1} - b_{k+2}, then
+    // dZ = d_0 + sum_dir (A b_1 - b_2).  b_k overwrites b_{k+2} in place (read and written by the
+    // same thread), so two temporaries per direction serve any K.
+    std::vector<const float *> f1(nch), f2(nch, nullptr), b1(nch), b2(nch, nullptr);
+    for (int c = 0; c < nch; ++c)
+      f1[c] = ch[c].dT + K * ch[c].mstride, b1[c] = ch[c].dT + 2 * K * ch[c].mstride;
+    int pp = 0;
+    for (int k = K - 1; k >= 1; --k) {
+      int nj = 0;
+      for (int c = 0; c < nch; ++c) {
+        SpmmJob f{}, b{};
+        set_term(f, 0, g, 1, g.PfT_val, f1[c]);
+        f.add = ch[c].dT + k * ch[c].mstride, f.add2 = f2[c], f.Y = ch[c].tf[pp];
+        set_term(b, 0, g, 0, g.PbT_val, b1[c]);
+        b.add = ch[c].dT + (K + k) * ch[c].mstride, b.add2 = b2[c], b.Y = ch[c].tb[pp];
+        for (SpmmJob *jb : {&f, &b})
+          jb->nterms = 1, jb->W = ch[c].W, jb->G = 1, jb->alpha = 2.f, jb->beta2 = -1.f;
+        jobs[nj++] = f, jobs[nj++] = b;
+        f2[c] = f1[c], f1[c] = ch[c].tf[pp], b2[c] = b1[c], b1[c] = ch[c].tb[pp];
+      }
+      cudaError_t e = launch_spmm(jobs, nj, d.N, s);
+      if (e != cudaSuccess) return e;
+      pp ^= 1;
+    }
+    for (int dir = 0; dir < 2; ++dir) {  // out (+)= d_0 + A_f b_1 - b_2, then += A_b b_1 - b_2
+      for (int c = 0; c < nch; ++c) {
+        SpmmJob j{};
+        if (dir == 0)
+          set_term(j, 0, g, 1, g.PfT_val, f1[c]), j.add = ch[c].dT, j.add2 = f2[c];
+        else
+          set_term(j, 0, g, 0, g.PbT_val, b1[c]), j.add2 = b2[c];
+        j.nterms = 1, j.beta2 = -1.f, j.Y = ch[c].out;
+        j.accumulate = dir == 1 || ch[c].accumulate, j.W = ch[c].W, j.G = 1;
+        jobs[c] = j;
+      }
+      cudaError_t e = launch_spmm(jobs, nch, d.N, s);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
   }
   std::vector<const float *> af(nch), ab(nch);
   for (int c = 0; c < nch; ++c)
@@ -479,6 +530,8 @@ size_t workspace_for(const Dims &d) {
 
 using namespace pgti;
 using namespace pgti::detail;
+
+extern "C" size_t pgti_dcrnn_desc_size(void) { return sizeof(pgti_dcrnn_desc); }
 
 extern "C" size_t pgti_dcrnn_num_params(const pgti_dcrnn_desc *desc) {
   Dims d;

@@ -17,6 +17,7 @@ struct Dims {
   int teacher;  // encoder-decoder: bit s-1 set = decoder step s is fed the previous target
   // decoder step s >= 1 fed the target y_{s-1} (else its own prediction yhat_{s-1})
   bool fed_truth(int s) const { return s >= 1 && ((teacher >> (s - 1)) & 1); }
+  int cheb;     // diffusion blocks by the Chebyshev recurrence (reading c25)
   // hidden-state steps: T_in (stepwise) or T_in + T_out (encoder then decoder)
   int steps() const { return T_in + (model ? T_out : 0); }
 };

@@ -25,6 +25,11 @@ struct SpmmJob {
   int G;
   int64_t gstride;
   int bf16;           // X, add, Y are __nv_bfloat16 (all jobs of a launch agree)
+  // Chebyshev recurrence / Clenshaw steps: Y = alpha * sum + beta * add + beta2 * add2
+  // (+ Y if accumulate); the defaults (1, 1, no add2) are the plain sum, bit for bit
+  float alpha = 1.f, beta = 1.f;
+  const float *add2 = nullptr;
+  float beta2 = 1.f;
   // shared-memory staging plan of each term's pattern (pgti_graph_windows); used when every
   // term of every job of the launch has one with the same win_rows
   const int32_t *win_ptr[2];

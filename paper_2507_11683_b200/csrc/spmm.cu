@@ -48,6 +48,12 @@ struct Lane<float> {
     acc[0] = __fadd2_rn(acc[0], make_float2(a.x, a.y));
     acc[1] = __fadd2_rn(acc[1], make_float2(a.z, a.w));
   }
+  static __device__ __forceinline__ void axpy(float2 *acc, float b, const float *p) {
+    const float4 a = *reinterpret_cast<const float4 *>(p);
+    const float2 bb = make_float2(b, b);
+    acc[0] = __ffma2_rn(bb, make_float2(a.x, a.y), acc[0]);
+    acc[1] = __ffma2_rn(bb, make_float2(a.z, a.w), acc[1]);
+  }
   static __device__ __forceinline__ void store(float *p, const float2 *v) {
     *reinterpret_cast<float4 *>(p) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
   }
@@ -80,6 +86,14 @@ struct Lane<__nv_bfloat16> {
     acc[2] = __fadd2_rn(acc[2], unpack(a.z));
     acc[3] = __fadd2_rn(acc[3], unpack(a.w));
   }
+  static __device__ __forceinline__ void axpy(float2 *acc, float b, const __nv_bfloat16 *p) {
+    const uint4 a = *reinterpret_cast<const uint4 *>(p);
+    const float2 bb = make_float2(b, b);
+    acc[0] = __ffma2_rn(bb, unpack(a.x), acc[0]);
+    acc[1] = __ffma2_rn(bb, unpack(a.y), acc[1]);
+    acc[2] = __ffma2_rn(bb, unpack(a.z), acc[2]);
+    acc[3] = __ffma2_rn(bb, unpack(a.w), acc[3]);
+  }
   static __device__ __forceinline__ void store(__nv_bfloat16 *p, const float2 *v) {
     uint4 a;
     __nv_bfloat162 h;
@@ -90,6 +104,29 @@ struct Lane<__nv_bfloat16> {
     *reinterpret_cast<uint4 *>(p) = a;
   }
 };
+
+// Y = alpha * acc + beta * add + beta2 * add2 (+ Y): the plain defaults keep the original
+// instruction sequence (FADD2 of the addend), so existing results are unchanged bit for bit
+template <typename L, typename T>
+__device__ __forceinline__ void finish(const SpmmJob &jb, float2 *acc, int64_t o) {
+  constexpr int P = L::V / 2;
+  if (jb.alpha != 1.f) {
+    const float2 a = make_float2(jb.alpha, jb.alpha);
+#pragma unroll
+    for (int q = 0; q < P; ++q) acc[q] = __fmul2_rn(a, acc[q]);
+  }
+  if (jb.add) {
+    const T *ad = reinterpret_cast<const T *>(jb.add) + o;
+    if (jb.beta == 1.f)
+      L::add(acc, ad);
+    else
+      L::axpy(acc, jb.beta, ad);
+  }
+  if (jb.add2) L::axpy(acc, jb.beta2, reinterpret_cast<const T *>(jb.add2) + o);
+  T *Y = reinterpret_cast<T *>(jb.Y) + o;
+  if (jb.accumulate) L::add(acc, Y);
+  L::store(Y, acc);
+}
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_spmm(const __grid_constant__ SpmmParams p) {
@@ -134,10 +171,7 @@ __global__ void __launch_bounds__(256) k_spmm(const __grid_constant__ SpmmParams
     for (; e < end; ++e) L::fma(acc, __ldg(jb.val[t] + e), X + __ldg(jb.col[t] + e) * W);
   }
   const int64_t o = goff + int64_t(n) * W + col0;
-  if (jb.add) L::add(acc, reinterpret_cast<const T *>(jb.add) + o);
-  T *Y = reinterpret_cast<T *>(jb.Y) + o;
-  if (jb.accumulate) L::add(acc, Y);
-  L::store(Y, acc);
+  finish<L, T>(jb, acc, o);
 }
 
 // Shared-memory staged variant (the plan of pgti_graph_windows): CTA = (window of win_rows
@@ -245,10 +279,7 @@ __global__ void __launch_bounds__(256) k_spmm_win(const __grid_constant__ WinPar
     const int r = warp + 8 * i, n = row0 + r;
     if (r >= p.win_rows || n >= p.N) continue;
     const int64_t o = goff + int64_t(n) * W + int64_t(vec) * V;
-    if (jb.add) L::add(acc[i], reinterpret_cast<const T *>(jb.add) + o);
-    T *Y = reinterpret_cast<T *>(jb.Y) + o;
-    if (jb.accumulate) L::add(acc[i], Y);
-    L::store(Y, acc[i]);
+    finish<L, T>(jb, acc[i], o);
   }
 }
 
@@ -332,7 +363,9 @@ __global__ void __launch_bounds__(256) k_spmm_scalar(const __grid_constant__ Spm
     for (int e = jb.rowptr[t][n]; e < jb.rowptr[t][n + 1]; ++e)
       acc = fmaf(jb.val[t][e], X[int64_t(jb.col[t][e]) * W + col], acc);
   }
-  if (jb.add) acc += jb.add[o];
+  if (jb.alpha != 1.f) acc *= jb.alpha;
+  if (jb.add) acc = jb.beta == 1.f ? acc + jb.add[o] : fmaf(jb.beta, jb.add[o], acc);
+  if (jb.add2) acc = fmaf(jb.beta2, jb.add2[o], acc);
   if (jb.accumulate) acc += jb.Y[o];
   jb.Y[o] = acc;
 }
@@ -375,7 +408,7 @@ cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s) {
   for (int i = 0; i < njobs; ++i) {
     const SpmmJob &j = jobs[i];
     const double nw = double(N) * double(j.W) * es * j.G;
-    bytes += nw * (1 + j.nterms + (j.add ? 1 : 0) + (j.accumulate ? 1 : 0));
+    bytes += nw * (1 + j.nterms + (j.add ? 1 : 0) + (j.add2 ? 1 : 0) + (j.accumulate ? 1 : 0));
     for (int t = 0; t < j.nterms; ++t) {
       bytes += (double(j.nnz[t]) * 8.0 + double(N + 1) * 4.0) * j.G;
       flops += 2.0 * double(j.nnz[t]) * double(j.W) * j.G;

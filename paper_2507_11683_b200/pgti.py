@@ -50,7 +50,7 @@ class DcrnnDesc(C.Structure):
                 ("at2_rowptr", _vp), ("at2_col", _vp), ("Pb2_val", _vp), ("Pf2T_val", _vp),
                 ("a2_win_ptr", _vp), ("a2_win_nodes", _vp), ("a2_lcol", _vp),
                 ("at2_win_ptr", _vp), ("at2_win_nodes", _vp), ("at2_lcol", _vp),
-                ("model", _i32), ("teacher_forcing", _i32)]
+                ("model", _i32), ("teacher_forcing", _i32), ("cheb", _i32)]
 
 
 def _sig(name, restype, *argtypes):
@@ -80,6 +80,10 @@ _make_index = _sig("pgti_make_index", C.c_int, _vp, _i64, _i64, C.c_int, C.c_int
                    _u64, C.c_int, C.c_int, _vp, C.POINTER(_i64), _vp)
 _gather = _sig("pgti_gather_batch", C.c_int, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp)
 _num_params = _sig("pgti_dcrnn_num_params", _sz, C.POINTER(DcrnnDesc))
+_desc_size = _sig("pgti_dcrnn_desc_size", _sz)()
+if _desc_size != C.sizeof(DcrnnDesc):
+    raise ImportError(f"libpgti's pgti_dcrnn_desc is {_desc_size} bytes, the binding's "
+                      f"{C.sizeof(DcrnnDesc)}: rebuild the extension")
 _ws_bytes = _sig("pgti_dcrnn_workspace_bytes", _sz, C.POINTER(DcrnnDesc))
 _step = _sig("pgti_dcrnn_step", C.c_int, C.POINTER(DcrnnDesc), _vp, _vp, _vp, _vp, _vp, _vp, _sz,
              _vp, _vp)
@@ -317,9 +321,10 @@ class DCRNN:
     """pgti_dcrnn_desc + the device CSR arrays it points to."""
 
     def __init__(self, N, F, F_out, L, H, K, T_in, T_out, B, ld, csr_dev: dict | None,
-                 precision: int = 0, model: int = 0, teacher_forcing: int = 0):
+                 precision: int = 0, model: int = 0, teacher_forcing: int = 0, cheb: bool = False):
         """model 0: stepwise stacked PGT-DCRNN; 1: Li et al. encoder-decoder (teacher_forcing:
-        decoder fed the previous target instead of its own prediction)."""
+        decoder fed the previous target instead of its own prediction).  cheb: diffusion blocks
+        by the Chebyshev recurrence T_k = 2 P T_{k-1} - T_{k-2} (reading c25)."""
         self.csr = csr_dev or {}
         g = lambda k: _ptr(self.csr.get(k))  # noqa: E731
         nnz = int(self.csr["a_col"].numel()) if csr_dev else 0
@@ -334,7 +339,7 @@ class DCRNN:
                               g("at2_rowptr"), g("at2_col"), g("Pb2_val"), g("Pf2T_val"),
                               g("a2_win_ptr"), g("a2_win_nodes"), g("a2_lcol"),
                               g("at2_win_ptr"), g("at2_win_nodes"), g("at2_lcol"),
-                              int(model), self._tf_mask(teacher_forcing, T_out))
+                              int(model), self._tf_mask(teacher_forcing, T_out), int(bool(cheb)))
         self.model = int(model)
         self.N, self.F, self.F_out, self.L, self.H, self.K = N, F, F_out, L, H, K
         self.T_in, self.T_out, self.B, self.ld = T_in, T_out, B, ld

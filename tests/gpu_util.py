@@ -38,7 +38,7 @@ def model_for(pgti, torch, cfg, graph, precision=0, win_rows=None, two_hop=False
     csr = pgti.add_windows(csr, cfg.N, win_rows)
     csr = pgti.csr_to_device(csr, "cuda")
     return pgti.DCRNN(cfg.N, cfg.F, cfg.F_out, cfg.L, cfg.H, cfg.K, cfg.T_in, cfg.T_out, cfg.B,
-                      ld_of(cfg), csr, precision)
+                      ld_of(cfg), csr, precision, cheb=getattr(cfg, "cheb", False))
 
 
 def run_step(pgti, torch, model, theta, x, y, dump=True):

@@ -144,6 +144,12 @@ def test_graph_windows_errors(pgti):
         pgti.graph_windows(4, csr["a_rowptr"], bad, 2)
 
 
+def test_desc_mirror_matches_the_library(pgti):
+    import ctypes
+    assert pgti._desc_size == ctypes.sizeof(pgti.DcrnnDesc)
+    assert pgti.DcrnnDesc.cheb.offset + 4 <= ctypes.sizeof(pgti.DcrnnDesc)
+
+
 def test_desc_validation_without_gpu(pgti):
     m = pgti.DCRNN(207, 2, 1, 2, 64, 2, 12, 12, 64, 416, None)
     with pytest.raises(pgti.PgtiError):  # K > 0 needs CSR pointers

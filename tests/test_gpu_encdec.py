@@ -40,7 +40,8 @@ def env():
 def _model(pgti, torch, cfg, graph, tf, precision=0):
     csr = pgti.csr_to_device(pgti.graph_build(cfg.N, *graph), "cuda")
     return pgti.DCRNN(cfg.N, cfg.F, cfg.F_out, cfg.L, cfg.H, cfg.K, cfg.T_in, cfg.T_out, cfg.B,
-                      ld_of(cfg), csr, precision, model=1, teacher_forcing=tf)
+                      ld_of(cfg), csr, precision, model=1, teacher_forcing=tf,
+                      cheb=cfg.cheb)
 
 
 MODES = {"own": 0, "tf": True, "mixed": 0b1}  # mixed: only decoder step 1 fed the target
