@@ -50,6 +50,17 @@ pgti_status check_desc(const pgti_dcrnn_desc *desc, Dims *out) {
   PGTI_REQUIRE(g.cheb == 0 || g.cheb == 1, PGTI_ERR_INVALID_ARG, "desc: cheb=%d", g.cheb);
   PGTI_REQUIRE(!g.cheb || !g.a2_rowptr, PGTI_ERR_INVALID_ARG,
                "desc: the two-hop operators are powers of P, not Chebyshev blocks");
+  if (g.win2_rows) {
+    PGTI_REQUIRE(g.win2_rows >= 1 && g.win2_rows <= 64 && g.win2_max_nodes > 0 &&
+                     g.win2_max_n1 > 0 && g.win2_max_n1 <= g.win2_max_nodes &&
+                     g.win2_max_entries >= 0 && !g.a2_rowptr,
+                 PGTI_ERR_INVALID_ARG, "desc: bad two-hop plan (win2_rows=%d) or with P^2",
+                 g.win2_rows);
+    PGTI_REQUIRE(g.a_w2_ptr && g.a_w2_nodes && g.a_w2_n1 && g.a_w2_eptr && g.a_w2_roff &&
+                     g.a_w2_eidx && g.a_w2_lcol && g.at_w2_ptr && g.at_w2_nodes && g.at_w2_n1 &&
+                     g.at_w2_eptr && g.at_w2_roff && g.at_w2_eidx && g.at_w2_lcol,
+                 PGTI_ERR_INVALID_ARG, "desc: win2_rows set but a two-hop plan pointer is null");
+  }
   PGTI_REQUIRE(g.model == 0 || g.model == 1, PGTI_ERR_INVALID_ARG,
                "desc: model=%d (0 = stepwise, 1 = encoder-decoder)", g.model);
   PGTI_REQUIRE(g.teacher_forcing == 0 ||
@@ -145,6 +156,31 @@ cudaError_t diffuse_fwd(const pgti_dcrnn_desc &g, const Dims &d, float *base, in
     r.X = z, r.N = d.N, r.K = d.K, r.W = W;
     for (int k = 1; k <= d.K; ++k) r.Y[0][k - 1] = blk(k), r.Y[1][k - 1] = blk(d.K + k);
     return launch_spmm_resident(r, s);
+  }
+  if (d.K == 2 && bf16 && !g.a2_rowptr && g.win2_rows > 0) {
+    // opt-in: both hops of both directions in one launch from the two-hop staging plan
+    // (bit-identical).  Measured slower inside the step (METR-LA 30.8 K vs 33.2 K samples/s,
+    // PeMS-All-LA 2.59 K vs 3.10 K): the window's U2 staging moves as many rows from L2 as the
+    // two one-hop launches together, hop 1 is recomputed for U1 (~2x the rows), and 100 KB of
+    // shared memory per CTA halves residency; PDL already hides most of the saved launch gap.
+    Win2Job j[2] = {};
+    const bool pa[2] = {transposed != 0, transposed == 0};  // pattern(A^T) for job q?
+    const float *vals[2] = {transposed ? g.PfT_val : g.Pf_val, transposed ? g.PbT_val : g.Pb_val};
+    for (int q = 0; q < 2; ++q) {
+      Win2Job &w = j[q];
+      const bool t = pa[q];
+      w.ptr = t ? g.at_w2_ptr : g.a_w2_ptr, w.nodes = t ? g.at_w2_nodes : g.a_w2_nodes;
+      w.n1 = t ? g.at_w2_n1 : g.a_w2_n1, w.eptr = t ? g.at_w2_eptr : g.a_w2_eptr;
+      w.roff = t ? g.at_w2_roff : g.a_w2_roff, w.eidx = t ? g.at_w2_eidx : g.a_w2_eidx;
+      w.lcol = t ? g.at_w2_lcol : g.a_w2_lcol, w.val = vals[q];
+      w.X = z, w.Y1 = blk(q * d.K + 1), w.Y2 = blk(q * d.K + 2);
+      w.W = W, w.G = G, w.gstride = gstride, w.nnz = g.nnz;
+      if (d.cheb) w.add = z, w.alpha = 2.f, w.beta = -1.f;
+    }
+    const Win2Plan plan{g.win2_rows, g.win2_max_nodes, g.win2_max_n1, g.win2_max_entries};
+    cudaError_t e = launch_spmm_win2(j, 2, d.N, plan, s);
+    if (e != cudaErrorNotSupported) return e;
+    cudaGetLastError();  // not resident-sized: the hop chain below
   }
   if (d.K == 2 && bf16 && g.a2_rowptr) {  // one launch: [P Z, P^2 Z] for both directions
     SpmmJob j[4] = {};

@@ -56,6 +56,25 @@ struct ResidentJob {
   int N, K;
   int64_t W;
 };
+// Two-hop staged diffusion (pgti_graph_windows2 plan, bf16): Y1 = P X, Y2 = P Y1 (Chebyshev:
+// Y2 = alpha P Y1 + beta add) in one launch, bit-identical to two launch_spmm hops.
+struct Win2Job {
+  const void *X;
+  void *Y1, *Y2;
+  const void *add;  // nullable: hop-2 epilogue alpha * acc + beta * add
+  float alpha, beta;
+  const float *val;
+  const int32_t *ptr, *nodes, *n1, *eptr, *roff, *eidx;
+  const uint16_t *lcol;
+  int64_t W, gstride, nnz;
+  int G;
+};
+struct Win2Plan {
+  int rows, max_nodes, max_n1, max_entries;
+};
+// cudaErrorNotSupported: the plan's windows do not fit shared memory (caller runs the chain)
+cudaError_t launch_spmm_win2(const Win2Job *jobs, int njobs, int N, const Win2Plan &plan,
+                             cudaStream_t s);
 bool spmm_resident_fits(int N, int K, int64_t W);
 cudaError_t launch_spmm_resident(const ResidentJob &p, cudaStream_t s);
 

@@ -296,6 +296,105 @@ __global__ void __launch_bounds__(256, RPW <= 4 ? 3 : 1) k_spmm_win(const __grid
   }
 }
 
+// ------------------------------------------------------------------ two-hop staged diffusion
+// CTA = (512-byte column chunk, window R, job x group).  The window's two-hop row set U2 is staged
+// once (cp.async); hop 1 is computed for the U1 prefix into shared memory (rounded to bf16, as the
+// chain stores it; R's rows also go to Y1), then hop 2 for R reads those.  Each row's terms are
+// summed in CSR order with the same FFMA2 sequence as k_spmm_win: bit-identical to two launches.
+// The plan (node lists, local columns, values) is a step constant: staged before
+// griddepcontrol.wait, overlapping the previous kernel's tail.
+constexpr int kMaxW2Jobs = 4;
+struct Win2Params {
+  Win2Job job[kMaxW2Jobs];
+  int z_begin[kMaxW2Jobs + 1];
+  int nchunk[kMaxW2Jobs];
+  int vecs[kMaxW2Jobs];
+  int njobs, N, rows, max_nodes, max_n1, max_entries;
+};
+
+// acc += sum_{e in [e0, e1)} val[e] * rows[col[e]] in entry order, four staged rows in flight
+__device__ __forceinline__ void row_terms(float2 *acc, const uint4 *rows, const uint16_t *col,
+                                          const float *val, int e0, int e1, int lane) {
+  using L = Lane<__nv_bfloat16>;
+  int e = e0;
+  for (; e + 4 <= e1; e += 4) {
+    const uint4 v0 = rows[col[e] * 32 + lane], v1 = rows[col[e + 1] * 32 + lane],
+                v2 = rows[col[e + 2] * 32 + lane], v3 = rows[col[e + 3] * 32 + lane];
+    L::fma_v(acc, val[e], v0);
+    L::fma_v(acc, val[e + 1], v1);
+    L::fma_v(acc, val[e + 2], v2);
+    L::fma_v(acc, val[e + 3], v3);
+  }
+  for (; e < e1; ++e) L::fma_v(acc, val[e], rows[col[e] * 32 + lane]);
+}
+
+template <bool EPI>
+__global__ void __launch_bounds__(256) k_spmm_win2(const __grid_constant__ Win2Params p) {
+  using L = Lane<__nv_bfloat16>;
+  extern __shared__ uint4 sm2[];
+  griddep_launch_dependents();
+  const int z = int(blockIdx.z);
+  int j = 0;
+#pragma unroll
+  for (int q = 1; q < kMaxW2Jobs; ++q)
+    if (q < p.njobs && z >= p.z_begin[q]) j = q;
+  const int chunk = int(blockIdx.x);
+  if (chunk >= p.nchunk[j]) return;
+  const Win2Job &jb = p.job[j];
+  uint4 *stage = sm2;                                        // [max_nodes][32]
+  uint4 *h1 = stage + p.max_nodes * 32;                      // [max_n1][32]
+  float *s_val = reinterpret_cast<float *>(h1 + p.max_n1 * 32);
+  int *s_off = reinterpret_cast<int *>(s_val + p.max_entries);
+  int *s_nodes = s_off + p.max_n1 + 1;
+  uint16_t *s_col = reinterpret_cast<uint16_t *>(s_nodes + p.max_nodes);
+  const int win = int(blockIdx.y), tid = int(threadIdx.x);
+  const int nb = __ldg(jb.ptr + win), nn = __ldg(jb.ptr + win + 1) - nb;
+  const int u1 = __ldg(jb.n1 + win);
+  const int eb = __ldg(jb.eptr + win), ne = __ldg(jb.eptr + win + 1) - eb;
+  for (int i = tid; i < nn; i += 256) s_nodes[i] = __ldg(jb.nodes + nb + i);
+  for (int i = tid; i <= u1; i += 256) s_off[i] = __ldg(jb.roff + nb + win + i);
+  for (int i = tid; i < ne; i += 256)
+    s_col[i] = __ldg(jb.lcol + eb + i), s_val[i] = __ldg(jb.val + __ldg(jb.eidx + eb + i));
+  griddep_wait();
+  __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31;
+  const int vec = chunk * 32 + lane;
+  const bool act = vec < p.vecs[j];
+  const int64_t W = jb.W, goff = int64_t(z - p.z_begin[j]) * jb.gstride;
+  const __nv_bfloat16 *X = static_cast<const __nv_bfloat16 *>(jb.X) + goff + int64_t(vec) * 8;
+  if (act)
+    for (int k = warp; k < nn; k += 8) cp_async16(stage + k * 32 + lane, X + int64_t(s_nodes[k]) * W);
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  const int row0 = win * p.rows, nrows = min(p.rows, p.N - row0);
+  for (int i = warp; i < u1; i += 8) {  // hop 1 over U1 (R first)
+    float2 acc[4] = {};
+    row_terms(acc, stage, s_col, s_val, s_off[i], s_off[i + 1], lane);
+    L::store(reinterpret_cast<__nv_bfloat16 *>(h1 + i * 32 + lane), acc);
+    if (act && i < nrows)
+      L::store(static_cast<__nv_bfloat16 *>(jb.Y1) + goff + int64_t(row0 + i) * W + int64_t(vec) * 8,
+               acc);
+  }
+  __syncthreads();
+  for (int r = warp; r < nrows; r += 8) {  // hop 2 over R from the hop-1 rows
+    float2 acc[4] = {};
+    row_terms(acc, h1, s_col, s_val, s_off[r], s_off[r + 1], lane);
+    if (!act) continue;
+    const int64_t o = goff + int64_t(row0 + r) * W + int64_t(vec) * 8;
+    if (EPI) {  // as finish<.., true>: alpha scaling, then beta * add
+      const float2 a = make_float2(jb.alpha, jb.alpha);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = __fmul2_rn(a, acc[q]);
+      const __nv_bfloat16 *ad = static_cast<const __nv_bfloat16 *>(jb.add) + o;
+      if (jb.beta == 1.f)
+        L::add(acc, ad);
+      else
+        L::axpy(acc, jb.beta, ad);
+    }
+    L::store(static_cast<__nv_bfloat16 *>(jb.Y2) + o, acc);
+  }
+}
+
 // ------------------------------------------------------------------ resident small-graph diffusion
 constexpr int kResThreads = 512, kResMaxSmem = 200 * 1024;
 
@@ -489,6 +588,48 @@ cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s) {
     return gen ? pdl_launch(k_spmm<float, true>, dim3(blocks), dim3(256), 0, s, p)
                : pdl_launch(k_spmm<float, false>, dim3(blocks), dim3(256), 0, s, p);
   return pdl_launch(k_spmm_scalar, dim3(blocks), dim3(256), 0, s, p);
+}
+
+cudaError_t launch_spmm_win2(const Win2Job *jobs, int njobs, int N, const Win2Plan &plan,
+                             cudaStream_t s) {
+  if (njobs < 1 || njobs > kMaxW2Jobs || plan.rows < 1) return cudaErrorInvalidValue;
+  const size_t smem = size_t(plan.max_nodes + plan.max_n1) * 512 + size_t(plan.max_entries) * 6 +
+                      size_t(plan.max_n1 + 1 + plan.max_nodes) * 4 + 16;
+  if (smem > size_t(kWinMaxSmem)) return cudaErrorNotSupported;
+  Win2Params w{};
+  w.njobs = njobs, w.N = N, w.rows = plan.rows, w.max_nodes = plan.max_nodes;
+  w.max_n1 = plan.max_n1, w.max_entries = plan.max_entries;
+  int nz = 0, maxc = 0;
+  bool epi = false;
+  double bytes = 0.0, flops = 0.0;
+  for (int i = 0; i < njobs; ++i) {
+    const Win2Job &j = jobs[i];
+    if (j.W % 8 || !j.X || !j.Y1 || !j.Y2 || j.G < 1) return cudaErrorInvalidValue;
+    w.job[i] = j;
+    w.vecs[i] = int(j.W / 8);
+    w.nchunk[i] = int(ceil_div(w.vecs[i], 32));
+    w.z_begin[i] = nz;
+    nz += j.G;
+    maxc = std::max(maxc, w.nchunk[i]);
+    epi = epi || j.add;
+    // algorithmic bytes: X read once, Y1 and Y2 written once, the addend read once, the CSR
+    // once; flops: both hops over the graph (the recomputed U1 \ R rows are overhead, not work)
+    const double nw = double(N) * double(j.W) * 2.0 * j.G;
+    bytes += nw * (3 + (j.add ? 1 : 0)) + (double(j.nnz) * 8.0 + double(N + 1) * 4.0) * j.G;
+    flops += 4.0 * double(j.nnz) * double(j.W) * j.G;
+  }
+  w.z_begin[njobs] = nz;
+  const int nwin = int(ceil_div(N, plan.rows));
+  if (nz > 65535 || nwin > 65535) return cudaErrorNotSupported;
+  ProfScope prof(kProfSpmm, s, bytes, flops);
+  const dim3 grid{unsigned(maxc), unsigned(nwin), unsigned(nz)};
+  auto go = [&](auto kernel) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem));
+    if (e != cudaSuccess) return e;
+    return pdl_launch(kernel, grid, dim3(256), int(smem), s, w);
+  };
+  return epi ? go(k_spmm_win2<true>) : go(k_spmm_win2<false>);
 }
 
 bool spmm_resident_fits(int N, int K, int64_t W) {

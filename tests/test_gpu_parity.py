@@ -243,6 +243,32 @@ def test_step_staged_plan_bitexact_both_precisions(env):
             assert r[0] == res[0][0] and np.array_equal(r[1], res[0][1]), precision
 
 
+@pytest.mark.parametrize("name,B,rows,cheb", [("tc_tiny", 3, None, False), ("tc_big", 64, 32, False),
+                                               ("tc_l1", 5, 7, False), ("tc_tiny", 3, 5, True),
+                                               ("metr_la", 64, None, False),
+                                               ("metr_la", 16, 16, True)])
+def test_step_two_hop_plan_bitexact(env, name, B, rows, cheb):
+    """K = 2 bf16 diffusions in one launch from the two-hop staging plan (pgti_graph_windows2):
+    loss and every gradient bit-identical to the two-launch hop chain (powers and Chebyshev)."""
+    pgti, torch = env
+    cfg = (TC_CONFIGS.get(name) or synth.CONFIGS[name]).replace(B=B, K=2, cheb=cheb)
+    cfg = cfg.replace(name=f"{name}_k2_{int(cheb)}")  # ref_for caches by name
+    ref = ref_for(cfg)
+    s = load_series(pgti, torch, ref.v, 0, cfg, ref.mu, ref.sigma)
+    idx = torch.from_numpy(ref.plan(1, 0, epoch=0)[:cfg.B].astype(np.int32)).cuda()
+    ld = ld_of(cfg)
+    x = torch.empty(cfg.B * cfg.T_in * ld, device="cuda")
+    y = torch.empty(cfg.B * cfg.T_out * ld, device="cuda")
+    s.gather(idx, cfg.B, cfg.T_in, cfg.T_out, x, y)
+    theta = synth.make_params(cfg, kind="random")
+    res = []
+    for win2 in (True, False):
+        model = model_for(pgti, torch, cfg, ref.graph, precision=1, win_rows=rows, win2=win2)
+        assert (model.desc.win2_rows > 0) == win2
+        res.append(run_step(pgti, torch, model, theta, x, y, dump=False))
+    assert res[0][0] == res[1][0] and np.array_equal(res[0][1], res[1][1])
+
+
 # ------------------------------------------------------------------ full step (K1..K5)
 def _step_case(env, cfg, seed=0, B=None, scale=1.0):
     pgti, torch = env
