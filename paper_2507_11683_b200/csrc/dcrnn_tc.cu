@@ -32,13 +32,15 @@ struct StreamPool {
   size_t next = 0;
 };
 
-// One pool per (host thread, device): side streams for layers 1.., a ring of events.
-StreamPool *pool(int nside, cudaError_t *err) {
-  thread_local std::map<int, StreamPool> pools;
+// One pool per (host thread, device, caller stream): side streams for layers 1.., a ring of
+// events.  Steps issued on different caller streams get different side streams, so they stay
+// independent (no false ordering between their layer chains, also under graph capture).
+StreamPool *pool(int nside, cudaStream_t caller, cudaError_t *err) {
+  thread_local std::map<std::pair<int, cudaStream_t>, StreamPool> pools;
   int dev = 0;
   *err = cudaGetDevice(&dev);
   if (*err != cudaSuccess) return nullptr;
-  StreamPool &p = pools[dev];
+  StreamPool &p = pools[{dev, caller}];
   while (int(p.side.size()) < nside) {
     cudaStream_t st;
     *err = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
@@ -153,7 +155,7 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
   unsigned *err = device_error_flag();
   PGTI_REQUIRE(err, PGTI_ERR_CUDA, "device error flag unavailable");
   cudaError_t perr = cudaSuccess;
-  StreamPool *sp = pool(L - 1, &perr);
+  StreamPool *sp = pool(L - 1, s, &perr);
   CU(perr);
   std::vector<cudaStream_t> st(L);
   st[0] = s;

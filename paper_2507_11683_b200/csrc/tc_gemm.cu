@@ -39,8 +39,11 @@ __device__ __forceinline__ Barriers *carve(uint8_t *smem) {
   return reinterpret_cast<Barriers *>(smem + NST * (A_BYTES + B_BYTES));
 }
 
+// Offset arithmetic on the shared-memory pointer itself (not an integer round trip), so the
+// compiler keeps the shared address space and emits STS/LDS instead of generic ST/LD.
 __device__ __forceinline__ uint8_t *align1024(uint8_t *p) {
-  return reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  return p + ((1024u - (a & 1023u)) & 1023u);
 }
 
 __device__ __forceinline__ void setup(Barriers *bar, uint32_t ncols) {
@@ -107,8 +110,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
   Barriers *bar = carve<A_BYTES, B_BYTES, kStages>(smem);
   float *wx_s = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(bar) + 256);  // [20][64]
   float *tile_s = reinterpret_cast<float *>(smem);                                  // [128][68]
-  float *xs_s = tile_s + kBM * kTileLd;                                             // [128][<=20]
-  static_assert(kStages * STAGE >= kBM * (kTileLd + 20) * 4, "x rows fit behind the tile");
+  float *xs_s = wx_s + 20 * 64;  // [128][<=20]: own region, filled while the MMAs run
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int row0 = blockIdx.x * kBM, ct0 = blockIdx.y * NSUB;
   griddep_launch_dependents();
@@ -182,6 +184,16 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
           }
         }
     }
+    // layer-0 x part while the MMAs run: the tile's 128 rows of the diffused input and the
+    // first sub-tile's weight rows (visible to every epilogue thread after phase 1's barrier)
+    for (int i = et; i < nx * 64; i += kEpiThreads) {
+      const int mf = i / 64, j = i % 64, m = mf / p.F, f = mf % p.F;
+      wx_s[i] = __ldg(p.Wx + int64_t(m * p.C_in + f) * p.Nout + ct0 * 64 + j);
+    }
+    for (int i = et; i < nx * kBM; i += kEpiThreads) {
+      const int rl = i / nx, mf = i - rl * nx, m = mf / p.F, f = mf - m * p.F;
+      xs_s[i] = row0 + rl < p.R ? __ldg(p.Dx + m * p.dx_mstride + int64_t(row0 + rl) * p.F + f) : 0.f;
+    }
     mbar_wait(&bar->tfull, 0);  // MMAs done => every stage buffer is free for the tile
     tc_fence_after();
 #pragma unroll 1
@@ -205,14 +217,10 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
 #pragma unroll
         for (int i = 0; i < 32; i += 4) st4(dst + i, make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]));
       }
-      for (int i = et; i < nx * 64; i += kEpiThreads) {  // x-part weight rows of this tile
-        const int mf = i / 64, j = i % 64, m = mf / p.F, f = mf % p.F;
-        wx_s[i] = __ldg(p.Wx + int64_t(m * p.C_in + f) * p.Nout + ct * 64 + j);
-      }
-      if (sub == 0)  // x-part row values of the tile's 128 rows (diffused layer-0 input)
-        for (int i = et; i < nx * kBM; i += kEpiThreads) {
-          const int rl = i / nx, mf = i - rl * nx, m = mf / p.F, f = mf - m * p.F;
-          xs_s[i] = row0 + rl < p.R ? __ldg(p.Dx + m * p.dx_mstride + int64_t(row0 + rl) * p.F + f) : 0.f;
+      if (sub > 0)  // x-part weight rows of this sub-tile
+        for (int i = et; i < nx * 64; i += kEpiThreads) {
+          const int mf = i / 64, j = i % 64, m = mf / p.F, f = mf % p.F;
+          wx_s[i] = __ldg(p.Wx + int64_t(m * p.C_in + f) * p.Nout + ct * 64 + j);
         }
       epi_bar();
       // ---- phase 2: coalesced element-wise epilogue: 16 threads per row, 4 columns each
@@ -438,7 +446,8 @@ cudaError_t set_smem(K kernel, int bytes) {
 
 constexpr int wg_smem_bytes(int b_rows) { return kStages * (kBM * kBK * 2 + b_rows * kBK * 2) + 1024 + 256; }
 constexpr int fwd_smem_bytes(int nsub) {
-  return fwd_stages(nsub) * (kBM * kBK * 2 + 64 * nsub * kBK * 2) + 1024 + 256 + 20 * 64 * 4;
+  return fwd_stages(nsub) * (kBM * kBK * 2 + 64 * nsub * kBK * 2) + 1024 + 256 + 20 * 64 * 4 +
+         kBM * 20 * 4;
 }
 
 }  // namespace
