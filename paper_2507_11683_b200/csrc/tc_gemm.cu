@@ -402,8 +402,17 @@ __global__ void k_tc_reduce(const float *__restrict__ partial, int nchunks, int 
   const int64_t n = int64_t(V) * Nout;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
+    // chunks summed in index order (bitwise reproducible); eight loads in flight per batch
     float s = 0.f;
-    for (int c = 0; c < nchunks; ++c) s += partial[int64_t(c) * n + i];
+    int c = 0;
+    for (; c + 8 <= nchunks; c += 8) {
+      float v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = __ldg(partial + int64_t(c + k) * n + i);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s += v[k];
+    }
+    for (; c < nchunks; ++c) s += __ldg(partial + int64_t(c) * n + i);
     const int v = int(i / Nout), j = int(i - int64_t(v) * Nout);
     const int m = v / vseg;
     out[int64_t(m * C_in + coff + (v - m * vseg)) * Nout + j] = s;
