@@ -190,3 +190,31 @@ def test_cheb_rejects_two_hop_operators(env):
     with pytest.raises(pgti.PgtiError) as e:  # the descriptor check runs before any launch
         m.step(buf(1 << 16), buf(1 << 16), buf(1 << 16), buf(1 << 16), buf(4), ws)
     assert e.value.name == "INVALID_ARG"
+
+
+def test_cheb_trainer_graph_zero_copy_first_loss(env):
+    """Trainer(cheb=True) on the bf16 path under CUDA-graph replay with zero-copy windows: the
+    first step's loss equals the oracle's Chebyshev loss on the same sampled windows (2e-2), and
+    zero-copy and gather give the same parameters after 3 steps (bitwise)."""
+    pgti, torch = env
+    from paper_2507_11683_b200.trainer import Trainer
+    cfg = TC["ch_tc_k2"]
+    ref = pipeline.Reference(cfg)
+    theta = synth.make_params(cfg, kind="random")
+    res = []
+    for zc in (False, True):
+        tr = Trainer(cfg, ref.graph, lambda a, b: ref.v[a:b], theta, precision=1,
+                     use_cuda_graph=True, zero_copy=zc)
+        assert tr.cheb and tr.model.desc.cheb == 1
+        tr.start_epoch(0)
+        tr.step(0)
+        idx = tr.epoch_plan()[:cfg.B].cpu().numpy()
+        xo, yo = ref.batch(idx)
+        want = dcgru.forward(theta.astype(np.float64), ref.d, ref.Pf, ref.Pb,
+                             xo.astype(np.float64), yo.astype(np.float64))["loss"]
+        assert abs(tr.loss.item() - want) <= 2e-2 * abs(want)
+        for j in (1, 2):
+            tr.step(j)
+        tr.check()
+        res.append(tr.params.cpu().numpy())
+    assert np.array_equal(res[0], res[1])
