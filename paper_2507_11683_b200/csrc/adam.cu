@@ -10,6 +10,8 @@ namespace {
 __global__ void k_adam(float4 *__restrict__ p, const float4 *__restrict__ g, float4 *__restrict__ m,
                        float4 *__restrict__ v, int64_t n4, int64_t step, const int64_t *dev_step,
                        float lr, float b1, float b2, float eps, float gs) {
+  pgti::griddep_launch_dependents();
+  pgti::griddep_wait();
   const int64_t t = dev_step ? *dev_step + 1 : step;
   // bias corrections in double, applied once per element in fp32
   const float bc1 = float(1.0 - pow(double(b1), double(t)));
@@ -71,11 +73,11 @@ extern "C" pgti_status pgti_adam_step(float *params, const float *grads, float *
                        (n4 > 0) + (int64_t(n) > n4 * 4) + (ds != nullptr));
   if (n4 > 0) {
     const int grid = int(std::min<int64_t>(pgti::ceil_div(n4, 256), 148 * 8));
-    k_adam<<<grid, 256, 0, s>>>(reinterpret_cast<float4 *>(params),
-                                reinterpret_cast<const float4 *>(grads),
-                                reinterpret_cast<float4 *>(m), reinterpret_cast<float4 *>(v), n4,
-                                step, ds, lr, beta1, beta2, eps, grad_scale);
-    PGTI_LAUNCH_TRY();
+    PGTI_CUDA_TRY(pgti::pdl_launch(k_adam, dim3(grid), dim3(256), 0, s,
+                                   reinterpret_cast<float4 *>(params),
+                                   reinterpret_cast<const float4 *>(grads),
+                                   reinterpret_cast<float4 *>(m), reinterpret_cast<float4 *>(v), n4,
+                                   step, ds, lr, beta1, beta2, eps, grad_scale));
   }
   if (int64_t(n) > n4 * 4) {
     k_adam_tail<<<1, 32, 0, s>>>(params, grads, m, v, n4 * 4, int64_t(n), step, ds, lr, beta1,

@@ -60,6 +60,8 @@ __global__ void k_dec_input(const __grid_constant__ WindowSrc ys, int tt, int B,
 __global__ void k_loss_partial(const float *__restrict__ yhat, const __grid_constant__ WindowSrc ys,
                                int T_out, int N, int B, int F, int F_out, int64_t ld,
                                float *__restrict__ dyhat, double *__restrict__ partials) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int64_t R = int64_t(N) * B, total = int64_t(T_out) * R * F_out;
   const float inv = float(1.0 / double(total));
   double acc = 0.0;
@@ -89,6 +91,8 @@ __global__ void k_loss_partial(const float *__restrict__ yhat, const __grid_cons
 
 __global__ void k_loss_final(const double *__restrict__ partials, int n, int64_t count,
                              float *__restrict__ loss, unsigned *__restrict__ err) {
+  griddep_launch_dependents();
+  griddep_wait();
   if (threadIdx.x != 0) return;
   double s = 0.0;
   for (int i = 0; i < n; ++i) s += partials[i];
@@ -281,6 +285,8 @@ __global__ void k_xpart_dgrad(const __nv_bfloat16 *__restrict__ grad,
     const int m = i / (F_out * NG), o = (i / NG) % F_out, j = i % NG;
     wsm[i] = W[int64_t(m * C_in + o) * NG + j];
   }
+  griddep_launch_dependents();
+  griddep_wait();  // the weights are step constants; the gradients come from the predecessor
   __syncthreads();
   for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < R;
        r += int64_t(gridDim.x) * blockDim.x) {
@@ -307,10 +313,9 @@ cudaError_t launch_xpart_dgrad(const void *grad, const void *Q, int64_t mstride,
   if (F_out > 4 || NG % 2) return cudaErrorInvalidValue;
   ProfScope prof(kProfElementwise, s, double(R) * (2.0 * M * NG + 8.0 * F_out), 2.0 * R * M * NG * F_out);
   const int smem = M * F_out * NG * 4;
-  k_xpart_dgrad<<<grid_for(R), kT, smem, s>>>(static_cast<const __nv_bfloat16 *>(grad),
-                                             static_cast<const __nv_bfloat16 *>(Q), mstride, M,
-                                             NG, W, C_in, F_out, R, out);
-  return cudaGetLastError();
+  return pdl_launch(k_xpart_dgrad, dim3(grid_for(R)), dim3(kT), smem, s,
+                    static_cast<const __nv_bfloat16 *>(grad), static_cast<const __nv_bfloat16 *>(Q),
+                    mstride, M, NG, W, C_in, F_out, R, out);
 }
 
 __global__ void k_bf16_to_f32(const __nv_bfloat16 *__restrict__ src, float *__restrict__ dst,
@@ -337,11 +342,11 @@ cudaError_t launch_loss(const float *yhat, const WindowSrc &y, int T_out, int N,
                         int F_out, int64_t ld, float *dyhat, double *partials, float *loss,
                         unsigned *err, cudaStream_t s) {
   ProfScope prof(kProfLoss, s, 12.0 * double(T_out) * N * B * F_out, 0.0, 2);
-  k_loss_partial<<<kLossBlocks, kT, 0, s>>>(yhat, y, T_out, N, B, F, F_out, ld, dyhat, partials);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = pdl_launch(k_loss_partial, dim3(kLossBlocks), dim3(kT), 0, s, yhat, y, T_out,
+                             N, B, F, F_out, ld, dyhat, partials);
   if (e != cudaSuccess) return e;
-  k_loss_final<<<1, 32, 0, s>>>(partials, kLossBlocks, int64_t(T_out) * N * B * F_out, loss, err);
-  return cudaGetLastError();
+  return pdl_launch(k_loss_final, dim3(1), dim3(32), 0, s, static_cast<const double *>(partials),
+                    kLossBlocks, int64_t(T_out) * N * B * F_out, loss, err);
 }
 
 cudaError_t launch_cand_bwd(int64_t RH, int H, const float *dHcur, const float *dHcur2,

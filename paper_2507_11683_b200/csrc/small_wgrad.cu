@@ -30,6 +30,8 @@ __global__ void __launch_bounds__(kThr) k_small_wgrad(const __grid_constant__ Sm
                                                       Plan q) {
   __shared__ float S[kTile][kSmallMax];
   __shared__ float red[kThr / 128][kSmallMax][129];
+  griddep_launch_dependents();
+  griddep_wait();
   const int chunk = blockIdx.x, t = chunk / q.cpt;
   const int r0 = (chunk - t * q.cpt) * q.RC, r1 = min(p.R, r0 + q.RC);
   const int j = threadIdx.x % 128, lg = threadIdx.x / 128;
@@ -79,6 +81,8 @@ __global__ void __launch_bounds__(kThr) k_small_wgrad_bf(const __grid_constant__
                                                          Plan q) {
   __shared__ float S[kTile][kSmallMax];
   __shared__ float2 red[kSmallMax][64];
+  griddep_launch_dependents();
+  griddep_wait();
   const int chunk = blockIdx.x, t = chunk / q.cpt;
   const int r0 = (chunk - t * q.cpt) * q.RC, r1 = min(p.R, r0 + q.RC);
   const int cpr = p.NG / 2, ng = kThr / cpr;
@@ -136,6 +140,8 @@ __global__ void __launch_bounds__(kThr) k_small_wgrad_bf(const __grid_constant__
 
 // One warp per output: lane l sums chunks l, l+32, ... (fixed order), then a fixed xor-tree.
 __global__ void k_small_reduce(const __grid_constant__ SmallWgrad p, Plan q) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int n = q.ns * q.ngt;
   const int lane = threadIdx.x & 31;
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
@@ -169,21 +175,21 @@ cudaError_t launch_small_wgrad(const SmallWgrad &p, cudaStream_t s) {
   if (q.ns > kSmallMax || q.ngt > 128 || p.NG > 128) return cudaErrorInvalidValue;
   if (p.Gb && (p.mode != kSmallBiasX || p.NG % 64)) return cudaErrorInvalidValue;
   if (int64_t(q.nchunks) * q.ns * q.ngt > p.partial_cap) return cudaErrorInvalidValue;
+  cudaError_t e;
   {
     const double tr = double(p.T) * p.R;
     ProfScope prof(kProfGemmWgrad, s, tr * ((p.Gb ? 2.0 : 4.0) * p.NG + 4.0 * q.ns),
                    2.0 * tr * q.ns * q.ngt);
     if (p.Gb)
-      k_small_wgrad_bf<<<unsigned(q.nchunks), kThr, 0, s>>>(p, q);
+      e = pdl_launch(k_small_wgrad_bf, dim3(unsigned(q.nchunks)), dim3(kThr), 0, s, p, q);
     else
-      k_small_wgrad<<<unsigned(q.nchunks), kThr, 0, s>>>(p, q);
+      e = pdl_launch(k_small_wgrad, dim3(unsigned(q.nchunks)), dim3(kThr), 0, s, p, q);
   }
-  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   ProfScope prof(kProfReduce, s, 4.0 * double(q.nchunks + 1) * q.ns * q.ngt,
                  double(q.nchunks) * q.ns * q.ngt);
-  k_small_reduce<<<unsigned(ceil_div(q.ns * q.ngt, 8)), 256, 0, s>>>(p, q);
-  return cudaGetLastError();
+  return pdl_launch(k_small_reduce, dim3(unsigned(ceil_div(q.ns * q.ngt, 8))), dim3(256), 0, s,
+                    p, q);
 }
 
 }  // namespace pgti

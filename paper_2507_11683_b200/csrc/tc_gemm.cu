@@ -334,8 +334,10 @@ __global__ void __launch_bounds__(kWgThreads, 1)
   const int rbeg = (chunk - t * chunks_per_t) * kWKC;
   const int rend = min(p.R, rbeg + kWKC);
   const int nst = (rend - rbeg + kBK - 1) / kBK;
+  griddep_launch_dependents();
   if (threadIdx.x == 0) tma_prefetch(&mA_in), tma_prefetch(&mA_h), tma_prefetch(&mG);
-  setup(bar, NOUT);
+  setup(bar, NOUT);  // barriers + TMEM while the predecessor drains
+  griddep_wait();    // every operand is a predecessor's output
   const uint32_t tmem = bar->tmem;
   if (warp == 0) {
     if (lane == 0)
@@ -399,6 +401,8 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 
 __global__ void k_tc_reduce(const float *__restrict__ partial, int nchunks, int V, int Nout,
                             int vseg, int coff, int C_in, float *__restrict__ out) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int64_t n = int64_t(V) * Nout;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
@@ -525,6 +529,7 @@ cudaError_t launch_tc_wgrad(const TcWgrad &p, cudaStream_t s) {
   if (int64_t(nchunks) * p.V * p.Nout > p.partial_cap) return cudaErrorInvalidValue;
   const dim3 grid(unsigned(ceil_div(p.V, kBM)), unsigned(nchunks));
   const int64_t n = int64_t(p.V) * p.Nout;
+  cudaError_t e;
   {
     const double TR = double(p.T) * p.R;
     ProfScope prof(kProfGemmWgrad, s, 2.0 * TR * p.V + 2.0 * TR * p.Nout + 4.0 * nchunks * n,
@@ -532,19 +537,20 @@ cudaError_t launch_tc_wgrad(const TcWgrad &p, cudaStream_t s) {
     if (p.Nout == 128) {
       static cudaError_t once = set_smem(k_tc_wgrad<128>, wg_smem_bytes(128));
       if (once != cudaSuccess) return once;
-      k_tc_wgrad<128><<<grid, kWgThreads, wg_smem_bytes(128), s>>>(ma_in, ma_h, mg, p, cpt);
+      e = pdl_launch(k_tc_wgrad<128>, grid, dim3(kWgThreads), wg_smem_bytes(128), s, ma_in, ma_h,
+                     mg, p, cpt);
     } else {
       static cudaError_t once = set_smem(k_tc_wgrad<64>, wg_smem_bytes(64));
       if (once != cudaSuccess) return once;
-      k_tc_wgrad<64><<<grid, kWgThreads, wg_smem_bytes(64), s>>>(ma_in, ma_h, mg, p, cpt);
+      e = pdl_launch(k_tc_wgrad<64>, grid, dim3(kWgThreads), wg_smem_bytes(64), s, ma_in, ma_h,
+                     mg, p, cpt);
     }
   }
-  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   ProfScope prof(kProfReduce, s, 4.0 * double(n) * (nchunks + 1), double(n) * nchunks);
-  k_tc_reduce<<<unsigned(std::min<int64_t>(ceil_div(n, 256), 1184)), 256, 0, s>>>(
-      p.partial, nchunks, p.V, p.Nout, p.vseg, p.coff, p.C_in, p.out);
-  return cudaGetLastError();
+  return pdl_launch(k_tc_reduce, dim3(unsigned(std::min<int64_t>(ceil_div(n, 256), 1184))),
+                    dim3(256), 0, s, static_cast<const float *>(p.partial), nchunks, p.V, p.Nout,
+                    p.vseg, p.coff, p.C_in, p.out);
 }
 
 }  // namespace pgti
