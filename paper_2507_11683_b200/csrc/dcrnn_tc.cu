@@ -74,8 +74,8 @@ cudaError_t record(StreamPool *p, cudaStream_t st, cudaEvent_t *out) {
 struct LayoutTC {
   size_t Dx, Dy, yhat, dyhat, lossp, total;
   std::vector<size_t> DHb, DrHb, H32, Rg, Ug, Cg, dGb, dCb, Wf_ru, Wf_c, Wd_ru, Wd_c;
-  std::vector<size_t> Q, wpart, dHrec0, dHrec1, dHup0, dHup1;
-  size_t wpart_floats;
+  std::vector<size_t> Q, wpart, spart, dHrec0, dHrec1, dHup0, dHup1;
+  size_t wpart_floats, spart_floats;
 };
 
 int nkb_total(const Dims &d, int l) { return l == 0 ? d.M : 2 * d.M; }
@@ -94,8 +94,10 @@ LayoutTC make_layout_tc(const Dims &d) {
   L.Dx = take(M * T * R * d.F * 4);
   L.Dy = take(d.model ? size_t(d.T_out) * M * R * d.F_out * 4 : 0);
   const int Tmax = std::max(d.T_in, d.model ? d.T_out : 0);
-  size_t wp = std::max(small_wgrad_partial_floats(Tmax, int(d.R), 2 * d.H),
-                       small_wgrad_partial_floats(d.T_out, int(d.R), d.H));
+  const size_t spf = std::max(small_wgrad_partial_floats(Tmax, int(d.R), 2 * d.H),
+                              small_wgrad_partial_floats(d.T_out, int(d.R), d.H));
+  L.spart_floats = spf;
+  size_t wp = spf;
   for (int l = 0; l < d.L; ++l)
     wp = std::max(wp, tc_wgrad_partial_floats(vrows(d, l), 2 * d.H, Tmax, int(d.R)));
   L.wpart_floats = wp;
@@ -118,6 +120,7 @@ LayoutTC make_layout_tc(const Dims &d) {
     // per-layer (= per-stream) scratch
     L.Q.push_back(take(M * R * 2 * H * 2));
     L.wpart.push_back(take(wp * 4));
+    L.spart.push_back(take(spf * 4));  // the skinny reductions' own partials (aux stream)
     L.dHrec0.push_back(take(R * H * 4));
     L.dHrec1.push_back(take(R * H * 4));
     L.dHup0.push_back(take(R * H * 4));
@@ -155,7 +158,7 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
   unsigned *err = device_error_flag();
   PGTI_REQUIRE(err, PGTI_ERR_CUDA, "device error flag unavailable");
   cudaError_t perr = cudaSuccess;
-  StreamPool *sp = pool(L - 1, s, &perr);
+  StreamPool *sp = pool(2 * L - 1, s, &perr);  // L - 1 layer streams + L weight-gradient aux
   CU(perr);
   std::vector<cudaStream_t> st(L);
   st[0] = s;
@@ -367,6 +370,8 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
   for (int ll = 0; ll < L * (d.model ? 2 : 1); ++ll) {  // (encoder) stack, then the decoder
     const int l = ll % L, dec = ll >= L, t0 = dec ? T : 0, nt = dec ? d.T_out : T;
     cudaStream_t ss = st[l];  // layer l's backward is complete in stream order
+    cudaStream_t as = sp->side[L - 1 + l];
+    CU(depend(sp, ss, as));
     const int Fin = l > 0 ? d.H : (dec ? d.F_out : d.F), C = Fin + d.H;
     const int V = vrows(d, l), vseg = l == 0 ? 64 : 2 * d.H, coff = l == 0 ? Fin : 0;
     const bf16 *Ain = l == 0 ? nullptr : Bp(Ly.DHb[l - 1]) + t0 * MRH;
@@ -379,20 +384,22 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
     tw.A_h = Bp(Ly.DrHb[l]) + t0 * MRH, tw.h_toff = 0, tw.G = Bp(Ly.dCb[l]) + int64_t(t0) * RH;
     tw.Nout = d.H, tw.out = grads + P.Wc[ll];
     CU(launch_tc_wgrad(tw, ss));
-    // input rows of layer 0 (fp32 x part) and the bias rows: skinny reduction over nt*R rows
+    // input rows of layer 0 (fp32 x part) and the bias rows: skinny reduction over nt*R rows,
+    // on the layer's aux stream (own partials; disjoint output rows) next to the tcgen05 wgrads
     SmallWgrad sw{};
     sw.mode = kSmallBiasX, sw.T = nt, sw.R = int(R);
     if (l == 0 && !dec) sw.Dx = Dx, sw.dx_mstride = int64_t(T) * RF, sw.dx_tstride = RF;
     if (l == 0 && dec) sw.Dx = Dy, sw.dx_mstride = RFo, sw.dx_tstride = M * RFo;
     sw.M = d.M, sw.F = Fin, sw.C_in = C;
-    sw.partial = wpart, sw.partial_cap = int64_t(Ly.wpart_floats);
+    sw.partial = Fp(Ly.spart[l]), sw.partial_cap = int64_t(Ly.spart_floats);
     sw.Gb = Bp(Ly.dGb[l]) + int64_t(t0) * 2 * RH, sw.g_tstride = 2 * RH, sw.NG = 2 * d.H;
     sw.out = grads + P.Wru[ll];
-    CU(launch_small_wgrad(sw, ss));
+    CU(launch_small_wgrad(sw, as));
     sw.Gb = Bp(Ly.dCb[l]) + int64_t(t0) * RH, sw.g_tstride = RH, sw.NG = d.H;
     sw.out = grads + P.Wc[ll];
-    CU(launch_small_wgrad(sw, ss));
+    CU(launch_small_wgrad(sw, as));
   }
+  for (int l = 0; l < L; ++l) CU(depend(sp, sp->side[L - 1 + l], s));  // join the aux streams
   SmallWgrad rw{};
   rw.mode = kSmallReadout, rw.T = d.T_out, rw.R = int(R);
   rw.dy = Fp(Ly.dyhat), rw.F_out = d.F_out;
