@@ -399,16 +399,14 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
     sw.out = grads + P.Wc[ll];
     CU(launch_small_wgrad(sw, as));
   }
+  for (int l = 0; l < L; ++l) CU(depend(sp, sp->side[L - 1 + l], s));  // join the aux streams
   SmallWgrad rw{};
   rw.mode = kSmallReadout, rw.T = d.T_out, rw.R = int(R);
   rw.dy = Fp(Ly.dyhat), rw.F_out = d.F_out;
   rw.G = Fp(Ly.H32[L - 1]) + int64_t(TT - d.T_out) * RH, rw.g_tstride = RH, rw.NG = d.H;
-  rw.partial = Fp(Ly.spart[L - 1]), rw.partial_cap = int64_t(Ly.spart_floats);
+  rw.partial = Fp(Ly.wpart[L - 1]), rw.partial_cap = int64_t(Ly.wpart_floats);
   rw.out = grads + P.Wout;
-  // after the top layer's skinny reductions on its aux stream (same partials), off the layer
-  // stream's tcgen05 wgrads
-  CU(launch_small_wgrad(rw, sp->side[2 * L - 2]));
-  for (int l = 0; l < L; ++l) CU(depend(sp, sp->side[L - 1 + l], s));  // join the aux streams
+  CU(launch_small_wgrad(rw, top));
   for (int l = 1; l < L; ++l) CU(depend(sp, st[l], s));  // join
 
   if (act_dump) {
