@@ -386,6 +386,20 @@ def main():
             roof["traffic_source"] = f"profiles/traffic_{cfg.name}.json ({tj[tk]['source']})"
     roof["algorithmic_per_launch"] = {"bytes": d["bytes"] / d["launches"],
                                       "flops": d["flops"] / d["launches"]}
+    # the gate GEMMs against the tensor-core roofline (north star: "the gate GEMMs report
+    # tensor-pipe utilisation"): every tcgen05 GEMM class of the step, live event times
+    gemm_roof = None
+    gk = [k for k in ("gemm_fwd", "gemm_dgrad", "gemm_wgrad") if k in ours]
+    if gk and args.precision == 1:
+        gf = sum(ours[k]["flops"] for k in gk)
+        gms = sum(ours[k]["ms"] for k in gk)
+        pk = peaks.get("bf16_tflops_sustained") or peaks["bf16_tflops"]
+        ach = gf / (gms / 1e3) / 1e12
+        gemm_roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": pk, "unit": "TFLOP/s",
+                     "frac": round(ach / pk, 4), "kernels": gk,
+                     "per_class_tflops": {k: round(ours[k]["flops"] / (ours[k]["ms"] / 1e3) / 1e12,
+                                                   2) for k in gk},
+                     "share_of_step": round(gms / P / eager_ms, 4), "peak_source": src}
 
     # ---------------------------------------------------------------- end to end (host buffers)
     e2e = None
@@ -483,7 +497,7 @@ def main():
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps,
                 "launches_per_step": launches_per_step, "clocks": ck,
-                "step_roofline": step_roof,
+                "step_roofline": step_roof, "gemm_roofline": gemm_roof,
                 "kernels": kernels, "eager_ms_per_step": round(eager_ms, 4),
                 "loss_last": loss_last, "steps_per_epoch": spe}
         if epoch is not None:
