@@ -1,0 +1,121 @@
+"""Parity at BASELINE.json's full sizes (PeMS-All-LA and full PeMS, B = 64 per GPU, the bf16
+tcgen05 path with the library's default SpMM window plan -- the model bench.py's Trainer builds),
+on sampled outputs the oracle computes one by one and on properties that hold at any size.
+
+* The series buffer spans all E rows of the workload (full PeMS: 105,120 x 22,320 = 2.35e9
+  floats, past 2^31), and the sampled windows sit at its end, so the gather and the layer-0
+  reads use 64-bit offsets.  Only the last rows hold synthetic data (synth.make_series); the
+  rest are zeros that no window reads.
+* Per sample: the DCRNN forward of one window depends on that window only (PAPER.md P:164-166,
+  f applied per sample; P:297 batches are index lists), so the oracle's B = 1 forward of
+  sample b must equal the step's predictions and hidden states for b (2e-2 scale-relative,
+  BASELINE.json's bf16 bar).
+* Properties of the whole batch, from the step's own predictions:
+  loss = mean|yhat - y|; d loss / d b_out = sum sign(yhat - y) / count; d loss / d W_out =
+  sum H_top^T sign(yhat - y) / count over the T_out output steps (a5: yhat = H W_out + b_out).
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import dcgru, transitions, windows
+
+from gpu_util import ld_of, model_for, run_step, scale_rel
+
+pytestmark = pytest.mark.gpu
+
+TOL_BF16 = 2e-2
+TAIL_ROWS = 400  # rows of real data at the end of the series
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    from paper_2507_11683_b200 import build
+    build.build()
+    from paper_2507_11683_b200 import pgti
+    return pgti, torch
+
+
+@pytest.mark.parametrize("name", ["pems_all_la", "pems"])
+def test_step_fullsize_sampled(env, name):
+    pgti, torch = env
+    cfg = synth.CONFIGS[name]
+    B, TW = cfg.B, cfg.T_in + cfg.T_out
+    assert B == 64
+    N, F, H, L, T_in, T_out, F_out = cfg.N, cfg.F, cfg.H, cfg.L, cfg.T_in, cfg.T_out, cfg.F_out
+    ld = ld_of(cfg)
+    row_tail = cfg.E - TAIL_ROWS
+    v_tail = synth.make_series(cfg, row_lo=row_tail, row_hi=cfg.E)
+    mu, sigma = float(v_tail.mean(dtype=np.float64)), float(v_tail.std(dtype=np.float64))
+
+    # series: every row of the workload on the device, data in the tail
+    host = np.zeros((cfg.E, N, F), np.float32)
+    host[row_tail:] = v_tail
+    buf = torch.empty(cfg.E * ld, dtype=torch.float32, device="cuda")
+    s = pgti.Series(host, 0, N, F, buf, ld)
+    s.normalize(mu, sigma)
+    del host
+
+    rng = np.random.default_rng(2507)
+    idx_np = row_tail + rng.choice(TAIL_ROWS - TW + 1, size=B, replace=False)
+    idx_np[-1] = cfg.E - TW  # the last window reads the last row of the series
+    idx = torch.from_numpy(idx_np.astype(np.int32)).cuda()
+    x = torch.empty(B * T_in * ld, device="cuda")
+    y = torch.empty(B * T_out * ld, device="cuda")
+    s.gather(idx, B, T_in, T_out, x, y)
+
+    graph = synth.make_graph(N, cfg.knn)
+    model = model_for(pgti, torch, cfg, graph, precision=1)
+    theta = synth.make_params(cfg, seed=synth.SEED_PARAMS, kind="random")
+    n = model.num_params()
+    params = torch.from_numpy(theta).cuda()
+    grads = torch.full((n,), float("nan"), dtype=torch.float32, device="cuda")
+    loss = torch.zeros(1, dtype=torch.float32, device="cuda")
+    ws = torch.empty(model.workspace_bytes(), dtype=torch.uint8, device="cuda")
+    act = torch.empty(model.act_dump_floats(), dtype=torch.float32, device="cuda")
+    model.step(params, grads, x, y, loss, ws, act)
+    pgti.check_device_error()
+    del ws, x, buf
+    R = N * B
+    n1 = T_in * L * 4 * R * H
+    acts = act[:n1].view(T_in, L, 4, N, B, H)
+    yhat = act[n1:].view(T_out, N, B, F_out)
+    g = grads.cpu().numpy()
+    assert np.all(np.isfinite(g))
+
+    # oracle inputs: Alg. 1 windows of the host rows, standardised in fp32 (reading O4)
+    xo, yo = windows.materialize(v_tail, T_in, T_out, mu, sigma, starts=idx_np - row_tail)
+    Pf, Pb = transitions.transition_matrices(N, *graph)
+    d = dcgru.Dims.of(cfg)
+    theta64 = theta.astype(np.float64)
+
+    # ---- sampled samples through the oracle, one by one
+    for b in (0, 29, B - 1):
+        fwd = dcgru.forward(theta64, d, Pf, Pb, xo[b:b + 1].astype(np.float64))
+        e = scale_rel(yhat[:, :, b].cpu().numpy(), fwd["yhat"][0])
+        assert e <= TOL_BF16, (b, "yhat", e)
+        for t in (0, T_in - 1):
+            for l in range(L):
+                st = fwd["cache"][t][l]
+                for q, nm in enumerate("Hruc"):
+                    e = scale_rel(acts[t, l, q, :, b].cpu().numpy(), st[nm][0])
+                    assert e <= TOL_BF16, (b, t, l, nm, e)
+
+    # ---- whole-batch properties from the step's own predictions
+    y_dev = torch.from_numpy(np.ascontiguousarray(
+        yo[..., :F_out].transpose(1, 2, 0, 3))).cuda()  # [T_out][N][B][F_out] like yhat
+    diff = yhat - y_dev  # fp32, as the loss kernel forms it
+    count = B * T_out * N * F_out
+    loss_ref = float(diff.double().abs().sum().item()) / count
+    assert abs(float(loss.item()) - loss_ref) <= 1e-5 * loss_ref, (float(loss.item()), loss_ref)
+    sgn = torch.sign(diff).double()
+    db_ref = (sgn.sum(dim=(0, 1, 2)) / count).cpu().numpy()
+    top = acts[T_in - T_out:T_in, L - 1, 0].double()  # H of the top layer at the output steps
+    dW_ref = (torch.einsum("tnbh,tnbf->hf", top, sgn) / count).cpu().numpy()
+    db, dW = g[-F_out:], g[-F_out - H * F_out:-F_out].reshape(H, F_out)
+    assert np.max(np.abs(db - db_ref)) <= 1e-4, (db, db_ref)
+    assert scale_rel(dW, dW_ref) <= 1e-3, scale_rel(dW, dW_ref)
+    print(f"{name}: loss {float(loss.item()):.6f} ref {loss_ref:.6f}; db_out {db} ref {db_ref}; "
+          f"dW_out scale-rel {scale_rel(dW, dW_ref):.2e}")
