@@ -69,6 +69,11 @@ def test_step_fullsize_sampled(env, name):
     graph = synth.make_graph(N, cfg.knn)
     model = model_for(pgti, torch, cfg, graph, precision=1)
     theta = synth.make_params(cfg, seed=synth.SEED_PARAMS, kind="random")
+    # oracle inputs: Alg. 1 windows of the host rows, standardised in fp32 (reading O4)
+    xo, yo = windows.materialize(v_tail, T_in, T_out, mu, sigma, starts=idx_np - row_tail)
+    # b_out at the targets' mean, so sign(yhat - y) takes both values and the b_out / W_out
+    # properties below are not a constant sign
+    theta[-F_out:] = yo[..., :F_out].mean(axis=(0, 1, 2))
     n = model.num_params()
     params = torch.from_numpy(theta).cuda()
     grads = torch.full((n,), float("nan"), dtype=torch.float32, device="cuda")
@@ -85,23 +90,24 @@ def test_step_fullsize_sampled(env, name):
     g = grads.cpu().numpy()
     assert np.all(np.isfinite(g))
 
-    # oracle inputs: Alg. 1 windows of the host rows, standardised in fp32 (reading O4)
-    xo, yo = windows.materialize(v_tail, T_in, T_out, mu, sigma, starts=idx_np - row_tail)
     Pf, Pb = transitions.transition_matrices(N, *graph)
     d = dcgru.Dims.of(cfg)
     theta64 = theta.astype(np.float64)
 
     # ---- sampled samples through the oracle, one by one
+    worst = 0.0
     for b in (0, 29, B - 1):
         fwd = dcgru.forward(theta64, d, Pf, Pb, xo[b:b + 1].astype(np.float64))
         e = scale_rel(yhat[:, :, b].cpu().numpy(), fwd["yhat"][0])
         assert e <= TOL_BF16, (b, "yhat", e)
+        worst = max(worst, e)
         for t in (0, T_in - 1):
             for l in range(L):
                 st = fwd["cache"][t][l]
                 for q, nm in enumerate("Hruc"):
                     e = scale_rel(acts[t, l, q, :, b].cpu().numpy(), st[nm][0])
                     assert e <= TOL_BF16, (b, t, l, nm, e)
+                    worst = max(worst, e)
 
     # ---- whole-batch properties from the step's own predictions
     y_dev = torch.from_numpy(np.ascontiguousarray(
@@ -111,11 +117,16 @@ def test_step_fullsize_sampled(env, name):
     loss_ref = float(diff.double().abs().sum().item()) / count
     assert abs(float(loss.item()) - loss_ref) <= 1e-5 * loss_ref, (float(loss.item()), loss_ref)
     sgn = torch.sign(diff).double()
+    pos = float((sgn > 0).double().mean().item())
+    assert 0.1 < pos < 0.9, pos
     db_ref = (sgn.sum(dim=(0, 1, 2)) / count).cpu().numpy()
     top = acts[T_in - T_out:T_in, L - 1, 0].double()  # H of the top layer at the output steps
     dW_ref = (torch.einsum("tnbh,tnbf->hf", top, sgn) / count).cpu().numpy()
     db, dW = g[-F_out:], g[-F_out - H * F_out:-F_out].reshape(H, F_out)
-    assert np.max(np.abs(db - db_ref)) <= 1e-4, (db, db_ref)
+    # db_out is an fp32 sum of count = B*T_out*N*F_out terms +-1/count (8.6e6 at full PeMS):
+    # 1e-3 of its unit scale bounds that summation's rounding, far below a dropped or
+    # mis-signed term (>= 1/count per term, and a wrong sign flips the whole sum's share)
+    assert np.max(np.abs(db - db_ref)) <= 1e-3, (db, db_ref)
     assert scale_rel(dW, dW_ref) <= 1e-3, scale_rel(dW, dW_ref)
-    print(f"{name}: loss {float(loss.item()):.6f} ref {loss_ref:.6f}; db_out {db} ref {db_ref}; "
+    print(f"{name}: sampled worst scale-rel {worst:.2e}; sign(yhat-y)>0 {pos:.3f}; loss {float(loss.item()):.6f} ref {loss_ref:.6f}; db_out {db} ref {db_ref}; "
           f"dW_out scale-rel {scale_rel(dW, dW_ref):.2e}")
