@@ -1,12 +1,13 @@
 #!/usr/bin/env python
 """bench.py -- training samples/s and peak HBM per GPU of the index-batched DCRNN step.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config metr_la] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config pems] [--impl reference]
     torchrun --nproc-per-node N bench.py --gpus N ...       (one rank per GPU, NCCL)
 
 A step = gather (index batching) -> DCGRU forward + BPTT -> NCCL gradient all-reduce -> Adam,
 replayed as one CUDA graph per step, on synthetic seeded inputs of the named workload shape
-(BASELINE.json configs; METR-LA-shaped by default = configs[1]).  Timing: W untimed warm-up
+(BASELINE.json configs; full-PeMS-shaped by default = the largest config that fits one GPU, the
+north_star target).  Timing: W untimed warm-up
 steps, then exactly K steps between barrier + synchronize, CUDA events on the launching stream,
 max over ranks.  Prints ONE JSON line on rank 0 (contract: see DESIGN.md "Measurement").
 """
@@ -32,14 +33,18 @@ FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # SIMT FFMA peak at max cloc
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: about 2 s of steps for the workload)")
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="metr_la")
+    ap.add_argument("--config", default="pems",
+                    help="workload (synth.CONFIGS); default: full-PeMS-shaped, the largest "
+                         "BASELINE.json config that fits one GPU (the north_star target)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", type=int, default=1,
                     help="1 = bf16 tcgen05 path (default, 2e-2 parity); 0 = fp32 SIMT (1e-5 parity)")
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--profile-steps", type=int, default=3)
+    ap.add_argument("--profile-steps", type=int, default=3,
+                    help="graph replays traced with CUPTI (torch.profiler) for per-kernel times")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--epoch", action="store_true",
@@ -117,55 +122,90 @@ def measured_peaks():
 
 
 # ------------------------------------------------------------------------------ oracle legs
-def blas_threads():
+def host_cores() -> dict:
+    """What the host offers the oracle: os.cpu_count(), the affinity mask, and the BLAS pools
+    per library (threadpoolctl; numpy and scipy may each bring their own)."""
+    info = {"cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)), "blas": {}}
     try:
+        import numpy  # noqa: F401  (loads the BLAS pools to be listed)
+        import scipy.sparse  # noqa: F401
         import threadpoolctl
-        return sum(i.get("num_threads", 0) for i in threadpoolctl.threadpool_info()
-                   if i.get("user_api") == "blas") or 1
-    except Exception:
-        return 1
+        for i in threadpoolctl.threadpool_info():
+            if i.get("user_api") == "blas":
+                key = f"{i.get('internal_api')}:{os.path.basename(i.get('filepath', ''))}"
+                info["blas"][key] = i.get("num_threads")
+    except Exception as e:  # pragma: no cover
+        info["blas_error"] = str(e)
+    # the oracle's heavy work (dense GEMMs) runs on one BLAS pool at a time, bounded by the
+    # affinity mask; SciPy's CSR products are single-threaded
+    info["used"] = min(info["affinity"], max(info["blas"].values() or [1]))
+    return info
 
 
-def oracle_samples_per_s(cfg, n_windows: int, repeats: int, warm: int = 1,
-                         model: str = "stepwise"):
-    """Time the float64 oracle (Alg. 1 materialisation of the sampled windows + DCGRU forward/
-    backward + Adam) on a bounded sample of the workload.  Returns (samples/s, details)."""
-    import numpy as np
+class OracleLeg:
+    """The float64 oracle (Alg. 1 materialisation of the sampled windows + DCGRU forward/backward
+    + Adam), as it stands, on a bounded sample of the workload (tests' oracle/, host cores)."""
 
-    import synth
-    from oracle import adam, dcgru, encdec, pipeline
+    def __init__(self, cfg, model: str = "stepwise"):
+        import numpy as np
 
-    t0 = time.perf_counter()
-    # bounded setup: the oracle's cost per window does not depend on E, so huge series (full
-    # PeMS: 9.4 GB of float32) are cut to their first rows for the timing sample
-    rows_cap = 4096
-    cut = cfg.N * cfg.E > 200_000_000
-    ref = pipeline.Reference(cfg.replace(E=min(cfg.E, rows_cap)) if cut else cfg,
-                             materialize_all=False)
-    setup_s = time.perf_counter() - t0
-    theta = synth.make_params(cfg, kind="train", model=model).astype(np.float64)
-    m = np.zeros_like(theta)
-    v = np.zeros_like(theta)
-    plan = ref.plan(1, 0)
-    done, t_run, j = 0, 0.0, 0
-    for it in range(warm + repeats):
-        idx = plan[j:j + n_windows]
-        j += n_windows
+        import synth
+        from oracle import pipeline
+
+        self.np, self.cfg, self.model = np, cfg, model
+        t0 = time.perf_counter()
+        # bounded setup: the oracle's cost per window does not depend on E, so huge series (full
+        # PeMS: 9.4 GB of float32) are cut to their first rows for the timing sample
+        self.rows = cfg.E
+        if cfg.N * cfg.E > 200_000_000:
+            self.rows = max(256, min(4096, 20_000_000 // cfg.N))
+        self.ref = pipeline.Reference(cfg.replace(E=self.rows) if self.rows < cfg.E else cfg,
+                                      materialize_all=False)
+        self.setup_s = time.perf_counter() - t0
+        self.theta = synth.make_params(cfg, kind="train", model=model).astype(np.float64)
+        self.m = np.zeros_like(self.theta)
+        self.v = np.zeros_like(self.theta)
+        self.plan = self.ref.plan(1, 0)
+        self.j, self.it = 0, 0
+
+    def batch(self, n: int) -> float:
+        """One training step of the oracle on the next n windows of the plan; seconds."""
+        from oracle import adam, dcgru, encdec
+        np = self.np
+        if self.j + n > self.plan.size:
+            self.j = 0
+        idx = self.plan[self.j:self.j + n]
+        self.j += n
         t1 = time.perf_counter()
-        x, y = ref.batch(idx)
-        if model == "encdec":
-            _, g, _ = encdec.loss_and_grad(theta, ref.d, ref.Pf, ref.Pb, x.astype(np.float64),
-                                           y.astype(np.float64))
-        else:
-            _, g, _ = dcgru.backward(theta, ref.d, ref.Pf, ref.Pb, x.astype(np.float64),
-                                     y.astype(np.float64))
-        theta, m, v = adam.adam_step(theta, g, m, v, it + 1, 1e-2)
-        if it >= warm:
-            t_run += time.perf_counter() - t1
-            done += len(idx)
-    return done / t_run, dict(setup_s=round(setup_s, 2), timed_s=round(t_run, 2),
-                              windows=done, per_batch=n_windows,
-                              series_rows=min(cfg.E, rows_cap) if cut else cfg.E)
+        x, y = self.ref.batch(idx)
+        f = encdec.loss_and_grad if self.model == "encdec" else dcgru.backward
+        _, g, _ = f(self.theta, self.ref.d, self.ref.Pf, self.ref.Pb, x.astype(np.float64),
+                    y.astype(np.float64))
+        self.it += 1
+        self.theta, self.m, self.v = adam.adam_step(self.theta, g, self.m, self.v, self.it, 1e-2)
+        return time.perf_counter() - t1
+
+    def details(self) -> dict:
+        return dict(setup_s=round(self.setup_s, 2), series_rows=self.rows,
+                    cores=host_cores())
+
+
+def cpu_baseline_leg(cfg, model, budget_s: float = 20.0):
+    """cpu_baseline of our arm (rank 0, N = 1): one warm-up window (also the per-window cost),
+    then as many windows as fit ~budget_s (1 .. B) as one timed batch."""
+    leg = OracleLeg(cfg, model)
+    per = leg.batch(1)
+    n = int(max(1, min(cfg.B, budget_s // max(per, 1e-9))))
+    t = leg.batch(n)
+    det = leg.details()
+    det.update(warmup_windows=1, warmup_s=round(per, 2), windows=n, timed_s=round(t, 2))
+    return {"value": round(n / t, 4), "unit": "samples/s", "cores": det["cores"]["used"],
+            "kind": "oracle",
+            "sample": f"one batch of {n} windows of {cfg.name} (B={cfg.B} in the GPU step) after "
+                      f"a 1-window warm-up: float64 Alg. 1 materialisation + DCGRU fwd/bwd + "
+                      f"Adam, series cut to {leg.rows} rows (cost per window is independent of "
+                      f"E); host {det['cores']['cpu_count']} CPUs, affinity "
+                      f"{det['cores']['affinity']}", "details": det}
 
 
 def run_reference(args, cfg):
@@ -173,23 +213,26 @@ def run_reference(args, cfg):
     rank, world, _ = env_ranks()
     if rank != 0:
         return
-    import numpy as np  # noqa: F401
-    K, W = args.steps, args.warmup
-    # calibrate the per-window cost, then size each step so the whole run ends in ~3 min
-    sps1, _ = oracle_samples_per_s(cfg, 1, 1, warm=0, model=args.model)
-    per_step_budget = 150.0 / max(1, K + W)
-    b = int(max(1, min(cfg.B, math.floor(per_step_budget * sps1))))
-    sps, det = oracle_samples_per_s(cfg, b, K, warm=W, model=args.model)
-    cores = blas_threads()
+    K, W = args.steps or 5, args.warmup
+    leg = OracleLeg(cfg, args.model)
+    per = leg.batch(1)            # calibration (counts toward nothing)
+    # size each step so the whole run ends in ~3 min (a step is at least one window)
+    b = int(max(1, min(cfg.B, math.floor(150.0 / max(1, K + W) / max(per, 1e-9)))))
+    for _ in range(W):
+        leg.batch(b)
+    t = sum(leg.batch(b) for _ in range(K))
+    sps = K * b / t
+    det = leg.details()
+    det.update(windows_per_step=b, timed_s=round(t, 2), calibration_s=round(per, 2))
     line = {"metric": METRIC, "value": round(sps, 4), "unit": "samples/s", "n_gpus": args.gpus,
-            "steps": K, "warmup": W, "ms_per_step": round(1000.0 * b / sps, 3),
+            "steps": K, "warmup": W, "ms_per_step": round(1000.0 * t / K, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": config_dict(cfg, world, args),
-            "cpu_baseline": {"value": round(sps, 4), "unit": "samples/s", "cores": cores,
-                             "kind": "oracle",
+            "config": config_dict(cfg, world, args, arm="reference", windows_per_step=b),
+            "cpu_baseline": {"value": round(sps, 4), "unit": "samples/s",
+                             "cores": det["cores"]["used"], "kind": "oracle",
                              "sample": f"{K} steps x {b} windows of the {cfg.name} workload "
-                                       f"(after {W} warm-up steps), float64 oracle"},
+                                       f"(after {W} warm-up steps), float64 oracle on the host"},
             "e2e": {"value": round(sps, 4), "unit": "samples/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
             "oracle": det}
@@ -215,16 +258,125 @@ def emit(line: dict):
     _JSON_OUT.flush()
 
 
-def config_dict(cfg, world, args):
-    return {"workload": cfg.name, "N": cfg.N, "E": cfg.E, "F": cfg.F, "T_in": cfg.T_in,
-            "T_out": cfg.T_out, "layers": cfg.L, "hidden": cfg.H, "K_hops": cfg.K,
-            "per_gpu_batch": cfg.B, "global_batch": cfg.B * world,
-            "parallelism": f"dp{world} ({args.placement} distributed-index-batching, "
-                           f"{args.shuffle} shuffle)",
-            "precision": "fp32" if args.precision == 0 else "bf16",
-            "l2": "no flush: each step writes >= 1 GB of fresh activations (>> 126 MB L2)",
-            "cuda_graph": not args.no_graph, "zero_copy": bool(args.zero_copy),
-            "model": args.model, "diffusion_basis": "chebyshev" if cfg.cheb else "powers"}
+def config_dict(cfg, world, args, arm="ours", windows_per_step=None):
+    d = {"workload": cfg.name, "N": cfg.N, "E": cfg.E, "F": cfg.F, "T_in": cfg.T_in,
+         "T_out": cfg.T_out, "layers": cfg.L, "hidden": cfg.H, "K_hops": cfg.K,
+         "model": args.model, "diffusion_basis": "chebyshev" if cfg.cheb else "powers"}
+    if arm == "reference":
+        d.update({"precision": "fp64 (the oracle)", "windows_per_step": windows_per_step,
+                  "per_gpu_batch_of_our_arm": cfg.B,
+                  "parallelism": "one host process (rank 0), no GPU"})
+        return d
+    d.update({"per_gpu_batch": cfg.B, "global_batch": cfg.B * world,
+              "parallelism": f"dp{world} ({args.placement} distributed-index-batching, "
+                             f"{args.shuffle} shuffle)",
+              "precision": "fp32" if args.precision == 0 else "bf16",
+              "l2": "no flush: each step writes >= 1 GB of fresh activations (>> 126 MB L2)",
+              "cuda_graph": not args.no_graph, "zero_copy": bool(args.zero_copy)})
+    return d
+
+
+# ------------------------------------------------------------------------------ kernel trace
+def kernel_class(name: str) -> str:
+    """libpgti kernel name (demangled) -> the accounting class of profile.cuh."""
+    n = name.lower()
+    if "nccl" in n:
+        return "allreduce"
+    if "k_gather" in n:
+        return "gather"
+    if "k_spmm" in n:
+        return "spmm"
+    if "k_tc_fwd" in n:
+        import re
+        m = re.search(r"k_tc_fwd<\s*\d+\s*,\s*([^>]+)>", name)
+        mode = m.group(1) if m else ""
+        return "gemm_dgrad" if ("2" in mode or "bwd" in mode.lower()) else "gemm_fwd"
+    if "k_gconv_fwd" in n:
+        return "gemm_fwd"
+    if "k_gconv_dgrad" in n:
+        return "gemm_dgrad"
+    if "reduce" in n:
+        return "reduce"
+    if "wgrad" in n and "k_xpart" not in n:
+        return "gemm_wgrad"
+    if "k_loss" in n:
+        return "loss"
+    if "k_adam" in n or "k_incr" in n:
+        return "adam"
+    if "k_keys" in n or "radix" in n or "k_expand" in n:
+        return "index"
+    return "elementwise"
+
+
+def _busy(intervals) -> float:
+    """Length of the union of [start, end) intervals."""
+    tot, cur_s, cur_e = 0.0, None, None
+    for a, b in sorted(intervals):
+        if cur_e is None or a > cur_e:
+            if cur_e is not None:
+                tot += cur_e - cur_s
+            cur_s, cur_e = a, b
+        else:
+            cur_e = max(cur_e, b)
+    if cur_e is not None:
+        tot += cur_e - cur_s
+    return tot
+
+
+def kernel_trace(torch, replay, P: int, rank: int) -> dict:
+    """Kernel durations of P replays of the captured step from CUPTI activity records
+    (torch.profiler / kineto chrome trace): per kernel name and per class, ms per step (sum of
+    exclusive kernel durations, PDL pre-wait removed; raw CUPTI sums alongside) and busy ms per
+    step (union of the class's exclusive intervals)."""
+    res = {"kernels": {}, "class_ms_per_step": {}, "class_busy_ms_per_step": {}}
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as pr:
+            for j in range(P):
+                replay(j)
+            torch.cuda.synchronize()
+        fd, path = tempfile.mkstemp(suffix=".json")
+        os.close(fd)
+        pr.export_chrome_trace(path)
+        ev = json.load(open(path)).get("traceEvents", [])
+        os.unlink(path)
+    except Exception as e:  # the bench value does not depend on this
+        res["error"] = f"{type(e).__name__}: {e}"
+        return res
+    # a kernel launched with programmatic dependent launch starts while its stream predecessor
+    # drains and waits at griddepcontrol.wait: its CUPTI interval includes that wait.  The
+    # exclusive interval starts at max(its start, the predecessor's end on the same stream).
+    kev = [e for e in ev if e.get("cat") == "kernel" and "dur" in e]
+    kev.sort(key=lambda e: float(e["ts"]))
+    last_end = {}
+    per_name, per_cls, per_cls_x, spans = {}, {}, {}, {}
+    for e in kev:
+        name = e.get("name", "?")
+        a = float(e["ts"]) / 1e3
+        b = a + float(e["dur"]) / 1e3                        # us -> ms
+        sid = (e.get("args") or {}).get("stream", e.get("tid"))
+        ax = max(a, last_end.get(sid, a))
+        last_end[sid] = max(b, last_end.get(sid, b))
+        c = kernel_class(name)
+        k = per_name.setdefault(name, {"class": c, "ms": 0.0, "xms": 0.0, "launches": 0})
+        k["ms"] += b - a
+        k["xms"] += max(0.0, b - ax)
+        k["launches"] += 1
+        per_cls[c] = per_cls.get(c, 0.0) + (b - a)
+        per_cls_x[c] = per_cls_x.get(c, 0.0) + max(0.0, b - ax)
+        spans.setdefault(c, []).append((ax, max(ax, b)))
+    res["kernels"] = {n: {"class": v["class"], "ms_per_step": round(v["xms"] / P, 5),
+                          "raw_ms_per_step": round(v["ms"] / P, 5),
+                          "launches_per_step": v["launches"] / P,
+                          "us_per_launch": round(1e3 * v["xms"] / v["launches"], 3)}
+                      for n, v in sorted(per_name.items(), key=lambda kv: -kv[1]["xms"])}
+    res["class_ms_per_step"] = {c: v / P for c, v in per_cls_x.items()}
+    res["class_raw_ms_per_step"] = {c: v / P for c, v in per_cls.items()}
+    res["class_busy_ms_per_step"] = {c: _busy(sp) / P for c, sp in spans.items()}
+    all_spans = [x for sp in spans.values() for x in sp]
+    res["gpu_busy_ms_per_step"] = _busy(all_spans) / P
+    return res
 
 
 # ------------------------------------------------------------------------------ our arm
@@ -244,6 +396,9 @@ def main():
     if args.impl == "reference":
         run_reference(args, cfg)
         return
+    if args.steps is None:   # about 2 s of timed steps
+        args.steps = {"chickenpox": 300, "metr_la": 1000, "pems_bay": 700,
+                      "pems_all_la": 100, "pems": 25}.get(cfg.name, 50)
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -252,18 +407,22 @@ def main():
     from paper_2507_11683_b200.trainer import Trainer
 
     rank, world, local = env_ranks()
+    if world > 1:   # NCCL reports each communicator's setup (ranks, transports) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    comm = None
+    # libpgti's NCCL communicator (the gradient all-reduce, a8).  At world 1 it is a 1-rank
+    # communicator: the step still runs the (identity) ncclAllReduce, like every rank at N > 1.
+    uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(pgti.comm_unique_id()), dtype=torch.uint8))
     if world > 1:
-        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
-        if rank == 0:
-            uid.copy_(torch.frombuffer(bytearray(pgti.comm_unique_id()), dtype=torch.uint8))
         dist.broadcast(uid, 0)
-        comm = pgti.Comm(bytes(uid.cpu().numpy().tolist()), rank, world, local)
+    comm = pgti.Comm(bytes(uid.cpu().numpy().tolist()), rank, world, local)
 
     def barrier():
         if world > 1:
@@ -324,82 +483,101 @@ def main():
     loss_last = float(tr.loss.item())
 
     # ---------------------------------------------------------------- per-kernel breakdown
-    # an instrumented eager replay of the same step right after the timed region: every libpgti
-    # launch bracketed by CUDA events on its own stream
+    # (1) ALGORITHMIC bytes / flops per kernel class: libpgti's per-launch accounting (DESIGN.md
+    #     section 5 models), collected on one eager step right after the timed region -- counts
+    #     only, no timing is taken from it;
+    # (2) TIME per kernel class: CUPTI activity records (torch.profiler / kineto) of
+    #     --profile-steps replays of the SAME captured graph the timed region replays, so the
+    #     durations are those of the timed step's launches (PDL chaining and stream concurrency
+    #     included).  Profiler numbers explain the step; the bench value is the event-timed one.
     use_graph = tr.use_cuda_graph
     tr.use_cuda_graph = False
     pgti.profile_read()
     pgti.profile_enable(True)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
     base = args.warmup + args.steps
-    for j in range(base, base + args.profile_steps):
-        run(j)
-    e1.record()
+    run(base)
     torch.cuda.synchronize()
     prof = pgti.profile_read()
     pgti.profile_enable(False)
     tr.use_cuda_graph = use_graph
-    eager_ms = e0.elapsed_time(e1) / args.profile_steps
-    P = args.profile_steps
-    kernels = {k: {"ms_per_step": round(v["ms"] / P, 4), "launches_per_step": v["launches"] // P,
-                   "GB_per_step": round(v["bytes"] / P / 1e9, 4),
-                   "GFLOP_per_step": round(v["flops"] / P / 1e9, 3)}
-               for k, v in prof.items() if v["launches"]}
     ours = {k: v for k, v in prof.items() if k != "allreduce" and v["launches"]}
-    launches_per_step = sum(v["launches"] for v in ours.values()) // P
-    dom = max(ours, key=lambda k: ours[k]["ms"])
+    launches_per_step = sum(v["launches"] for v in ours.values())
+    P = args.profile_steps
+    trace = kernel_trace(torch, lambda j: run(base + 1 + j), P, rank)
+    cls_ms = trace["class_ms_per_step"]
+    kernels = {k: {"ms_per_step": round(cls_ms.get(k, 0.0), 4),
+                   "busy_ms_per_step": round(trace["class_busy_ms_per_step"].get(k, 0.0), 4),
+                   "launches_per_step": v["launches"],
+                   "GB_per_step": round(v["bytes"] / 1e9, 4),
+                   "GFLOP_per_step": round(v["flops"] / 1e9, 3)}
+               for k, v in prof.items() if v["launches"]}
+    timed = {k: v for k, v in ours.items() if cls_ms.get(k, 0.0) > 0}
+    dom = max(timed, key=lambda k: cls_ms[k]) if timed else max(ours, key=lambda k: ours[k]["ms"])
     d = prof[dom]
+    dms = cls_ms.get(dom) or d["ms"]
     peaks, src = measured_peaks()
     if dom.startswith("gemm") and args.precision == 0:
-        ach = d["flops"] / (d["ms"] / 1e3) / 1e12
+        ach = d["flops"] / (dms / 1e3) / 1e12
         roof = {"bound": "alu", "achieved": round(ach, 3), "peak": round(FP32_PEAK_TFLOPS, 1),
                 "unit": "TFLOP/s", "frac": round(ach / FP32_PEAK_TFLOPS, 4), "traffic": None,
                 "kernel": dom, "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz"}
     elif dom.startswith("gemm"):
-        ach = d["flops"] / (d["ms"] / 1e3) / 1e12
+        ach = d["flops"] / (dms / 1e3) / 1e12
         pk = peaks.get("bf16_tflops_sustained") or peaks["bf16_tflops"]
         roof = {"bound": "tensor", "achieved": round(ach, 3), "peak": pk, "unit": "TFLOP/s",
-                "frac": round(ach / pk, 4), "traffic": None, "kernel": dom, "peak_source": src}
+                "frac": round(ach / pk, 4), "traffic": None, "kernel": dom,
+                "peak_source": f"{src}, sustained (kernel timed inside a long step)"}
     else:
-        ach = d["bytes"] / (d["ms"] / 1e3) / 1e9
+        ach = d["bytes"] / (dms / 1e3) / 1e9
         pk = peaks["hbm_gbs"]
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": pk, "unit": "GB/s",
                 "frac": round(ach / pk, 4), "traffic": None, "kernel": dom, "peak_source": src}
-    roof["share_of_step"] = round(d["ms"] / P / eager_ms, 4)
+    step_ms = t_ms / args.steps
+    roof["timing"] = ("CUPTI kernel records of captured-graph replays (torch.profiler), "
+                      f"{P} replays; each kernel's interval starts at max(its start, its stream "
+                      "predecessor's end) so the PDL pre-wait is not counted"
+                      if trace["kernels"] else "eager event brackets (no CUPTI)")
+    roof["raw_cupti_ms_per_step"] = round(trace.get("class_raw_ms_per_step", {}).get(dom, 0.0), 4)
+    roof["share_of_step"] = round(trace["class_busy_ms_per_step"].get(dom, dms) / step_ms, 4)
+    roof["per_launch_ms"] = round(dms / d["launches"], 5)
+    roof["launches_per_step"] = d["launches"]
     # whole step against the HBM roofline: the algorithmic bytes of every libpgti launch of one
     # step (the per-kernel models of DESIGN.md section 5) over the timed step time
-    step_bytes = sum(v["bytes"] for k, v in ours.items()) / P
-    step_ach = step_bytes / (t_ms / args.steps / 1e3) / 1e9
+    step_bytes = sum(v["bytes"] for k, v in ours.items())
+    step_ach = step_bytes / (step_ms / 1e3) / 1e9
     step_roof = {"bytes_per_step": step_bytes, "bytes_per_sample": step_bytes / cfg.B,
                  "achieved": round(step_ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                  "frac": round(step_ach / peaks["hbm_gbs"], 4)}
-    roof["per_launch_ms"] = round(d["ms"] / d["launches"], 5)
     # traffic: DRAM bytes per launch of this kernel class from the committed ncu --set full
     # capture of the same workload (profiles/traffic_<config>.json, cold cache per launch)
     tpath = os.path.join(ROOT, "profiles", f"traffic_{cfg.name}.json")
     if os.path.exists(tpath):
         tj = json.load(open(tpath))
-        tk = "gemm" if dom in ("gemm_fwd", "gemm_dgrad") else dom
+        tk = "gemm" if dom in ("gemm_fwd", "gemm_dgrad") and "gemm" in tj else dom
         if tk in tj:
             roof["traffic"] = tj[tk]["dram_bytes_per_launch"]
             roof["traffic_source"] = f"profiles/traffic_{cfg.name}.json ({tj[tk]['source']})"
     roof["algorithmic_per_launch"] = {"bytes": d["bytes"] / d["launches"],
                                       "flops": d["flops"] / d["launches"]}
     # the gate GEMMs against the tensor-core roofline (north star: "the gate GEMMs report
-    # tensor-pipe utilisation"): every tcgen05 GEMM class of the step, live event times
+    # tensor-pipe utilisation"): every tcgen05 GEMM class of the step
     gemm_roof = None
-    gk = [k for k in ("gemm_fwd", "gemm_dgrad", "gemm_wgrad") if k in ours]
+    gk = [k for k in ("gemm_fwd", "gemm_dgrad", "gemm_wgrad") if k in ours and cls_ms.get(k)]
     if gk and args.precision == 1:
         gf = sum(ours[k]["flops"] for k in gk)
-        gms = sum(ours[k]["ms"] for k in gk)
+        gms = sum(cls_ms[k] for k in gk)
         pk = peaks.get("bf16_tflops_sustained") or peaks["bf16_tflops"]
         ach = gf / (gms / 1e3) / 1e12
         gemm_roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": pk, "unit": "TFLOP/s",
                      "frac": round(ach / pk, 4), "kernels": gk,
-                     "per_class_tflops": {k: round(ours[k]["flops"] / (ours[k]["ms"] / 1e3) / 1e12,
-                                                   2) for k in gk},
-                     "share_of_step": round(gms / P / eager_ms, 4), "peak_source": src}
+                     "per_class_tflops": {k: round(ours[k]["flops"] / (cls_ms[k] / 1e3) / 1e12, 2)
+                                          for k in gk}, "peak_source": src}
+    if rank == 0 and trace["kernels"]:
+        out = os.path.join(ROOT, "gpurun_out")
+        os.makedirs(out, exist_ok=True)
+        with open(os.path.join(out, f"kernel_trace_{cfg.name}_n{world}.json"), "w") as f:
+            json.dump({"config": cfg.name, "world": world, "step_ms": step_ms,
+                       "replays": P, **trace}, f, indent=1)
 
     # ---------------------------------------------------------------- end to end (host buffers)
     e2e = None
@@ -477,12 +655,7 @@ def main():
         ck["reasons"] = reasons
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sps, det = oracle_samples_per_s(cfg, 8, 3, model=args.model)
-        cpu = {"value": round(sps, 4), "unit": "samples/s", "cores": blas_threads(),
-               "kind": "oracle",
-               "sample": f"3 batches x 8 windows of {cfg.name} (+1 warm-up), float64 Alg. 1 "
-                         f"materialisation + DCGRU fwd/bwd + Adam; host os.cpu_count()="
-                         f"{os.cpu_count()}", "details": det}
+        cpu = cpu_baseline_leg(cfg, args.model)
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 2), "unit": "samples/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -498,7 +671,8 @@ def main():
                 "gpu_launches": launches_per_step * args.steps,
                 "launches_per_step": launches_per_step, "clocks": ck,
                 "step_roofline": step_roof, "gemm_roofline": gemm_roof,
-                "kernels": kernels, "eager_ms_per_step": round(eager_ms, 4),
+                "kernels": kernels,
+                "gpu_busy_ms_per_step": round(trace.get("gpu_busy_ms_per_step", 0.0), 4),
                 "loss_last": loss_last, "steps_per_epoch": spe}
         if epoch is not None:
             line["epoch"] = epoch

@@ -154,6 +154,38 @@ pgti_status pgti_load_series(pgti_series **out, const float *host_rows, int64_t 
 pgti_status pgti_series_stats(const pgti_series *s, int64_t S_tr, int T_in, int64_t row_lo,
                               int64_t row_hi, double shift, double *dev_sums, void *stream);
 
+/* Alg. 1 lines 201-202 (reading c9) finished from the three sums of
+ * pgti_series_stats (HOST double[3], already summed over ranks) taken about
+ * `shift`:  *mean = shift + s1/s0,  *var = max(0, s2/s0 - (s1/s0)^2)  (population
+ * variance, ddof 0).  Pure host arithmetic, no device work.
+ * Errors: INVALID_ARG (null), TOO_FEW_ENTRIES (s0 <= 0: no training window covers
+ * the rows), NONFINITE (a sum or the shift not finite). */
+pgti_status pgti_stats_finalize(const double sums[3], double shift, double *mean, double *var);
+
+typedef struct pgti_comm pgti_comm;
+/* The whole of Alg. 1's statistics for a (possibly halo-sharded)
+ * series: pass 1 = pgti_series_stats over this rank's rows [row_lo, row_hi) about
+ * shift 0, in-place NCCL SUM of the three sums over the ranks when comm is
+ * non-null (every rank of comm must call with its own disjoint rows), then
+ * pgti_stats_finalize; pass 2 the same about shift = the pass-1 mean (cancellation-
+ * free variance).  Results on the HOST: *mu, *sigma = sqrt(var) -- identical on
+ * every rank.  dev_sums: caller-owned device double[3] scratch.  Synchronises
+ * `stream` twice.  Errors: as pgti_series_stats and pgti_stats_finalize, NCCL,
+ * CUDA, ZERO_VARIANCE (sigma == 0). */
+pgti_status pgti_series_moments(const pgti_series *s, int64_t S_tr, int T_in, int64_t row_lo,
+                                int64_t row_hi, pgti_comm *comm, double *dev_sums, double *mu,
+                                double *sigma, void *stream);
+
+/* Mean of per-batch losses over every rank (the per-epoch validation MAE of
+ * distributed-index-batching and its AllReduce): the n device
+ * floats dev_losses are summed in float64 in a fixed order into dev_scratch[0]
+ * (dev_scratch[1] = n; caller-owned device double[2]), the pair is NCCL-summed
+ * over the ranks when comm is non-null, and *mean (HOST) = sum / count (NaN when
+ * no rank had a batch).  Every batch must have the same element count (equal-
+ * weight mean).  Synchronises `stream`.  Errors: INVALID_ARG, NCCL, CUDA. */
+pgti_status pgti_mean_losses(pgti_comm *comm, const float *dev_losses, int64_t n,
+                             double *dev_scratch, double *mean, void *stream);
+
 /* In-place z-score (Alg. 1 lines 203-204 applied once to the single copy, the
  * in-place standardisation of P:249): v <- fl32(fl32(v - fl32(mu)) / fl32(sigma)),
  * IEEE round-to-nearest float32 sub and div (reading O4); pads stay +0.0.
@@ -326,7 +358,6 @@ pgti_status pgti_diffuse_adjoint(const pgti_dcrnn_desc *d, const float *dT, int6
                                  float *dZ, void *stream);
 
 /* ----------------------------------------------------- distributed + optimiser */
-typedef struct pgti_comm pgti_comm;
 /* NCCL unique id (rank 0), to be broadcast to the other ranks (torch PG). */
 pgti_status pgti_comm_unique_id(uint8_t id[128]);
 /* ncclCommInitRank on CUDA device `device`.  Errors: INVALID_ARG, NCCL, CUDA. */

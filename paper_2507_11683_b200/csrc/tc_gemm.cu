@@ -316,13 +316,34 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
 
 // ================================================================== wgrad (MN-major A and B)
 constexpr int kWgThreads = 192;
-constexpr int kWKC = 2048;  // rows per split-K chunk
+
+// Split-K plan of the weight gradient.  The reduction dimension is the (t, row) index space,
+// walked as k-steps of kBK rows that never cross a time step: k-step ks covers rows
+// [(ks % nrb) kBK, +kBK) of step t = ks / nrb (nrb = ceil(R / kBK); rows >= R are TMA zero
+// fill).  The T nrb k-steps are cut into `nchunks` contiguous ranges, one CTA per (v tile,
+// range), so the grid is about one wave of the 148 SMs at any R (one CTA per SM: 128 KB of
+// stages) and each CTA accumulates its whole range in TMEM: at full PeMS 29 partial tiles per
+// output instead of 12 x 349, i.e. ~20 MB of partials instead of 1.4 GB.
+struct WgPlan {
+  int nrb;       // k-steps per time step
+  int total;     // T * nrb
+  int nchunks;   // contiguous k-step ranges (split-K factor)
+};
+
+WgPlan wg_plan(int V, int T, int R) {
+  WgPlan q;
+  q.nrb = int(ceil_div(R, kBK));
+  q.total = T * q.nrb;
+  const int tiles = int(ceil_div(V, kBM));
+  q.nchunks = std::max(1, std::min(q.total, kNumSMs / tiles));
+  return q;
+}
 
 template <int NOUT>
 __global__ void __launch_bounds__(kWgThreads, 1)
     k_tc_wgrad(const __grid_constant__ CUtensorMap mA_in, const __grid_constant__ CUtensorMap mA_h,
                const __grid_constant__ CUtensorMap mG, const __grid_constant__ TcWgrad p,
-               int chunks_per_t) {
+               WgPlan q) {
   constexpr int A_BYTES = kBM * kBK * 2, B_BYTES = NOUT * kBK * 2, STAGE = A_BYTES + B_BYTES;
   constexpr int NCH_B = NOUT / 64;
   extern __shared__ uint8_t smem_raw[];
@@ -330,10 +351,11 @@ __global__ void __launch_bounds__(kWgThreads, 1)
   Barriers *bar = carve<A_BYTES, B_BYTES>(smem);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tile = blockIdx.x, chunk = blockIdx.y;
-  const int t = chunk / chunks_per_t;
-  const int rbeg = (chunk - t * chunks_per_t) * kWKC;
-  const int rend = min(p.R, rbeg + kWKC);
-  const int nst = (rend - rbeg + kBK - 1) / kBK;
+  // k-steps [ks0, ks1) of this chunk: an even split of the T nrb k-steps (fixed, so the
+  // partials and their fixed-order reduction are bitwise reproducible)
+  const int ks0 = int(int64_t(q.total) * chunk / q.nchunks);
+  const int ks1 = int(int64_t(q.total) * (chunk + 1) / q.nchunks);
+  const int nst = ks1 - ks0;
   griddep_launch_dependents();
   if (threadIdx.x == 0) tma_prefetch(&mA_in), tma_prefetch(&mA_h), tma_prefetch(&mG);
   setup(bar, NOUT);  // barriers + TMEM while the predecessor drains
@@ -341,8 +363,8 @@ __global__ void __launch_bounds__(kWgThreads, 1)
   const uint32_t tmem = bar->tmem;
   if (warp == 0) {
     if (lane == 0)
-      for (int st = 0; st < nst; ++st) {
-        const int s = st % kStages, row = rbeg + st * kBK;
+      for (int st = 0, t = ks0 / q.nrb, rb = ks0 - t * q.nrb; st < nst; ++st) {
+        const int s = st % kStages, row = rb * kBK;
         mbar_wait(&bar->empty[s], ((st / kStages) & 1) ^ 1);
         mbar_expect_tx(&bar->full[s], STAGE);
         uint8_t *a = smem + s * STAGE;
@@ -358,6 +380,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 #pragma unroll
         for (int qc = 0; qc < NCH_B; ++qc)
           tma_load_3d(a + A_BYTES + qc * 8192, &mG, &bar->full[s], qc * 64, row, t);
+        if (++rb == q.nrb) rb = 0, ++t;
       }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -510,7 +533,7 @@ cudaError_t launch_tc_fwd(const TcFwd &p, cudaStream_t s) {
 }
 
 size_t tc_wgrad_partial_floats(int V, int Nout, int T, int R) {
-  return size_t(T) * size_t(ceil_div(R, kWKC)) * size_t(V) * size_t(Nout);
+  return size_t(wg_plan(V, T, R).nchunks) * size_t(V) * size_t(Nout);
 }
 
 cudaError_t launch_tc_wgrad(const TcWgrad &p, cudaStream_t s) {
@@ -524,8 +547,8 @@ cudaError_t launch_tc_wgrad(const TcWgrad &p, cudaStream_t s) {
   if (!make_map(&ma_in, p.A_in, 4, dA, sA, bA) || !make_map(&ma_h, p.A_h, 4, dA, sA, bA) ||
       !make_map(&mg, p.G, 3, dG, sG, bG))
     return cudaErrorInvalidValue;
-  const int cpt = int(ceil_div(p.R, kWKC));
-  const int nchunks = p.T * cpt;
+  const WgPlan q = wg_plan(p.V, p.T, p.R);
+  const int nchunks = q.nchunks;
   if (int64_t(nchunks) * p.V * p.Nout > p.partial_cap) return cudaErrorInvalidValue;
   const dim3 grid(unsigned(ceil_div(p.V, kBM)), unsigned(nchunks));
   const int64_t n = int64_t(p.V) * p.Nout;
@@ -534,16 +557,17 @@ cudaError_t launch_tc_wgrad(const TcWgrad &p, cudaStream_t s) {
     const double TR = double(p.T) * p.R;
     ProfScope prof(kProfGemmWgrad, s, 2.0 * TR * p.V + 2.0 * TR * p.Nout + 4.0 * nchunks * n,
                    2.0 * TR * p.V * p.Nout);
+    // the >48 KB opt-in is per device: set on every launch (cheap), as launch_tc_fwd does
     if (p.Nout == 128) {
-      static cudaError_t once = set_smem(k_tc_wgrad<128>, wg_smem_bytes(128));
-      if (once != cudaSuccess) return once;
+      e = set_smem(k_tc_wgrad<128>, wg_smem_bytes(128));
+      if (e != cudaSuccess) return e;
       e = pdl_launch(k_tc_wgrad<128>, grid, dim3(kWgThreads), wg_smem_bytes(128), s, ma_in, ma_h,
-                     mg, p, cpt);
+                     mg, p, q);
     } else {
-      static cudaError_t once = set_smem(k_tc_wgrad<64>, wg_smem_bytes(64));
-      if (once != cudaSuccess) return once;
+      e = set_smem(k_tc_wgrad<64>, wg_smem_bytes(64));
+      if (e != cudaSuccess) return e;
       e = pdl_launch(k_tc_wgrad<64>, grid, dim3(kWgThreads), wg_smem_bytes(64), s, ma_in, ma_h,
-                     mg, p, cpt);
+                     mg, p, q);
     }
   }
   if (e != cudaSuccess) return e;

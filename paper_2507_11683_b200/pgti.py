@@ -80,6 +80,10 @@ _load = _sig("pgti_load_series", C.c_int, C.POINTER(_vp), _vp, _i64, _i64, _i64,
              _vp)
 _stats = _sig("pgti_series_stats", C.c_int, _vp, _i64, C.c_int, _i64, _i64, _f64, _vp, _vp)
 _normalize = _sig("pgti_series_normalize", C.c_int, _vp, _f64, _f64, _vp)
+_stats_fin = _sig("pgti_stats_finalize", C.c_int, _vp, _f64, C.POINTER(_f64), C.POINTER(_f64))
+_moments = _sig("pgti_series_moments", C.c_int, _vp, _i64, C.c_int, _i64, _i64, _vp, _vp,
+                C.POINTER(_f64), C.POINTER(_f64), _vp)
+_mean_losses = _sig("pgti_mean_losses", C.c_int, _vp, _vp, _i64, _vp, C.POINTER(_f64), _vp)
 _info = _sig("pgti_series_info", C.c_int, _vp, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64),
              C.POINTER(_i64), C.POINTER(_i64))
 _destroy = _sig("pgti_series_destroy", C.c_int, _vp)
@@ -334,6 +338,14 @@ class Series:
               stream=None):
         _ok(_stats(self.h, S_tr, T_in, row_lo, row_hi, shift, _ptr(dev_sums), _stream(stream)))
 
+    def moments(self, S_tr: int, T_in: int, row_lo: int, row_hi: int, dev_sums, comm=None,
+                stream=None):
+        """pgti_series_moments: Alg. 1's (mu, sigma), summed over the ranks of `comm`."""
+        mu, sigma = _f64(), _f64()
+        _ok(_moments(self.h, S_tr, T_in, row_lo, row_hi, comm.h if comm is not None else None,
+                     _ptr(dev_sums), C.byref(mu), C.byref(sigma), _stream(stream)))
+        return mu.value, sigma.value
+
     def normalize(self, mu: float, sigma: float, stream=None):
         _ok(_normalize(self.h, mu, sigma, _stream(stream)))
 
@@ -460,6 +472,22 @@ def csr_to_device(csr: dict, device):
 
 
 # ------------------------------------------------------------------------------ comm / adam
+def stats_finalize(sums, shift: float):
+    """pgti_stats_finalize: host sums (s0, s1, s2) about `shift` -> (mean, population var)."""
+    a = (_f64 * 3)(*[float(v) for v in sums])
+    mean, var = _f64(), _f64()
+    _ok(_stats_fin(C.cast(a, _vp), shift, C.byref(mean), C.byref(var)))
+    return mean.value, var.value
+
+
+def mean_losses(dev_losses, n: int, dev_scratch, comm=None, stream=None) -> float:
+    """pgti_mean_losses: mean of n device per-batch losses over every rank of `comm`."""
+    out = _f64()
+    _ok(_mean_losses(comm.h if comm is not None else None, _ptr(dev_losses), n,
+                     _ptr(dev_scratch), C.byref(out), _stream(stream)))
+    return out.value
+
+
 def comm_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     _ok(_uid(C.cast(buf, _vp)))

@@ -154,22 +154,13 @@ class Trainer:
 
     # ------------------------------------------------------------------ setup
     def _stats(self):
-        torch = self.torch
-        p, cfg = self.plan, self.cfg
-        out = []
-        shift = 0.0
-        for _ in range(2):   # pass 1: mean; pass 2: variance about the mean (no cancellation)
-            sums = torch.zeros(3, dtype=torch.float64, device=self.dev)
-            self.series.stats(self.S_tr, cfg.T_in, p.stat_lo, p.stat_hi, shift, sums)
-            if self.comm is not None and self.world > 1 and self.placement == "halo":
-                self.comm.allreduce_f64(sums)
-            s0, s1, s2 = sums.cpu().tolist()
-            mean_d = s1 / s0
-            out.append((shift, mean_d, s2 / s0 - mean_d * mean_d))
-            shift = shift + mean_d
-        mu = out[1][0] + out[1][1]
-        var = out[1][2]
-        return mu, math.sqrt(max(var, 0.0))
+        """Alg. 1's mu, sigma over the training windows: both passes, the cross-rank
+        sum of the halo shards' partial sums and the finalisation run inside libpgti
+        (pgti_series_moments); the replicated placement holds every row and sums locally."""
+        p = self.plan
+        sums = self.torch.zeros(3, dtype=self.torch.float64, device=self.dev)
+        comm = self.comm if self.placement == "halo" else None
+        return self.series.moments(self.S_tr, self.cfg.T_in, p.stat_lo, p.stat_hi, sums, comm)
 
     def steps_per_epoch(self) -> int:
         return self.S_r // self.cfg.B
@@ -210,12 +201,9 @@ class Trainer:
         for j in range(nb):
             self.series.gather(vidx[j * B:(j + 1) * B], B, cfg.T_in, cfg.T_out, self.x, self.y)
             self.model.loss(self.params, self.x, self.y, losses[j:j + 1], self.ws)
-        host = losses[:nb].cpu().numpy().astype(np.float64)
-        sums = torch.tensor([host.sum(), float(nb)], dtype=torch.float64, device=self.dev)
-        if self.comm is not None and self.world > 1:
-            self.comm.allreduce_f64(sums)
-        total, count = sums.cpu().tolist()
-        return total / count if count else float("nan")
+        scratch = torch.zeros(2, dtype=torch.float64, device=self.dev)
+        return pgti.mean_losses(losses, nb, scratch,
+                                self.comm)
 
     # ------------------------------------------------------------------ one step
     def _body(self, idx):
@@ -231,7 +219,7 @@ class Trainer:
         else:
             self.series.gather(idx, cfg.B, cfg.T_in, cfg.T_out, self.x, self.y)
             self.model.step(self.params, self.grads, self.x, self.y, self.loss, self.ws)
-        if self.comm is not None and self.world > 1:
+        if self.comm is not None:   # a 1-rank communicator (world 1) runs the same identity SUM
             self.comm.allreduce_grads(self.grads)
         pgti.adam_step(self.params, self.grads, self.m, self.v, 0, self.lr,
                        grad_scale=1.0 / self.world, dev_step=self.dev_step)

@@ -228,3 +228,34 @@ def test_shard_plan_vs_oracle(pgti, name):
         assert covered[0][0] == 0 and covered[-1][1] == S_tr + cfg.T_in - 1
         assert all(covered[i][1] == covered[i + 1][0] for i in range(R - 1))
     assert trainer.row_pitch(207, 2) == 416 and trainer.row_pitch(325, 2) == 652
+
+
+@pytest.mark.parametrize("E,N,F,T_in,T_out,seed", [(60, 12, 2, 3, 2, 0), (521, 20, 1, 4, 1, 1),
+                                                   (200, 7, 3, 12, 12, 2)])
+def test_stats_finalize_matches_alg1(pgti, E, N, F, T_in, T_out, seed):
+    """pgti_stats_finalize (host part of pgti_series_moments) turns the three sums over the
+    STACKED x_train (Alg. 1, here formed literally by the oracle) into Alg. 1's
+    mean and population std (lines 201-202) to 1e-12, about shift 0 and about the mean."""
+    rng = np.random.default_rng(seed)
+    v = (50.0 + 10.0 * rng.standard_normal((E, N, F))).astype(np.float32)
+    x, _ = windows.alg1_stack(v.astype(np.float64), T_in, T_out)
+    x_train = x[:windows.split_counts(x.shape[0])[0]]
+    mu_ref, sd_ref = windows.alg1_stats(v, T_in, T_out)
+    for shift in (0.0, mu_ref, -3.25):
+        d = x_train - shift
+        mean, var = pgti.stats_finalize((d.size, d.sum(), (d * d).sum()), shift)
+        assert abs(mean - mu_ref) <= 1e-12 * abs(mu_ref), (shift, mean, mu_ref)
+        # about shift 0 the one-pass form E[v^2] - E[v]^2 cancels ~ (mu/sigma)^2 = 25 -> 2.5e-14 rel
+        assert abs(np.sqrt(var) - sd_ref) <= 1e-12 * sd_ref, (shift, np.sqrt(var), sd_ref)
+
+
+def test_stats_finalize_errors(pgti):
+    with pytest.raises(pgti.PgtiError) as e:
+        pgti.stats_finalize((0.0, 0.0, 0.0), 0.0)
+    assert e.value.name == "TOO_FEW_ENTRIES"
+    with pytest.raises(pgti.PgtiError) as e:
+        pgti.stats_finalize((4.0, float("nan"), 1.0), 0.0)
+    assert e.value.name == "NONFINITE"
+    # values {1, 2}: mean 1.5, var 0.25; a constant series has var 0 (clamped, never < 0)
+    assert pgti.stats_finalize((2.0, 3.0, 5.0), 0.0) == (1.5, 0.25)
+    assert pgti.stats_finalize((3.0, 6.0, 12.0), 0.0) == (2.0, 0.0)

@@ -100,7 +100,7 @@ def _check(cfg, loss, g, loss_ref, g_ref, tol):
     off = 0
     for name, shp in synth.param_shapes(cfg):
         n = int(np.prod(shp))
-        den = max(np.max(np.abs(g_ref[off:off + n])), 1e-2 * gscale)
+        den = max(np.max(np.abs(g_ref[off:off + n])), 1e-3 * gscale)
         e = np.max(np.abs(g[off:off + n].astype(np.float64) - g_ref[off:off + n])) / den
         assert e <= tol, (name, e)
         off += n
@@ -175,7 +175,7 @@ def test_cheb_encdec_vs_oracle(env, precision, tol):
     off = 0
     for nm, shp in encdec.layer_shapes(d):
         k = int(np.prod(shp))
-        den = max(np.max(np.abs(g_ref[off:off + k])), 1e-2 * gscale)
+        den = max(np.max(np.abs(g_ref[off:off + k])), 1e-3 * gscale)
         assert np.max(np.abs(g[off:off + k] - g_ref[off:off + k])) / den <= tol, nm
         off += k
 

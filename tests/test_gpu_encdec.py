@@ -100,7 +100,7 @@ def test_encdec_step_vs_oracle(env, name, tf):
     for nm, shp in encdec.layer_shapes(c["d"]):
         n = int(np.prod(shp))
         g, gr = c["g"][off:off + n].astype(np.float64), c["g_ref"][off:off + n]
-        den = max(np.max(np.abs(gr)), 1e-2 * gscale)
+        den = max(np.max(np.abs(gr)), 1e-3 * gscale)
         assert np.max(np.abs(g - gr)) / den <= TOL32, (nm, np.max(np.abs(g - gr)) / den)
         off += n
     assert off == c["g"].size
@@ -144,7 +144,7 @@ def _check(c, tol):
     for nm, shp in encdec.layer_shapes(c["d"]):
         n = int(np.prod(shp))
         g, gr = c["g"][off:off + n].astype(np.float64), c["g_ref"][off:off + n]
-        den = max(np.max(np.abs(gr)), 1e-2 * gscale)
+        den = max(np.max(np.abs(gr)), 1e-3 * gscale)
         assert np.max(np.abs(g - gr)) / den <= tol, (nm, np.max(np.abs(g - gr)) / den)
         off += n
 

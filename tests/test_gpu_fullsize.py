@@ -130,3 +130,77 @@ def test_step_fullsize_sampled(env, name):
     assert scale_rel(dW, dW_ref) <= 1e-3, scale_rel(dW, dW_ref)
     print(f"{name}: sampled worst scale-rel {worst:.2e}; sign(yhat-y)>0 {pos:.3f}; loss {float(loss.item()):.6f} ref {loss_ref:.6f}; db_out {db} ref {db_ref}; "
           f"dW_out scale-rel {scale_rel(dW, dW_ref):.2e}")
+
+
+@pytest.mark.parametrize("name", ["pems_all_la", "pems"])
+def test_step_fullsize_gradients_repeated_windows(env, name):
+    """Every gradient tensor at the full size (B = 64, R = N B rows: 173,824 at PeMS-All-LA,
+    714,240 at full PeMS; 349 split-K chunks per (layer, gate) weight gradient; backward buffers
+    past 2^31 floats) against the oracle, at the cost of 4 oracle backward passes: the batch is
+    4 distinct windows each repeated 16 times in a shuffled order.  The loss is a mean over
+    samples, so d loss / d theta = (1/B) sum_b d l_b / d theta = sum_w (16/64) g_w with
+    g_w the oracle gradient of window w alone (a batch of one); the kernel still processes all
+    64 samples as distinct rows.  Bar: 2e-2 scale-relative per tensor (BJ, reading c19)."""
+    pgti, torch = env
+    cfg = synth.CONFIGS[name]
+    B, TW = cfg.B, cfg.T_in + cfg.T_out
+    N, F, T_in, T_out, F_out = cfg.N, cfg.F, cfg.T_in, cfg.T_out, cfg.F_out
+    ld = ld_of(cfg)
+    row_tail = cfg.E - TAIL_ROWS
+    v_tail = synth.make_series(cfg, row_lo=row_tail, row_hi=cfg.E)
+    mu, sigma = float(v_tail.mean(dtype=np.float64)), float(v_tail.std(dtype=np.float64))
+    host = np.zeros((cfg.E, N, F), np.float32)
+    host[row_tail:] = v_tail
+    buf = torch.empty(cfg.E * ld, dtype=torch.float32, device="cuda")
+    s = pgti.Series(host, 0, N, F, buf, ld)
+    s.normalize(mu, sigma)
+    del host
+
+    rng = np.random.default_rng(11683)
+    distinct = row_tail + rng.choice(TAIL_ROWS - TW + 1, size=4, replace=False)
+    distinct[-1] = cfg.E - TW
+    idx_np = rng.permutation(np.repeat(distinct, B // 4))
+    idx = torch.from_numpy(idx_np.astype(np.int32)).cuda()
+    x = torch.empty(B * T_in * ld, device="cuda")
+    y = torch.empty(B * T_out * ld, device="cuda")
+    s.gather(idx, B, T_in, T_out, x, y)
+    graph = synth.make_graph(N, cfg.knn)
+    model = model_for(pgti, torch, cfg, graph, precision=1)
+    theta = synth.make_params(cfg, seed=synth.SEED_PARAMS, kind="random")
+    xo, yo = windows.materialize(v_tail, T_in, T_out, mu, sigma, starts=distinct - row_tail)
+    theta[-F_out:] = yo[..., :F_out].mean(axis=(0, 1, 2))
+    n = model.num_params()
+    grads = torch.full((n,), float("nan"), dtype=torch.float32, device="cuda")
+    loss = torch.zeros(1, dtype=torch.float32, device="cuda")
+    ws = torch.empty(model.workspace_bytes(), dtype=torch.uint8, device="cuda")
+    model.step(torch.from_numpy(theta).cuda(), grads, x, y, loss, ws)
+    pgti.check_device_error()
+    g = grads.cpu().numpy().astype(np.float64)
+    del ws, x, y, buf
+    assert np.all(np.isfinite(g))
+
+    Pf, Pb = transitions.transition_matrices(N, *graph)
+    d = dcgru.Dims.of(cfg)
+    theta64 = theta.astype(np.float64)
+    g_ref = np.zeros_like(g)
+    loss_ref = 0.0
+    for w in range(4):
+        lw, gw, _ = dcgru.backward(theta64, d, Pf, Pb, xo[w:w + 1].astype(np.float64),
+                                   yo[w:w + 1].astype(np.float64))
+        g_ref += 0.25 * gw
+        loss_ref += 0.25 * lw
+    assert abs(float(loss.item()) - loss_ref) <= TOL_BF16 * loss_ref, (float(loss.item()), loss_ref)
+    gscale = np.max(np.abs(g_ref))
+    off, report = 0, []
+    for pname, shp in synth.param_shapes(cfg):
+        k = int(np.prod(shp))
+        gr = g_ref[off:off + k]
+        den = max(np.max(np.abs(gr)), 1e-3 * gscale)
+        e = float(np.max(np.abs(g[off:off + k] - gr)) / den)
+        report.append((pname, round(e, 5), float(np.max(np.abs(gr)) / gscale)))
+        off += k
+    print(f"{name}: loss {float(loss.item()):.6f} ref {loss_ref:.6f}; per tensor (err, ref/gscale) "
+          f"{report}")
+    for pname, e, _ in report:
+        assert e <= TOL_BF16, (pname, e)
+    assert scale_rel(g, g_ref) <= TOL_BF16

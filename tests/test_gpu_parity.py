@@ -314,10 +314,16 @@ def _check_step(c, tol=TOL32):
         n = int(np.prod(shp))
         g, gr = c["g"][off:off + n], c["g_ref"][off:off + n]
         # per tensor scale-relative; a tensor whose reference is (near) zero -- e.g. db_out =
-        # sum of +-1/count with balanced signs, where fp32 summation leaves ~count*eps/count
-        # absolute noise -- is measured against 1e-2 of the whole gradient's scale (reading c19)
-        den = max(np.max(np.abs(gr)), 1e-2 * gscale)
-        e = np.max(np.abs(g.astype(np.float64) - gr)) / den
+        # sum of +-1/count with balanced signs -- is measured against 1e-3 of the whole
+        # gradient's scale (reading c19)
+        den = max(np.max(np.abs(gr)), 1e-3 * gscale)
+        err = np.max(np.abs(g.astype(np.float64) - gr))
+        if name == "b_out":
+            # db_out = sum_i sign_i / count over count = B T_out N F_out terms, accumulated in
+            # fp32 on both paths: the summation bound gamma_n sum|x_i| = count * 2^-24 * 1 is
+            # an absolute error the tolerance must admit when the signs balance (ref ~ 0)
+            err = max(0.0, err - (B * cfg.T_out * cfg.N * cfg.F_out) * 2.0 ** -24)
+        e = err / den
         assert e <= tol, (name, e)
         off += n
     assert scale_rel(c["g"], c["g_ref"]) <= tol
@@ -607,6 +613,43 @@ def test_step_indexed_bitexact_vs_gather(env, name, precision, B):
     with pytest.raises(pgti.PgtiError) as e:
         pgti.check_device_error()
     assert e.value.name == "OUT_OF_RANGE"
+
+
+@pytest.mark.parametrize("name,precision,B", [("odd", 0, None), ("metr_la", 0, 16),
+                                              ("tc_big", 1, None), ("metr_la", 1, 64)])
+def test_step_indexed_vs_oracle(env, name, precision, B):
+    """f2 against the oracle (not only against the gather path): the zero-copy step reads
+    sample b's windows from a halo shard of the resident series by start index ("views,
+    not copies"); loss, every activation and every gradient tensor match the float64 oracle's
+    materialised-snapshot step (1e-5 fp32, 2e-2 bf16)."""
+    pgti, torch = env
+    from paper_2507_11683_b200 import trainer
+    cfg = TC_CONFIGS.get(name) or SMALL_CONFIGS.get(name) or synth.CONFIGS[name]
+    cfg = cfg.replace(B=B or cfg.B)
+    ref = ref_for(cfg)
+    p = trainer.shard_plan(ref.n_train, 2, 1, cfg.T_in, cfg.T_out)
+    s = load_series(pgti, torch, ref.v[p.row_lo:p.row_hi], p.row_lo, cfg, ref.mu, ref.sigma)
+    # rank 1's windows (global starts past row 0); drawn with replacement so that configs with
+    # fewer windows per rank than B still fill the batch
+    idx_np = np.random.default_rng(7).integers(p.win_lo, p.win_hi, size=cfg.B)
+    model = model_for(pgti, torch, cfg, ref.graph, precision=precision)
+    theta = synth.make_params(cfg, kind="random")
+    n = model.num_params()
+    ws = torch.empty(model.workspace_bytes(), dtype=torch.uint8, device="cuda")
+    grads = torch.full((n,), float("nan"), device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    act = torch.empty(model.act_dump_floats(), device="cuda")
+    model.step_indexed(torch.from_numpy(theta).cuda(), grads, s,
+                       torch.from_numpy(idx_np.astype(np.int32)).cuda(), loss, ws, act)
+    pgti.check_device_error()
+    xo, yo = ref.batch(idx_np)
+    loss_ref, g_ref, fwd = dcgru.backward(theta.astype(np.float64), ref.d, ref.Pf, ref.Pb,
+                                          xo.astype(np.float64), yo.astype(np.float64))
+    resid = np.abs(fwd["yhat"] - yo[..., :cfg.F_out])
+    c = dict(loss=float(loss.item()), g=grads.cpu().numpy(), act=act.cpu().numpy(),
+             loss_ref=loss_ref, g_ref=g_ref, fwd=fwd, cfg=cfg, ref=ref,
+             margin=float(resid.min()) if precision == 0 else 1.0, B=cfg.B)
+    _check_step(c, tol=TOL32 if precision == 0 else TOL_BF16)
 
 
 def test_trainer_zero_copy_graph_matches_gather(env):
