@@ -88,42 +88,6 @@ pgti_status pgti_graph_windows(int32_t N, const int32_t *rowptr, const int32_t *
                                int32_t rows_per_window, int32_t *win_ptr, int32_t *win_nodes,
                                uint16_t *lcol, int32_t *max_union);
 
-/* Two-hop staging plan (K = 2 diffusion in ONE launch on the tensor-core path,
- * without forming P^2): on ONE CSR pattern (host arrays), window w of
- * rows_per_window consecutive nodes R (1..64) stages the rows of
- * U2 = U1 + neighbours(U1), U1 = R + neighbours(R), so a CTA computes hop 1 for
- * U1 from staged rows and hop 2 for R from its own hop-1 results.  Per window:
- * nodes[win_ptr[w] .. win_ptr[w+1]) lists U2 ordered R (ascending), then U1 \ R
- * (ascending), then U2 \ U1 (ascending); n1[w] = |U1|; the CSR entries of the
- * U1 rows, in U1 order and CSR order, are ent_ptr[w] .. ent_ptr[w+1]) with
- * lcol = the column's position in the window's U2 list and eidx = the entry's
- * index in the global CSR (its value); row_off[win_ptr[w] + w + i] (i = 0..n1[w])
- * = entry offset of U1 row i within the window.  Call once with nodes = NULL to
- * get *total_nodes and *total_entries (win_ptr, n1, ent_ptr are still written),
- * then with arrays of those sizes (row_off: total_nodes + nwin).  *max_nodes,
- * *max_n1, *max_entries = the largest per-window counts (shared-memory sizing).
- * Index bookkeeping only.  Errors: INVALID_ARG (null, rows_per_window outside
- * [1,64], column outside [0,N), a window's U2 > 65535). */
-pgti_status pgti_graph_windows2(int32_t N, const int32_t *rowptr, const int32_t *col,
-                                int32_t rows_per_window, int32_t *win_ptr, int32_t *nodes,
-                                int32_t *n1, int32_t *ent_ptr, int32_t *row_off, uint16_t *lcol,
-                                int32_t *eidx, int64_t *total_nodes, int64_t *total_entries,
-                                int32_t *max_nodes, int32_t *max_n1, int32_t *max_entries);
-
-/* Two-hop operators for the single-launch K = 2 diffusion (reading c23): S = M M
- * for a CSR M (host arrays) carrying two value arrays val_a, val_b on one
- * pattern -- called on pattern(A) with (P_f, P_b^T) it yields pattern(A^2) with
- * (P_f^2, (P_b^2)^T); on pattern(A^T) with (P_b, P_f^T) it yields (P_b^2,
- * (P_f^2)^T).  Products summed in double, stored as float; the pattern is the
- * boolean square (explicit zeros kept), columns ascending.  Two calls: with
- * out_col = NULL only *out_nnz is computed; then out_rowptr [N+1], out_col,
- * out_val_a, out_val_b [*out_nnz] are filled.  Errors: INVALID_ARG (null,
- * non-monotone rowptr, column outside [0,N), nnz >= 2^31). */
-pgti_status pgti_graph_square(int32_t N, const int32_t *rowptr, const int32_t *col,
-                              const float *val_a, const float *val_b, int32_t *out_rowptr,
-                              int32_t *out_col, float *out_val_a, float *out_val_b,
-                              int64_t *out_nnz);
-
 /* ----------------------------------------------------------------- the series */
 typedef struct pgti_series pgti_series; /* opaque; BORROWS dev_buf */
 
@@ -259,21 +223,6 @@ typedef struct {
   const uint16_t *a_lcol;
   const int32_t *at_win_ptr, *at_win_nodes; /* pattern(A^T) plan                 */
   const uint16_t *at_lcol;
-  /* Optional two-hop matrices (pgti_graph_square; device CSR, nnz2 entries each):
-   * when set, K = 2 and precision = 1, each diffusion of the step runs as ONE
-   * launch [P_f Z, P_f^2 Z, P_b Z, P_b^2 Z] instead of the hop chain P_f (P_f Z)
-   * (reading c23: same operator, one fewer dependent launch; the bf16 rounding
-   * of the intermediate hop disappears).  Null -> the chain.  Window plans of the
-   * squared patterns are optional as above (win_max then covers all four). */
-  int64_t nnz2;
-  const int32_t *a2_rowptr, *a2_col;   /* pattern(A^2): values P_f^2, (P_b^2)^T   */
-  const float *Pf2_val, *Pb2T_val;
-  const int32_t *at2_rowptr, *at2_col; /* pattern((A^T)^2): P_b^2, (P_f^2)^T      */
-  const float *Pb2_val, *Pf2T_val;
-  const int32_t *a2_win_ptr, *a2_win_nodes;
-  const uint16_t *a2_lcol;
-  const int32_t *at2_win_ptr, *at2_win_nodes;
-  const uint16_t *at2_lcol;
   /* Model family.  0 = the stepwise stacked PGT-DCRNN above.  1 = Li et al.'s
    * DCRNN encoder-decoder (reading c24): the L-layer
    * stack above run as the encoder over x_0..x_{T_in-1} (no readout), then a
@@ -292,17 +241,6 @@ typedef struct {
    * P^k Z; 1 = the Chebyshev recurrence T_1 = P Z, T_k = 2 P T_{k-1} - T_{k-2}
    * per direction (T_0 = Z); the adjoint is the same polynomial in P^T. */
   int32_t cheb;
-  /* Optional two-hop staging plans (pgti_graph_windows2 on each pattern, same
-   * rows_per_window; device arrays): with K = 2 and precision = 1 each diffusion
-   * runs both hops of both directions in ONE launch (hop 1 of the window's U1
-   * recomputed per window from staged rows, rounded to bf16 exactly as the
-   * two-launch chain stores it: results bit-identical to the chain).  win2_rows
-   * = 0 or a null pointer -> the chain.  Not with the P^2 operators. */
-  int32_t win2_rows, win2_max_nodes, win2_max_n1, win2_max_entries;
-  const int32_t *a_w2_ptr, *a_w2_nodes, *a_w2_n1, *a_w2_eptr, *a_w2_roff, *a_w2_eidx;
-  const uint16_t *a_w2_lcol;
-  const int32_t *at_w2_ptr, *at_w2_nodes, *at_w2_n1, *at_w2_eptr, *at_w2_roff, *at_w2_eidx;
-  const uint16_t *at_w2_lcol;
 } pgti_dcrnn_desc;
 
 /* sizeof(pgti_dcrnn_desc) as this build lays it out: bindings check their mirror of the

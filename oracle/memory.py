@@ -31,13 +31,17 @@ def index_elements(E: int, T_in: int, T_out: int, N: int, F: int) -> tuple[int, 
     return E * N * F, E - T_in - T_out + 1
 
 
-def index_bytes(E, T_in, T_out, N, F, elem_bytes=4, idx_bytes=4) -> int:
+def index_bytes(E, T_in, T_out, N, F, elem_bytes=4, idx_bytes=8) -> int:
+    """Eq. 2 in bytes: data elements at their width plus index entries counted as 8-byte
+    integers (reading c12); idx_bytes=4 gives the device footprint of the int32
+    plan libpgti keeps."""
     d, i = index_elements(E, T_in, T_out, N, F)
     return d * elem_bytes + i * idx_bytes
 
 
-def ratio(E, T_in, T_out, N, F, elem_bytes=8, idx_bytes=4) -> float:
-    """Materialised / index-batched bytes (Eq. 1 / Eq. 2, reading c12)."""
+def ratio(E, T_in, T_out, N, F, elem_bytes=8, idx_bytes=8) -> float:
+    """Materialised / index-batched bytes (Eq. 1 / Eq. 2, reading c12; 8-byte index entries,
+    S:281 -- idx_bytes=4 for the int32 device plan)."""
     return materialized_elements(E, T_in, T_out, N, F) * elem_bytes / \
         index_bytes(E, T_in, T_out, N, F, elem_bytes, idx_bytes)
 

@@ -48,19 +48,6 @@ pgti_status check_desc(const pgti_dcrnn_desc *desc, Dims *out) {
                PGTI_ERR_SHAPE, "desc: N=%d F=%d L=%d K=%d T_in=%d B=%d", g.N, g.F, g.L, g.K,
                g.T_in, g.B);
   PGTI_REQUIRE(g.cheb == 0 || g.cheb == 1, PGTI_ERR_INVALID_ARG, "desc: cheb=%d", g.cheb);
-  PGTI_REQUIRE(!g.cheb || !g.a2_rowptr, PGTI_ERR_INVALID_ARG,
-               "desc: the two-hop operators are powers of P, not Chebyshev blocks");
-  if (g.win2_rows) {
-    PGTI_REQUIRE(g.win2_rows >= 1 && g.win2_rows <= 64 && g.win2_max_nodes > 0 &&
-                     g.win2_max_n1 > 0 && g.win2_max_n1 <= g.win2_max_nodes &&
-                     g.win2_max_entries >= 0 && !g.a2_rowptr,
-                 PGTI_ERR_INVALID_ARG, "desc: bad two-hop plan (win2_rows=%d) or with P^2",
-                 g.win2_rows);
-    PGTI_REQUIRE(g.a_w2_ptr && g.a_w2_nodes && g.a_w2_n1 && g.a_w2_eptr && g.a_w2_roff &&
-                     g.a_w2_eidx && g.a_w2_lcol && g.at_w2_ptr && g.at_w2_nodes && g.at_w2_n1 &&
-                     g.at_w2_eptr && g.at_w2_roff && g.at_w2_eidx && g.at_w2_lcol,
-                 PGTI_ERR_INVALID_ARG, "desc: win2_rows set but a two-hop plan pointer is null");
-  }
   PGTI_REQUIRE(g.model == 0 || g.model == 1, PGTI_ERR_INVALID_ARG,
                "desc: model=%d (0 = stepwise, 1 = encoder-decoder)", g.model);
   PGTI_REQUIRE(g.teacher_forcing == 0 ||
@@ -92,11 +79,6 @@ pgti_status check_desc(const pgti_dcrnn_desc *desc, Dims *out) {
     PGTI_REQUIRE(g.a_rowptr && g.a_col && g.Pf_val && g.PbT_val && g.at_rowptr && g.at_col &&
                      g.Pb_val && g.PfT_val && g.nnz >= 0,
                  PGTI_ERR_INVALID_ARG, "desc: CSR pointers must be set when K > 0");
-  if (g.a2_rowptr || g.at2_rowptr)
-    PGTI_REQUIRE(g.K == 2 && g.a2_rowptr && g.a2_col && g.Pf2_val && g.Pb2T_val && g.at2_rowptr &&
-                     g.at2_col && g.Pb2_val && g.Pf2T_val && g.nnz2 >= 0,
-                 PGTI_ERR_INVALID_ARG,
-                 "desc: two-hop matrices need K = 2 and all eight pointers (K=%d)", g.K);
   if (g.K > 0 && g.win_rows != 0)
     PGTI_REQUIRE(g.win_rows >= 1 && g.win_rows <= 64 && g.win_max >= 0 && g.a_win_ptr &&
                      g.a_win_nodes && g.a_lcol && g.at_win_ptr && g.at_win_nodes && g.at_lcol,
@@ -114,20 +96,15 @@ namespace {
 // term t of a job: pattern(A) (pat 0) or pattern(A^T) (pat 1) with values val, operand X
 void set_term(SpmmJob &j, int t, const pgti_dcrnn_desc &g, int pat, const float *val,
               const float *X) {
-  // pat: 0 = pattern(A), 1 = pattern(A^T), 2 = pattern(A^2), 3 = pattern((A^T)^2)
-  const int32_t *rp[4] = {g.a_rowptr, g.at_rowptr, g.a2_rowptr, g.at2_rowptr};
-  const int32_t *cl[4] = {g.a_col, g.at_col, g.a2_col, g.at2_col};
-  const int32_t *wp[4] = {g.a_win_ptr, g.at_win_ptr, g.a2_win_ptr, g.at2_win_ptr};
-  const int32_t *wn[4] = {g.a_win_nodes, g.at_win_nodes, g.a2_win_nodes, g.at2_win_nodes};
-  const uint16_t *lc[4] = {g.a_lcol, g.at_lcol, g.a2_lcol, g.at2_lcol};
-  j.rowptr[t] = rp[pat];
-  j.col[t] = cl[pat];
+  // pat: 0 = pattern(A), 1 = pattern(A^T)
+  j.rowptr[t] = pat ? g.at_rowptr : g.a_rowptr;
+  j.col[t] = pat ? g.at_col : g.a_col;
   j.val[t] = val;
   j.X[t] = X;
-  j.nnz[t] = pat < 2 ? g.nnz : g.nnz2;
-  j.win_ptr[t] = wp[pat];
-  j.win_nodes[t] = wn[pat];
-  j.lcol[t] = lc[pat];
+  j.nnz[t] = g.nnz;
+  j.win_ptr[t] = pat ? g.at_win_ptr : g.a_win_ptr;
+  j.win_nodes[t] = pat ? g.at_win_nodes : g.a_win_nodes;
+  j.lcol[t] = pat ? g.at_lcol : g.a_lcol;
   j.win_rows = g.win_rows, j.win_max = g.win_max;
 }
 }  // namespace
@@ -139,65 +116,6 @@ cudaError_t diffuse_fwd(const pgti_dcrnn_desc &g, const Dims &d, float *base, in
   char *b = reinterpret_cast<char *>(base);
   const char *z = src0 ? static_cast<const char *>(src0) : b;
   auto blk = [&](int m) { return b + int64_t(m) * mstride * es; };
-  // opt-in (PGTI_RESIDENT=1): one launch per diffusion, but only W/64 CTAs -- measured slower
-  // inside the step (METR-LA 26.0 K vs 32.3 K samples/s) than one wide launch per hop
-  const char *res_env = std::getenv("PGTI_RESIDENT");
-  const bool resident_on = res_env && res_env[0] == '1';
-  if (bf16 && G == 1 && !g.a2_rowptr && !d.cheb && resident_on &&
-      spmm_resident_fits(d.N, d.K, W)) {
-    // small graph: both directions' hop chain in one launch, the chunk resident in smem
-    ResidentJob r{};
-    const int pf = transposed ? 1 : 0, pb = transposed ? 0 : 1;  // 0: pattern(A), 1: A^T
-    const int32_t *rp[2] = {g.a_rowptr, g.at_rowptr};
-    const int32_t *cl[2] = {g.a_col, g.at_col};
-    r.rowptr[0] = rp[pf], r.col[0] = cl[pf], r.val[0] = transposed ? g.PfT_val : g.Pf_val;
-    r.rowptr[1] = rp[pb], r.col[1] = cl[pb], r.val[1] = transposed ? g.PbT_val : g.Pb_val;
-    r.nnz[0] = r.nnz[1] = g.nnz;
-    r.X = z, r.N = d.N, r.K = d.K, r.W = W;
-    for (int k = 1; k <= d.K; ++k) r.Y[0][k - 1] = blk(k), r.Y[1][k - 1] = blk(d.K + k);
-    return launch_spmm_resident(r, s);
-  }
-  if (d.K == 2 && bf16 && !g.a2_rowptr && g.win2_rows > 0) {
-    // opt-in: both hops of both directions in one launch from the two-hop staging plan
-    // (bit-identical).  Measured slower inside the step (METR-LA 30.8 K vs 33.2 K samples/s,
-    // PeMS-All-LA 2.59 K vs 3.10 K): the window's U2 staging moves as many rows from L2 as the
-    // two one-hop launches together, hop 1 is recomputed for U1 (~2x the rows), and 100 KB of
-    // shared memory per CTA halves residency; PDL already hides most of the saved launch gap.
-    Win2Job j[2] = {};
-    const bool pa[2] = {transposed != 0, transposed == 0};  // pattern(A^T) for job q?
-    const float *vals[2] = {transposed ? g.PfT_val : g.Pf_val, transposed ? g.PbT_val : g.Pb_val};
-    for (int q = 0; q < 2; ++q) {
-      Win2Job &w = j[q];
-      const bool t = pa[q];
-      w.ptr = t ? g.at_w2_ptr : g.a_w2_ptr, w.nodes = t ? g.at_w2_nodes : g.a_w2_nodes;
-      w.n1 = t ? g.at_w2_n1 : g.a_w2_n1, w.eptr = t ? g.at_w2_eptr : g.a_w2_eptr;
-      w.roff = t ? g.at_w2_roff : g.a_w2_roff, w.eidx = t ? g.at_w2_eidx : g.a_w2_eidx;
-      w.lcol = t ? g.at_w2_lcol : g.a_w2_lcol, w.val = vals[q];
-      w.X = z, w.Y1 = blk(q * d.K + 1), w.Y2 = blk(q * d.K + 2);
-      w.W = W, w.G = G, w.gstride = gstride, w.nnz = g.nnz;
-      if (d.cheb) w.add = z, w.alpha = 2.f, w.beta = -1.f;
-    }
-    const Win2Plan plan{g.win2_rows, g.win2_max_nodes, g.win2_max_n1, g.win2_max_entries};
-    cudaError_t e = launch_spmm_win2(j, 2, d.N, plan, s);
-    if (e != cudaErrorNotSupported) return e;
-    cudaGetLastError();  // not resident-sized: the hop chain below
-  }
-  if (d.K == 2 && bf16 && g.a2_rowptr) {  // one launch: [P Z, P^2 Z] for both directions
-    SpmmJob j[4] = {};
-    const float *x0 = reinterpret_cast<const float *>(z);
-    if (!transposed) {
-      set_term(j[0], 0, g, 0, g.Pf_val, x0), set_term(j[1], 0, g, 2, g.Pf2_val, x0);
-      set_term(j[2], 0, g, 1, g.Pb_val, x0), set_term(j[3], 0, g, 3, g.Pb2_val, x0);
-    } else {
-      set_term(j[0], 0, g, 1, g.PfT_val, x0), set_term(j[1], 0, g, 3, g.Pf2T_val, x0);
-      set_term(j[2], 0, g, 0, g.PbT_val, x0), set_term(j[3], 0, g, 2, g.Pb2T_val, x0);
-    }
-    for (int q = 0; q < 4; ++q) {
-      j[q].Y = reinterpret_cast<float *>(blk(q + 1));
-      j[q].nterms = 1, j[q].W = W, j[q].G = G, j[q].gstride = gstride, j[q].bf16 = bf16;
-    }
-    return launch_spmm(j, 4, d.N, s);
-  }
   for (int k = 1; k <= d.K; ++k) {
     SpmmJob j[2] = {};
     const float *xf = reinterpret_cast<const float *>(k == 1 ? z : blk(k - 1));

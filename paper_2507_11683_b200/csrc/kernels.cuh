@@ -42,42 +42,6 @@ struct SpmmJob {
 constexpr int kMaxSpmmJobs = 4;
 cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s);
 
-// Small-graph diffusion in one launch (bf16, K <= 2): each CTA keeps one 128-byte column chunk of
-// X for ALL N nodes in shared memory and computes both directions' hops 1..K from it (hop 2 from
-// the bf16 hop-1 rows it keeps), so the hop chain needs no second launch.  Y[d][k-1] = hop k of
-// direction d ([N][W] bf16).  Same CSR order and arithmetic as launch_spmm: bit-identical.
-// Opt-in (PGTI_RESIDENT=1): with only W/64 CTAs per launch it measured slower in the step.
-struct ResidentJob {
-  const int32_t *rowptr[2], *col[2];
-  const float *val[2];
-  int64_t nnz[2];
-  const void *X;
-  void *Y[2][2];
-  int N, K;
-  int64_t W;
-};
-// Two-hop staged diffusion (pgti_graph_windows2 plan, bf16): Y1 = P X, Y2 = P Y1 (Chebyshev:
-// Y2 = alpha P Y1 + beta add) in one launch, bit-identical to two launch_spmm hops.
-struct Win2Job {
-  const void *X;
-  void *Y1, *Y2;
-  const void *add;  // nullable: hop-2 epilogue alpha * acc + beta * add
-  float alpha, beta;
-  const float *val;
-  const int32_t *ptr, *nodes, *n1, *eptr, *roff, *eidx;
-  const uint16_t *lcol;
-  int64_t W, gstride, nnz;
-  int G;
-};
-struct Win2Plan {
-  int rows, max_nodes, max_n1, max_entries;
-};
-// cudaErrorNotSupported: the plan's windows do not fit shared memory (caller runs the chain)
-cudaError_t launch_spmm_win2(const Win2Job *jobs, int njobs, int N, const Win2Plan &plan,
-                             cudaStream_t s);
-bool spmm_resident_fits(int N, int K, int64_t W);
-cudaError_t launch_spmm_resident(const ResidentJob &p, cudaStream_t s);
-
 // ------------------------------------------------------------------ K3' fp32 SIMT GEMMs
 // Virtual A operand of the diffusion convolution: row r, column k = m*C_in + c reads
 //   c <  Fin : in[m*in_mstride + r*Fin + c]

@@ -45,16 +45,7 @@ class DcrnnDesc(C.Structure):
                 ("win_rows", _i32), ("win_max", _i32),
                 ("a_win_ptr", _vp), ("a_win_nodes", _vp), ("a_lcol", _vp),
                 ("at_win_ptr", _vp), ("at_win_nodes", _vp), ("at_lcol", _vp),
-                ("nnz2", _i64),
-                ("a2_rowptr", _vp), ("a2_col", _vp), ("Pf2_val", _vp), ("Pb2T_val", _vp),
-                ("at2_rowptr", _vp), ("at2_col", _vp), ("Pb2_val", _vp), ("Pf2T_val", _vp),
-                ("a2_win_ptr", _vp), ("a2_win_nodes", _vp), ("a2_lcol", _vp),
-                ("at2_win_ptr", _vp), ("at2_win_nodes", _vp), ("at2_lcol", _vp),
-                ("model", _i32), ("teacher_forcing", _i32), ("cheb", _i32),
-                ("win2_rows", _i32), ("win2_max_nodes", _i32), ("win2_max_n1", _i32),
-                ("win2_max_entries", _i32)] + \
-        [(f"{p}_w2_{k}", _vp) for p in ("a", "at")
-         for k in ("ptr", "nodes", "n1", "eptr", "roff", "eidx", "lcol")]
+                ("model", _i32), ("teacher_forcing", _i32), ("cheb", _i32)]
 
 
 def _sig(name, restype, *argtypes):
@@ -71,11 +62,6 @@ _graph_build = _sig("pgti_graph_build", C.c_int, _i32, _i64, _vp, _vp, _vp, _vp,
                     _vp, _vp, _vp, _vp)
 _graph_windows = _sig("pgti_graph_windows", C.c_int, _i32, _vp, _vp, _i32, _vp, _vp, _vp,
                       C.POINTER(_i32))
-_graph_windows2 = _sig("pgti_graph_windows2", C.c_int, _i32, _vp, _vp, _i32, _vp, _vp, _vp, _vp,
-                       _vp, _vp, _vp, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i32),
-                       C.POINTER(_i32), C.POINTER(_i32))
-_graph_square = _sig("pgti_graph_square", C.c_int, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
-                     C.POINTER(_i64))
 _load = _sig("pgti_load_series", C.c_int, C.POINTER(_vp), _vp, _i64, _i64, _i64, _i64, _vp, _i64,
              _vp)
 _stats = _sig("pgti_series_stats", C.c_int, _vp, _i64, C.c_int, _i64, _i64, _f64, _vp, _vp)
@@ -230,93 +216,20 @@ def graph_windows(N: int, rowptr, col, rows: int) -> dict:
                 lcol=lcol.view(np.int16), max_union=int(mx.value))
 
 
-W2_KEYS = ("ptr", "nodes", "n1", "eptr", "roff", "eidx", "lcol")
-
-
-def graph_windows2(N: int, rowptr, col, rows: int) -> dict:
-    """pgti_graph_windows2 on one CSR pattern: the two-hop staging plan (ptr, nodes, n1, eptr,
-    roff, eidx, lcol as int16 bits) and its per-window maxima."""
-    rowptr = np.ascontiguousarray(rowptr, np.int32)
-    col = np.ascontiguousarray(col, np.int32)
-    nwin = (N + rows - 1) // rows
-    ptr, n1, eptr = (np.zeros(nwin + 1, np.int32), np.zeros(nwin, np.int32),
-                     np.zeros(nwin + 1, np.int32))
-    tn, te = _i64(0), _i64(0)
-    mn, m1, me = _i32(0), _i32(0), _i32(0)
-    args = lambda *a: (N, _ptr(rowptr), _ptr(col), rows, _ptr(ptr), *a,  # noqa: E731
-                       C.byref(tn), C.byref(te), C.byref(mn), C.byref(m1), C.byref(me))
-    _ok(_graph_windows2(*args(None, _ptr(n1), _ptr(eptr), None, None, None)))
-    nodes = np.zeros(max(int(tn.value), 1), np.int32)
-    roff = np.zeros(int(tn.value) + nwin, np.int32)
-    lcol = np.zeros(max(int(te.value), 1), np.uint16)
-    eidx = np.zeros(max(int(te.value), 1), np.int32)
-    _ok(_graph_windows2(*args(_ptr(nodes), _ptr(n1), _ptr(eptr), _ptr(roff), _ptr(lcol),
-                              _ptr(eidx))))
-    return dict(ptr=ptr, nodes=nodes, n1=n1, eptr=eptr, roff=roff, eidx=eidx,
-                lcol=lcol.view(np.int16), max_nodes=int(mn.value), max_n1=int(m1.value),
-                max_entries=int(me.value))
-
-
-def graph_square(N: int, rowptr, col, val_a, val_b) -> tuple:
-    """pgti_graph_square: (rowptr, col, val_a^2, val_b^2) of the two-hop operators."""
-    rowptr = np.ascontiguousarray(rowptr, np.int32)
-    col = np.ascontiguousarray(col, np.int32)
-    val_a = np.ascontiguousarray(val_a, np.float32)
-    val_b = np.ascontiguousarray(val_b, np.float32)
-    nnz = _i64(0)
-    _ok(_graph_square(N, _ptr(rowptr), _ptr(col), _ptr(val_a), _ptr(val_b), None, None, None,
-                      None, C.byref(nnz)))
-    n = int(nnz.value)
-    orp = np.zeros(N + 1, np.int32)
-    oc, oa, ob = np.zeros(max(n, 1), np.int32), np.zeros(max(n, 1), np.float32), \
-        np.zeros(max(n, 1), np.float32)
-    _ok(_graph_square(N, _ptr(rowptr), _ptr(col), _ptr(val_a), _ptr(val_b), _ptr(orp), _ptr(oc),
-                      _ptr(oa), _ptr(ob), C.byref(nnz)))
-    return orp, oc[:n], oa[:n], ob[:n]
-
-
-def add_squares(csr: dict, N: int) -> dict:
-    """Adds the two-hop operators (P_f^2, (P_b^2)^T on pattern(A^2); P_b^2, (P_f^2)^T on
-    pattern((A^T)^2)) that let the K = 2 tensor-core path diffuse in one launch."""
-    out = dict(csr)
-    out["a2_rowptr"], out["a2_col"], out["Pf2_val"], out["Pb2T_val"] = graph_square(
-        N, csr["a_rowptr"], csr["a_col"], csr["Pf_val"], csr["PbT_val"])
-    out["at2_rowptr"], out["at2_col"], out["Pb2_val"], out["Pf2T_val"] = graph_square(
-        N, csr["at_rowptr"], csr["at_col"], csr["Pb_val"], csr["PfT_val"])
-    return out
-
-
-def add_windows(csr: dict, N: int, rows: int | None = None, two_hop_plan: bool | None = None
-                ) -> dict:
-    """Adds the SpMM staging plans of every pattern present (one-hop, and two-hop if
-    add_squares ran) to a graph_build dict (rows=0: none).  two_hop_plan (default: env
-    PGTI_WIN2=1): also the pgti_graph_windows2 plans (opt-in one-launch K = 2 diffusion)."""
-    if two_hop_plan is None:
-        two_hop_plan = os.environ.get("PGTI_WIN2", "0") == "1"
+def add_windows(csr: dict, N: int, rows: int | None = None) -> dict:
+    """Adds the SpMM staging plans of both patterns to a graph_build dict (rows=0: none)."""
     rows = default_win_rows(N) if rows is None else rows
     out = dict(csr)
     if rows <= 0 or csr["a_col"].size == 0:
         out["win_rows"], out["win_max"] = 0, 0
         return out
     mx = 0
-    for pat in ("a", "at", "a2", "at2"):
-        if pat + "_rowptr" not in csr:
-            continue
+    for pat in ("a", "at"):
         w = graph_windows(N, csr[pat + "_rowptr"], csr[pat + "_col"], rows)
         out[pat + "_win_ptr"], out[pat + "_win_nodes"] = w["win_ptr"], w["win_nodes"]
         out[pat + "_lcol"] = w["lcol"]
         mx = max(mx, w["max_union"])
     out["win_rows"], out["win_max"] = rows, mx
-    if two_hop_plan and "a2_rowptr" not in csr:  # used by K = 2 bf16 diffusions
-        m = dict(max_nodes=0, max_n1=0, max_entries=0)
-        for pat in ("a", "at"):
-            w = graph_windows2(N, csr[pat + "_rowptr"], csr[pat + "_col"], rows)
-            for k in W2_KEYS:
-                out[f"{pat}_w2_{k}"] = w[k]
-            for k in m:
-                m[k] = max(m[k], w[k])
-        out["win2_rows"] = rows
-        out.update({"win2_" + k: v for k, v in m.items()})
     return out
 
 
@@ -394,15 +307,7 @@ class DCRNN:
                               int(self.csr.get("win_rows", 0)), int(self.csr.get("win_max", 0)),
                               g("a_win_ptr"), g("a_win_nodes"), g("a_lcol"),
                               g("at_win_ptr"), g("at_win_nodes"), g("at_lcol"),
-                              int(self.csr["a2_col"].numel()) if "a2_col" in self.csr else 0,
-                              g("a2_rowptr"), g("a2_col"), g("Pf2_val"), g("Pb2T_val"),
-                              g("at2_rowptr"), g("at2_col"), g("Pb2_val"), g("Pf2T_val"),
-                              g("a2_win_ptr"), g("a2_win_nodes"), g("a2_lcol"),
-                              g("at2_win_ptr"), g("at2_win_nodes"), g("at2_lcol"),
-                              int(model), self._tf_mask(teacher_forcing, T_out), int(bool(cheb)),
-                              *[int(self.csr.get("win2_" + k, 0))
-                                for k in ("rows", "max_nodes", "max_n1", "max_entries")],
-                              *[g(f"{p}_w2_{k}") for p in ("a", "at") for k in W2_KEYS])
+                              int(model), self._tf_mask(teacher_forcing, T_out), int(bool(cheb)))
         self.model = int(model)
         self.N, self.F, self.F_out, self.L, self.H, self.K = N, F, F_out, L, H, K
         self.T_in, self.T_out, self.B, self.ld = T_in, T_out, B, ld

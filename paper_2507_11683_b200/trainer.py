@@ -84,7 +84,7 @@ class Trainer:
 
     def __init__(self, cfg, graph, series_fn, params0, rank=0, world=1, device=0, comm=None,
                  seed=3, lr=1e-2, precision=0, shuffle=True, use_cuda_graph=True,
-                 two_hop=False, placement="halo", zero_copy=False, model=0, teacher_forcing=0,
+                 placement="halo", zero_copy=False, model=0, teacher_forcing=0,
                  scheduled_sampling=None, cheb=None):
         import torch
 
@@ -126,8 +126,6 @@ class Trainer:
 
         csr = pgti.graph_build(cfg.N, *graph)
         self.cheb = bool(getattr(cfg, "cheb", False) if cheb is None else cheb)
-        if two_hop and cfg.K == 2 and precision == 1 and not self.cheb:  # one-launch two-hop diffusion (c23)
-            csr = pgti.add_squares(csr, cfg.N)
         csr = pgti.add_windows(csr, cfg.N)
         self.csr = pgti.csr_to_device(csr, self.dev)
         self.model = pgti.DCRNN(cfg.N, cfg.F, cfg.F_out, cfg.L, cfg.H, cfg.K, cfg.T_in,

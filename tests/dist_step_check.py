@@ -68,6 +68,25 @@ def main():
               f"mu rel {e_mu:.1e} sigma rel {e_sd:.1e}", flush=True)
         if not (err <= tol and e_mu <= 1e-12 and e_sd <= 1e-12):
             ok.zero_()
+    # the bench's captured step (gather -> fwd/bwd -> NCCL all-reduce -> Adam, per-layer and aux
+    # streams, PDL) against eager launches on every rank: parameters after 3 steps bitwise equal
+    params = []
+    for use_graph in (False, True):
+        t2 = Trainer(cfg, graph, lambda a, b: rows, theta, rank, world, local, comm,
+                     precision=precision, use_cuda_graph=use_graph)
+        t2.start_epoch(0)
+        for j in range(3):
+            t2.step(j)
+        t2.check()
+        params.append(t2.params.cpu().numpy().view(np.uint32))
+        t2.graph = None
+        del t2
+    torch.cuda.synchronize()
+    same = np.array_equal(params[0], params[1])
+    print(f"rank {rank}: captured step == eager after 3 steps: {same}", flush=True)
+    if not same:
+        ok.zero_()
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
     dist.broadcast(ok, 0)
     comm.close()
     dist.destroy_process_group()

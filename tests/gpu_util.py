@@ -29,15 +29,10 @@ def load_series(pgti, torch, v_rows, row0, cfg, mu=None, sigma=None):
     return s
 
 
-def model_for(pgti, torch, cfg, graph, precision=0, win_rows=None, two_hop=False,
-              win2=False):
-    """win_rows: SpMM staging window (None = the library default, 0 = no staging plan);
-    two_hop: pass the P^2 operators (opt-in single-launch K = 2 diffusion, reading c23);
-    win2: add the two-hop staging plan (opt-in one-launch K = 2 bf16 diffusion)."""
+def model_for(pgti, torch, cfg, graph, precision=0, win_rows=None):
+    """win_rows: SpMM staging window (None = the library default, 0 = no staging plan)."""
     csr = pgti.graph_build(cfg.N, *graph)
-    if two_hop and cfg.K == 2 and precision == 1:
-        csr = pgti.add_squares(csr, cfg.N)
-    csr = pgti.add_windows(csr, cfg.N, win_rows, two_hop_plan=win2)
+    csr = pgti.add_windows(csr, cfg.N, win_rows)
     csr = pgti.csr_to_device(csr, "cuda")
     return pgti.DCRNN(cfg.N, cfg.F, cfg.F_out, cfg.L, cfg.H, cfg.K, cfg.T_in, cfg.T_out, cfg.B,
                       ld_of(cfg), csr, precision, cheb=getattr(cfg, "cheb", False))

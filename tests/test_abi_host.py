@@ -96,86 +96,6 @@ def test_graph_windows_plan(pgti, N, rows, graph):
     assert pgti.add_windows(csr, N, 0)["win_rows"] == 0
 
 
-@pytest.mark.parametrize("N,rows,graph", [(207, 32, "knn"), (37, 7, "er"), (100, 1, "knn"),
-                                           (45, 64, "ring"), (2716, 32, "knn"), (1, 4, "er")])
-def test_graph_windows2_plan(pgti, N, rows, graph):
-    """Two-hop staging plan (pgti_graph_windows2) against brute force: per window the node list
-    is [R, U1 minus R, U2 minus U1] each ascending, n1 = |U1|, and the U1 rows' entries (in CSR
-    order) carry their column's list position and their global CSR index."""
-    g = {"er": lambda: synth.random_graph(N, 0.15, seed=N), "knn": lambda: synth.make_graph(N, 8),
-         "ring": lambda: synth.ring_graph(N)}[graph]()
-    csr = pgti.graph_build(N, *g)
-    full = pgti.add_windows(csr, N, rows, two_hop_plan=True)
-    assert full["win2_rows"] == rows
-    assert "win2_rows" not in pgti.add_windows(csr, N, rows, two_hop_plan=False)
-    mx = dict(max_nodes=0, max_n1=0, max_entries=0)
-    for pat in ("a", "at"):
-        rp, col = csr[pat + "_rowptr"], csr[pat + "_col"]
-        w2 = {k: full[f"{pat}_w2_{k}"] for k in pgti.W2_KEYS}
-        lc = w2["lcol"].view(np.uint16)
-        nwin = -(-N // rows)
-        nbr = lambda S: {int(c) for u in S for c in col[rp[u]:rp[u + 1]]}  # noqa: E731
-        for w in range(nwin):
-            R = list(range(w * rows, min(N, (w + 1) * rows)))
-            U1 = set(R) | nbr(R)
-            U2 = U1 | nbr(U1)
-            want = R + sorted(U1 - set(R)) + sorted(U2 - U1)
-            nodes = w2["nodes"][w2["ptr"][w]:w2["ptr"][w + 1]]
-            assert nodes.tolist() == want
-            assert w2["n1"][w] == len(U1)
-            e0 = w2["eptr"][w]
-            roff = w2["roff"][w2["ptr"][w] + w:]
-            for i, u in enumerate(want[:len(U1)]):
-                ents = np.arange(rp[u], rp[u + 1])
-                sl = slice(e0 + roff[i], e0 + roff[i + 1])
-                assert np.array_equal(w2["eidx"][sl], ents)
-                assert np.array_equal(nodes[lc[sl]], col[ents])
-                if i < len(R):  # hop-2 rows read only hop-1 rows
-                    assert np.all(lc[sl] < len(U1))
-            assert roff[len(U1)] == w2["eptr"][w + 1] - e0
-            mx["max_nodes"] = max(mx["max_nodes"], len(U2))
-            mx["max_n1"] = max(mx["max_n1"], len(U1))
-            mx["max_entries"] = max(mx["max_entries"], int(roff[len(U1)]))
-    for k, v in mx.items():
-        assert full["win2_" + k] == v, k
-
-
-@pytest.mark.parametrize("N,graph", [(207, "knn"), (37, "er"), (45, "ring"), (1, "er")])
-def test_graph_square_matches_oracle_powers(pgti, N, graph):
-    """Two-hop operators (reading c23) against the oracle's dense P_f, P_b squared in float64:
-    P_f^2 and (P_b^2)^T on pattern(A^2), P_b^2 and (P_f^2)^T on pattern((A^T)^2)."""
-    g = {"er": lambda: synth.random_graph(N, 0.15, seed=N), "knn": lambda: synth.make_graph(N, 8),
-         "ring": lambda: synth.ring_graph(N)}[graph]()
-    csr = pgti.add_squares(pgti.graph_build(N, *g), N)
-    Pf, Pb = transitions.transition_matrices(N, *g)
-    Pf, Pb = np.asarray(Pf.todense() if hasattr(Pf, "todense") else Pf), \
-        np.asarray(Pb.todense() if hasattr(Pb, "todense") else Pb)
-
-    def dense(rp, col, val):
-        D = np.zeros((N, N))
-        for i in range(N):
-            assert np.all(np.diff(col[rp[i]:rp[i + 1]]) > 0)  # ascending, no duplicates
-            D[i, col[rp[i]:rp[i + 1]]] = val[rp[i]:rp[i + 1]]
-        return D
-    for (pat, va, vb), (A, Bm) in ((("a2", "Pf2_val", "Pb2T_val"), (Pf @ Pf, (Pb @ Pb).T)),
-                                   (("at2", "Pb2_val", "Pf2T_val"), (Pb @ Pb, (Pf @ Pf).T))):
-        rp, col = csr[pat + "_rowptr"], csr[pat + "_col"]
-        assert rp[-1] == col.size
-        for name, want in ((va, A), (vb, Bm)):
-            got = dense(rp, col, csr[name])
-            assert np.abs(got - want).max() <= 1e-6 * max(1.0, np.abs(want).max()), name
-        # the pattern is the boolean square of the one-hop pattern (explicit zeros included)
-        one = pat[:-1]
-        S = np.zeros((N, N), bool)
-        for i in range(N):
-            S[i, csr[one + "_col"][csr[one + "_rowptr"][i]:csr[one + "_rowptr"][i + 1]]] = True
-        S2 = (S.astype(np.int64) @ S.astype(np.int64)) > 0
-        got = np.zeros((N, N), bool)
-        for i in range(N):
-            got[i, col[rp[i]:rp[i + 1]]] = True
-        assert np.array_equal(got, S2)
-
-
 def test_graph_windows_errors(pgti):
     csr = pgti.graph_build(4, [0, 1], [1, 2], [1.0, 1.0])
     for rows in (0, 65):

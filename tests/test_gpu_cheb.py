@@ -180,18 +180,6 @@ def test_cheb_encdec_vs_oracle(env, precision, tol):
         off += k
 
 
-def test_cheb_rejects_two_hop_operators(env):
-    pgti, torch = env
-    cfg = synth.Config("d", N=30, E=60, F=2, T_in=3, T_out=2, L=1, H=64, K=2, B=2, cheb=True)
-    g = _graph(cfg.N, "knn")
-    m = model_for(pgti, torch, cfg, g, precision=1, two_hop=True)
-    buf = lambda n: torch.zeros(n, device="cuda")  # noqa: E731
-    ws = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
-    with pytest.raises(pgti.PgtiError) as e:  # the descriptor check runs before any launch
-        m.step(buf(1 << 16), buf(1 << 16), buf(1 << 16), buf(1 << 16), buf(4), ws)
-    assert e.value.name == "INVALID_ARG"
-
-
 def test_cheb_trainer_graph_zero_copy_first_loss(env):
     """Trainer(cheb=True) on the bf16 path under CUDA-graph replay with zero-copy windows: the
     first step's loss equals the oracle's Chebyshev loss on the same sampled windows (2e-2), and

@@ -1,4 +1,5 @@
-"""Multi-GPU (real NCCL over NVLink) parity of distributed-index-batching; needs >= 2 GPUs."""
+"""Multi-GPU (real NCCL over NVLink) parity of distributed-index-batching: world = 2, 4, 8 as
+many GPUs as the box has (tests/dist_step_check.py, one rank per GPU under torchrun)."""
 import os
 import subprocess
 import sys
@@ -14,13 +15,15 @@ def _ngpus():
     return torch.cuda.device_count()
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("precision", [0, 1])
-def test_two_rank_nccl_gradient_equals_union_batch(precision):
-    if _ngpus() < 2:
-        pytest.skip("needs 2 GPUs")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr", "127.0.0.1", "--master-port", str(29500 + 11 + precision),
+def test_nccl_gradient_equals_union_batch(precision, world):
+    if _ngpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr", "127.0.0.1", "--master-port",
+           str(29500 + 11 + precision + 2 * world),
            os.path.join(ROOT, "tests", "dist_step_check.py"), str(precision)]
-    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
-    print(p.stdout[-2000:], p.stderr[-2000:])
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    print(p.stdout[-3000:], p.stderr[-2000:])
     assert p.returncode == 0, p.stderr[-3000:]

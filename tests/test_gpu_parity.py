@@ -243,32 +243,6 @@ def test_step_staged_plan_bitexact_both_precisions(env):
             assert r[0] == res[0][0] and np.array_equal(r[1], res[0][1]), precision
 
 
-@pytest.mark.parametrize("name,B,rows,cheb", [("tc_tiny", 3, None, False), ("tc_big", 64, 32, False),
-                                               ("tc_l1", 5, 7, False), ("tc_tiny", 3, 5, True),
-                                               ("metr_la", 64, None, False),
-                                               ("metr_la", 16, 16, True)])
-def test_step_two_hop_plan_bitexact(env, name, B, rows, cheb):
-    """K = 2 bf16 diffusions in one launch from the two-hop staging plan (pgti_graph_windows2):
-    loss and every gradient bit-identical to the two-launch hop chain (powers and Chebyshev)."""
-    pgti, torch = env
-    cfg = (TC_CONFIGS.get(name) or synth.CONFIGS[name]).replace(B=B, K=2, cheb=cheb)
-    cfg = cfg.replace(name=f"{name}_k2_{int(cheb)}")  # ref_for caches by name
-    ref = ref_for(cfg)
-    s = load_series(pgti, torch, ref.v, 0, cfg, ref.mu, ref.sigma)
-    idx = torch.from_numpy(ref.plan(1, 0, epoch=0)[:cfg.B].astype(np.int32)).cuda()
-    ld = ld_of(cfg)
-    x = torch.empty(cfg.B * cfg.T_in * ld, device="cuda")
-    y = torch.empty(cfg.B * cfg.T_out * ld, device="cuda")
-    s.gather(idx, cfg.B, cfg.T_in, cfg.T_out, x, y)
-    theta = synth.make_params(cfg, kind="random")
-    res = []
-    for win2 in (True, False):
-        model = model_for(pgti, torch, cfg, ref.graph, precision=1, win_rows=rows, win2=win2)
-        assert (model.desc.win2_rows > 0) == win2
-        res.append(run_step(pgti, torch, model, theta, x, y, dump=False))
-    assert res[0][0] == res[1][0] and np.array_equal(res[0][1], res[1][1])
-
-
 # ------------------------------------------------------------------ full step (K1..K5)
 def _step_case(env, cfg, seed=0, B=None, scale=1.0):
     pgti, torch = env
@@ -449,7 +423,7 @@ TC_CONFIGS = {
 }
 
 
-def _step_case_tc(env, cfg, B=None, seed=0, two_hop=False, win_rows=None):
+def _step_case_tc(env, cfg, B=None, seed=0, win_rows=None):
     pgti, torch = env
     B = B or cfg.B
     cfg = cfg.replace(B=B)
@@ -461,8 +435,7 @@ def _step_case_tc(env, cfg, B=None, seed=0, two_hop=False, win_rows=None):
     x = torch.empty(B * cfg.T_in * ld, device="cuda")
     y = torch.empty(B * cfg.T_out * ld, device="cuda")
     s.gather(idx, B, cfg.T_in, cfg.T_out, x, y)
-    model = model_for(pgti, torch, cfg, ref.graph, precision=1, two_hop=two_hop,
-                      win_rows=win_rows)
+    model = model_for(pgti, torch, cfg, ref.graph, precision=1, win_rows=win_rows)
     theta = synth.make_params(cfg, seed=synth.SEED_PARAMS + seed, kind="random")
     loss, g, act = run_step(pgti, torch, model, theta, x, y)
     xo, yo = ref.batch(idx_np)
@@ -483,17 +456,14 @@ def test_step_parity_bf16_traffic(env, name, B):
     _check_step(_step_case_tc(env, synth.CONFIGS[name], B=B), tol=TOL_BF16)
 
 
-@pytest.mark.parametrize("name,B,two_hop,win_rows", [("tc_tiny", None, True, 0),
-                                                      ("tc_big", None, True, None),
-                                                      ("tc_big", None, True, 16),
-                                                      ("tc_big", None, False, 16),
-                                                      ("metr_la", 64, True, 0),
-                                                      ("metr_la", 64, True, 32)])
-def test_step_parity_bf16_diffusion_variants(env, name, B, two_hop, win_rows):
-    """The bf16 path with the single-launch two-hop operators (P^2, reading c23) and with
-    staged SpMM (window plans, also of the squared patterns)."""
+@pytest.mark.parametrize("name,B,win_rows", [("tc_tiny", None, 0), ("tc_big", None, 16),
+                                             ("tc_big", None, 32), ("metr_la", 64, 0),
+                                             ("metr_la", 64, 16)])
+def test_step_parity_bf16_staging_plans(env, name, B, win_rows):
+    """The bf16 path with the unstaged SpMM (win_rows 0) and other staging windows than the
+    library default."""
     cfg = TC_CONFIGS.get(name) or synth.CONFIGS[name]
-    _check_step(_step_case_tc(env, cfg, B=B, two_hop=two_hop, win_rows=win_rows), tol=TOL_BF16)
+    _check_step(_step_case_tc(env, cfg, B=B, win_rows=win_rows), tol=TOL_BF16)
 
 
 # ------------------------------------------------------------------ NEXT f4 / f1 index plans
@@ -717,19 +687,16 @@ def test_step_parity_batch_of_one(env, name, precision):
         _check_step(_step_case_tc(env, cfg, B=1 if name != "tc_k3" else None), tol=TOL_BF16)
 
 
-@pytest.mark.parametrize("name,B,transposed", [("tc_tiny", None, 0), ("tc_odd", None, 0),
-                                               ("metr_la", 64, 0), ("pems_bay", 16, 0)])
-def test_step_resident_diffusion_bitexact(env, name, B, transposed, monkeypatch):
-    """The small-graph one-launch diffusion (column chunk of every node resident in shared memory,
-    hop 2 from the bf16 hop-1 rows) gives the bf16 step bit-identical results to the launch-per-hop
-    SpMM path (the default; the resident kernel is opt-in, PGTI_RESIDENT=1)."""
-    pgti, torch = env
+@pytest.mark.parametrize("name,B", [("tc_big", None), ("metr_la", 64)])
+def test_step_spmm_two_vectors_per_lane_bitexact(env, name, B, monkeypatch):
+    """The staged SpMM with two 16-byte vectors per lane (1 KB column chunks, the default for
+    wide bf16 operands) only regroups columns across threads: loss, activations and gradients
+    bit-identical to one vector per lane (PGTI_SPMM_VPL=1)."""
     cfg = TC_CONFIGS.get(name) or synth.CONFIGS[name]
-    cfg = cfg.replace(B=B or cfg.B)
     res = []
-    for flag in ("1", "0"):
-        monkeypatch.setenv("PGTI_RESIDENT", flag)
-        c = _step_case_tc(env, cfg)
+    for flag in ("1", "2"):
+        monkeypatch.setenv("PGTI_SPMM_VPL", flag)
+        c = _step_case_tc(env, cfg, B=B)
         res.append((c["loss"], c["g"], c["act"]))
     assert res[0][0] == res[1][0]
     assert np.array_equal(res[0][1], res[1][1]) and np.array_equal(res[0][2], res[1][2])

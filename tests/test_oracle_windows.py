@@ -134,8 +134,11 @@ def test_eq2_and_ratio():
     # closed-form ratio ~24x at h=12 (-95.8 %)
     r = memory.ratio(105120, 12, 12, 11160, 2)
     assert 23.9 < r < 24.0 and abs((1 - 1 / r) - 0.958) < 1e-3
-    # Chickenpox: Eq. 1 bytes 657,920 (Table 1) over 521*20*8 data + 514 int32 indices
-    assert memory.ratio(521, 4, 4, 20, 1) == 657920 / (83360 + 514 * 4)
+    # Chickenpox: Eq. 1 bytes 657,920 (Table 1) over 521*20*8 data + 514 8-byte indices
+    assert memory.ratio(521, 4, 4, 20, 1) == 657920 / (83360 + 514 * 8)
+    # the int32 device plan (idx_bytes=4)
+    assert memory.ratio(521, 4, 4, 20, 1, idx_bytes=4) == 657920 / (83360 + 514 * 4)
+    assert memory.index_bytes(521, 4, 4, 20, 1, elem_bytes=8) == 83360 + 514 * 8
 
 
 def test_table1_before_sizes_are_eq2_data_term():
