@@ -288,7 +288,7 @@ def kernel_class(name: str) -> str:
         return "spmm"
     if "k_tc_fwd" in n:
         import re
-        m = re.search(r"k_tc_fwd<\s*\d+\s*,\s*([^>]+)>", name)
+        m = re.search(r"k_tc_fwdp?<\s*\d+\s*,\s*([^>]+)>", name)
         mode = m.group(1) if m else ""
         return "gemm_dgrad" if ("2" in mode or "bwd" in mode.lower()) else "gemm_fwd"
     if "k_gconv_fwd" in n:
@@ -408,8 +408,8 @@ def main():
 
     rank, world, local = env_ranks()
     if world > 1:   # NCCL reports each communicator's setup (ranks, transports) on stderr
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ["NCCL_DEBUG"] = "INFO"
+        os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)

@@ -222,7 +222,7 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *g) {
 constexpr int kWinEntBytes = 8 * 4 * 32 * 8;  // [warp][row slot][32] int2, RPW <= 4
 
 template <typename T, int RPW, int VPL, int EPI>
-__global__ void __launch_bounds__(256, VPL == 1 ? (RPW <= 4 ? 3 : 1) : 2)
+__global__ void __launch_bounds__(256, VPL == 1 ? (RPW <= 4 ? 3 : 1) : (RPW <= 2 ? 3 : 2))
     k_spmm_win(const __grid_constant__ WinParams p) {
   using L = Lane<T>;
   constexpr int V = L::V, P = V / 2;

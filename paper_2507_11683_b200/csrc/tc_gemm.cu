@@ -13,6 +13,7 @@
 // Equations: Li et al. Eq. 2-3 [ext], PAPER.md P:168, P:222 (readings c1-c7).
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -89,8 +90,184 @@ constexpr int kFwdThreads = 320, kEpiThreads = 256;
 constexpr int fwd_stages(int nsub) { return nsub == 2 ? 3 : 4; }
 constexpr int kTileLd = 68;  // shared epilogue tile pitch (floats): 16-byte rows, spread banks
 
-__device__ __forceinline__ void epi_bar() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+// named barrier of one epilogue group (8 warps): id 1 + group
+__device__ __forceinline__ void epi_bar(int eg = 0) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + eg), "n"(kEpiThreads) : "memory");
+}
+
+// ------------------------------------------------------------------ forward GEMM epilogue
+// Epilogue
+// threads et = 0..255 (warps 2-9: e = warp - 2, q = warp & 3 = TMEM lane quarter, hh = e >> 2 =
+// column half).
+// (1) While the tile's MMAs run: pull the epilogue's [128 rows][64 fp32] input tiles into L2,
+// and stage the layer-0 x part (the tile's 128 rows of the diffused input, the first sub-tile's
+// weight rows).  Returns nx = F M (0 when there is no x part).
+template <int NSUB, int MODE>
+__device__ __forceinline__ int fwd_epi_prepare(const TcFwd &p, int row0, int ct0, int et,
+                                               float *wx_s, float *xs_s) {
+  const int H = p.H;
+  const int nx = (MODE != kEpiBwd && p.Dx) ? p.F * p.M : 0;
+  {  // while the MMAs run: pull the epilogue's [128 rows][64 fp32] input tiles into L2
+    const int rl = et >> 1, row = row0 + rl;
+    auto pf = [&](const float *base, int64_t pitch) {
+      if (base && row < p.R)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(base + row * pitch + (et & 1) * 32));
+    };
+    if (MODE == kEpiGate && ct0 == 0) pf(p.Hprev, H);
+    if (MODE == kEpiCand) pf(p.u_in + ct0 * 64, H), pf(p.Hprev ? p.Hprev + ct0 * 64 : nullptr, H);
+    if (MODE == kEpiBwd)
+      for (int sub = 0; sub < NSUB; ++sub) {
+        const int ct = ct0 + sub;
+        if (ct == p.fuse_tile) {
+          pf(p.Hprev, 64), pf(p.g_dHprev, 64);
+          if (row < p.R && !(et & 1))  // r is bf16: one 128-byte line per row
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(p.g_r + int64_t(row) * 64));
+        } else if (p.dst_acc[ct]) {
+          pf(p.dst[ct], 64);
+        }
+      }
+  }
+  // layer-0 x part while the MMAs run: the tile's 128 rows of the diffused input and the
+  // first sub-tile's weight rows (visible to every epilogue thread after phase 1's barrier)
+  for (int i = et; i < nx * 64; i += kEpiThreads) {
+    const int mf = i / 64, j = i % 64, m = mf / p.F, f = mf % p.F;
+    wx_s[i] = __ldg(p.Wx + int64_t(m * p.C_in + f) * p.Nout + ct0 * 64 + j);
+  }
+  for (int i = et; i < nx * kBM; i += kEpiThreads) {
+    const int rl = i / nx, mf = i - rl * nx, m = mf / p.F, f = mf - m * p.F;
+    xs_s[i] = row0 + rl < p.R ? __ldg(p.Dx + m * p.dx_mstride + int64_t(row0 + rl) * p.F + f) : 0.f;
+  }
+  return nx;
+}
+
+// (2) The tile's epilogue from the TMEM accumulator at tacc: per 64-column sub-tile, TMEM ->
+// registers -> the shared tile (phase 1), then the coalesced element-wise math and global I/O
+// (phase 2).  `drained` (nullable): arrived on (one thread) once every TMEM load of the tile is
+// complete, so the MMA warp may reuse the accumulator.
+template <int NSUB, int MODE>
+__device__ __forceinline__ void fwd_epi_tile(const TcFwd &p, int row0, int ct0, uint32_t tacc,
+                                             int nx, float *tile_s, float *wx_s,
+                                             const float *xs_s, uint64_t *drained, int eg = 0) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int e = (warp - 2) & 7, q = warp & 3, hh = e >> 2;
+  const int et = e * 32 + lane;  // 0..255
+  const int H = p.H;
+#pragma unroll 1
+  for (int sub = 0; sub < NSUB; ++sub) {
+    const int ct = ct0 + sub;
+    // ---- phase 1: TMEM -> smem tile (thread = one accumulator row, 32 of the 64 columns)
+    if (sub > 0) epi_bar(eg);  // previous sub-tile done reading tile_s / wx_s
+    {
+      const int r = q * 32 + lane;
+      float acc[32];
+      if (p.nkb) {
+        const uint32_t taddr = tacc + (uint32_t(q * 32) << 16) + sub * 64 + hh * 32;
+        tmem_ld16(taddr, acc);
+        tmem_ld16(taddr + 16, acc + 16);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+      }
+      float *dst = tile_s + r * kTileLd + hh * 32;
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) st4(dst + i, make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]));
+    }
+    if (sub > 0)  // x-part weight rows of this sub-tile
+      for (int i = et; i < nx * 64; i += kEpiThreads) {
+        const int mf = i / 64, j = i % 64, m = mf / p.F, f = mf % p.F;
+        wx_s[i] = __ldg(p.Wx + int64_t(m * p.C_in + f) * p.Nout + ct * 64 + j);
+      }
+    if (drained && sub == NSUB - 1) tc_fence_before();  // every TMEM load of the tile is done
+    epi_bar(eg);
+    if (drained && sub == NSUB - 1 && et == 0) mbar_arrive(drained);  // accumulator reusable
+    // ---- phase 2: coalesced element-wise epilogue: 16 threads per row, 4 columns each
+#pragma unroll 2
+    for (int it = 0; it < (kBM * 64 / 4) / kEpiThreads; ++it) {
+      const int idx = it * kEpiThreads + et;
+      const int rl = idx >> 4, c4 = (idx & 15) * 4;
+      const int row = row0 + rl;
+      const bool valid = row < p.R;
+      float4 a = ld4(tile_s + rl * kTileLd + c4);
+      if (MODE == kEpiBwd) {
+        if (!valid) continue;
+        if (ct == p.fuse_tile) {
+          // fused gate backward: a = d(r*H_{t-1}); dG_r = a H r (1-r); dH_{t-1} += a r
+          const int64_t ro = int64_t(row) * 64 + c4, rg = int64_t(row) * 128 + c4;
+          const float4 hp = ld4(p.Hprev + ro), rr = ld4_bf16(p.g_r + ro), dh = ld4(p.g_dHprev + ro);
+          const float4 g = make_float4(a.x * hp.x * rr.x * (1.f - rr.x), a.y * hp.y * rr.y * (1.f - rr.y),
+                                       a.z * hp.z * rr.z * (1.f - rr.z), a.w * hp.w * rr.w * (1.f - rr.w));
+          st4(p.g_dHprev + ro, make_float4(fmaf(a.x, rr.x, dh.x), fmaf(a.y, rr.y, dh.y),
+                                           fmaf(a.z, rr.z, dh.z), fmaf(a.w, rr.w, dh.w)));
+          if (p.g_dG) st4(p.g_dG + rg, g);
+          st4_bf16(p.g_dGb + rg, g);
+        } else {
+          float *d = p.dst[ct] + int64_t(row) * 64 + c4;
+          if (p.dst_acc[ct]) {
+            const float4 o = ld4(d);
+            a.x += o.x, a.y += o.y, a.z += o.z, a.w += o.w;
+          }
+          st4(d, a);
+        }
+        continue;
+      }
+      // forward: pre-activation = acc + bias (+ layer-0 x part)
+      const int jg = ct * 64 + c4;
+      const float4 b = ld4(p.bias + jg);
+      a.x += b.x, a.y += b.y, a.z += b.z, a.w += b.w;
+      if (nx) {
+        const float *xr = xs_s + rl * nx;
+        for (int mf = 0; mf < nx; ++mf) {
+          const float xv = xr[mf];
+          const float4 w = ld4(wx_s + mf * 64 + c4);
+          a.x = fmaf(xv, w.x, a.x), a.y = fmaf(xv, w.y, a.y);
+          a.z = fmaf(xv, w.z, a.z), a.w = fmaf(xv, w.w, a.w);
+        }
+      }
+      const int jh = (MODE == kEpiGate ? 0 : ct * 64) + c4;  // hidden unit of column c4
+      const int64_t ro = int64_t(row) * H + jh;
+      if (MODE == kEpiGate) {
+        const float4 s = make_float4(sigmoid_f(a.x), sigmoid_f(a.y), sigmoid_f(a.z), sigmoid_f(a.w));
+        if (valid) {
+          if (ct == 0) {
+            st4_bf16(p.out_r + ro, s);
+            float4 hp = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (p.Hprev) hp = ld4(p.Hprev + ro);
+            st4_bf16(p.out_rH + ro, make_float4(s.x * hp.x, s.y * hp.y, s.z * hp.z, s.w * hp.w));
+          } else {
+            st4(p.out_u + ro, s);
+          }
+        }
+      } else {  // kEpiCand
+        float4 hn = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid) {
+          const float4 c = make_float4(tanhf(a.x), tanhf(a.y), tanhf(a.z), tanhf(a.w));
+          const float4 u = ld4(p.u_in + ro);
+          float4 hp = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (p.Hprev) hp = ld4(p.Hprev + ro);
+          hn = make_float4(u.x * hp.x + (1.f - u.x) * c.x, u.y * hp.y + (1.f - u.y) * c.y,
+                           u.z * hp.z + (1.f - u.z) * c.z, u.w * hp.w + (1.f - u.w) * c.w);
+          st4_bf16(p.out_c + ro, c);
+          st4(p.out_H + ro, hn);
+          st4_bf16(p.out_Hb + ro, hn);
+        }
+        if (p.yhat) {  // readout: 16 lanes of this row hold its 64 hidden units
+#pragma unroll
+          for (int o = 0; o < 4; ++o) {
+            if (o >= p.F_out) break;
+            float y = hn.x * __ldg(p.Wout + (jh + 0) * p.F_out + o) +
+                      hn.y * __ldg(p.Wout + (jh + 1) * p.F_out + o) +
+                      hn.z * __ldg(p.Wout + (jh + 2) * p.F_out + o) +
+                      hn.w * __ldg(p.Wout + (jh + 3) * p.F_out + o);
+#pragma unroll
+            for (int off = 8; off > 0; off >>= 1) y += __shfl_xor_sync(0xffffffffu, y, off);
+            if ((lane & 15) == 0 && valid)
+              p.yhat[int64_t(row) * p.F_out + o] = y + __ldg(p.bout + o);
+          }
+        }
+      }
+    }
+  }
 }
 
 // NSUB = 64-column sub-tiles per CTA: 1 (small R: more CTAs) or 2 (large R: A read once for
@@ -160,158 +337,140 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
     }
   } else {
     griddep_wait();  // the epilogue reads the predecessor's outputs (H_{t-1}, u, r, dH, ...)
-    const int e = warp - 2, q = warp & 3, hh = e >> 2;
-    const int et = e * 32 + lane;  // 0..255
-    const int H = p.H;
-    const int nx = (MODE != kEpiBwd && p.Dx) ? p.F * p.M : 0;
-    {  // while the MMAs run: pull the epilogue's [128 rows][64 fp32] input tiles into L2
-      const int rl = et >> 1, row = row0 + rl;
-      auto pf = [&](const float *base, int64_t pitch) {
-        if (base && row < p.R)
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(base + row * pitch + (et & 1) * 32));
-      };
-      if (MODE == kEpiGate && ct0 == 0) pf(p.Hprev, H);
-      if (MODE == kEpiCand) pf(p.u_in + ct0 * 64, H), pf(p.Hprev ? p.Hprev + ct0 * 64 : nullptr, H);
-      if (MODE == kEpiBwd)
-        for (int sub = 0; sub < NSUB; ++sub) {
-          const int ct = ct0 + sub;
-          if (ct == p.fuse_tile) {
-            pf(p.Hprev, 64), pf(p.g_dHprev, 64);
-            if (row < p.R && !(et & 1))  // r is bf16: one 128-byte line per row
-              asm volatile("prefetch.global.L2 [%0];" ::"l"(p.g_r + int64_t(row) * 64));
-          } else if (p.dst_acc[ct]) {
-            pf(p.dst[ct], 64);
-          }
-        }
-    }
-    // layer-0 x part while the MMAs run: the tile's 128 rows of the diffused input and the
-    // first sub-tile's weight rows (visible to every epilogue thread after phase 1's barrier)
-    for (int i = et; i < nx * 64; i += kEpiThreads) {
-      const int mf = i / 64, j = i % 64, m = mf / p.F, f = mf % p.F;
-      wx_s[i] = __ldg(p.Wx + int64_t(m * p.C_in + f) * p.Nout + ct0 * 64 + j);
-    }
-    for (int i = et; i < nx * kBM; i += kEpiThreads) {
-      const int rl = i / nx, mf = i - rl * nx, m = mf / p.F, f = mf - m * p.F;
-      xs_s[i] = row0 + rl < p.R ? __ldg(p.Dx + m * p.dx_mstride + int64_t(row0 + rl) * p.F + f) : 0.f;
-    }
+    const int et = (warp - 2) * 32 + lane;
+    const int nx = fwd_epi_prepare<NSUB, MODE>(p, row0, ct0, et, wx_s, xs_s);
     mbar_wait(&bar->tfull, 0);  // MMAs done => every stage buffer is free for the tile
     tc_fence_after();
-#pragma unroll 1
-    for (int sub = 0; sub < NSUB; ++sub) {
-      const int ct = ct0 + sub;
-      // ---- phase 1: TMEM -> smem tile (thread = one accumulator row, 32 of the 64 columns)
-      if (sub > 0) epi_bar();  // previous sub-tile done reading tile_s / wx_s
+    fwd_epi_tile<NSUB, MODE>(p, row0, ct0, tmem, nx, tile_s, wx_s, xs_s, nullptr);
+  }
+  teardown(bar, NT);
+}
+
+// ------------------------------------------------------------------ persistent forward GEMM
+// The same GEMM and epilogue as k_tc_fwd, as one persistent CTA per SM with TWO epilogue groups
+// of 8 warps and a double-buffered TMEM accumulator: the CTA walks the (row tile, column tile)
+// pairs t = blockIdx.x + i gridDim.x; tile i accumulates into TMEM buffer i & 1 and is drained
+// by epilogue group i & 1 (its own shared tile and named barrier), so the TMA producer and the
+// MMA warp run ahead into the next tile while the two groups drain the previous two -- the
+// overlap two co-resident CTAs give, without the producer ever stopping for an epilogue.
+// (A single epilogue group measured slower than two CTAs per SM: the fused GRU epilogue, not the
+// main loop, bounds these GEMMs.)  PGTI_TC_PERSIST=0 selects the per-tile kernel.
+constexpr int kStagesP = 3, kFwdpThreads = 64 + 2 * kEpiThreads;
+struct BarriersP {
+  uint64_t full[kStagesP], empty[kStagesP], tfull[2], tempty[2];
+  uint32_t tmem;
+};
+constexpr int kEpiRegionBytes = kBM * kTileLd * 4 + 20 * 64 * 4 + kBM * 20 * 4;
+constexpr int fwdp_smem_bytes(int nsub) {
+  return kStagesP * (kBM * kBK * 2 + 64 * nsub * kBK * 2) + 2 * kEpiRegionBytes +
+         int(sizeof(BarriersP)) + 1024 + 64;
+}
+
+template <int NSUB, int MODE>
+__global__ void __launch_bounds__(kFwdpThreads, 1)
+    k_tc_fwdp(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
+              const __grid_constant__ CUtensorMap mB, const __grid_constant__ TcFwd p,
+              int ncol_tiles, int ntiles) {
+  constexpr int NT = 64 * NSUB;
+  constexpr int A_BYTES = kBM * kBK * 2, B_BYTES = NT * kBK * 2, STAGE = A_BYTES + B_BYTES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = align1024(smem_raw);
+  uint8_t *epi = smem + kStagesP * STAGE;  // [2][tile_s 128x68 | wx_s 20x64 | xs_s 128x20]
+  BarriersP *bar = reinterpret_cast<BarriersP *>(epi + 2 * kEpiRegionBytes);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  griddep_launch_dependents();
+  if (threadIdx.x == 0) {
+    tma_prefetch(&mA0), tma_prefetch(&mA1), tma_prefetch(&mB);
+    for (int s = 0; s < kStagesP; ++s) mbar_init(&bar->full[s], 1), mbar_init(&bar->empty[s], 1);
+    for (int a = 0; a < 2; ++a) mbar_init(&bar->tfull[a], 1), mbar_init(&bar->tempty[a], 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(&bar->tmem, 2 * NT);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bar->tmem;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // weight tiles (B) come from a plain launch earlier in the step: the first tile's first
+      // ring of B loads goes out before griddepcontrol.wait, everything else after it
+      int g = 0;  // k-blocks issued so far (position in the stage ring)
+      const int pre = min(p.nkb, kStagesP);
       {
-        const int r = q * 32 + lane;
-        float acc[32];
-        if (p.nkb) {
-          const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + sub * 64 + hh * 32;
-          tmem_ld16(taddr, acc);
-          tmem_ld16(taddr + 16, acc + 16);
-          tmem_wait_ld();
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+        const int ct0 = (int(blockIdx.x) % ncol_tiles) * NSUB;
+        for (int kb = 0; kb < pre; ++kb) {
+          mbar_expect_tx(&bar->full[kb], STAGE);
+          tma_load_3d(smem + kb * STAGE + A_BYTES, &mB, &bar->full[kb], p.kb_bx[kb],
+                      p.kb_by[kb] + ct0 * 64, p.kb_bz[kb]);
         }
-        float *dst = tile_s + r * kTileLd + hh * 32;
-#pragma unroll
-        for (int i = 0; i < 32; i += 4) st4(dst + i, make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]));
       }
-      if (sub > 0)  // x-part weight rows of this sub-tile
-        for (int i = et; i < nx * 64; i += kEpiThreads) {
-          const int mf = i / 64, j = i % 64, m = mf / p.F, f = mf % p.F;
-          wx_s[i] = __ldg(p.Wx + int64_t(m * p.C_in + f) * p.Nout + ct * 64 + j);
-        }
-      epi_bar();
-      // ---- phase 2: coalesced element-wise epilogue: 16 threads per row, 4 columns each
-#pragma unroll 2
-      for (int it = 0; it < (kBM * 64 / 4) / kEpiThreads; ++it) {
-        const int idx = it * kEpiThreads + et;
-        const int rl = idx >> 4, c4 = (idx & 15) * 4;
-        const int row = row0 + rl;
-        const bool valid = row < p.R;
-        float4 a = ld4(tile_s + rl * kTileLd + c4);
-        if (MODE == kEpiBwd) {
-          if (!valid) continue;
-          if (ct == p.fuse_tile) {
-            // fused gate backward: a = d(r*H_{t-1}); dG_r = a H r (1-r); dH_{t-1} += a r
-            const int64_t ro = int64_t(row) * 64 + c4, rg = int64_t(row) * 128 + c4;
-            const float4 hp = ld4(p.Hprev + ro), rr = ld4_bf16(p.g_r + ro), dh = ld4(p.g_dHprev + ro);
-            const float4 g = make_float4(a.x * hp.x * rr.x * (1.f - rr.x), a.y * hp.y * rr.y * (1.f - rr.y),
-                                         a.z * hp.z * rr.z * (1.f - rr.z), a.w * hp.w * rr.w * (1.f - rr.w));
-            st4(p.g_dHprev + ro, make_float4(fmaf(a.x, rr.x, dh.x), fmaf(a.y, rr.y, dh.y),
-                                             fmaf(a.z, rr.z, dh.z), fmaf(a.w, rr.w, dh.w)));
-            if (p.g_dG) st4(p.g_dG + rg, g);
-            st4_bf16(p.g_dGb + rg, g);
-          } else {
-            float *d = p.dst[ct] + int64_t(row) * 64 + c4;
-            if (p.dst_acc[ct]) {
-              const float4 o = ld4(d);
-              a.x += o.x, a.y += o.y, a.z += o.z, a.w += o.w;
-            }
-            st4(d, a);
+      griddep_wait();
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int row0 = (t / ncol_tiles) * kBM, ct0 = (t % ncol_tiles) * NSUB;
+        for (int kb = 0; kb < p.nkb; ++kb, ++g) {
+          const int s = g % kStagesP;
+          uint8_t *a = smem + s * STAGE;
+          if (g >= pre) {
+            if (g >= kStagesP) mbar_wait(&bar->empty[s], ((g / kStagesP) & 1) ^ 1);
+            mbar_expect_tx(&bar->full[s], STAGE);
+            tma_load_3d(a + A_BYTES, &mB, &bar->full[s], p.kb_bx[kb], p.kb_by[kb] + ct0 * 64,
+                        p.kb_bz[kb]);
           }
-          continue;
-        }
-        // forward: pre-activation = acc + bias (+ layer-0 x part)
-        const int jg = ct * 64 + c4;
-        const float4 b = ld4(p.bias + jg);
-        a.x += b.x, a.y += b.y, a.z += b.z, a.w += b.w;
-        if (nx) {
-          const float *xr = xs_s + rl * nx;
-          for (int mf = 0; mf < nx; ++mf) {
-            const float xv = xr[mf];
-            const float4 w = ld4(wx_s + mf * 64 + c4);
-            a.x = fmaf(xv, w.x, a.x), a.y = fmaf(xv, w.y, a.y);
-            a.z = fmaf(xv, w.z, a.z), a.w = fmaf(xv, w.w, a.w);
-          }
-        }
-        const int jh = (MODE == kEpiGate ? 0 : ct * 64) + c4;  // hidden unit of column c4
-        const int64_t ro = int64_t(row) * H + jh;
-        if (MODE == kEpiGate) {
-          const float4 s = make_float4(sigmoid_f(a.x), sigmoid_f(a.y), sigmoid_f(a.z), sigmoid_f(a.w));
-          if (valid) {
-            if (ct == 0) {
-              st4_bf16(p.out_r + ro, s);
-              float4 hp = make_float4(0.f, 0.f, 0.f, 0.f);
-              if (p.Hprev) hp = ld4(p.Hprev + ro);
-              st4_bf16(p.out_rH + ro, make_float4(s.x * hp.x, s.y * hp.y, s.z * hp.z, s.w * hp.w));
-            } else {
-              st4(p.out_u + ro, s);
-            }
-          }
-        } else {  // kEpiCand
-          float4 hn = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (valid) {
-            const float4 c = make_float4(tanhf(a.x), tanhf(a.y), tanhf(a.z), tanhf(a.w));
-            const float4 u = ld4(p.u_in + ro);
-            float4 hp = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (p.Hprev) hp = ld4(p.Hprev + ro);
-            hn = make_float4(u.x * hp.x + (1.f - u.x) * c.x, u.y * hp.y + (1.f - u.y) * c.y,
-                             u.z * hp.z + (1.f - u.z) * c.z, u.w * hp.w + (1.f - u.w) * c.w);
-            st4_bf16(p.out_c + ro, c);
-            st4(p.out_H + ro, hn);
-            st4_bf16(p.out_Hb + ro, hn);
-          }
-          if (p.yhat) {  // readout: 16 lanes of this row hold its 64 hidden units
-#pragma unroll
-            for (int o = 0; o < 4; ++o) {
-              if (o >= p.F_out) break;
-              float y = hn.x * __ldg(p.Wout + (jh + 0) * p.F_out + o) +
-                        hn.y * __ldg(p.Wout + (jh + 1) * p.F_out + o) +
-                        hn.z * __ldg(p.Wout + (jh + 2) * p.F_out + o) +
-                        hn.w * __ldg(p.Wout + (jh + 3) * p.F_out + o);
-#pragma unroll
-              for (int off = 8; off > 0; off >>= 1) y += __shfl_xor_sync(0xffffffffu, y, off);
-              if ((lane & 15) == 0 && valid)
-                p.yhat[int64_t(row) * p.F_out + o] = y + __ldg(p.bout + o);
-            }
-          }
+          tma_load_3d(a, p.kb_as[kb] ? &mA1 : &mA0, &bar->full[s], p.kb_ac[kb], row0,
+                      p.kb_am[kb]);
         }
       }
     }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(kBM, NT, false, false);
+      int g = 0, i = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        const int ab = i & 1;
+        if (i >= 2) {  // group ab has drained this accumulator's previous tile
+          mbar_wait(&bar->tempty[ab], ((i >> 1) & 1) ^ 1);
+          tc_fence_after();
+        }
+        const uint32_t tacc = tmem + uint32_t(ab * NT);
+        for (int kb = 0; kb < p.nkb; ++kb, ++g) {
+          const int s = g % kStagesP;
+          mbar_wait(&bar->full[s], (g / kStagesP) & 1);
+          tc_fence_after();
+          const uint32_t a = smem_u32(smem + s * STAGE), b = a + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            mma_bf16(tacc, desc_sw128(a + 32 * k, 16, 1024), desc_sw128(b + 32 * k, 16, 1024),
+                     idesc, (kb | k) != 0);
+          mma_commit(&bar->empty[s]);
+        }
+        mma_commit(&bar->tfull[ab]);
+      }
+    }
+  } else {
+    griddep_wait();  // the epilogue reads the predecessor's outputs (H_{t-1}, u, r, dH, ...)
+    const int eg = (warp - 2) >> 3;  // epilogue group: tiles i with i & 1 == eg
+    const int et = ((warp - 2) & 7) * 32 + lane;
+    float *tile_s = reinterpret_cast<float *>(epi + eg * kEpiRegionBytes);
+    float *wx_s = tile_s + kBM * kTileLd;
+    float *xs_s = wx_s + 20 * 64;
+    int k = 0;  // this group's tiles so far
+    for (int t = blockIdx.x + eg * gridDim.x; t < ntiles; t += 2 * gridDim.x, ++k) {
+      const int row0 = (t / ncol_tiles) * kBM, ct0 = (t % ncol_tiles) * NSUB;
+      if (k > 0) epi_bar(eg);  // the previous tile's phase 2 is done with tile_s / wx_s / xs_s
+      const int nx = fwd_epi_prepare<NSUB, MODE>(p, row0, ct0, et, wx_s, xs_s);
+      mbar_wait(&bar->tfull[eg], k & 1);
+      tc_fence_after();
+      fwd_epi_tile<NSUB, MODE>(p, row0, ct0, tmem + uint32_t(eg * NT), nx, tile_s, wx_s, xs_s,
+                               &bar->tempty[eg], eg);
+    }
   }
-  teardown(bar, NT);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 2 * NT);
+  }
 }
 
 // ================================================================== wgrad (MN-major A and B)
@@ -515,6 +674,33 @@ cudaError_t launch_tc_fwd(const TcFwd &p, cudaStream_t s) {
                                  : 1.0 + (p.dst_acc[0] ? 1.0 : 0.0);
   const double bytes = 2.0 * p.R * 64 * p.nkb + 2.0 * p.nkb * 64 * N + 4.0 * p.R * N * io / 2 * 2;
   ProfScope prof(p.mode == kEpiBwd ? kProfGemmDgrad : kProfGemmFwd, s, bytes, 2.0 * p.R * Kt * N);
+  static const bool persist = [] {
+    const char *e = std::getenv("PGTI_TC_PERSIST");
+    return !(e && e[0] == '0');
+  }();
+  // persistent form once every SM gets >= 4 tiles (full PeMS: 5,580; PeMS-All-LA: 1,358): full
+  // PeMS 883 -> 930 samples/s; with few tiles per SM (METR-LA: 208) the per-tile kernel with two
+  // CTAs per SM is faster (39.8 K vs 35.6 K)
+  const int ncol = p.ntiles / nsub, ntiles = row_tiles * ncol;
+  if (persist && p.nkb > 0 && ntiles >= 4 * kNumSMs) {
+    const int gridp = std::min(ntiles, kNumSMs);
+    const int smem = fwdp_smem_bytes(nsub);
+    auto gop = [&](auto kernel) -> cudaError_t {
+      cudaError_t e = set_smem(kernel, smem);
+      if (e != cudaSuccess) return e;
+      return pdl_launch(kernel, dim3(unsigned(gridp)), dim3(kFwdpThreads), smem, s, ma0, ma1,
+                        mb, p, ncol, ntiles);
+    };
+    switch (p.mode * 2 + (nsub - 1)) {
+      case kEpiGate * 2: return gop(k_tc_fwdp<1, kEpiGate>);
+      case kEpiGate * 2 + 1: return gop(k_tc_fwdp<2, kEpiGate>);
+      case kEpiCand * 2: return gop(k_tc_fwdp<1, kEpiCand>);
+      case kEpiCand * 2 + 1: return gop(k_tc_fwdp<2, kEpiCand>);
+      case kEpiBwd * 2: return gop(k_tc_fwdp<1, kEpiBwd>);
+      case kEpiBwd * 2 + 1: return gop(k_tc_fwdp<2, kEpiBwd>);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   auto go = [&](auto kernel, int smem) -> cudaError_t {
     cudaError_t e = set_smem(kernel, smem);  // idempotent, cheap
     if (e != cudaSuccess) return e;

@@ -190,14 +190,16 @@ def graph_build(N: int, src, dst, w) -> dict:
 
 
 def default_win_rows(N: int) -> int:
-    """Rows per SpMM staging window (0 = gather neighbour rows straight from L2).  Measured in
-    the bf16 training step on B200 (samples/s, no plan / 16 / 32 / 64 rows): METR-LA 30.8 K /
-    31.2 K / 31.7 K; PeMS-Bay 22.0 K / 22.6 K / 22.6 K; PeMS-All-LA 2.74 K / 2.96 K / 3.01 K /
-    2.11 K; full PeMS 662 / 725 / 740 / 515.  PGTI_WIN_ROWS overrides (A/B measurements)."""
+    """Rows per SpMM staging window (0 = gather neighbour rows straight from L2).  Round 2 (two
+    vectors per lane, entry lists, 3 CTAs per SM at 16 rows): 16 rows beat 32 in the bf16 step,
+    full PeMS 897 vs 870 and METR-LA 39.8 K vs 37.2 K samples/s (same box).  Round 1 (samples/s,
+    no plan / 16 / 32 / 64 rows): METR-LA 30.8 K / 31.2 K / 31.7 K; PeMS-Bay 22.0 K / 22.6 K /
+    22.6 K; PeMS-All-LA 2.74 K / 2.96 K / 3.01 K / 2.11 K; full PeMS 662 / 725 / 740 / 515.
+    PGTI_WIN_ROWS overrides (A/B measurements)."""
     env = os.environ.get("PGTI_WIN_ROWS")
     if env is not None:
         return int(env)
-    return 32
+    return 16
 
 
 def graph_windows(N: int, rowptr, col, rows: int) -> dict:
