@@ -88,7 +88,6 @@ pgti_status check_desc(const pgti_dcrnn_desc *desc, Dims *out) {
                  g.win_rows);
   Dims d{g.N, g.F, g.F_out, g.L, g.H, g.K, g.T_in, g.T_out, g.B, 2 * g.K + 1,
          int64_t(g.N) * g.B, g.ld, g.precision, g.model, g.teacher_forcing, g.cheb};
-  if (g.K > 0 && g.win_rows > 0) d.win_rows = g.win_rows, d.win_max = g.win_max;
   *out = d;
   return PGTI_OK;
 }
@@ -96,7 +95,7 @@ pgti_status check_desc(const pgti_dcrnn_desc *desc, Dims *out) {
 namespace {
 // term t of a job: pattern(A) (pat 0) or pattern(A^T) (pat 1) with values val, operand X
 void set_term(SpmmJob &j, int t, const pgti_dcrnn_desc &g, int pat, const float *val,
-              const float *X, const Dims *d = nullptr) {
+              const float *X) {
   // pat: 0 = pattern(A), 1 = pattern(A^T)
   j.rowptr[t] = pat ? g.at_rowptr : g.a_rowptr;
   j.col[t] = pat ? g.at_col : g.a_col;
@@ -107,11 +106,6 @@ void set_term(SpmmJob &j, int t, const pgti_dcrnn_desc &g, int pat, const float 
   j.win_nodes[t] = pat ? g.at_win_nodes : g.a_win_nodes;
   j.lcol[t] = pat ? g.at_lcol : g.a_lcol;
   j.win_rows = g.win_rows, j.win_max = g.win_max;
-  j.ent[t] = nullptr, j.npad[t] = nullptr;
-  if (d && d->ent[0]) {  // the step's packed plan (tensor-core path)
-    const int c = val == g.Pf_val ? 0 : val == g.PbT_val ? 1 : val == g.Pb_val ? 2 : 3;
-    j.ent[t] = d->ent[c], j.npad[t] = d->npad[pat];
-  }
 }
 }  // namespace
 
@@ -127,11 +121,11 @@ cudaError_t diffuse_fwd(const pgti_dcrnn_desc &g, const Dims &d, float *base, in
     const float *xf = reinterpret_cast<const float *>(k == 1 ? z : blk(k - 1));
     const float *xb = reinterpret_cast<const float *>(k == 1 ? z : blk(d.K + k - 1));
     if (!transposed) {
-      set_term(j[0], 0, g, 0, g.Pf_val, xf, &d);
-      set_term(j[1], 0, g, 1, g.Pb_val, xb, &d);
+      set_term(j[0], 0, g, 0, g.Pf_val, xf);
+      set_term(j[1], 0, g, 1, g.Pb_val, xb);
     } else {
-      set_term(j[0], 0, g, 1, g.PfT_val, xf, &d);
-      set_term(j[1], 0, g, 0, g.PbT_val, xb, &d);
+      set_term(j[0], 0, g, 1, g.PfT_val, xf);
+      set_term(j[1], 0, g, 0, g.PbT_val, xb);
     }
     j[0].Y = reinterpret_cast<float *>(blk(k));
     j[1].Y = reinterpret_cast<float *>(blk(d.K + k));

@@ -18,14 +18,6 @@ struct Dims {
   // decoder step s >= 1 fed the target y_{s-1} (else its own prediction yhat_{s-1})
   bool fed_truth(int s) const { return s >= 1 && ((teacher >> (s - 1)) & 1); }
   int cheb;     // diffusion blocks by the Chebyshev recurrence (reading c25)
-  int win_rows = 0, win_max = 0;  // the SpMM staging plan of the desc (0: none)
-  // step-local packed copy of the staging plan (tensor-core path, built per step into the
-  // workspace by launch_pack_plan): per (pattern, values) combo c -- 0 (A, P_f), 1 (A, P_b^T),
-  // 2 (A^T, P_b), 3 (A^T, P_f^T) -- ent[c][(win * win_rows + i) * 32 + u] = (staged-row byte
-  // offset at 512-byte rows, value bits) of entry u of row i of the window (zero padded); per
-  // pattern npad[p][win * win_max + k] = node k of the window's union.  Null: not packed.
-  const int2 *ent[4] = {nullptr, nullptr, nullptr, nullptr};
-  const int32_t *npad[2] = {nullptr, nullptr};
   // hidden-state steps: T_in (stepwise) or T_in + T_out (encoder then decoder)
   int steps() const { return T_in + (model ? T_out : 0); }
 };

@@ -72,7 +72,7 @@ cudaError_t record(StreamPool *p, cudaStream_t st, cudaEvent_t *out) {
 
 // ------------------------------------------------------------------ workspace
 struct LayoutTC {
-  size_t Dx, Dy, yhat, dyhat, lossp, pent, pnodes, total;
+  size_t Dx, Dy, yhat, dyhat, lossp, total;
   std::vector<size_t> DHb, DrHb, H32, Rg, Ug, Cg, dGb, dCb, Wf_ru, Wf_c, Wd_ru, Wd_c;
   std::vector<size_t> Q, wpart, spart, dHrec0, dHrec1, dHup0, dHup1;
   size_t wpart_floats, spart_floats;
@@ -129,12 +129,6 @@ LayoutTC make_layout_tc(const Dims &d) {
   L.yhat = take(size_t(d.T_out) * R * d.F_out * 4);
   L.dyhat = take(size_t(d.T_out) * R * d.F_out * 4);
   L.lossp = take(size_t(kLossBlocks) * 8);
-  L.pent = L.pnodes = 0;
-  if (d.win_rows > 0 && d.win_max > 0) {  // packed SpMM staging plan (rebuilt every step)
-    const size_t nwin = size_t(ceil_div(d.N, d.win_rows));
-    L.pent = take(4 * nwin * d.win_rows * 32 * 8);
-    L.pnodes = take(2 * nwin * d.win_max * 4);
-  }
   L.total = off;
   return L;
 }
@@ -143,11 +137,10 @@ LayoutTC make_layout_tc(const Dims &d) {
 
 size_t workspace_tc(const Dims &d) { return make_layout_tc(d).total; }
 
-pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d0, const float *params,
+pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *params,
                         float *grads, const WindowSrc &x, const WindowSrc &y, float *loss_dev,
                         char *ws, float *act_dump, cudaStream_t s) {
-  const LayoutTC Ly = make_layout_tc(d0);
-  Dims d = d0;
+  const LayoutTC Ly = make_layout_tc(d);
   const ParamOffsets P = param_offsets(d);
   auto Fp = [&](size_t off) { return reinterpret_cast<float *>(ws + off); };
   auto Bp = [&](size_t off) { return reinterpret_cast<bf16 *>(ws + off); };
@@ -172,15 +165,6 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d0, const float *p
   for (int l = 1; l < L; ++l) st[l] = sp->side[l - 1];
 
   // ------------------------------------------------------------------ prologue on s
-  if (d.win_rows > 0 && d.win_max > 0 && !std::getenv("PGTI_NO_PACKED_PLAN")) {
-    int2 *pe = reinterpret_cast<int2 *>(ws + Ly.pent);
-    int32_t *pn = reinterpret_cast<int32_t *>(ws + Ly.pnodes);
-    CU(launch_pack_plan(g, pe, pn, s));
-    const size_t per_c = size_t(ceil_div(d.N, d.win_rows)) * d.win_rows * 32;
-    const size_t per_p = size_t(ceil_div(d.N, d.win_rows)) * d.win_max;
-    for (int c = 0; c < 4; ++c) d.ent[c] = pe + c * per_c;
-    for (int q = 0; q < 2; ++q) d.npad[q] = pn + q * per_p;
-  }
   {
     WeightJob jobs[32];
     int nj = 0;

@@ -36,19 +36,11 @@ struct SpmmJob {
   const int32_t *win_nodes[2];
   const uint16_t *lcol[2];
   int win_rows, win_max;
-  // optional packed plan of each term (Dims::ent / npad): entries at fixed per-row slots and
-  // the union's node ids at a fixed per-window stride, so no load address depends on rowptr /
-  // win_ptr
-  const int2 *ent[2];
-  const int32_t *npad[2];
   // filled by launch_spmm
   int64_t warp_begin, chunks;
 };
 constexpr int kMaxSpmmJobs = 4;
 cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s);
-// Builds the packed staging plan (see Dims::ent / npad) of a desc's two CSR patterns into
-// ent[4][nwin * win_rows * 32] and npad[2][nwin * win_max].
-cudaError_t launch_pack_plan(const pgti_dcrnn_desc &g, int2 *ent, int32_t *npad, cudaStream_t s);
 
 // ------------------------------------------------------------------ K3' fp32 SIMT GEMMs
 // Virtual A operand of the diffusion convolution: row r, column k = m*C_in + c reads

@@ -262,14 +262,7 @@ __global__ void __launch_bounds__(256, VPL == 1 ? (RPW <= 4 ? 3 : 1) : (RPW <= 2
     // overlap: warp w stages union rows w, w+8, .. -- lane l holds the node id of row w + 8 l
     // (rows past 8 x 32 come through the fallback loop below); and each of this warp's rows'
     // first 32 CSR entries (lane u: entry u) as (staged-row byte offset, value)
-    const int32_t *npad = jb.npad[t];
-    const int2 *pent = jb.ent[t];
-    // packed plan: every index address is known up front (one round trip instead of the
-    // win_ptr -> win_nodes and rowptr -> (lcol, val) chains)
-    const int my_node = warp + 8 * lane < nu
-                            ? __ldg(npad ? npad + int64_t(win) * p.win_max + warp + 8 * lane
-                                         : jb.win_nodes[t] + ub + warp + 8 * lane)
-                            : 0;
+    const int my_node = warp + 8 * lane < nu ? __ldg(jb.win_nodes[t] + ub + warp + 8 * lane) : 0;
     const uint16_t *lc = jb.lcol[t];
     const float *val = jb.val[t];
     int beg[RPW], cnt[RPW];
@@ -280,13 +273,9 @@ __global__ void __launch_bounds__(256, VPL == 1 ? (RPW <= 4 ? 3 : 1) : (RPW <= 2
       beg[i] = cnt[i] = 0;
       if (i < SLOTS) ent[i] = make_int2(0, 0);
       if (r >= p.win_rows || n >= p.N) continue;  // warp-uniform
-      if (pent && i < SLOTS) {
-        const int2 e = __ldg(pent + (int64_t(win) * p.win_rows + r) * 32 + lane);
-        ent[i] = make_int2(e.x * VPL, e.y);
-      }
       beg[i] = __ldg(jb.rowptr[t] + n);
       cnt[i] = __ldg(jb.rowptr[t] + n + 1) - beg[i];
-      if (!pent && i < SLOTS && lane < cnt[i])
+      if (i < SLOTS && lane < cnt[i])
         ent[i] = make_int2(int(__ldg(lc + beg[i] + lane)) * ROWB,
                            __float_as_int(__ldg(val + beg[i] + lane)));
     }
@@ -373,43 +362,6 @@ __global__ void __launch_bounds__(256, VPL == 1 ? (RPW <= 4 ? 3 : 1) : (RPW <= 2
 #pragma unroll
     for (int v = 0; v < VPL; ++v)
       if (vec0 + 32 * v < vecs) finish<L, T, EPI>(jb, acc[i][v], o + 32 * v * V);
-  }
-}
-
-// Packed staging plan (Dims::ent / npad), rebuilt at the start of every tensor-core step from
-// the desc's CSR and window plan (a few MB, microseconds): thread = (combo, window row, slot) or
-// (pattern, window, union position).
-__global__ void k_pack_plan(const __grid_constant__ pgti_dcrnn_desc g, int nwin, int2 *ent,
-                            int32_t *npad) {
-  griddep_launch_dependents();
-  const int64_t per_c = int64_t(nwin) * g.win_rows * 32;
-  const int64_t per_p = int64_t(nwin) * g.win_max;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < 4 * per_c + 2 * per_p;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    if (i < 4 * per_c) {
-      const int c = int(i / per_c);
-      const int64_t q = i - c * per_c;
-      const int u = int(q & 31), wr = int(q >> 5), n = wr;  // window row == node (win*rows + i)
-      const int pat = c >> 1;
-      const int32_t *rp = pat ? g.at_rowptr : g.a_rowptr;
-      const uint16_t *lc = pat ? g.at_lcol : g.a_lcol;
-      const float *val = c == 0 ? g.Pf_val : c == 1 ? g.PbT_val : c == 2 ? g.Pb_val : g.PfT_val;
-      int2 e = make_int2(0, 0);
-      if (n < g.N) {
-        const int b = rp[n], cnt = rp[n + 1] - b;
-        if (u < cnt) e = make_int2(int(lc[b + u]) * 512, __float_as_int(val[b + u]));
-      }
-      ent[i] = e;
-    } else {
-      const int64_t j = i - 4 * per_c;
-      const int pat = int(j / per_p);
-      const int64_t q = j - pat * per_p;
-      const int w = int(q / g.win_max), k = int(q - int64_t(w) * g.win_max);
-      const int32_t *wp = pat ? g.at_win_ptr : g.a_win_ptr;
-      const int32_t *wn = pat ? g.at_win_nodes : g.a_win_nodes;
-      const int b = wp[w], nu = wp[w + 1] - b;
-      npad[j] = k < nu ? wn[b + k] : 0;
-    }
   }
 }
 
@@ -571,16 +523,6 @@ cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s) {
     return gen ? pdl_launch(k_spmm<float, true>, dim3(blocks), dim3(256), 0, s, p)
                : pdl_launch(k_spmm<float, false>, dim3(blocks), dim3(256), 0, s, p);
   return pdl_launch(k_spmm_scalar, dim3(blocks), dim3(256), 0, s, p);
-}
-
-cudaError_t launch_pack_plan(const pgti_dcrnn_desc &g, int2 *ent, int32_t *npad, cudaStream_t s) {
-  if (g.win_rows <= 0 || g.win_max <= 0) return cudaErrorInvalidValue;
-  const int nwin = int(ceil_div(g.N, g.win_rows));
-  const int64_t n = 4 * int64_t(nwin) * g.win_rows * 32 + 2 * int64_t(nwin) * g.win_max;
-  ProfScope prof(kProfSpmm, s, double(n) * 8.0, 0.0);
-  k_pack_plan<<<unsigned(std::min<int64_t>(ceil_div(n, 256), 4 * kNumSMs)), 256, 0, s>>>(
-      g, nwin, ent, npad);
-  return cudaGetLastError();
 }
 
 }  // namespace pgti

@@ -702,28 +702,10 @@ def test_step_spmm_two_vectors_per_lane_bitexact(env, name, B, monkeypatch):
     assert np.array_equal(res[0][1], res[1][1]) and np.array_equal(res[0][2], res[1][2])
 
 
-@pytest.mark.parametrize("name,B", [("tc_big", None), ("metr_la", 64)])
-def test_step_packed_spmm_plan_bitexact(env, name, B, monkeypatch):
-    """The step-local packed staging plan (entries at fixed per-row slots, union node ids at a
-    fixed per-window stride, rebuilt from the CSR each step) only changes where the SpMM reads
-    its indices: loss, activations and gradients bit-identical to the unpacked plan."""
-    cfg = TC_CONFIGS.get(name) or synth.CONFIGS[name]
-    res = []
-    for flag in ("1", None):
-        if flag:
-            monkeypatch.setenv("PGTI_NO_PACKED_PLAN", flag)
-        else:
-            monkeypatch.delenv("PGTI_NO_PACKED_PLAN", raising=False)
-        c = _step_case_tc(env, cfg, B=B)
-        res.append((c["loss"], c["g"], c["act"]))
-    assert res[0][0] == res[1][0]
-    assert np.array_equal(res[0][1], res[1][1]) and np.array_equal(res[0][2], res[1][2])
-
-
-def test_step_dense_rows_packed_and_unpacked(env, monkeypatch):
+def test_step_dense_rows(env):
     """Rows with more than 32 CSR entries (an Erdos-Renyi graph with p = 0.5: ~40 per row) on the
-    bf16 path: the entry lists hold 32 per pass, the rest is read in further passes (packed plan
-    or not).  Against the oracle at 2e-2, and packed == unpacked bitwise."""
+    bf16 path: the staged SpMM's per-warp entry lists hold 32 entries per pass, the rest is read
+    in further passes.  Against the oracle at 2e-2."""
     pgti, torch = env
     cfg = synth.Config("tc_dense", N=80, E=60, F=2, T_in=3, T_out=2, L=2, H=64, K=2, B=8)
     ref = pipeline.Reference(cfg, graph=synth.random_graph(cfg.N, 0.5, seed=5))
@@ -735,17 +717,10 @@ def test_step_dense_rows_packed_and_unpacked(env, monkeypatch):
     y = torch.empty(cfg.B * cfg.T_out * ld, device="cuda")
     s.gather(torch.from_numpy(idx_np.astype(np.int32)).cuda(), cfg.B, cfg.T_in, cfg.T_out, x, y)
     theta = synth.make_params(cfg, kind="random")
-    res = []
-    for flag in ("1", None):
-        if flag:
-            monkeypatch.setenv("PGTI_NO_PACKED_PLAN", flag)
-        else:
-            monkeypatch.delenv("PGTI_NO_PACKED_PLAN", raising=False)
-        model = model_for(pgti, torch, cfg, ref.graph, precision=1)
-        res.append(run_step(pgti, torch, model, theta, x, y))
-    assert res[0][0] == res[1][0] and np.array_equal(res[0][1], res[1][1])
+    model = model_for(pgti, torch, cfg, ref.graph, precision=1)
+    loss, g, act = run_step(pgti, torch, model, theta, x, y)
     xo, yo = ref.batch(idx_np)
     loss_ref, g_ref, fwd = dcgru.backward(theta.astype(np.float64), ref.d, ref.Pf, ref.Pb,
                                           xo.astype(np.float64), yo.astype(np.float64))
-    _check_step(dict(loss=res[1][0], g=res[1][1], act=res[1][2], loss_ref=loss_ref, g_ref=g_ref,
-                     fwd=fwd, cfg=cfg, ref=ref, margin=1.0, B=cfg.B), tol=TOL_BF16)
+    _check_step(dict(loss=loss, g=g, act=act, loss_ref=loss_ref, g_ref=g_ref, fwd=fwd, cfg=cfg,
+                     ref=ref, margin=1.0, B=cfg.B), tol=TOL_BF16)
