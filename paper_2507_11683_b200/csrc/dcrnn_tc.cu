@@ -13,6 +13,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <vector>
 
@@ -72,13 +73,15 @@ cudaError_t record(StreamPool *p, cudaStream_t st, cudaEvent_t *out) {
 
 // ------------------------------------------------------------------ workspace
 struct LayoutTC {
-  size_t Dx, Dy, yhat, dyhat, lossp, total;
+  size_t Dx, Dy, Xb, yhat, dyhat, lossp, total;
   std::vector<size_t> DHb, DrHb, H32, Rg, Ug, Cg, dGb, dCb, Wf_ru, Wf_c, Wd_ru, Wd_c;
   std::vector<size_t> Q, wpart, spart, dHrec0, dHrec1, dHup0, dHup1;
   size_t wpart_floats, spart_floats;
 };
 
-int nkb_total(const Dims &d, int l) { return l == 0 ? d.M : 2 * d.M; }
+// forward B k-blocks per layer: layer 0 = the M hidden blocks + one x k-block (the layer-0
+// input channels folded into the MMA); layer > 0 = M x (input, hidden)
+int nkb_total(const Dims &d, int l) { return l == 0 ? d.M + 1 : 2 * d.M; }
 int vrows(const Dims &d, int l) { return l == 0 ? d.M * 64 : d.M * (d.H + d.H); }
 
 LayoutTC make_layout_tc(const Dims &d) {
@@ -93,6 +96,7 @@ LayoutTC make_layout_tc(const Dims &d) {
   const size_t TT = size_t(d.steps());  // hidden-state steps (encoder + decoder for model 1)
   L.Dx = take(M * T * R * d.F * 4);
   L.Dy = take(d.model ? size_t(d.T_out) * M * R * d.F_out * 4 : 0);
+  L.Xb = take(T * R * 64 * 2);  // layer-0 input channels as one bf16 k-block per row
   const int Tmax = std::max(d.T_in, d.model ? d.T_out : 0);
   const size_t spf = std::max(small_wgrad_partial_floats(Tmax, int(d.R), 2 * d.H),
                               small_wgrad_partial_floats(d.T_out, int(d.R), d.H));
@@ -179,6 +183,11 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
   }
   CU(launch_x_prep(x, d.B, T, d.ld, d.N, d.F, Dx, err, s));
   CU(diffuse_fwd(g, d, Dx, int64_t(T) * RF, T, RF, int64_t(d.B) * d.F, s));
+  // the encoder's layer-0 input part goes through the MMA: all M F diffused input channels of a
+  // row packed into one bf16 k-block (the decoder's per-step input keeps the FFMA epilogue)
+  bf16 *Xb = Bp(Ly.Xb);
+  const bool xfold = !std::getenv("PGTI_NO_XFOLD");
+  if (xfold) CU(launch_xpack(Dx, int64_t(T) * RF, T, R, d.F, d.M, Xb, s));
   for (int l = 1; l < L; ++l) CU(depend(sp, s, st[l]));  // fork
 
   // ------------------------------------------------------------------ forward
@@ -212,10 +221,16 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
       bf16 *r = Bp(Ly.Rg[l]) + t * RH, *c = Bp(Ly.Cg[l]) + t * RH;
       float *u = Fp(Ly.Ug[l]) + t * RH;
       // k-blocks: (input block m: map A0) and (hidden block m: map A1), B = Wf[kb] tiles
+      const bool fold = l == 0 && xfold && !is_dec(t);
       auto fill_kb = [&](TcFwd &f, const bf16 *Ah, int Nout) {
         f.A0 = Ain, f.A1 = Ah, f.CA = 64, f.M0 = d.M, f.M1 = d.M;
         f.bX = 64, f.bY = Nout, f.bZ = nkb_total(d, l);
         f.nkb = 0;
+        if (fold) {  // the x k-block: A0 = this step's packed input rows, B k-block M
+          f.A0 = Xb + int64_t(t) * R * 64, f.M0 = 1;
+          f.kb_as[f.nkb] = 0, f.kb_am[f.nkb] = 0, f.kb_ac[f.nkb] = 0;
+          f.kb_bx[f.nkb] = 0, f.kb_by[f.nkb] = 0, f.kb_bz[f.nkb] = d.M, ++f.nkb;
+        }
         for (int m = 0; m < d.M; ++m) {
           if (l > 0) {
             f.kb_as[f.nkb] = 0, f.kb_am[f.nkb] = m, f.kb_ac[f.nkb] = 0;
@@ -232,7 +247,7 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
       fill_kb(gate, DHp, 2 * d.H);
       gate.Bw = Bp(Ly.Wf_ru[ps]);
       gate.bias = params + P.bru[ps];
-      if (l == 0)
+      if (l == 0 && !fold)
         gate.Dx = Xin, gate.dx_mstride = x_ms, gate.F = Fin, gate.C_in = C, gate.M = d.M,
         gate.Wx = params + P.Wru[ps];
       gate.Hprev = Hp32;
@@ -245,7 +260,7 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
       fill_kb(cand, t > 0 ? DrHt : nullptr, d.H);
       cand.Bw = Bp(Ly.Wf_c[ps]);
       cand.bias = params + P.bc[ps];
-      if (l == 0)
+      if (l == 0 && !fold)
         cand.Dx = Xin, cand.dx_mstride = x_ms, cand.F = Fin, cand.C_in = C, cand.M = d.M,
         cand.Wx = params + P.Wc[ps];
       cand.Hprev = Hp32, cand.u_in = u, cand.out_c = c;

@@ -2,6 +2,7 @@
 #include <cuda_bf16.h>
 
 #include "kernels.cuh"
+#include "tc_ptx.cuh"
 #include "profile.cuh"
 
 namespace pgti {
@@ -240,7 +241,7 @@ struct WeightParams {
 __global__ void k_convert_weights(const __grid_constant__ WeightParams p) {
   for (int q = 0; q < p.njobs; ++q) {
     const WeightJob &w = p.job[q];
-    const int nkb = w.layer0 ? w.M : 2 * w.M;
+    const int nkb = w.layer0 ? w.M + 1 : 2 * w.M;
     const int64_t nf = int64_t(nkb) * w.Nout * 64;
     __nv_bfloat16 *wf = static_cast<__nv_bfloat16 *>(w.Wf);
     __nv_bfloat16 *wd = static_cast<__nv_bfloat16 *>(w.Wd);
@@ -249,6 +250,12 @@ __global__ void k_convert_weights(const __grid_constant__ WeightParams p) {
       const int c = int(i % 64);
       const int j = int((i / 64) % w.Nout);
       const int kb = int(i / (64 * w.Nout));
+      if (w.layer0 && kb == w.M) {  // the x k-block: column c = m*Fin + f
+        const int m = c / w.Fin, f = c - m * w.Fin;
+        wf[i] = c < w.M * w.Fin ? __float2bfloat16_rn(w.W[int64_t(m * w.C_in + f) * w.Nout + j])
+                                : __float2bfloat16_rn(0.f);
+        continue;
+      }
       const int row = w.layer0 ? kb * w.C_in + w.Fin + c : (kb / 2) * w.C_in + (kb % 2) * 64 + c;
       wf[i] = __float2bfloat16_rn(w.W[int64_t(row) * w.Nout + j]);
     }
@@ -265,6 +272,37 @@ __global__ void k_convert_weights(const __grid_constant__ WeightParams p) {
 }
 
 }  // namespace
+
+namespace {
+// thread = 8 columns (16 bytes) of one row of Xb
+__global__ void k_xpack(const float *__restrict__ Dx, int64_t x_mstride, int T, int64_t R, int F,
+                        int M, __nv_bfloat16 *__restrict__ Xb) {
+  griddep_launch_dependents();
+  griddep_wait();
+  const int64_t n = int64_t(T) * R * 8;
+  const int mf = M * F;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int c8 = int(i & 7);
+    const int64_t tr = i >> 3, t = tr / R, r = tr - t * R;
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int c = c8 * 8 + k, m = c / F, f = c - m * F;
+      v[k] = c < mf ? __ldg(Dx + m * x_mstride + (t * R + r) * F + f) : 0.f;
+    }
+    reinterpret_cast<uint4 *>(Xb)[i] = tc::pack8_bf16(v);
+  }
+}
+}  // namespace
+
+cudaError_t launch_xpack(const float *Dx, int64_t x_mstride, int T, int64_t R, int F, int M,
+                         __nv_bfloat16 *Xb, cudaStream_t s) {
+  if (M * F > 64) return cudaErrorInvalidValue;
+  const int64_t n = int64_t(T) * R * 8;
+  ProfScope prof(kProfElementwise, s, double(T) * R * (4.0 * M * F + 128.0), 0.0);
+  return pdl_launch(k_xpack, dim3(grid_for(n)), dim3(kT), 0, s, Dx, x_mstride, T, R, F, M, Xb);
+}
 
 cudaError_t launch_x_prep(const WindowSrc &xs, int B, int T_in, int64_t ld, int N, int F,
                           float *X0, unsigned *err, cudaStream_t s) {

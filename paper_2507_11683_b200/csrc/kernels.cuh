@@ -205,10 +205,16 @@ cudaError_t launch_xpart_dgrad(const void *grad, const void *Q, int64_t mstride,
 struct WeightJob {
   const float *W;        // [M*C_in][Nout] fp32 (params)
   int Nout, C_in, M, Fin;
-  int layer0;            // 1: blocks are the hidden part only (kb = m, rows m*C_in + Fin)
+  int layer0;            // 1: blocks are the hidden part only (kb = m, rows m*C_in + Fin), then
+                         //    one x k-block (kb = M): column c = m*Fin + f < M*Fin holds row
+                         //    m*C_in + f (the layer-0 input channels folded into the MMA)
   void *Wf;              // bf16
   void *Wd;              // bf16
 };
 cudaError_t launch_convert_weights(const WeightJob *jobs, int njobs, cudaStream_t s);
+// Layer-0 input channels as one 64-wide bf16 k-block per row: Xb[t][r][m*F + f] =
+// bf16(Dx[m*x_mstride + t*R*F + r*F + f]) for m*F + f < M*F, zeros in the other columns.
+cudaError_t launch_xpack(const float *Dx, int64_t x_mstride, int T, int64_t R, int F, int M,
+                         __nv_bfloat16 *Xb, cudaStream_t s);
 
 }  // namespace pgti
