@@ -102,8 +102,9 @@ LayoutTC make_layout_tc(const Dims &d) {
                               small_wgrad_partial_floats(d.T_out, int(d.R), d.H));
   L.spart_floats = spf;
   size_t wp = spf;
-  for (int l = 0; l < d.L; ++l)
-    wp = std::max(wp, tc_wgrad_partial_floats(vrows(d, l), 2 * d.H, Tmax, int(d.R)));
+  for (int l = 0; l < d.L; ++l)  // layer 0: + the packed input rows' chunk (x fold)
+    wp = std::max(wp, tc_wgrad_partial_floats(vrows(d, l) + (l == 0 ? 64 : 0), 2 * d.H, Tmax,
+                                              int(d.R)));
   L.wpart_floats = wp;
   for (int ll = 0; ll < d.L * (d.model ? 2 : 1); ++ll) {  // bf16 weight tiles per layer set
     const int l = ll % d.L;
@@ -395,6 +396,10 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
     TcWgrad tw{Ain, dec ? Bp(Ly.DHb[l]) + (t0 - 1) * MRH : Bp(Ly.DHb[l]), dec ? 0 : -1, nt,
                d.M, int(R), Bp(Ly.dGb[l]) + int64_t(t0) * 2 * RH, 2 * d.H, V, vseg, coff, C,
                wpart, int64_t(Ly.wpart_floats), grads + P.Wru[ll]};
+    // the encoder's layer-0 input rows (x fold): the packed rows Xb are chunk M of the v range
+    // (they fill the otherwise empty half of the last 128-row tile), not a skinny reduction
+    const bool xw = l == 0 && !dec && xfold;
+    if (xw) tw.A_in = Xb, tw.V = V + 64, tw.x_F = d.F;
     CU(launch_tc_wgrad(tw, ss));
     tw.A_h = Bp(Ly.DrHb[l]) + t0 * MRH, tw.h_toff = 0, tw.G = Bp(Ly.dCb[l]) + int64_t(t0) * RH;
     tw.Nout = d.H, tw.out = grads + P.Wc[ll];
@@ -403,7 +408,7 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
     // on the layer's aux stream (own partials; disjoint output rows) next to the tcgen05 wgrads
     SmallWgrad sw{};
     sw.mode = kSmallBiasX, sw.T = nt, sw.R = int(R);
-    if (l == 0 && !dec) sw.Dx = Dx, sw.dx_mstride = int64_t(T) * RF, sw.dx_tstride = RF;
+    if (l == 0 && !dec && !xw) sw.Dx = Dx, sw.dx_mstride = int64_t(T) * RF, sw.dx_tstride = RF;
     if (l == 0 && dec) sw.Dx = Dy, sw.dx_mstride = RFo, sw.dx_tstride = M * RFo;
     sw.M = d.M, sw.F = Fin, sw.C_in = C;
     sw.partial = Fp(Ly.spart[l]), sw.partial_cap = int64_t(Ly.spart_floats);

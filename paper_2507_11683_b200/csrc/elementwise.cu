@@ -274,34 +274,38 @@ __global__ void k_convert_weights(const __grid_constant__ WeightParams p) {
 }  // namespace
 
 namespace {
-// thread = 8 columns (16 bytes) of one row of Xb
-__global__ void k_xpack(const float *__restrict__ Dx, int64_t x_mstride, int T, int64_t R, int F,
-                        int M, __nv_bfloat16 *__restrict__ Xb) {
+// grid.y = time step; thread = 8 columns (16 bytes) of one row of Xb (32-bit index math)
+__global__ void k_xpack(const float *__restrict__ Dx, int64_t x_mstride, int R, int F, int M,
+                        __nv_bfloat16 *__restrict__ Xb) {
   griddep_launch_dependents();
   griddep_wait();
-  const int64_t n = int64_t(T) * R * 8;
-  const int mf = M * F;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int c8 = int(i & 7);
-    const int64_t tr = i >> 3, t = tr / R, r = tr - t * R;
-    float v[8];
+  const int t = blockIdx.y, mf = M * F, n = R * 8;
+  const float *src = Dx + int64_t(t) * R * F;
+  uint4 *dst = reinterpret_cast<uint4 *>(Xb) + int64_t(t) * n;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int c8 = i & 7, r = i >> 3;
+    uint4 o = make_uint4(0u, 0u, 0u, 0u);
+    if (c8 * 8 < mf) {
+      float v[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int c = c8 * 8 + k, m = c / F, f = c - m * F;
-      v[k] = c < mf ? __ldg(Dx + m * x_mstride + (t * R + r) * F + f) : 0.f;
+      for (int k = 0; k < 8; ++k) {
+        const int c = c8 * 8 + k, m = c / F, f = c - m * F;
+        v[k] = c < mf ? __ldg(src + m * x_mstride + int64_t(r) * F + f) : 0.f;
+      }
+      o = tc::pack8_bf16(v);
     }
-    reinterpret_cast<uint4 *>(Xb)[i] = tc::pack8_bf16(v);
+    dst[i] = o;
   }
 }
 }  // namespace
 
 cudaError_t launch_xpack(const float *Dx, int64_t x_mstride, int T, int64_t R, int F, int M,
                          __nv_bfloat16 *Xb, cudaStream_t s) {
-  if (M * F > 64) return cudaErrorInvalidValue;
-  const int64_t n = int64_t(T) * R * 8;
+  if (M * F > 64 || R * 8 >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   ProfScope prof(kProfElementwise, s, double(T) * R * (4.0 * M * F + 128.0), 0.0);
-  return pdl_launch(k_xpack, dim3(grid_for(n)), dim3(kT), 0, s, Dx, x_mstride, T, R, F, M, Xb);
+  const int64_t n = R * 8;
+  const dim3 grid(unsigned(std::min<int64_t>(ceil_div(n, kT), 2 * 148)), unsigned(T));
+  return pdl_launch(k_xpack, grid, dim3(kT), 0, s, Dx, x_mstride, int(R), F, M, Xb);
 }
 
 cudaError_t launch_x_prep(const WindowSrc &xs, int B, int T_in, int64_t ld, int N, int F,

@@ -533,6 +533,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
           int src, m;
           if (p.vseg == 128) src = qc, m = tile;
           else src = 1, m = 2 * tile + qc;
+          if (p.x_F && m == p.M) src = 0, m = 0;  // layer 0: the packed input rows
           const int tt = src ? t + p.h_toff : t;     // tt < 0 or m >= M -> TMA zero fill
           tma_load_4d(a + qc * (A_BYTES / 2), src ? &mA_h : &mA_in, &bar->full[s], 0, row, m, tt);
         }
@@ -582,7 +583,8 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 }
 
 __global__ void k_tc_reduce(const float *__restrict__ partial, int nchunks, int V, int Nout,
-                            int vseg, int coff, int C_in, float *__restrict__ out) {
+                            int vseg, int coff, int C_in, int M, int x_F,
+                            float *__restrict__ out) {
   griddep_launch_dependents();
   griddep_wait();
   const int64_t n = int64_t(V) * Nout;
@@ -601,6 +603,11 @@ __global__ void k_tc_reduce(const float *__restrict__ partial, int nchunks, int 
     for (; c < nchunks; ++c) s += __ldg(partial + int64_t(c) * n + i);
     const int v = int(i / Nout), j = int(i - int64_t(v) * Nout);
     const int m = v / vseg;
+    if (x_F && m == M) {  // packed input channel c = m' x_F + f -> row m' C_in + f
+      const int c = v - m * vseg, mm = c / x_F, f = c - mm * x_F;
+      if (c < M * x_F) out[int64_t(mm * C_in + f) * Nout + j] = s;
+      continue;
+    }
     out[int64_t(m * C_in + coff + (v - m * vseg)) * Nout + j] = s;
   }
 }
@@ -730,7 +737,11 @@ cudaError_t launch_tc_wgrad(const TcWgrad &p, cudaStream_t s) {
   const uint32_t bA[4] = {64, 64, 1, 1};
   const uint64_t dG[3] = {uint64_t(p.Nout), R, T}, sG[2] = {uint64_t(p.Nout) * 2, R * p.Nout * 2};
   const uint32_t bG[3] = {64, 64, 1};
-  if (!make_map(&ma_in, p.A_in, 4, dA, sA, bA) || !make_map(&ma_h, p.A_h, 4, dA, sA, bA) ||
+  if (p.x_F && (p.vseg != 64 || p.V != (p.M + 1) * 64 || !p.A_in)) return cudaErrorInvalidValue;
+  // A_in is [T][M][R][64] (layer > 0) or, with x_F, the packed input rows [T][1][R][64]
+  const uint64_t Min = p.x_F ? 1 : M;
+  const uint64_t dAi[4] = {64, R, Min, T}, sAi[3] = {128, R * 128, Min * R * 128};
+  if (!make_map(&ma_in, p.A_in, 4, dAi, sAi, bA) || !make_map(&ma_h, p.A_h, 4, dA, sA, bA) ||
       !make_map(&mg, p.G, 3, dG, sG, bG))
     return cudaErrorInvalidValue;
   const WgPlan q = wg_plan(p.V, p.T, p.R);
@@ -760,7 +771,7 @@ cudaError_t launch_tc_wgrad(const TcWgrad &p, cudaStream_t s) {
   ProfScope prof(kProfReduce, s, 4.0 * double(n) * (nchunks + 1), double(n) * nchunks);
   return pdl_launch(k_tc_reduce, dim3(unsigned(std::min<int64_t>(ceil_div(n, 256), 1184))),
                     dim3(256), 0, s, static_cast<const float *>(p.partial), nchunks, p.V, p.Nout,
-                    p.vseg, p.coff, p.C_in, p.out);
+                    p.vseg, p.coff, p.C_in, p.M, p.x_F, p.out);
 }
 
 }  // namespace pgti

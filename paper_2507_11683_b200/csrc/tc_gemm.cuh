@@ -78,6 +78,10 @@ struct TcWgrad {
   float *partial;
   int64_t partial_cap;
   float *out;                       // layer's [M*C_in + 1][Nout] block of grads
+  // layer 0 ("h only", vseg = 64) with x_F > 0: the packed input rows Xb [T][R][64] (A_in,
+  // one block) are chunk M of the v range, i.e. V = (M + 1) 64, and their reduced rows
+  // v = M*64 + m*x_F + f (< M*x_F) go to grads rows m*C_in + f (the layer-0 input part)
+  int x_F = 0;
 };
 cudaError_t launch_tc_wgrad(const TcWgrad &p, cudaStream_t s);
 size_t tc_wgrad_partial_floats(int V, int Nout, int T, int R);
