@@ -88,21 +88,6 @@ pgti_status pgti_graph_windows(int32_t N, const int32_t *rowptr, const int32_t *
                                int32_t rows_per_window, int32_t *win_ptr, int32_t *win_nodes,
                                uint16_t *lcol, int32_t *max_union);
 
-/* The staging plan with ONE window union shared by the two patterns (host arrays):
- * window w of rows_per_window consecutive nodes (1..64) stages the ascending union of
- * its rows' columns in pattern(A) and in pattern(A^T), written to
- * win_nodes[win_ptr[w] .. win_ptr[w+1]) (win_nodes needs at most a_rowptr[N] +
- * at_rowptr[N] entries); a_lcol[e] / at_lcol[e] = the position of a_col[e] /
- * at_col[e] in its window's list.  Passing the same win_ptr / win_nodes for both
- * patterns in the desc lets one CTA stage a hop-1 operand once for P_f and P_b (the
- * SpMM detects the shared plan).  Index bookkeeping only.  Errors: as
- * pgti_graph_windows. */
-pgti_status pgti_graph_windows_pair(int32_t N, const int32_t *a_rowptr, const int32_t *a_col,
-                                    const int32_t *at_rowptr, const int32_t *at_col,
-                                    int32_t rows_per_window, int32_t *win_ptr,
-                                    int32_t *win_nodes, uint16_t *a_lcol, uint16_t *at_lcol,
-                                    int32_t *max_union);
-
 /* ----------------------------------------------------------------- the series */
 typedef struct pgti_series pgti_series; /* opaque; BORROWS dev_buf */
 

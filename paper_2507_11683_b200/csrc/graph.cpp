@@ -110,56 +110,3 @@ extern "C" pgti_status pgti_graph_windows(int32_t N, const int32_t *rowptr, cons
   return PGTI_OK;
 }
 
-
-// The same plan with ONE window union shared by both CSR patterns: window w stages the union of
-// its rows' columns in pattern(A) AND pattern(A^T), and each pattern's entries get their column's
-// position in that shared list.  A hop-1 diffusion applies P_f (pattern A) and P_b (pattern A^T)
-// to the same operand, so one staged set then serves both directions (at full-PeMS shapes the
-// shared unions hold 52 % of the rows of the two separate ones).
-extern "C" pgti_status pgti_graph_windows_pair(int32_t N, const int32_t *a_rowptr,
-                                               const int32_t *a_col, const int32_t *at_rowptr,
-                                               const int32_t *at_col, int32_t rows_per_window,
-                                               int32_t *win_ptr, int32_t *win_nodes,
-                                               uint16_t *a_lcol, uint16_t *at_lcol,
-                                               int32_t *max_union) {
-  pgti::clear_error();
-  PGTI_REQUIRE(N > 0 && a_rowptr && at_rowptr && win_ptr && max_union, PGTI_ERR_INVALID_ARG,
-               "pgti_graph_windows_pair: null pointer or N=%d", N);
-  PGTI_REQUIRE(rows_per_window >= 1 && rows_per_window <= 64, PGTI_ERR_INVALID_ARG,
-               "pgti_graph_windows_pair: rows_per_window=%d outside [1, 64]", rows_per_window);
-  const int32_t *rp[2] = {a_rowptr, at_rowptr}, *cl[2] = {a_col, at_col};
-  uint16_t *lc[2] = {a_lcol, at_lcol};
-  for (int p = 0; p < 2; ++p) {
-    PGTI_REQUIRE(rp[p][0] == 0 && rp[p][N] >= 0 &&
-                     (rp[p][N] == 0 || (cl[p] && lc[p] && win_nodes)),
-                 PGTI_ERR_INVALID_ARG, "pgti_graph_windows_pair: bad rowptr / null arrays");
-    for (int32_t i = 0; i < N; ++i)
-      PGTI_REQUIRE(rp[p][i + 1] >= rp[p][i], PGTI_ERR_INVALID_ARG, "rowptr not monotone at %d",
-                   i);
-  }
-  const int32_t nwin = (N + rows_per_window - 1) / rows_per_window;
-  std::vector<int32_t> u;
-  int64_t pos = 0;
-  int32_t mx = 0;
-  win_ptr[0] = 0;
-  for (int32_t w = 0; w < nwin; ++w) {
-    const int32_t r0 = w * rows_per_window, r1 = std::min(N, r0 + rows_per_window);
-    u.clear();
-    for (int p = 0; p < 2; ++p) u.insert(u.end(), cl[p] + rp[p][r0], cl[p] + rp[p][r1]);
-    for (int32_t c : u)
-      PGTI_REQUIRE(c >= 0 && c < N, PGTI_ERR_INVALID_ARG, "column %d outside [0, %d)", c, N);
-    std::sort(u.begin(), u.end());
-    u.erase(std::unique(u.begin(), u.end()), u.end());
-    PGTI_REQUIRE(u.size() <= 65535, PGTI_ERR_INVALID_ARG, "window %d union %zu > 65535", w,
-                 u.size());
-    for (int p = 0; p < 2; ++p)
-      for (int64_t e = rp[p][r0]; e < rp[p][r1]; ++e)
-        lc[p][e] = uint16_t(std::lower_bound(u.begin(), u.end(), cl[p][e]) - u.begin());
-    std::copy(u.begin(), u.end(), win_nodes + pos);
-    pos += int64_t(u.size());
-    win_ptr[w + 1] = int32_t(pos);
-    mx = std::max(mx, int32_t(u.size()));
-  }
-  *max_union = mx;
-  return PGTI_OK;
-}

@@ -221,13 +221,9 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *g) {
 // LDS.128 of the staged neighbour slice, the bf16 -> fp32 unpack and the FFMA2s.
 constexpr int kWinEntBytes = 8 * 4 * 32 * 8;  // [warp][row slot][32] int2, RPW <= 4
 
-// NJ = 2 (dual): the launch's two jobs apply P_f (pattern A) and P_b (pattern A^T) to the SAME
-// operand with one shared window plan (a hop-1 diffusion); a CTA stages the shared union once
-// and computes both jobs' rows -- row slots [0, RPW/2) for job 0, [RPW/2, RPW) for job 1.
-template <typename T, int RPW, int VPL, int EPI, int NJ = 1>
-__global__ void __launch_bounds__(256, VPL == 1 ? (RPW <= 2 ? 4 : RPW <= 4 ? 3 : 1) : (RPW <= 1 ? 4 : RPW <= 2 ? 3 : 2))
+template <typename T, int RPW, int VPL, int EPI>
+__global__ void __launch_bounds__(256, VPL == 1 ? (RPW <= 4 ? 3 : 1) : (RPW <= 2 ? 3 : 2))
     k_spmm_win(const __grid_constant__ WinParams p) {
-  constexpr int RJ = RPW / NJ;  // row slots per job
   using L = Lane<T>;
   constexpr int V = L::V, P = V / 2;
   constexpr int SLOTS = RPW <= 4 ? RPW : 4;  // entry lists held at once (RPW 8: two passes)
@@ -236,11 +232,9 @@ __global__ void __launch_bounds__(256, VPL == 1 ? (RPW <= 2 ? 4 : RPW <= 4 ? 3 :
   griddep_launch_dependents();
   const int z = int(blockIdx.z);
   int j = 0;
-  if (NJ == 1) {
 #pragma unroll
-    for (int q = 1; q < kMaxSpmmJobs; ++q)
-      if (q < p.njobs && z >= p.z_begin[q]) j = q;
-  }
+  for (int q = 1; q < kMaxSpmmJobs; ++q)
+    if (q < p.njobs && z >= p.z_begin[q]) j = q;
   const int chunk = int(blockIdx.x);
   if (chunk >= p.nchunk[j]) return;  // jobs narrower than the widest one
   const SpmmJob &jb = p.job[j];
@@ -269,20 +263,21 @@ __global__ void __launch_bounds__(256, VPL == 1 ? (RPW <= 2 ? 4 : RPW <= 4 ? 3 :
     // (rows past 8 x 32 come through the fallback loop below); and each of this warp's rows'
     // first 32 CSR entries (lane u: entry u) as (staged-row byte offset, value)
     const int my_node = warp + 8 * lane < nu ? __ldg(jb.win_nodes[t] + ub + warp + 8 * lane) : 0;
+    const uint16_t *lc = jb.lcol[t];
+    const float *val = jb.val[t];
     int beg[RPW], cnt[RPW];
     int2 ent[SLOTS];
 #pragma unroll
     for (int i = 0; i < RPW; ++i) {
-      const SpmmJob &ji = NJ == 1 ? jb : p.job[i / RJ];
-      const int r = warp + 8 * (i % RJ), n = row0 + r;
+      const int r = warp + 8 * i, n = row0 + r;
       beg[i] = cnt[i] = 0;
       if (i < SLOTS) ent[i] = make_int2(0, 0);
       if (r >= p.win_rows || n >= p.N) continue;  // warp-uniform
-      beg[i] = __ldg(ji.rowptr[t] + n);
-      cnt[i] = __ldg(ji.rowptr[t] + n + 1) - beg[i];
+      beg[i] = __ldg(jb.rowptr[t] + n);
+      cnt[i] = __ldg(jb.rowptr[t] + n + 1) - beg[i];
       if (i < SLOTS && lane < cnt[i])
-        ent[i] = make_int2(int(__ldg(ji.lcol[t] + beg[i] + lane)) * ROWB,
-                           __float_as_int(__ldg(ji.val[t] + beg[i] + lane)));
+        ent[i] = make_int2(int(__ldg(lc + beg[i] + lane)) * ROWB,
+                           __float_as_int(__ldg(val + beg[i] + lane)));
     }
     // the plan and CSR are step constants: read above while the previous kernel drains; the
     // dense operand (and the epilogue's addends) only after it has completed
@@ -305,8 +300,6 @@ __global__ void __launch_bounds__(256, VPL == 1 ? (RPW <= 2 ? 4 : RPW <= 4 ? 3 :
     for (int i = 0; i < RPW; ++i) {
       const int slot = i % SLOTS;
       const int2 *E = s_ent + slot * 32;
-      const uint16_t *lc = (NJ == 1 ? jb : p.job[i / RJ]).lcol[t];
-      const float *val = (NJ == 1 ? jb : p.job[i / RJ]).val[t];
       if (i >= SLOTS && cnt[i] > 0) {  // RPW 8: refill the slot (warp-private list)
         __syncwarp();
         if (lane < cnt[i])
@@ -363,13 +356,12 @@ __global__ void __launch_bounds__(256, VPL == 1 ? (RPW <= 2 ? 4 : RPW <= 4 ? 3 :
   }
 #pragma unroll
   for (int i = 0; i < RPW; ++i) {
-    const int r = warp + 8 * (i % RJ), n = row0 + r;
+    const int r = warp + 8 * i, n = row0 + r;
     if (r >= p.win_rows || n >= p.N) continue;
     const int64_t o = goff + int64_t(n) * W + int64_t(vec0) * V;
 #pragma unroll
     for (int v = 0; v < VPL; ++v)
-      if (vec0 + 32 * v < vecs)
-        finish<L, T, EPI>(NJ == 1 ? jb : p.job[i / RJ], acc[i][v], o + 32 * v * V);
+      if (vec0 + 32 * v < vecs) finish<L, T, EPI>(jb, acc[i][v], o + 32 * v * V);
   }
 }
 
@@ -519,25 +511,6 @@ cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s) {
     // epilogue of the plain hops (no predicated addend / accumulator code per row)
     bool store_only = true;
     for (int i = 0; i < njobs; ++i) store_only = store_only && !jobs[i].add && !jobs[i].accumulate;
-    // dual: a hop-1 launch (P_f and P_b of one operand) on a shared window plan -- one CTA
-    // stages the shared union once for both jobs (PGTI_SPMM_DUAL=0 disables)
-    const char *dual_env = std::getenv("PGTI_SPMM_DUAL");  // read per call (A/B, tests)
-    const bool dual_on = !(dual_env && dual_env[0] == '0');
-    const SpmmJob &a = jobs[0], &b = jobs[njobs > 1 ? 1 : 0];
-    const bool dual = dual_on && njobs == 2 && bf && vpl == 2 && rpw <= 2 && store_only && !gen &&
-                      a.nterms == 1 && b.nterms == 1 && a.X[0] == b.X[0] &&
-                      a.win_ptr[0] == b.win_ptr[0] && a.win_nodes[0] == b.win_nodes[0] &&
-                      a.W == b.W && a.G == b.G && a.gstride == b.gstride;
-    if (dual) {
-      const dim3 grid2(unsigned(w.nchunk[0]), unsigned(w.nwin), unsigned(a.G));
-      auto go2 = [&](auto kernel) -> cudaError_t {
-        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        return pdl_launch(kernel, grid2, dim3(256), smem, s, w);
-      };
-      return rpw <= 1 ? go2(k_spmm_win<__nv_bfloat16, 2, 2, 0, 2>)
-                      : go2(k_spmm_win<__nv_bfloat16, 4, 2, 0, 2>);
-    }
     if (gen) return pick(std::integral_constant<int, 2>{});
     return store_only ? pick(std::integral_constant<int, 0>{})
                       : pick(std::integral_constant<int, 1>{});

@@ -62,8 +62,6 @@ _graph_build = _sig("pgti_graph_build", C.c_int, _i32, _i64, _vp, _vp, _vp, _vp,
                     _vp, _vp, _vp, _vp)
 _graph_windows = _sig("pgti_graph_windows", C.c_int, _i32, _vp, _vp, _i32, _vp, _vp, _vp,
                       C.POINTER(_i32))
-_graph_windows_pair = _sig("pgti_graph_windows_pair", C.c_int, _i32, _vp, _vp, _vp, _vp, _i32,
-                           _vp, _vp, _vp, _vp, C.POINTER(_i32))
 _load = _sig("pgti_load_series", C.c_int, C.POINTER(_vp), _vp, _i64, _i64, _i64, _i64, _vp, _i64,
              _vp)
 _stats = _sig("pgti_series_stats", C.c_int, _vp, _i64, C.c_int, _i64, _i64, _f64, _vp, _vp)
@@ -220,40 +218,12 @@ def graph_windows(N: int, rowptr, col, rows: int) -> dict:
                 lcol=lcol.view(np.int16), max_union=int(mx.value))
 
 
-def graph_windows_pair(N: int, csr: dict, rows: int) -> dict:
-    """pgti_graph_windows_pair: one union per window for both patterns -> win_ptr, win_nodes,
-    a_lcol, at_lcol (int16 bits), max."""
-    arp, acol = (np.ascontiguousarray(csr[k], np.int32) for k in ("a_rowptr", "a_col"))
-    trp, tcol = (np.ascontiguousarray(csr[k], np.int32) for k in ("at_rowptr", "at_col"))
-    nwin = (N + rows - 1) // rows
-    win_ptr = np.zeros(nwin + 1, np.int32)
-    win_nodes = np.zeros(max(int(arp[N]) + int(trp[N]), 1), np.int32)
-    alc = np.zeros(max(int(arp[N]), 1), np.uint16)
-    tlc = np.zeros(max(int(trp[N]), 1), np.uint16)
-    mx = _i32(0)
-    _ok(_graph_windows_pair(N, _ptr(arp), _ptr(acol), _ptr(trp), _ptr(tcol), rows,
-                            _ptr(win_ptr), _ptr(win_nodes), _ptr(alc), _ptr(tlc), C.byref(mx)))
-    return dict(win_ptr=win_ptr, win_nodes=win_nodes[:max(int(win_ptr[-1]), 1)].copy(),
-                a_lcol=alc.view(np.int16), at_lcol=tlc.view(np.int16), max_union=int(mx.value))
-
-
-def add_windows(csr: dict, N: int, rows: int | None = None, shared: bool | None = None) -> dict:
-    """Adds the SpMM staging plans of both patterns to a graph_build dict (rows=0: none).
-    shared (default; PGTI_SHARED_WINDOWS=0 disables): one window union for both patterns
-    (pgti_graph_windows_pair), the same win_ptr / win_nodes arrays in both pattern slots."""
+def add_windows(csr: dict, N: int, rows: int | None = None) -> dict:
+    """Adds the SpMM staging plans of both patterns to a graph_build dict (rows=0: none)."""
     rows = default_win_rows(N) if rows is None else rows
-    if shared is None:
-        shared = os.environ.get("PGTI_SHARED_WINDOWS", "1") != "0"
     out = dict(csr)
     if rows <= 0 or csr["a_col"].size == 0:
         out["win_rows"], out["win_max"] = 0, 0
-        return out
-    if shared:
-        w = graph_windows_pair(N, csr, rows)
-        for pat in ("a", "at"):
-            out[pat + "_win_ptr"], out[pat + "_win_nodes"] = w["win_ptr"], w["win_nodes"]
-            out[pat + "_lcol"] = w[pat + "_lcol"]
-        out["win_rows"], out["win_max"], out["win_shared"] = rows, w["max_union"], 1
         return out
     mx = 0
     for pat in ("a", "at"):
@@ -403,18 +373,9 @@ class DCRNN:
 
 
 def csr_to_device(csr: dict, device):
-    """Host plan arrays -> device tensors; arrays shared between keys (the shared window plan)
-    stay shared on the device (one tensor, so the desc carries equal pointers)."""
     import torch
-    out, seen = {}, {}
-    for k, v in csr.items():
-        if isinstance(v, np.ndarray):
-            if id(v) not in seen:
-                seen[id(v)] = torch.from_numpy(v).to(device)
-            out[k] = seen[id(v)]
-        else:
-            out[k] = v
-    return out
+    return {k: torch.from_numpy(v).to(device) if isinstance(v, np.ndarray) else v
+            for k, v in csr.items()}
 
 
 # ------------------------------------------------------------------------------ comm / adam

@@ -77,7 +77,7 @@ def test_graph_windows_plan(pgti, N, rows, graph):
     g = {"er": lambda: synth.random_graph(N, 0.15, seed=N), "knn": lambda: synth.make_graph(N, 8),
          "ring": lambda: synth.ring_graph(N)}[graph]()
     csr = pgti.graph_build(N, *g)
-    full = pgti.add_windows(csr, N, rows, shared=False)
+    full = pgti.add_windows(csr, N, rows)
     mx = 0
     for pat in ("a", "at"):
         rp, col = csr[pat + "_rowptr"], csr[pat + "_col"]
@@ -94,37 +94,6 @@ def test_graph_windows_plan(pgti, N, rows, graph):
             mx = max(mx, u.size)
     assert full["win_max"] == mx and full["win_rows"] == rows
     assert pgti.add_windows(csr, N, 0)["win_rows"] == 0
-
-
-@pytest.mark.parametrize("N,rows,graph", [(207, 16, "knn"), (37, 7, "er"), (100, 1, "knn"),
-                                           (45, 64, "ring"), (2716, 16, "knn")])
-def test_graph_windows_pair_plan(pgti, N, rows, graph):
-    """Shared staging plan (pgti_graph_windows_pair, the default of add_windows): each window's
-    list is exactly the sorted set of its rows' columns in BOTH patterns, both patterns' lcol map
-    every CSR entry back to its column in it, and both pattern slots carry the same arrays."""
-    g = {"er": lambda: synth.random_graph(N, 0.15, seed=N), "knn": lambda: synth.make_graph(N, 8),
-         "ring": lambda: synth.ring_graph(N)}[graph]()
-    csr = pgti.graph_build(N, *g)
-    full = pgti.add_windows(csr, N, rows)
-    assert full["a_win_ptr"] is full["at_win_ptr"] and full["a_win_nodes"] is full["at_win_nodes"]
-    wp, wn = full["a_win_ptr"], full["a_win_nodes"]
-    nwin = -(-N // rows)
-    assert wp.shape == (nwin + 1,) and wp[0] == 0
-    mx = 0
-    for w in range(nwin):
-        r0, r1 = w * rows, min(N, (w + 1) * rows)
-        u = wn[wp[w]:wp[w + 1]]
-        both = np.concatenate([csr[p + "_col"][csr[p + "_rowptr"][r0]:csr[p + "_rowptr"][r1]]
-                               for p in ("a", "at")])
-        assert np.array_equal(u, np.unique(both))
-        for pat in ("a", "at"):
-            rp, col = csr[pat + "_rowptr"], csr[pat + "_col"]
-            e = np.arange(rp[r0], rp[r1])
-            assert np.array_equal(u[full[pat + "_lcol"].view(np.uint16)[e]], col[e])
-        mx = max(mx, u.size)
-    assert full["win_max"] == mx and full["win_rows"] == rows
-    d = pgti.csr_to_device(full, "cpu")  # shared arrays stay one tensor (equal desc pointers)
-    assert d["a_win_ptr"].data_ptr() == d["at_win_ptr"].data_ptr()
 
 
 def test_graph_windows_errors(pgti):

@@ -724,22 +724,3 @@ def test_step_dense_rows(env):
                                           xo.astype(np.float64), yo.astype(np.float64))
     _check_step(dict(loss=loss, g=g, act=act, loss_ref=loss_ref, g_ref=g_ref, fwd=fwd, cfg=cfg,
                      ref=ref, margin=1.0, B=cfg.B), tol=TOL_BF16)
-
-
-@pytest.mark.parametrize("name,B", [("tc_big", None), ("metr_la", 64)])
-@pytest.mark.parametrize("env_off", ["PGTI_SPMM_DUAL", "PGTI_SHARED_WINDOWS"])
-def test_step_shared_windows_and_dual_spmm_bitexact(env, name, B, env_off, monkeypatch):
-    """The shared window plan of both CSR patterns (default) and the dual-job hop-1 SpMM (one
-    CTA stages the operand once for P_f and P_b) only change what is staged where: loss,
-    activations and gradients bit-identical with either switched off."""
-    cfg = TC_CONFIGS.get(name) or synth.CONFIGS[name]
-    res = []
-    for flag in ("0", None):
-        if flag:
-            monkeypatch.setenv(env_off, flag)
-        else:
-            monkeypatch.delenv(env_off, raising=False)
-        c = _step_case_tc(env, cfg, B=B)
-        res.append((c["loss"], c["g"], c["act"]))
-    assert res[0][0] == res[1][0]
-    assert np.array_equal(res[0][1], res[1][1]) and np.array_equal(res[0][2], res[1][2])
