@@ -227,7 +227,9 @@ __device__ __forceinline__ void fwd_epi_tile(const TcFwd &p, int row0, int ct0, 
       const int jh = (MODE == kEpiGate ? 0 : ct * 64) + c4;  // hidden unit of column c4
       const int64_t ro = int64_t(row) * H + jh;
       if (MODE == kEpiGate) {
-        const float4 s = make_float4(sigmoid_f(a.x), sigmoid_f(a.y), sigmoid_f(a.z), sigmoid_f(a.w));
+        const float4 s = p.exact ? make_float4(sigmoid_f(a.x), sigmoid_f(a.y), sigmoid_f(a.z), sigmoid_f(a.w))
+                                 : make_float4(sigmoid_mufu(a.x), sigmoid_mufu(a.y),
+                                               sigmoid_mufu(a.z), sigmoid_mufu(a.w));
         if (valid) {
           if (ct == 0) {
             st4_bf16(p.out_r + ro, s);
@@ -241,7 +243,9 @@ __device__ __forceinline__ void fwd_epi_tile(const TcFwd &p, int row0, int ct0, 
       } else {  // kEpiCand
         float4 hn = make_float4(0.f, 0.f, 0.f, 0.f);
         if (valid) {
-          const float4 c = make_float4(tanhf(a.x), tanhf(a.y), tanhf(a.z), tanhf(a.w));
+          const float4 c = p.exact ? make_float4(tanhf(a.x), tanhf(a.y), tanhf(a.z), tanhf(a.w))
+                                   : make_float4(tanh_mufu(a.x), tanh_mufu(a.y), tanh_mufu(a.z),
+                                                 tanh_mufu(a.w));
           const float4 u = ld4(p.u_in + ro);
           float4 hp = make_float4(0.f, 0.f, 0.f, 0.f);
           if (p.Hprev) hp = ld4(p.Hprev + ro);
@@ -654,7 +658,12 @@ constexpr int fwd_smem_bytes(int nsub) {
 
 }  // namespace
 
-cudaError_t launch_tc_fwd(const TcFwd &p, cudaStream_t s) {
+cudaError_t launch_tc_fwd(const TcFwd &p_in, cudaStream_t s) {
+  TcFwd p = p_in;
+  {  // gate / candidate activations by the MUFU tanh (bf16 path); PGTI_TC_EXACT=1: libm forms
+    const char *e = std::getenv("PGTI_TC_EXACT");
+    p.exact = (e && e[0] == '1') ? 1 : 0;
+  }
   if (p.H != 64 || p.nkb > kTcMaxKb || (p.Dx && p.F * p.M > 20) || p.F_out > 4 ||
       p.ntiles < 1 || p.ntiles > 2 || (p.CA != 64 && p.CA != 128))
     return cudaErrorInvalidValue;

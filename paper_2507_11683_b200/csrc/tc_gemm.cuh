@@ -55,6 +55,8 @@ struct TcFwd {
   // gate backward there: dG_r = acc H_{t-1} r (1-r) (fp32 g_dG + bf16 g_dGb, [R][2H], columns
   // [0,H)), g_dHprev += acc r.  Uses Hprev.  -1 = off.  g_dG may be null (bf16 copy only).
   int fuse_tile = -1;
+  // set by launch_tc_fwd: 1 = libm tanhf / expf activations, 0 = MUFU tanh (default)
+  int exact = 0;
   const __nv_bfloat16 *g_r;
   float *g_dG;
   __nv_bfloat16 *g_dGb;

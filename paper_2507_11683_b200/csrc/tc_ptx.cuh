@@ -144,6 +144,14 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool 
 }
 
 __device__ __forceinline__ float sigmoid_f(float a) { return 1.0f / (1.0f + __expf(-a)); }
+// hardware tanh (MUFU.TANH, max relative error ~2^-11): the bf16 path's gate activations;
+// sigma(a) = 0.5 tanh(a / 2) + 0.5
+__device__ __forceinline__ float tanh_mufu(float a) {
+  float r;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(r) : "f"(a));
+  return r;
+}
+__device__ __forceinline__ float sigmoid_mufu(float a) { return fmaf(0.5f, tanh_mufu(0.5f * a), 0.5f); }
 
 // 8 floats -> 8 bf16 (round to nearest) packed in 16 bytes, register-only.
 __device__ __forceinline__ uint4 pack8_bf16(const float *v) {
