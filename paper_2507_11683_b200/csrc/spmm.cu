@@ -365,6 +365,114 @@ __global__ void __launch_bounds__(256, VPL == 1 ? (RPW <= 4 ? 3 : 1) : (RPW <= 2
   }
 }
 
+// Window-resident, chunk-pipelined form (the default for staged launches): CTA = (window, job x
+// group) walks ALL column chunks of its rows.  The window's index work -- union node ids (one
+// per lane in registers), row pointers, the rows' CSR entries as (staged-row byte offset, value)
+// lists in shared memory -- is done once and reused by every chunk, and the chunks are
+// double-buffered with cp.async groups: chunk c + 1's neighbour slices are in flight while chunk
+// c is reduced.  Per row: the same terms in the same CSR order with the same FFMA2 sequence as
+// k_spmm / k_spmm_win (bit-identical).  One term per job, <= 4 rows per warp.
+template <typename T, int RPW, int EPI>
+__global__ void __launch_bounds__(256, RPW <= 2 ? 3 : 2)
+    k_spmm_wp(const __grid_constant__ WinParams p, int cpc) {
+  using L = Lane<T>;
+  constexpr int V = L::V, P = V / 2;
+  extern __shared__ uint4 stage[];  // [2][win_max][32] | entries [8][RPW][32]
+  griddep_launch_dependents();
+  const int z = int(blockIdx.y);
+  int j = 0;
+#pragma unroll
+  for (int q = 1; q < kMaxSpmmJobs; ++q)
+    if (q < p.njobs && z >= p.z_begin[q]) j = q;
+  const SpmmJob &jb = p.job[j];
+  const int g = z - p.z_begin[j], win = int(blockIdx.x);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int vecs = p.vecs[j];
+  const int c_lo = int(blockIdx.z) * cpc, nch = min(p.nchunk[j], c_lo + cpc);  // chunk group
+  if (c_lo >= nch) return;
+  const int W = int(jb.W);
+  const int64_t goff = int64_t(g) * jb.gstride;
+  const int row0 = win * p.win_rows;
+  const int SB = p.win_max * 32;  // uint4 per stage buffer
+  int2 *s_ent = reinterpret_cast<int2 *>(stage + 2 * SB) + warp * (RPW * 32);
+
+  // ---- the window's index work, once
+  const int ub = __ldg(jb.win_ptr[0] + win), nu = __ldg(jb.win_ptr[0] + win + 1) - ub;
+  const int my_node = warp + 8 * lane < nu ? __ldg(jb.win_nodes[0] + ub + warp + 8 * lane) : 0;
+  int beg[RPW], cnt[RPW];
+  int2 ent[RPW];
+#pragma unroll
+  for (int i = 0; i < RPW; ++i) {
+    const int r = warp + 8 * i, n = row0 + r;
+    beg[i] = cnt[i] = 0;
+    ent[i] = make_int2(0, 0);
+    if (r >= p.win_rows || n >= p.N) continue;  // warp-uniform
+    beg[i] = __ldg(jb.rowptr[0] + n);
+    cnt[i] = __ldg(jb.rowptr[0] + n + 1) - beg[i];
+    if (lane < cnt[i])
+      ent[i] = make_int2(int(__ldg(jb.lcol[0] + beg[i] + lane)) * 512,
+                         __float_as_int(__ldg(jb.val[0] + beg[i] + lane)));
+  }
+  griddep_wait();  // the dense operand (and the epilogue's addends) are predecessor outputs
+  const T *X = reinterpret_cast<const T *>(jb.X[0]) + goff + int64_t(lane) * V;
+  auto stage_chunk = [&](int c, int b) {  // chunk c's union slices -> buffer b (one group)
+    const int vec = c * 32 + lane;
+    for (int k = warp, i8 = 0; k < nu; k += 8, ++i8) {
+      const int node = i8 < 32 ? __shfl_sync(0xffffffffu, my_node, i8)
+                               : __ldg(jb.win_nodes[0] + ub + k);
+      if (vec < vecs) cp_async16(stage + b * SB + k * 32 + lane, X + int64_t(node) * W + c * 32 * V);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  stage_chunk(c_lo, 0);
+#pragma unroll
+  for (int i = 0; i < RPW; ++i)
+    if (lane < cnt[i]) s_ent[i * 32 + lane] = ent[i];
+  for (int c = c_lo; c < nch; ++c) {
+    const int b = (c - c_lo) & 1;
+    if (c + 1 < nch) {
+      stage_chunk(c + 1, b ^ 1);  // buffer b^1 was released by the previous chunk's barrier
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();  // chunk c staged by every warp; the entry lists written
+    const char *st = reinterpret_cast<const char *>(stage + b * SB + lane);
+    const int vec = c * 32 + lane;
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      const int r = warp + 8 * i, n = row0 + r;
+      if (r >= p.win_rows || n >= p.N) continue;
+      float2 acc[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) acc[q] = make_float2(0.f, 0.f);
+      const int2 *E = s_ent + i * 32;
+      const int n0 = min(cnt[i], 32);
+      int u = 0;
+      for (; u + 4 <= n0; u += 4) {
+        const int2 e0 = E[u], e1 = E[u + 1], e2 = E[u + 2], e3 = E[u + 3];
+        const uint4 x0 = *reinterpret_cast<const uint4 *>(st + e0.x);
+        const uint4 x1 = *reinterpret_cast<const uint4 *>(st + e1.x);
+        const uint4 x2 = *reinterpret_cast<const uint4 *>(st + e2.x);
+        const uint4 x3 = *reinterpret_cast<const uint4 *>(st + e3.x);
+        L::fma_v(acc, __int_as_float(e0.y), x0);
+        L::fma_v(acc, __int_as_float(e1.y), x1);
+        L::fma_v(acc, __int_as_float(e2.y), x2);
+        L::fma_v(acc, __int_as_float(e3.y), x3);
+      }
+      for (; u < n0; ++u) {
+        const int2 e = E[u];
+        L::fma_v(acc, __int_as_float(e.y), *reinterpret_cast<const uint4 *>(st + e.x));
+      }
+      for (int e = beg[i] + 32; e < beg[i] + cnt[i]; ++e)  // rows with > 32 entries
+        L::fma_v(acc, __ldg(jb.val[0] + e),
+                 *reinterpret_cast<const uint4 *>(st + int(__ldg(jb.lcol[0] + e)) * 512));
+      if (vec < vecs) finish<L, T, EPI>(jb, acc, goff + int64_t(n) * W + int64_t(vec) * V);
+    }
+    __syncthreads();  // every warp is done with buffer b before chunk c + 2 refills it
+  }
+}
+
 // Scalar fp32 fallback for widths that are not a multiple of 4 (test shapes only).
 __global__ void __launch_bounds__(256) k_spmm_scalar(const __grid_constant__ SpmmParams p) {
   griddep_launch_dependents();
@@ -476,6 +584,59 @@ cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s) {
     }
     w.z_begin[njobs] = nz;
     if (nz > 65535 || w.nwin > 65535) win = false;
+  }
+  // window-resident, chunk-pipelined kernel: every job one term, <= 4 rows per warp
+  bool wp = win && (w.win_rows + 7) / 8 <= 4;
+  for (int i = 0; i < njobs && wp; ++i) wp = jobs[i].nterms == 1;
+  {
+    const char *e = std::getenv("PGTI_SPMM_WP");
+    if (e && e[0] == '0') wp = false;
+  }
+  // CTAs = windows x jobs x chunk groups, >= 4 waves of 148 SMs; a group must hold >= 4 chunks
+  // for the window's index work and the pipeline to pay (else the per-chunk kernel below:
+  // METR-LA has 13 windows of 16 rows, full PeMS 698)
+  int cpc = 0;
+  if (wp) {
+    const int V1 = bf ? 8 : 4;
+    int mc = 0;
+    for (int i = 0; i < njobs; ++i) mc = std::max<int>(mc, int(ceil_div(jobs[i].W / V1, 32)));
+    const int64_t base = int64_t(w.nwin) * nz;
+    const int ngrp = int(std::max<int64_t>(1, ceil_div(4 * kNumSMs, base)));
+    cpc = int(ceil_div(mc, ngrp));
+    wp = cpc >= 4;
+  }
+  if (wp) {
+    const int V1 = bf ? 8 : 4;
+    int mc = 0;
+    for (int i = 0; i < njobs; ++i) {  // one 16-byte vector per lane: 512-byte chunks
+      w.vecs[i] = int(jobs[i].W / V1);
+      w.nchunk[i] = int(ceil_div(w.vecs[i], 32));
+      mc = std::max(mc, w.nchunk[i]);
+    }
+    const int smem = 2 * jobs[0].win_max * 512 + 8 * 4 * 32 * 8;
+    const dim3 grid(unsigned(w.nwin), unsigned(nz), unsigned(ceil_div(mc, cpc)));
+    const int rpw = (w.win_rows + 7) / 8;
+    bool store_only = true;
+    for (int i = 0; i < njobs; ++i) store_only = store_only && !jobs[i].add && !jobs[i].accumulate;
+    auto go = [&](auto kernel) -> cudaError_t {
+      cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      return pdl_launch(kernel, grid, dim3(256), smem, s, w, cpc);
+    };
+    auto pick = [&](auto epi) -> cudaError_t {
+      constexpr int G = decltype(epi)::value;
+      if (bf) {
+        if (rpw <= 1) return go(k_spmm_wp<__nv_bfloat16, 1, G>);
+        if (rpw <= 2) return go(k_spmm_wp<__nv_bfloat16, 2, G>);
+        return go(k_spmm_wp<__nv_bfloat16, 4, G>);
+      }
+      if (rpw <= 1) return go(k_spmm_wp<float, 1, G>);
+      if (rpw <= 2) return go(k_spmm_wp<float, 2, G>);
+      return go(k_spmm_wp<float, 4, G>);
+    };
+    if (gen) return pick(std::integral_constant<int, 2>{});
+    return store_only ? pick(std::integral_constant<int, 0>{})
+                      : pick(std::integral_constant<int, 1>{});
   }
   if (win) {
     const dim3 grid(unsigned(maxc), unsigned(w.nwin), unsigned(nz));

@@ -688,18 +688,23 @@ def test_step_parity_batch_of_one(env, name, precision):
 
 
 @pytest.mark.parametrize("name,B", [("tc_big", None), ("metr_la", 64)])
-def test_step_spmm_two_vectors_per_lane_bitexact(env, name, B, monkeypatch):
-    """The staged SpMM with two 16-byte vectors per lane (1 KB column chunks, the default for
-    wide bf16 operands) only regroups columns across threads: loss, activations and gradients
-    bit-identical to one vector per lane (PGTI_SPMM_VPL=1)."""
+def test_step_spmm_variants_bitexact(env, name, B, monkeypatch):
+    """The staged SpMM's forms only regroup work across threads and CTAs: the window-resident,
+    chunk-pipelined kernel (default), the per-chunk kernel with two 16-byte vectors per lane
+    (PGTI_SPMM_WP=0) and with one (PGTI_SPMM_VPL=1) give bit-identical loss, activations and
+    gradients."""
     cfg = TC_CONFIGS.get(name) or synth.CONFIGS[name]
     res = []
-    for flag in ("1", "2"):
-        monkeypatch.setenv("PGTI_SPMM_VPL", flag)
+    for envs in ({}, {"PGTI_SPMM_WP": "0"}, {"PGTI_SPMM_WP": "0", "PGTI_SPMM_VPL": "1"}):
+        for k in ("PGTI_SPMM_WP", "PGTI_SPMM_VPL"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in envs.items():
+            monkeypatch.setenv(k, v)
         c = _step_case_tc(env, cfg, B=B)
         res.append((c["loss"], c["g"], c["act"]))
-    assert res[0][0] == res[1][0]
-    assert np.array_equal(res[0][1], res[1][1]) and np.array_equal(res[0][2], res[1][2])
+    for r in res[1:]:
+        assert r[0] == res[0][0]
+        assert np.array_equal(r[1], res[0][1]) and np.array_equal(r[2], res[0][2])
 
 
 def test_step_dense_rows(env):
@@ -724,3 +729,32 @@ def test_step_dense_rows(env):
                                           xo.astype(np.float64), yo.astype(np.float64))
     _check_step(dict(loss=loss, g=g, act=act, loss_ref=loss_ref, g_ref=g_ref, fwd=fwd, cfg=cfg,
                      ref=ref, margin=1.0, B=cfg.B), tol=TOL_BF16)
+
+
+def test_step_pipelined_spmm_bitexact_at_scale(env, monkeypatch):
+    """The window-resident, chunk-pipelined staged SpMM (chosen when windows x jobs x chunk groups
+    fill >= 4 waves with >= 4 chunks per CTA: full PeMS, PeMS-All-LA) against the per-chunk
+    kernel, bitwise, on a PeMS-All-LA-sized graph at B = 64 (its oracle parity is the full-size
+    test in test_gpu_fullsize.py)."""
+    pgti, torch = env
+    cfg = synth.Config("wp", N=2716, E=120, F=2, T_in=12, T_out=12, L=2, H=64, K=2, B=64)
+    v = synth.make_series(cfg)
+    s = load_series(pgti, torch, v, 0, cfg, float(v.mean()), float(v.std()))
+    graph = synth.make_graph(cfg.N, cfg.knn)
+    ld = ld_of(cfg)
+    idx = torch.arange(cfg.B, dtype=torch.int32, device="cuda")
+    x = torch.empty(cfg.B * cfg.T_in * ld, device="cuda")
+    y = torch.empty(cfg.B * cfg.T_out * ld, device="cuda")
+    s.gather(idx, cfg.B, cfg.T_in, cfg.T_out, x, y)
+    theta = synth.make_params(cfg, kind="random")
+    res = []
+    for flag in (None, "0"):
+        if flag:
+            monkeypatch.setenv("PGTI_SPMM_WP", flag)
+        else:
+            monkeypatch.delenv("PGTI_SPMM_WP", raising=False)
+        model = model_for(pgti, torch, cfg, graph, precision=1)
+        res.append(run_step(pgti, torch, model, theta, x, y))
+    assert np.all(np.isfinite(res[0][1]))
+    assert res[0][0] == res[1][0]
+    assert np.array_equal(res[0][1], res[1][1]) and np.array_equal(res[0][2], res[1][2])
