@@ -473,6 +473,203 @@ __global__ void __launch_bounds__(256, RPW <= 2 ? 3 : 2)
   }
 }
 
+// Tensor-core window SpMM (bf16 hops of the tensor-core step, 16-row windows, union <= 64).
+// The SIMT kernels above spend half their instructions unpacking bf16 operands to fp32 for
+// FFMA2 and are issue-bound well below HBM bandwidth; the tensor core consumes bf16 natively.
+// Per window the 16 x KP transition block P_w (KP = union rounded up to 16; 13 % nonzero on the
+// kNN graphs) is built once in shared memory as a bf16 pair hi + lo with hi = bf16(p),
+// lo = bf16(p - hi) (relative error of hi + lo <= 2^-17, far below the bf16 output rounding),
+// loaded into mma.sync A fragments once, and every column chunk of the window's staged union
+// rows X_U (bf16, the same cp.async double buffer as k_spmm_wp, rows XOR-swizzled per 16-byte
+// segment so ldmatrix.trans is conflict-free) is multiplied as Y_w = P_hi X_U + P_lo X_U with
+// fp32 accumulation (mma.sync.m16n8k16 bf16).  Same products as the SIMT kernels up to fp32
+// summation order and the 2^-17 weight split (not bit-identical to them: parity against the
+// oracle at the bf16 path's 2e-2; PGTI_SPMM_MMA=0 selects the SIMT kernels).
+constexpr int kMmaMaxK = 64, kMmaWin = 16, kMmaPld = kMmaMaxK + 8;  // P_w row pitch (bf16)
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t *r) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t *r) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+__device__ __forceinline__ void stsm_x4(uint32_t addr, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+  asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1,%2,%3,%4};"
+               ::"r"(addr), "r"(r0), "r"(r1), "r"(r2), "r"(r3) : "memory");
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t *>(&v);
+}
+__device__ __forceinline__ void mma_bf16_16816(float *d, const uint32_t *a, uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, "
+               "{%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int NST>
+__global__ void __launch_bounds__(256, 2) k_spmm_mma(const __grid_constant__ WinParams p, int cpc) {
+  // [NST][win_max][32] swizzled stage ring | output tiles [2][16][32] swizzled | P_w hi, lo [16][72]
+  extern __shared__ __align__(128) uint4 stage[];
+  griddep_launch_dependents();
+  const int z = int(blockIdx.y);
+  int j = 0;
+#pragma unroll
+  for (int q = 1; q < kMaxSpmmJobs; ++q)
+    if (q < p.njobs && z >= p.z_begin[q]) j = q;
+  const SpmmJob &jb = p.job[j];
+  const int g = z - p.z_begin[j], win = int(blockIdx.x);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int vecs = p.vecs[j];
+  const int c_lo = int(blockIdx.z) * cpc, nch = min(p.nchunk[j], c_lo + cpc);
+  if (c_lo >= nch) return;
+  const int W = int(jb.W);
+  const int64_t goff = int64_t(g) * jb.gstride;
+  const int row0 = win * kMmaWin;
+  const int SB = p.win_max * 32;  // uint4 per stage buffer
+  const uint32_t obase = static_cast<uint32_t>(__cvta_generic_to_shared(stage + NST * SB));
+  __nv_bfloat16 *Ph = reinterpret_cast<__nv_bfloat16 *>(stage + NST * SB + 2 * kMmaWin * 32);
+  __nv_bfloat16 *Pl = Ph + kMmaWin * kMmaPld;
+
+  // ---- the window's index work and transition block, once
+  const int ub = __ldg(jb.win_ptr[0] + win), nu = __ldg(jb.win_ptr[0] + win + 1) - ub;
+  // warp w stages union rows k = w + 8 i (i < nrow): row offsets in elements (N W < 2^31)
+  const int my_node = warp + 8 * lane < nu ? __ldg(jb.win_nodes[0] + ub + warp + 8 * lane) : 0;
+  const int nrow = nu > warp ? (nu - warp + 7) >> 3 : 0;
+  int roff[kMmaMaxK / 8];
+#pragma unroll
+  for (int i = 0; i < kMmaMaxK / 8; ++i) roff[i] = __shfl_sync(0xffffffffu, my_node, i) * W;
+  const int KS = (nu + 15) >> 4;  // k-steps of 16 union rows; rows nu..16 KS-1 meet zero columns
+  for (int i = threadIdx.x; i < kMmaWin * kMmaPld; i += blockDim.x)
+    Ph[i] = __float2bfloat16_rn(0.f), Pl[i] = __float2bfloat16_rn(0.f);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {  // warp w: window rows w and w + 8
+    const int r = warp + 8 * i, n = row0 + r;
+    if (n >= p.N) continue;
+    const int beg = __ldg(jb.rowptr[0] + n), cnt = __ldg(jb.rowptr[0] + n + 1) - beg;
+    for (int e = lane; e < cnt; e += 32) {
+      const int c = int(__ldg(jb.lcol[0] + beg + e));
+      const float v = __ldg(jb.val[0] + beg + e);
+      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+      Ph[r * kMmaPld + c] = hi;
+      Pl[r * kMmaPld + c] = __float2bfloat16_rn(v - __bfloat162float(hi));
+    }
+  }
+  griddep_wait();  // the dense operand is the predecessor's output
+  // lane l's 16-byte vector of chunk c: global X + node W + 256 c + 8 l; shared row k, segment
+  // l ^ (k & 7) = l ^ w (k = w + 8 i)
+  const __nv_bfloat16 *Xl = reinterpret_cast<const __nv_bfloat16 *>(jb.X[0]) + goff + lane * 8;
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
+  const uint32_t sst = sbase + uint32_t(warp * 512 + ((lane ^ warp) << 4));
+  auto stage_chunk = [&](int c) {
+    if (c < nch && c * 32 + lane < vecs) {
+      const uint32_t dst = sst + uint32_t(((c - c_lo) % NST) * SB) * 16u;
+      const __nv_bfloat16 *src = Xl + c * 256;
+#pragma unroll
+      for (int i = 0; i < kMmaMaxK / 8; ++i)
+        if (i < nrow)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + i * 4096),
+                       "l"(src + roff[i])
+                       : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");  // (empty past the last chunk)
+  };
+#pragma unroll
+  for (int q = 0; q < NST - 1; ++q) stage_chunk(c_lo + q);
+  __syncthreads();  // P_w complete
+  // A fragments of all k-steps (hi and lo), kept in registers for every chunk of the window;
+  // B (ldmatrix.trans) offsets: matrix mi = lane / 8 holds k rows (mi & 1) 8 + lane % 8 of the
+  // k-step (padding rows read row nu - 1: finite values against zero weights) and the 8 columns
+  // of n-tile 2 h + (mi >> 1) of the warp's four
+  uint32_t ah[4][4], al[4][4], boff[4][2];
+  {
+    const int mi = lane >> 3, rr = lane & 7;
+    const int prow = (mi & 1) * 8 + rr, pcol = (mi >> 1) * 8;
+    const uint32_t hb = static_cast<uint32_t>(__cvta_generic_to_shared(Ph));
+    const uint32_t lb = static_cast<uint32_t>(__cvta_generic_to_shared(Pl));
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      if (ks < KS) {
+        const uint32_t off = uint32_t((prow * kMmaPld + ks * 16 + pcol) * 2);
+        ldsm_x4(hb + off, ah[ks]);
+        ldsm_x4(lb + off, al[ks]);
+      }
+      const int k = max(min(ks * 16 + (mi & 1) * 8 + rr, nu - 1), 0);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int seg = warp * 4 + 2 * h + (mi >> 1);
+        boff[ks][h] = uint32_t(k * 512 + ((seg ^ (k & 7)) << 4));
+      }
+    }
+  }
+  // output: D fragments go to a swizzled [16][512 B] shared tile by stmatrix (matrix mi of
+  // stmatrix q: n-tile 2 q + (mi >> 1), rows 8 (mi & 1) + lane % 8), stored to global one
+  // chunk later as full 512-byte row segments (warp w: window rows w and w + 8)
+  uint32_t soff[2];
+  {
+    const int mi = lane >> 3, rr = lane & 7;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int row = 8 * (mi & 1) + rr, seg = warp * 4 + 2 * q + (mi >> 1);
+      soff[q] = uint32_t(row * 512 + ((seg ^ rr) << 4));
+    }
+  }
+  const uint32_t lds0 = uint32_t(warp * 512 + ((lane ^ warp) << 4));  // rows w, w + 8: same swizzle
+  __nv_bfloat16 *Yw = reinterpret_cast<__nv_bfloat16 *>(jb.Y) + goff + int64_t(row0 + warp) * W +
+                      lane * 8;
+  const bool w0ok = row0 + warp < p.N, w1ok = row0 + warp + 8 < p.N;
+  auto store_chunk = [&](int c) {
+    if (c * 32 + lane < vecs) {
+      const uint32_t ob = obase + uint32_t((c - c_lo) & 1) * (kMmaWin * 512);
+      uint4 v0, v1;
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(v0.x), "=r"(v0.y), "=r"(v0.z), "=r"(v0.w) : "r"(ob + lds0));
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(v1.x), "=r"(v1.y), "=r"(v1.z), "=r"(v1.w) : "r"(ob + lds0 + 8 * 512));
+      if (w0ok) *reinterpret_cast<uint4 *>(Yw + c * 256) = v0;
+      if (w1ok) *reinterpret_cast<uint4 *>(Yw + int64_t(8) * W + c * 256) = v1;
+    }
+  };
+  for (int c = c_lo; c < nch; ++c) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(NST - 2) : "memory");
+    __syncthreads();  // chunk c landed; buffer of chunk c - 1 and output tile of c - 2 are free
+    stage_chunk(c + NST - 1);
+    if (c > c_lo) store_chunk(c - 1);
+    const uint32_t bb = sbase + uint32_t(((c - c_lo) % NST) * SB) * 16u;
+    float acc[4][4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[t][q] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      if (ks >= KS) break;
+      uint32_t bf[2][4];
+      ldsm_x4_t(bb + boff[ks][0], bf[0]);
+      ldsm_x4_t(bb + boff[ks][1], bf[1]);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const uint32_t b0 = bf[t >> 1][(t & 1) * 2], b1 = bf[t >> 1][(t & 1) * 2 + 1];
+        mma_bf16_16816(acc[t], ah[ks], b0, b1);
+        mma_bf16_16816(acc[t], al[ks], b0, b1);
+      }
+    }
+    const uint32_t ob = obase + uint32_t((c - c_lo) & 1) * (kMmaWin * 512);
+#pragma unroll
+    for (int q = 0; q < 2; ++q)  // matrices (tile 2q, rows 0-7), (2q, 8-15), (2q+1, 0-7), (2q+1, 8-15)
+      stsm_x4(ob + soff[q], pack_bf16x2(acc[2 * q][0], acc[2 * q][1]),
+              pack_bf16x2(acc[2 * q][2], acc[2 * q][3]), pack_bf16x2(acc[2 * q + 1][0], acc[2 * q + 1][1]),
+              pack_bf16x2(acc[2 * q + 1][2], acc[2 * q + 1][3]));
+  }
+  __syncthreads();
+  store_chunk(nch - 1);
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 // Scalar fp32 fallback for widths that are not a multiple of 4 (test shapes only).
 __global__ void __launch_bounds__(256) k_spmm_scalar(const __grid_constant__ SpmmParams p) {
   griddep_launch_dependents();
@@ -596,6 +793,7 @@ cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s) {
   // for the window's index work and the pipeline to pay (else the per-chunk kernel below:
   // METR-LA has 13 windows of 16 rows, full PeMS 698)
   int cpc = 0;
+  const bool one_term = wp;
   if (wp) {
     const int V1 = bf ? 8 : 4;
     int mc = 0;
@@ -604,6 +802,36 @@ cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s) {
     const int ngrp = int(std::max<int64_t>(1, ceil_div(4 * kNumSMs, base)));
     cpc = int(ceil_div(mc, ngrp));
     wp = cpc >= 4;
+  }
+  // tensor-core window SpMM: bf16, 16-row windows, union <= 64, plain hops (store only)
+  bool mma = one_term && bf && w.win_rows == kMmaWin && w.win_max <= kMmaMaxK && !gen;
+  for (int i = 0; i < njobs && mma; ++i)
+    mma = !jobs[i].add && !jobs[i].accumulate && jobs[i].W % 8 == 0 &&
+          int64_t(N) * jobs[i].W < (int64_t(1) << 31);
+  {  // default where the window-resident kernel would run (>= 4 chunks per CTA); 0 = off,
+     // 1 = wherever eligible
+    const char *e = std::getenv("PGTI_SPMM_MMA");
+    if (e && e[0] == '0') mma = false;
+    else if (!(e && e[0] == '1')) mma = mma && wp;
+  }
+  if (mma) {
+    int mc = 0;
+    for (int i = 0; i < njobs; ++i) {
+      w.vecs[i] = int(jobs[i].W / 8);
+      w.nchunk[i] = int(ceil_div(w.vecs[i], 32));
+      mc = std::max(mc, w.nchunk[i]);
+    }
+    // stage ring depth: NST - 1 chunks in flight per CTA while one is multiplied (2 CTAs / SM)
+    const char *e = std::getenv("PGTI_SPMM_NST");
+    const int nst = (e && e[0] >= '2' && e[0] <= '4') ? e[0] - '0' : 3;
+    const int smem = nst * w.win_max * 512 + 2 * kMmaWin * 512 + 2 * kMmaWin * kMmaPld * 2;
+    const dim3 grid(unsigned(w.nwin), unsigned(nz), unsigned(ceil_div(mc, cpc)));
+    auto go = [&](auto kern) -> cudaError_t {
+      cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (r != cudaSuccess) return r;
+      return pdl_launch(kern, grid, dim3(256), smem, s, w, cpc);
+    };
+    return nst == 2 ? go(k_spmm_mma<2>) : nst == 4 ? go(k_spmm_mma<4>) : go(k_spmm_mma<3>);
   }
   if (wp) {
     const int V1 = bf ? 8 : 4;

@@ -694,6 +694,7 @@ def test_step_spmm_variants_bitexact(env, name, B, monkeypatch):
     (PGTI_SPMM_WP=0) and with one (PGTI_SPMM_VPL=1) give bit-identical loss, activations and
     gradients."""
     cfg = TC_CONFIGS.get(name) or synth.CONFIGS[name]
+    monkeypatch.setenv("PGTI_SPMM_MMA", "0")
     res = []
     for envs in ({}, {"PGTI_SPMM_WP": "0"}, {"PGTI_SPMM_WP": "0", "PGTI_SPMM_VPL": "1"}):
         for k in ("PGTI_SPMM_WP", "PGTI_SPMM_VPL"):
@@ -747,6 +748,7 @@ def test_step_pipelined_spmm_bitexact_at_scale(env, monkeypatch):
     y = torch.empty(cfg.B * cfg.T_out * ld, device="cuda")
     s.gather(idx, cfg.B, cfg.T_in, cfg.T_out, x, y)
     theta = synth.make_params(cfg, kind="random")
+    monkeypatch.setenv("PGTI_SPMM_MMA", "0")
     res = []
     for flag in (None, "0"):
         if flag:
@@ -758,3 +760,20 @@ def test_step_pipelined_spmm_bitexact_at_scale(env, monkeypatch):
     assert np.all(np.isfinite(res[0][1]))
     assert res[0][0] == res[1][0]
     assert np.array_equal(res[0][1], res[1][1]) and np.array_equal(res[0][2], res[1][2])
+
+
+@pytest.mark.parametrize("name,B", [("tc_big", None), ("metr_la", 64)])
+def test_step_spmm_mma_oracle(env, name, B, monkeypatch):
+    """The tensor-core window SpMM (mma.sync bf16, P_w split hi + lo; forced everywhere it is
+    eligible by PGTI_SPMM_MMA=1, e.g. METR-LA's 13 windows) regroups the fp32 sums of the bf16
+    hops and rounds the weights to 2^-17: not bit-identical to the SIMT kernels
+    (PGTI_SPMM_MMA=0), so the step is checked against the oracle at the bf16 path's tolerance,
+    and against the SIMT step at the same bound."""
+    cfg = TC_CONFIGS.get(name) or synth.CONFIGS[name]
+    monkeypatch.setenv("PGTI_SPMM_MMA", "1")
+    c = _step_case_tc(env, cfg, B=B)
+    _check_step(c, tol=TOL_BF16)
+    monkeypatch.setenv("PGTI_SPMM_MMA", "0")
+    s = _step_case_tc(env, cfg, B=B)
+    assert abs(c["loss"] - s["loss"]) <= TOL_BF16 * abs(s["loss"])
+    assert scale_rel(c["g"], s["g"]) <= TOL_BF16
