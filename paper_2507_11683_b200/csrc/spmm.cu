@@ -534,31 +534,28 @@ __global__ void __launch_bounds__(256, 2) k_spmm_mma(const __grid_constant__ Win
   __nv_bfloat16 *Ph = reinterpret_cast<__nv_bfloat16 *>(stage + NST * SB + 2 * kMmaWin * 32);
   __nv_bfloat16 *Pl = Ph + kMmaWin * kMmaPld;
 
-  // ---- the window's index work and transition block, once
+  // ---- the window's index work and transition block, once.  Index loads are issued before the
+  // wait on the predecessor grid (they read only the graph), the first chunks' loads right after
+  // it, and P_w is scattered while those are in flight.
   const int ub = __ldg(jb.win_ptr[0] + win), nu = __ldg(jb.win_ptr[0] + win + 1) - ub;
   // warp w stages union rows k = w + 8 i (i < nrow): row offsets in elements (N W < 2^31)
   const int my_node = warp + 8 * lane < nu ? __ldg(jb.win_nodes[0] + ub + warp + 8 * lane) : 0;
   const int nrow = nu > warp ? (nu - warp + 7) >> 3 : 0;
+  int beg[2], cnt[2], ec[2] = {0, 0};
+  float ev[2] = {0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {  // warp w: window rows w and w + 8, first 32 entries in registers
+    const int n = row0 + warp + 8 * i;
+    beg[i] = n < p.N ? __ldg(jb.rowptr[0] + n) : 0;
+    cnt[i] = n < p.N ? __ldg(jb.rowptr[0] + n + 1) - beg[i] : 0;
+    if (lane < cnt[i]) ec[i] = int(__ldg(jb.lcol[0] + beg[i] + lane)), ev[i] = __ldg(jb.val[0] + beg[i] + lane);
+  }
   int roff[kMmaMaxK / 8];
 #pragma unroll
   for (int i = 0; i < kMmaMaxK / 8; ++i) roff[i] = __shfl_sync(0xffffffffu, my_node, i) * W;
   const int KS = (nu + 15) >> 4;  // k-steps of 16 union rows; rows nu..16 KS-1 meet zero columns
-  for (int i = threadIdx.x; i < kMmaWin * kMmaPld; i += blockDim.x)
-    Ph[i] = __float2bfloat16_rn(0.f), Pl[i] = __float2bfloat16_rn(0.f);
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {  // warp w: window rows w and w + 8
-    const int r = warp + 8 * i, n = row0 + r;
-    if (n >= p.N) continue;
-    const int beg = __ldg(jb.rowptr[0] + n), cnt = __ldg(jb.rowptr[0] + n + 1) - beg;
-    for (int e = lane; e < cnt; e += 32) {
-      const int c = int(__ldg(jb.lcol[0] + beg + e));
-      const float v = __ldg(jb.val[0] + beg + e);
-      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-      Ph[r * kMmaPld + c] = hi;
-      Pl[r * kMmaPld + c] = __float2bfloat16_rn(v - __bfloat162float(hi));
-    }
-  }
+  for (int i = threadIdx.x; i < kMmaWin * kMmaPld / 4; i += blockDim.x)  // Ph, Pl: 2 x 2304 B
+    reinterpret_cast<uint4 *>(Ph)[i] = make_uint4(0u, 0u, 0u, 0u);
   griddep_wait();  // the dense operand is the predecessor's output
   // lane l's 16-byte vector of chunk c: global X + node W + 256 c + 8 l; shared row k, segment
   // l ^ (k & 7) = l ^ w (k = w + 8 i)
@@ -580,6 +577,19 @@ __global__ void __launch_bounds__(256, 2) k_spmm_mma(const __grid_constant__ Win
   };
 #pragma unroll
   for (int q = 0; q < NST - 1; ++q) stage_chunk(c_lo + q);
+  __syncthreads();  // P_w zeroed
+  auto put = [&](int r, int c, float v) {
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    Ph[r * kMmaPld + c] = hi;
+    Pl[r * kMmaPld + c] = __float2bfloat16_rn(v - __bfloat162float(hi));
+  };
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int r = warp + 8 * i;
+    if (lane < cnt[i]) put(r, ec[i], ev[i]);
+    for (int e = 32 + lane; e < cnt[i]; e += 32)
+      put(r, int(__ldg(jb.lcol[0] + beg[i] + e)), __ldg(jb.val[0] + beg[i] + e));
+  }
   __syncthreads();  // P_w complete
   // A fragments of all k-steps (hi and lo), kept in registers for every chunk of the window;
   // B (ldmatrix.trans) offsets: matrix mi = lane / 8 holds k rows (mi & 1) 8 + lane % 8 of the
