@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-2 confirmation at HEAD on one B200 (b): smoke, the GPU suite, the default bench line (all
 # keys), the reference arm, the other workloads, the serialised launch list, and one ncu --set
-# full capture of the dominant kernel (the pipelined staged SpMM) after its plain command.
+# full capture of the dominant kernel (the tensor-core window SpMM) after its plain command.
 T=${1:-rd2d}
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1
 timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/${T}_gpu_suite.log 2>&1
@@ -15,5 +15,5 @@ timeout 300 python bench.py --config metr_la --model encdec --no-cpu-baseline > 
 bash profiles/launches.sh pems ${T}_pe
 CMD="python profiles/prof_step.py --config pems --steps 1"
 $CMD > gpurun_out/${T}_ncu_plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_spmm_wp -s 30 -c 2 \
+ncu --set full --clock-control none --import-source on -k regex:k_spmm_mma -s 30 -c 2 \
     -o gpurun_out/${T}_spmm $CMD > gpurun_out/${T}_ncu_spmm.log 2>&1
