@@ -11,4 +11,7 @@ for N in 2 4; do
   timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N \
       --master-addr 127.0.0.1 --master-port $((29700 + N)) bench.py --gpus $N --config metr_la \
       --no-e2e > gpurun_out/${T}_bench_ml_n$N.json 2> gpurun_out/${T}_bench_ml_n$N.err
+  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N \
+      --master-addr 127.0.0.1 --master-port $((29800 + N)) bench.py --gpus $N --config pems_all_la \
+      --no-e2e > gpurun_out/${T}_bench_pal_n$N.json 2> gpurun_out/${T}_bench_pal_n$N.err
 done
