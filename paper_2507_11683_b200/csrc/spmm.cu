@@ -680,273 +680,6 @@ __global__ void __launch_bounds__(256, 2) k_spmm_mma(const __grid_constant__ Win
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
-// Persistent form of k_spmm_mma: one CTA per resident slot walks items q = blockIdx.x + k G
-// (item = window x job-group x chunk group, windows fastest) as ONE continuous chunk stream: the
-// stage ring runs across item boundaries (the next item's first chunks are staged during the
-// current item's last two), the next item's index loads are issued at the start of the current
-// item's chunk loop and its P_w is zeroed and scattered into shared memory mid-loop (the current
-// item's A fragments are already in registers), so the per-window index latency and P_w build
-// that bound the one-window CTAs (ncu: 20 % of stall samples in the prologue) overlap the
-// streaming.  Same arithmetic per output as k_spmm_mma (bit-identical).  Host guarantees: every
-// item holds >= NST - 1 chunks.
-struct MmaItem {
-  int j, win, c_lo, nch;
-  int64_t goff;
-};
-
-template <int NST>
-__global__ void __launch_bounds__(256, 2)
-    k_spmm_mmap(const __grid_constant__ WinParams p, int cpc, int nitems) {
-  // [NST][win_max][32] stage ring | output tiles [2][16][32] | P_w hi, lo [16][72] | roff [2][8][8]
-  extern __shared__ __align__(128) uint4 stage[];
-  griddep_launch_dependents();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int SB = p.win_max * 32;
-  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
-  const uint32_t obase = sbase + uint32_t(NST * SB) * 16u;
-  __nv_bfloat16 *Ph = reinterpret_cast<__nv_bfloat16 *>(stage + NST * SB + 2 * kMmaWin * 32);
-  __nv_bfloat16 *Pl = Ph + kMmaWin * kMmaPld;
-  int *roffs = reinterpret_cast<int *>(Pl + kMmaWin * kMmaPld);  // [slot][warp][8]
-  const int nz = p.z_begin[p.njobs];
-  auto decode = [&](int q) {
-    MmaItem it;
-    it.win = q % p.nwin;
-    const int r = q / p.nwin, z = r % nz, grp = r / nz;
-    int j = 0;
-#pragma unroll
-    for (int k = 1; k < kMaxSpmmJobs; ++k)
-      if (k < p.njobs && z >= p.z_begin[k]) j = k;
-    it.j = j;
-    it.goff = int64_t(z - p.z_begin[j]) * p.job[j].gstride;
-    it.c_lo = grp * cpc;
-    it.nch = min(p.nchunk[j], it.c_lo + cpc);
-    return it;
-  };
-  int q = int(blockIdx.x);
-  if (q >= nitems) return;
-
-  // ---- per-item index state: window union, this warp's staged rows, the CSR rows w, w + 8
-  struct Idx {
-    int ub, nu, node, beg[2], cnt[2], ec[2];
-    float ev[2];
-  };
-  auto load_l1 = [&](const MmaItem &it, Idx &x) {  // union extent and CSR row extents
-    const SpmmJob &jb = p.job[it.j];
-    x.ub = __ldg(jb.win_ptr[0] + it.win);
-    x.nu = __ldg(jb.win_ptr[0] + it.win + 1) - x.ub;
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int n = it.win * kMmaWin + warp + 8 * i;
-      x.beg[i] = n < p.N ? __ldg(jb.rowptr[0] + n) : 0;
-      x.cnt[i] = n < p.N ? __ldg(jb.rowptr[0] + n + 1) - x.beg[i] : 0;
-    }
-  };
-  auto load_l2 = [&](const MmaItem &it, Idx &x) {  // union node ids, first 32 entries per row
-    const SpmmJob &jb = p.job[it.j];
-    x.node = warp + 8 * lane < x.nu ? __ldg(jb.win_nodes[0] + x.ub + warp + 8 * lane) : 0;
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      x.ec[i] = 0, x.ev[i] = 0.f;
-      if (lane < x.cnt[i])
-        x.ec[i] = int(__ldg(jb.lcol[0] + x.beg[i] + lane)), x.ev[i] = __ldg(jb.val[0] + x.beg[i] + lane);
-    }
-  };
-  auto put_roffs = [&](const MmaItem &it, const Idx &x, int slot) {
-    const int v = __shfl_sync(0xffffffffu, x.node, lane & 7) * int(p.job[it.j].W);
-    if (lane < 8) roffs[(slot * 8 + warp) * 8 + lane] = v;
-    __syncwarp();
-  };
-  auto zero_P = [&]() {
-    for (int i = threadIdx.x; i < kMmaWin * kMmaPld / 4; i += blockDim.x)
-      reinterpret_cast<uint4 *>(Ph)[i] = make_uint4(0u, 0u, 0u, 0u);
-  };
-  auto scatter_P = [&](const MmaItem &it, const Idx &x) {
-    const SpmmJob &jb = p.job[it.j];
-    auto put = [&](int r, int c, float v) {
-      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-      Ph[r * kMmaPld + c] = hi;
-      Pl[r * kMmaPld + c] = __float2bfloat16_rn(v - __bfloat162float(hi));
-    };
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int r = warp + 8 * i;
-      if (lane < x.cnt[i]) put(r, x.ec[i], x.ev[i]);
-      for (int e = 32 + lane; e < x.cnt[i]; e += 32)
-        put(r, int(__ldg(jb.lcol[0] + x.beg[i] + e)), __ldg(jb.val[0] + x.beg[i] + e));
-    }
-  };
-  // chunk c of an item into ring stage st: lane l's 16-byte vector, warp w's union rows w + 8 i
-  const uint32_t sst = sbase + uint32_t(warp * 512 + ((lane ^ warp) << 4));
-  auto issue = [&](const MmaItem &it, const Idx &x, int slot, int c, int st) {
-    if (c * 32 + lane < p.vecs[it.j]) {
-      const int nrow = x.nu > warp ? (x.nu - warp + 7) >> 3 : 0;
-      const int4 r0 = *reinterpret_cast<const int4 *>(roffs + (slot * 8 + warp) * 8);
-      const int4 r1 = *reinterpret_cast<const int4 *>(roffs + (slot * 8 + warp) * 8 + 4);
-      const int ro[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-      const __nv_bfloat16 *src = reinterpret_cast<const __nv_bfloat16 *>(p.job[it.j].X[0]) +
-                                 it.goff + c * 256 + lane * 8;
-      const uint32_t dst = sst + uint32_t(st * SB) * 16u;
-#pragma unroll
-      for (int i = 0; i < kMmaMaxK / 8; ++i)
-        if (i < nrow)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + i * 4096),
-                       "l"(src + ro[i])
-                       : "memory");
-    }
-  };
-  auto commit = [] { asm volatile("cp.async.commit_group;" ::: "memory"); };
-
-  // A fragments / B offsets of the current item
-  uint32_t ah[4][4], al[4][4], boff[4][2];
-  int KS = 0;
-  auto load_frags = [&](const Idx &x) {
-    const int mi = lane >> 3, rr = lane & 7;
-    const int prow = (mi & 1) * 8 + rr, pcol = (mi >> 1) * 8;
-    const uint32_t hb = static_cast<uint32_t>(__cvta_generic_to_shared(Ph));
-    const uint32_t lb = static_cast<uint32_t>(__cvta_generic_to_shared(Pl));
-    KS = (x.nu + 15) >> 4;
-#pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
-      if (ks < KS) {
-        const uint32_t off = uint32_t((prow * kMmaPld + ks * 16 + pcol) * 2);
-        ldsm_x4(hb + off, ah[ks]);
-        ldsm_x4(lb + off, al[ks]);
-      }
-      const int k = max(min(ks * 16 + (mi & 1) * 8 + rr, x.nu - 1), 0);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int seg = warp * 4 + 2 * h + (mi >> 1);
-        boff[ks][h] = uint32_t(k * 512 + ((seg ^ (k & 7)) << 4));
-      }
-    }
-  };
-
-  // ---- first item: the one-window prologue of k_spmm_mma
-  MmaItem cur = decode(q);
-  Idx cx;
-  load_l1(cur, cx);
-  load_l2(cur, cx);
-  zero_P();
-  griddep_wait();  // the dense operand is the predecessor's output
-  put_roffs(cur, cx, 0);
-#pragma unroll
-  for (int k = 0; k < NST - 1; ++k) {
-    issue(cur, cx, 0, cur.c_lo + k, k);
-    commit();
-  }
-  __syncthreads();  // P_w zeroed
-  scatter_P(cur, cx);
-  __syncthreads();
-  load_frags(cx);
-  int slot = 0, sidx = 0;  // roff slot of the current item; ring position of its next chunk
-
-  // output: stmatrix offsets, and the pending (previous chunk's) 512-byte row stores
-  uint32_t soff[2];
-  {
-    const int mi = lane >> 3, rr = lane & 7;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int row = 8 * (mi & 1) + rr, seg = warp * 4 + 2 * k + (mi >> 1);
-      soff[k] = uint32_t(row * 512 + ((seg ^ rr) << 4));
-    }
-  }
-  const uint32_t lds0 = uint32_t(warp * 512 + ((lane ^ warp) << 4));
-  __nv_bfloat16 *pend = nullptr;  // row w of the pending chunk (+ 8 W: row w + 8), null: none
-  int pend_W = 0, pend_ok = 0, oidx = 0;
-  auto store_pending = [&]() {
-    if (pend_ok & 1) {
-      const uint32_t ob = obase + uint32_t(oidx ^ 1) * (kMmaWin * 512);
-      uint4 v0, v1;
-      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(v0.x), "=r"(v0.y), "=r"(v0.z), "=r"(v0.w) : "r"(ob + lds0));
-      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(v1.x), "=r"(v1.y), "=r"(v1.z), "=r"(v1.w) : "r"(ob + lds0 + 8 * 512));
-      if (pend_ok & 2) *reinterpret_cast<uint4 *>(pend) = v0;
-      if (pend_ok & 4) *reinterpret_cast<uint4 *>(pend + int64_t(8) * pend_W) = v1;
-    }
-  };
-
-  for (;;) {
-    const int qn = q + int(gridDim.x);
-    const bool has_next = qn < nitems;
-    MmaItem nxt{};
-    Idx nx{};
-    if (has_next) {
-      nxt = decode(qn);
-      load_l1(nxt, nx);
-    }
-    bool nx_l2 = false, nx_roff = false, nx_zero = false, nx_P = false;
-    const int W = int(p.job[cur.j].W), vecs = p.vecs[cur.j];
-    __nv_bfloat16 *Yw = reinterpret_cast<__nv_bfloat16 *>(p.job[cur.j].Y) + cur.goff +
-                        int64_t(cur.win * kMmaWin + warp) * W + lane * 8;
-    const int okrows = (cur.win * kMmaWin + warp < p.N ? 2 : 0) |
-                       (cur.win * kMmaWin + warp + 8 < p.N ? 4 : 0);
-    for (int c = cur.c_lo; c < cur.nch; ++c) {
-      asm volatile("cp.async.wait_group %0;" ::"n"(NST - 2) : "memory");
-      __syncthreads();  // chunk c landed; its ring slot - 1 and output tile of c - 2 are free
-      // the chunk NST - 1 ahead in the stream: this item's, or the next item's
-      const int t = c + NST - 1;
-      const bool need_next = t >= cur.nch;
-      if (has_next) {
-        if (!nx_l2) load_l2(nxt, nx), nx_l2 = true;
-        if (!nx_roff && (c > cur.c_lo || need_next)) put_roffs(nxt, nx, slot ^ 1), nx_roff = true;
-        if (nx_zero && !nx_P) scatter_P(nxt, nx), nx_P = true;  // zeroed one barrier earlier
-        if (!nx_zero && c >= cur.c_lo + 2 && c + 1 < cur.nch) zero_P(), nx_zero = true;
-      }
-      const int st_issue = (sidx + NST - 1) % NST;
-      if (!need_next) issue(cur, cx, slot, t, st_issue);
-      else if (has_next) issue(nxt, nx, slot ^ 1, nxt.c_lo + (t - cur.nch), st_issue);
-      commit();
-      store_pending();
-      const uint32_t bb = sbase + uint32_t(sidx * SB) * 16u;
-      float acc[4][4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) acc[i][k] = 0.f;
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        if (ks >= KS) break;
-        uint32_t bf[2][4];
-        ldsm_x4_t(bb + boff[ks][0], bf[0]);
-        ldsm_x4_t(bb + boff[ks][1], bf[1]);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint32_t b0 = bf[i >> 1][(i & 1) * 2], b1 = bf[i >> 1][(i & 1) * 2 + 1];
-          mma_bf16_16816(acc[i], ah[ks], b0, b1);
-          mma_bf16_16816(acc[i], al[ks], b0, b1);
-        }
-      }
-      const uint32_t ob = obase + uint32_t(oidx) * (kMmaWin * 512);
-#pragma unroll
-      for (int k = 0; k < 2; ++k)
-        stsm_x4(ob + soff[k], pack_bf16x2(acc[2 * k][0], acc[2 * k][1]),
-                pack_bf16x2(acc[2 * k][2], acc[2 * k][3]),
-                pack_bf16x2(acc[2 * k + 1][0], acc[2 * k + 1][1]),
-                pack_bf16x2(acc[2 * k + 1][2], acc[2 * k + 1][3]));
-      pend = Yw + c * 256, pend_W = W, pend_ok = (c * 32 + lane < vecs ? 1 : 0) | okrows;
-      oidx ^= 1;
-      sidx = (sidx + 1) % NST;
-    }
-    if (!has_next) break;
-    // ---- switch to the next item: its P_w (if the loop was too short to build it), A fragments
-    if (!nx_zero) {
-      __syncthreads();  // every warp's last ldmatrix of P_w is long done; zero after all reads
-      zero_P();
-    }
-    __syncthreads();
-    if (!nx_P) {
-      scatter_P(nxt, nx);
-      __syncthreads();
-    }
-    load_frags(nx);
-    cur = nxt, cx = nx, q = qn, slot ^= 1;
-  }
-  __syncthreads();
-  store_pending();
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-}
-
 // Scalar fp32 fallback for widths that are not a multiple of 4 (test shapes only).
 __global__ void __launch_bounds__(256) k_spmm_scalar(const __grid_constant__ SpmmParams p) {
   griddep_launch_dependents();
@@ -1103,25 +836,6 @@ cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s) {
     const int nst = (e && e[0] >= '2' && e[0] <= '4') ? e[0] - '0' : 3;
     const int smem = nst * w.win_max * 512 + 2 * kMmaWin * 512 + 2 * kMmaWin * kMmaPld * 2;
     const int ngrp = int(ceil_div(mc, cpc));
-    // persistent chunk-stream form (PGTI_SPMM_PERSIST=1): every item must hold >= nst - 1 chunks
-    {
-      const char *ep = std::getenv("PGTI_SPMM_PERSIST");
-      bool persist = nst == 3 && ep && ep[0] == '1';
-      for (int i = 0; i < njobs && persist; ++i) {
-        const int last = w.nchunk[i] - (ngrp - 1) * cpc;  // chunks of the job's last group
-        persist = last >= nst - 1;
-      }
-      const int64_t nitems = int64_t(w.nwin) * nz * ngrp;
-      if (persist && nitems < (int64_t(1) << 31)) {
-        const int smem_p = smem + 2 * 8 * 8 * 4;
-        const int nblk = int(std::min<int64_t>(nitems, 2 * kNumSMs));
-        cudaError_t r = cudaFuncSetAttribute(k_spmm_mmap<3>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem_p);
-        if (r != cudaSuccess) return r;
-        return pdl_launch(k_spmm_mmap<3>, dim3(unsigned(nblk)), dim3(256), smem_p, s, w, cpc,
-                          int(nitems));
-      }
-    }
     const dim3 grid(unsigned(w.nwin), unsigned(nz), unsigned(ngrp));
     auto go = [&](auto kern) -> cudaError_t {
       cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -777,34 +777,3 @@ def test_step_spmm_mma_oracle(env, name, B, monkeypatch):
     s = _step_case_tc(env, cfg, B=B)
     assert abs(c["loss"] - s["loss"]) <= TOL_BF16 * abs(s["loss"])
     assert scale_rel(c["g"], s["g"]) <= TOL_BF16
-
-
-@pytest.mark.parametrize("name", ["tc_big", "wp"])
-def test_step_spmm_mma_persistent_bitexact(env, name, monkeypatch):
-    """The persistent chunk-stream form of the tensor-core window SpMM (PGTI_SPMM_PERSIST=1: one
-    CTA walks many (window, job, chunk-group) items with the stage ring running across item
-    boundaries and the next item's P_w built mid-loop) computes the same products in the same
-    order as the one-item-per-CTA kernel: bit-identical loss, activations and gradients.  tc_big
-    has 2-chunk items (the next item's chunks are staged from the first iteration); the
-    PeMS-All-LA-sized case 8-chunk items over two jobs (its oracle parity is the full-size test)."""
-    pgti, torch = env
-    cfg = TC_CONFIGS.get(name) or synth.Config("wp", N=2716, E=120, F=2, T_in=12, T_out=12, L=2,
-                                               H=64, K=2, B=64)
-    v = synth.make_series(cfg)
-    s = load_series(pgti, torch, v, 0, cfg, float(v.mean()), float(v.std()))
-    graph = synth.make_graph(cfg.N, cfg.knn)
-    ld = ld_of(cfg)
-    idx = torch.arange(cfg.B, dtype=torch.int32, device="cuda")
-    x = torch.empty(cfg.B * cfg.T_in * ld, device="cuda")
-    y = torch.empty(cfg.B * cfg.T_out * ld, device="cuda")
-    s.gather(idx, cfg.B, cfg.T_in, cfg.T_out, x, y)
-    theta = synth.make_params(cfg, kind="random")
-    monkeypatch.setenv("PGTI_SPMM_MMA", "1")
-    res = []
-    for flag in ("1", "0"):
-        monkeypatch.setenv("PGTI_SPMM_PERSIST", flag)
-        model = model_for(pgti, torch, cfg, graph, precision=1)
-        res.append(run_step(pgti, torch, model, theta, x, y))
-    assert np.all(np.isfinite(res[0][1]))
-    assert res[0][0] == res[1][0]
-    assert np.array_equal(res[0][1], res[1][1]) and np.array_equal(res[0][2], res[1][2])
