@@ -550,9 +550,10 @@ __global__ void __launch_bounds__(256, 2) k_spmm_mma(const __grid_constant__ Win
     cnt[i] = n < p.N ? __ldg(jb.rowptr[0] + n + 1) - beg[i] : 0;
     if (lane < cnt[i]) ec[i] = int(__ldg(jb.lcol[0] + beg[i] + lane)), ev[i] = __ldg(jb.val[0] + beg[i] + lane);
   }
-  int roff[kMmaMaxK / 8];
+  uint32_t roff[kMmaMaxK / 8];  // byte offsets (N W 2 < 2^32): one 64-bit add per row and chunk
 #pragma unroll
-  for (int i = 0; i < kMmaMaxK / 8; ++i) roff[i] = __shfl_sync(0xffffffffu, my_node, i) * W;
+  for (int i = 0; i < kMmaMaxK / 8; ++i)
+    roff[i] = uint32_t(__shfl_sync(0xffffffffu, my_node, i)) * uint32_t(2 * W);
   const int KS = (nu + 15) >> 4;  // k-steps of 16 union rows; rows nu..16 KS-1 meet zero columns
   for (int i = threadIdx.x; i < kMmaWin * kMmaPld / 4; i += blockDim.x)  // Ph, Pl: 2 x 2304 B
     reinterpret_cast<uint4 *>(Ph)[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -565,7 +566,7 @@ __global__ void __launch_bounds__(256, 2) k_spmm_mma(const __grid_constant__ Win
   auto stage_chunk = [&](int c) {
     if (c < nch && c * 32 + lane < vecs) {
       const uint32_t dst = sst + uint32_t(((c - c_lo) % NST) * SB) * 16u;
-      const __nv_bfloat16 *src = Xl + c * 256;
+      const char *src = reinterpret_cast<const char *>(Xl + c * 256);
 #pragma unroll
       for (int i = 0; i < kMmaMaxK / 8; ++i)
         if (i < nrow)
@@ -655,15 +656,20 @@ __global__ void __launch_bounds__(256, 2) k_spmm_mma(const __grid_constant__ Win
     for (int t = 0; t < 4; ++t)
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[t][q] = 0.f;
+    // B fragments one k-step ahead of the MMAs that consume them
+    uint32_t bf[2][2][4];
+    ldsm_x4_t(bb + boff[0][0], bf[0][0]);
+    ldsm_x4_t(bb + boff[0][1], bf[0][1]);
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
       if (ks >= KS) break;
-      uint32_t bf[2][4];
-      ldsm_x4_t(bb + boff[ks][0], bf[0]);
-      ldsm_x4_t(bb + boff[ks][1], bf[1]);
+      if (ks + 1 < 4 && ks + 1 < KS) {
+        ldsm_x4_t(bb + boff[ks + 1][0], bf[(ks + 1) & 1][0]);
+        ldsm_x4_t(bb + boff[ks + 1][1], bf[(ks + 1) & 1][1]);
+      }
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        const uint32_t b0 = bf[t >> 1][(t & 1) * 2], b1 = bf[t >> 1][(t & 1) * 2 + 1];
+        const uint32_t b0 = bf[ks & 1][t >> 1][(t & 1) * 2], b1 = bf[ks & 1][t >> 1][(t & 1) * 2 + 1];
         mma_bf16_16816(acc[t], ah[ks], b0, b1);
         mma_bf16_16816(acc[t], al[ks], b0, b1);
       }
