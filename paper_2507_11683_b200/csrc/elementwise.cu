@@ -277,24 +277,29 @@ namespace {
 // grid.y = time step; thread = 8 columns (16 bytes) of one row of Xb (32-bit index math)
 __global__ void k_xpack(const float *__restrict__ Dx, int64_t x_mstride, int R, int F, int M,
                         __nv_bfloat16 *__restrict__ Xb) {
+  // thread = one row r of step t: its M F diffused channels (F-float runs of the M blocks,
+  // coalesced across the warp's consecutive rows) packed into one 128-byte bf16 row, zero-padded
   griddep_launch_dependents();
   griddep_wait();
-  const int t = blockIdx.y, mf = M * F, n = R * 8;
+  const int t = blockIdx.y, mf = M * F;
   const float *src = Dx + int64_t(t) * R * F;
-  uint4 *dst = reinterpret_cast<uint4 *>(Xb) + int64_t(t) * n;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int c8 = i & 7, r = i >> 3;
-    uint4 o = make_uint4(0u, 0u, 0u, 0u);
-    if (c8 * 8 < mf) {
-      float v[8];
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
+    uint4 *dst = reinterpret_cast<uint4 *>(Xb + (int64_t(t) * R + r) * 64);
+    int m = 0, f = 0;  // channel c = m F + f, walked in order
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int c = c8 * 8 + k, m = c / F, f = c - m * F;
-        v[k] = c < mf ? __ldg(src + m * x_mstride + int64_t(r) * F + f) : 0.f;
+    for (int o = 0; o < 8; ++o) {
+      uint4 w = make_uint4(0u, 0u, 0u, 0u);
+      if (o * 8 < mf) {
+        float v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          v[k] = o * 8 + k < mf ? __ldg(src + m * x_mstride + int64_t(r) * F + f) : 0.f;
+          if (++f == F) f = 0, ++m;
+        }
+        w = tc::pack8_bf16(v);
       }
-      o = tc::pack8_bf16(v);
+      dst[o] = w;
     }
-    dst[i] = o;
   }
 }
 }  // namespace
@@ -303,8 +308,7 @@ cudaError_t launch_xpack(const float *Dx, int64_t x_mstride, int T, int64_t R, i
                          __nv_bfloat16 *Xb, cudaStream_t s) {
   if (M * F > 64 || R * 8 >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   ProfScope prof(kProfElementwise, s, double(T) * R * (4.0 * M * F + 128.0), 0.0);
-  const int64_t n = R * 8;
-  const dim3 grid(unsigned(std::min<int64_t>(ceil_div(n, kT), 2 * 148)), unsigned(T));
+  const dim3 grid(unsigned(std::min<int64_t>(ceil_div(R, kT), 4 * 148)), unsigned(T));
   return pdl_launch(k_xpack, grid, dim3(kT), 0, s, Dx, x_mstride, int(R), F, M, Xb);
 }
 
