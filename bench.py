@@ -376,7 +376,27 @@ def kernel_trace(torch, replay, P: int, rank: int) -> dict:
     res["class_busy_ms_per_step"] = {c: _busy(sp) / P for c, sp in spans.items()}
     all_spans = [x for sp in spans.values() for x in sp]
     res["gpu_busy_ms_per_step"] = _busy(all_spans) / P
+    # idle time: gaps between the merged busy intervals, by (kernel that ended last, kernel that
+    # starts next), ms per step; the largest ones say where the step waits on dependencies
+    named = sorted(((a, b, kernel_class(e.get("name", "?")), e.get("name", "?"))
+                    for e in kev for a, b in [(float(e["ts"]) / 1e3,
+                                               float(e["ts"]) / 1e3 + float(e["dur"]) / 1e3)]))
+    gaps, end, end_name = {}, None, None
+    for a, b, _, n in named:
+        if end is not None and a > end:
+            key = f"{_short(end_name)} -> {_short(n)}"
+            gaps[key] = gaps.get(key, 0.0) + (a - end) / P
+        if end is None or b > end:
+            end, end_name = b, n
+    res["idle_gaps_ms_per_step"] = {k: round(v, 4) for k, v in
+                                    sorted(gaps.items(), key=lambda kv: -kv[1])[:12]}
     return res
+
+
+def _short(name: str) -> str:
+    """Kernel name without namespaces and parameter list (for the gap table)."""
+    n = name.replace("(anonymous namespace)::", "").split("(")[0].replace("void ", "")
+    return n.split("::")[-1]
 
 
 # ------------------------------------------------------------------------------ our arm
