@@ -399,7 +399,9 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
     // the encoder's layer-0 input rows (x fold): the packed rows Xb are chunk M of the v range
     // (they fill the otherwise empty half of the last 128-row tile), not a skinny reduction
     const bool xw = l == 0 && !dec && xfold;
-    if (xw) tw.A_in = Xb, tw.V = V + 64, tw.x_F = d.F;
+    // (+ the bias rows from Xb's ones channel when there is room for it)
+    const bool xb = xw && d.M * d.F < 64;
+    if (xw) tw.A_in = Xb, tw.V = V + 64, tw.x_F = d.F, tw.x_bias = xb ? 1 : 0;
     CU(launch_tc_wgrad(tw, ss));
     tw.A_h = Bp(Ly.DrHb[l]) + t0 * MRH, tw.h_toff = 0, tw.G = Bp(Ly.dCb[l]) + int64_t(t0) * RH;
     tw.Nout = d.H, tw.out = grads + P.Wc[ll];
@@ -414,10 +416,10 @@ pgti_status run_step_tc(const pgti_dcrnn_desc &g, const Dims &d, const float *pa
     sw.partial = Fp(Ly.spart[l]), sw.partial_cap = int64_t(Ly.spart_floats);
     sw.Gb = Bp(Ly.dGb[l]) + int64_t(t0) * 2 * RH, sw.g_tstride = 2 * RH, sw.NG = 2 * d.H;
     sw.out = grads + P.Wru[ll];
-    CU(launch_small_wgrad(sw, as));
+    if (!xb) CU(launch_small_wgrad(sw, as));
     sw.Gb = Bp(Ly.dCb[l]) + int64_t(t0) * RH, sw.g_tstride = RH, sw.NG = d.H;
     sw.out = grads + P.Wc[ll];
-    CU(launch_small_wgrad(sw, as));
+    if (!xb) CU(launch_small_wgrad(sw, as));
   }
   for (int l = 0; l < L; ++l) CU(depend(sp, sp->side[L - 1 + l], s));  // join the aux streams
   SmallWgrad rw{};

@@ -278,7 +278,9 @@ namespace {
 __global__ void k_xpack(const float *__restrict__ Dx, int64_t x_mstride, int R, int F, int M,
                         __nv_bfloat16 *__restrict__ Xb) {
   // thread = one row r of step t: its M F diffused channels (F-float runs of the M blocks,
-  // coalesced across the warp's consecutive rows) packed into one 128-byte bf16 row, zero-padded
+  // coalesced across the warp's consecutive rows) packed into one 128-byte bf16 row, then a
+  // constant 1 (channel M F: its forward weight row is zero, its weight-gradient row is the
+  // bias gradient, sum_t,r dG), zero-padded
   griddep_launch_dependents();
   griddep_wait();
   const int t = blockIdx.y, mf = M * F;
@@ -293,7 +295,9 @@ __global__ void k_xpack(const float *__restrict__ Dx, int64_t x_mstride, int R, 
         float v[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          v[k] = o * 8 + k < mf ? __ldg(src + m * x_mstride + int64_t(r) * F + f) : 0.f;
+          v[k] = o * 8 + k < mf    ? __ldg(src + m * x_mstride + int64_t(r) * F + f)
+                 : o * 8 + k == mf ? 1.f  // the ones channel: the bias row of the weight gradient
+                                   : 0.f;
           if (++f == F) f = 0, ++m;
         }
         w = tc::pack8_bf16(v);

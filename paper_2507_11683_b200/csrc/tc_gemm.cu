@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 }
 
 __global__ void k_tc_reduce(const float *__restrict__ partial, int nchunks, int V, int Nout,
-                            int vseg, int coff, int C_in, int M, int x_F,
+                            int vseg, int coff, int C_in, int M, int x_F, int x_bias,
                             float *__restrict__ out) {
   griddep_launch_dependents();
   griddep_wait();
@@ -610,6 +610,7 @@ __global__ void k_tc_reduce(const float *__restrict__ partial, int nchunks, int 
     if (x_F && m == M) {  // packed input channel c = m' x_F + f -> row m' C_in + f
       const int c = v - m * vseg, mm = c / x_F, f = c - mm * x_F;
       if (c < M * x_F) out[int64_t(mm * C_in + f) * Nout + j] = s;
+      else if (x_bias && c == M * x_F) out[int64_t(M * C_in) * Nout + j] = s;  // sum of dG
       continue;
     }
     out[int64_t(m * C_in + coff + (v - m * vseg)) * Nout + j] = s;
@@ -780,7 +781,7 @@ cudaError_t launch_tc_wgrad(const TcWgrad &p, cudaStream_t s) {
   ProfScope prof(kProfReduce, s, 4.0 * double(n) * (nchunks + 1), double(n) * nchunks);
   return pdl_launch(k_tc_reduce, dim3(unsigned(std::min<int64_t>(ceil_div(n, 256), 1184))),
                     dim3(256), 0, s, static_cast<const float *>(p.partial), nchunks, p.V, p.Nout,
-                    p.vseg, p.coff, p.C_in, p.M, p.x_F, p.out);
+                    p.vseg, p.coff, p.C_in, p.M, p.x_F, p.x_bias, p.out);
 }
 
 }  // namespace pgti

@@ -84,6 +84,9 @@ struct TcWgrad {
   // one block) are chunk M of the v range, i.e. V = (M + 1) 64, and their reduced rows
   // v = M*64 + m*x_F + f (< M*x_F) go to grads rows m*C_in + f (the layer-0 input part)
   int x_F = 0;
+  // with x_F: packed channel M*x_F is the constant 1 (k_xpack), its reduced row is the layer's
+  // bias gradient (grads row M*C_in)
+  int x_bias = 0;
 };
 cudaError_t launch_tc_wgrad(const TcWgrad &p, cudaStream_t s);
 size_t tc_wgrad_partial_floats(int V, int Nout, int T, int R);
