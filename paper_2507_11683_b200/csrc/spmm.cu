@@ -824,11 +824,12 @@ cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s) {
   for (int i = 0; i < njobs && mma; ++i)
     mma = !jobs[i].add && !jobs[i].accumulate && jobs[i].W % 8 == 0 &&
           int64_t(N) * jobs[i].W < (int64_t(1) << 31);
-  {  // default where the window-resident kernel would run (>= 4 chunks per CTA); 0 = off,
-     // 1 = wherever eligible
+  {  // default where a CTA walks >= 2 chunks of its window (full PeMS 16, PeMS-All-LA 8,
+     // PeMS-Bay 2; METR-LA's 13 windows leave 1 and the per-chunk SIMT kernel is faster there);
+     // 0 = off, 1 = wherever eligible
     const char *e = std::getenv("PGTI_SPMM_MMA");
     if (e && e[0] == '0') mma = false;
-    else if (!(e && e[0] == '1')) mma = mma && wp;
+    else if (!(e && e[0] == '1')) mma = mma && cpc >= 2;
   }
   if (mma) {
     int mc = 0;
