@@ -2,7 +2,7 @@
 # Round-2 confirmation at HEAD on one B200 (b): smoke, the GPU suite, the default bench line (all
 # keys), the reference arm, the other workloads, the serialised launch list, and one ncu --set
 # full capture of the dominant kernel (the tensor-core window SpMM) after its plain command.
-T=${1:-rd2d}
+T=${1:-rd2f}
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1
 timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/${T}_gpu_suite.log 2>&1
 S0=$SECONDS; timeout 600 python bench.py > gpurun_out/${T}_bench_default.json 2> gpurun_out/${T}_bench_default.err
