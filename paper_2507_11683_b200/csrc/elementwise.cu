@@ -277,33 +277,29 @@ namespace {
 // grid.y = time step; thread = 8 columns (16 bytes) of one row of Xb (32-bit index math)
 __global__ void k_xpack(const float *__restrict__ Dx, int64_t x_mstride, int R, int F, int M,
                         __nv_bfloat16 *__restrict__ Xb) {
-  // thread = one row r of step t: its M F diffused channels (F-float runs of the M blocks,
-  // coalesced across the warp's consecutive rows) packed into one 128-byte bf16 row, then a
-  // constant 1 (channel M F: its forward weight row is zero, its weight-gradient row is the
-  // bias gradient, sum_t,r dG), zero-padded
+  // 8 lanes per row r of step t, lane o packing channels 8o..8o+7 (the M F diffused channels, then
+  // a constant 1 at channel M F: its forward weight row is zero, its weight-gradient row is the
+  // bias gradient sum_t,r dG; zero beyond): each row's 128 bytes are one coalesced store
   griddep_launch_dependents();
   griddep_wait();
-  const int t = blockIdx.y, mf = M * F;
+  const int t = blockIdx.y, mf = M * F, o = threadIdx.x & 7;
   const float *src = Dx + int64_t(t) * R * F;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
-    uint4 *dst = reinterpret_cast<uint4 *>(Xb + (int64_t(t) * R + r) * 64);
-    int m = 0, f = 0;  // channel c = m F + f, walked in order
+  const int m0 = (o * 8) / F, f0 = o * 8 - m0 * F;  // channel 8o = m0 F + f0
+  const int rows_per_iter = gridDim.x * (blockDim.x >> 3);
+  for (int r = blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3); r < R; r += rows_per_iter) {
+    uint4 w = make_uint4(0u, 0u, 0u, 0u);
+    if (o * 8 <= mf) {
+      float v[8];
+      int m = m0, f = f0;
 #pragma unroll
-    for (int o = 0; o < 8; ++o) {
-      uint4 w = make_uint4(0u, 0u, 0u, 0u);
-      if (o * 8 < mf) {
-        float v[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          v[k] = o * 8 + k < mf    ? __ldg(src + m * x_mstride + int64_t(r) * F + f)
-                 : o * 8 + k == mf ? 1.f  // the ones channel: the bias row of the weight gradient
-                                   : 0.f;
-          if (++f == F) f = 0, ++m;
-        }
-        w = tc::pack8_bf16(v);
+      for (int k = 0; k < 8; ++k) {
+        const int c = o * 8 + k;
+        v[k] = c < mf ? __ldg(src + m * x_mstride + int64_t(r) * F + f) : c == mf ? 1.f : 0.f;
+        if (++f == F) f = 0, ++m;
       }
-      dst[o] = w;
+      w = tc::pack8_bf16(v);
     }
+    reinterpret_cast<uint4 *>(Xb + (int64_t(t) * R + r) * 64)[o] = w;
   }
 }
 }  // namespace
@@ -312,7 +308,7 @@ cudaError_t launch_xpack(const float *Dx, int64_t x_mstride, int T, int64_t R, i
                          __nv_bfloat16 *Xb, cudaStream_t s) {
   if (M * F > 64 || R * 8 >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   ProfScope prof(kProfElementwise, s, double(T) * R * (4.0 * M * F + 128.0), 0.0);
-  const dim3 grid(unsigned(std::min<int64_t>(ceil_div(R, kT), 4 * 148)), unsigned(T));
+  const dim3 grid(unsigned(std::min<int64_t>(ceil_div(R * 8, kT), 4 * 148)), unsigned(T));
   return pdl_launch(k_xpack, grid, dim3(kT), 0, s, Dx, x_mstride, int(R), F, M, Xb);
 }
 
