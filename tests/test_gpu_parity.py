@@ -777,3 +777,43 @@ def test_step_spmm_mma_oracle(env, name, B, monkeypatch):
     s = _step_case_tc(env, cfg, B=B)
     assert abs(c["loss"] - s["loss"]) <= TOL_BF16 * abs(s["loss"])
     assert scale_rel(c["g"], s["g"]) <= TOL_BF16
+
+
+def _band_graph(N, half, seed=3):
+    """Directed band graph i -> j for |i - j| <= half (random float32 weights in [0.1, 1]): rows of
+    up to 2 half + 1 entries whose 16-row window unions are exactly 16 + 2 half nodes."""
+    rng = np.random.default_rng(seed)
+    src, dst = [], []
+    for i in range(N):
+        for j in range(max(0, i - half), min(N, i + half + 1)):
+            src.append(i), dst.append(j)
+    src, dst = np.array(src, np.int32), np.array(dst, np.int32)
+    return src, dst, (0.1 + 0.9 * rng.random(src.size)).astype(np.float32)
+
+
+@pytest.mark.parametrize("B", [5, 13])
+def test_step_spmm_mma_edge_cases(env, B, monkeypatch):
+    """The tensor-core window SpMM (forced) at its limits, against the oracle at 2e-2: window
+    unions of exactly 64 nodes (4 k-steps, no padding rows), rows of 49 CSR entries (the P_w
+    scatter's second pass), a ragged last window (N = 100), partial column chunks (W = 64 B with
+    B = 5, 13: 1.25 and 3.25 chunks of 256 columns)."""
+    pgti, torch = env
+    cfg = synth.Config("tc_band", N=100, E=60, F=2, T_in=3, T_out=2, L=2, H=64, K=2, B=B)
+    ref = pipeline.Reference(cfg, graph=_band_graph(cfg.N, 24))
+    csr = pgti.add_windows(pgti.graph_build(cfg.N, *ref.graph), cfg.N, 16)
+    assert csr["win_max"] == 64 and np.max(np.diff(csr["a_rowptr"])) == 49
+    monkeypatch.setenv("PGTI_SPMM_MMA", "1")
+    s = load_series(pgti, torch, ref.v, 0, cfg, ref.mu, ref.sigma)
+    idx_np = ref.plan(1, 0)[:cfg.B]
+    ld = ld_of(cfg)
+    x = torch.empty(cfg.B * cfg.T_in * ld, device="cuda")
+    y = torch.empty(cfg.B * cfg.T_out * ld, device="cuda")
+    s.gather(torch.from_numpy(idx_np.astype(np.int32)).cuda(), cfg.B, cfg.T_in, cfg.T_out, x, y)
+    theta = synth.make_params(cfg, kind="random")
+    model = model_for(pgti, torch, cfg, ref.graph, precision=1, win_rows=16)
+    loss, g, act = run_step(pgti, torch, model, theta, x, y)
+    xo, yo = ref.batch(idx_np)
+    loss_ref, g_ref, fwd = dcgru.backward(theta.astype(np.float64), ref.d, ref.Pf, ref.Pb,
+                                          xo.astype(np.float64), yo.astype(np.float64))
+    _check_step(dict(loss=loss, g=g, act=act, loss_ref=loss_ref, g_ref=g_ref, fwd=fwd, cfg=cfg,
+                     ref=ref, margin=1.0, B=cfg.B), tol=TOL_BF16)
