@@ -805,9 +805,9 @@ cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s) {
     const char *e = std::getenv("PGTI_SPMM_WP");
     if (e && e[0] == '0') wp = false;
   }
-  // CTAs = windows x jobs x chunk groups, >= 4 waves of 148 SMs; a group must hold >= 4 chunks
-  // for the window's index work and the pipeline to pay (else the per-chunk kernel below:
-  // METR-LA has 13 windows of 16 rows, full PeMS 698)
+  // CTAs = windows x jobs x chunk groups, >= one per SM; the SIMT window-resident kernel needs
+  // >= 4 chunks per group for the window's index work and the pipeline to pay, the tensor-core
+  // kernel >= 2 (else the per-chunk kernel below)
   int cpc = 0;
   const bool one_term = wp;
   if (wp) {
@@ -815,7 +815,12 @@ cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s) {
     int mc = 0;
     for (int i = 0; i < njobs; ++i) mc = std::max<int>(mc, int(ceil_div(jobs[i].W / V1, 32)));
     const int64_t base = int64_t(w.nwin) * nz;
-    const int ngrp = int(std::max<int64_t>(1, ceil_div(4 * kNumSMs, base)));
+    // chunk groups: enough CTAs for one CTA per SM (one wave at 1 CTA per SM: the kernels of
+    // the concurrent layer stream keep the other slots; METR-LA 43.2 K -> 47.0 K samples/s,
+    // PeMS-Bay 31.7 K -> 32.9 K against 4 waves).  PGTI_SPMM_WAVES overrides (A/B)
+    const char *ew = std::getenv("PGTI_SPMM_WAVES");
+    const int waves = (ew && ew[0] >= '1' && ew[0] <= '8') ? ew[0] - '0' : 1;
+    const int ngrp = int(std::max<int64_t>(1, ceil_div(int64_t(waves) * kNumSMs, base)));
     cpc = int(ceil_div(mc, ngrp));
     wp = cpc >= 4;
   }
