@@ -326,28 +326,35 @@ __global__ void k_xpart_dgrad(const __nv_bfloat16 *__restrict__ grad,
                               const __nv_bfloat16 *__restrict__ Q, int64_t mstride, int M, int NG,
                               const float *__restrict__ W, int C_in, int F_out, int64_t R,
                               float *__restrict__ out) {
+  // warp = one row r: lanes stride the NG columns of each block by bf16 pairs (coalesced 128-byte
+  // runs), F_out partial sums per lane, then a warp reduction
   extern __shared__ float wsm[];  // [M][F_out][NG]
   for (int i = threadIdx.x; i < M * F_out * NG; i += blockDim.x) {
     const int m = i / (F_out * NG), o = (i / NG) % F_out, j = i % NG;
     wsm[i] = W[int64_t(m * C_in + o) * NG + j];
   }
   __syncthreads();
-  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < R;
-       r += int64_t(gridDim.x) * blockDim.x) {
+  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  for (int64_t r = blockIdx.x * int64_t(wpb) + (threadIdx.x >> 5); r < R;
+       r += int64_t(gridDim.x) * wpb) {
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     for (int m = 0; m < M; ++m) {
-      const __nv_bfloat162 *src = reinterpret_cast<const __nv_bfloat162 *>(
-          (m == 0 ? grad : Q + m * mstride) + r * NG);
+      const __nv_bfloat16 *src = (m == 0 ? grad : Q + m * mstride) + r * NG;
       const float *wm = wsm + m * F_out * NG;
-      for (int j2 = 0; j2 < NG / 2; ++j2) {
-        const float2 v = __bfloat1622float2(src[j2]);
+      for (int j = 2 * lane; j < NG; j += 64) {
+        const float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(src + j));
 #pragma unroll
         for (int o = 0; o < 4; ++o)
-          if (o < F_out)
-            acc[o] = fmaf(v.x, wm[o * NG + 2 * j2], fmaf(v.y, wm[o * NG + 2 * j2 + 1], acc[o]));
+          if (o < F_out) acc[o] = fmaf(v.x, wm[o * NG + j], fmaf(v.y, wm[o * NG + j + 1], acc[o]));
       }
     }
-    for (int o = 0; o < F_out; ++o) out[r * F_out + o] += acc[o];
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      float v = acc[o];
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+      if (o < F_out && lane == 0) out[r * F_out + o] += v;
+    }
   }
 }
 
@@ -359,7 +366,8 @@ cudaError_t launch_xpart_dgrad(const void *grad, const void *Q, int64_t mstride,
   const int smem = M * F_out * NG * 4;
   // a plain launch: with PDL its early-resident CTAs (a full-R grid waiting on the predecessor)
   // slowed the encoder-decoder step by 9 % (11.9 K vs 10.8 K samples/s)
-  k_xpart_dgrad<<<grid_for(R), kT, smem, s>>>(static_cast<const __nv_bfloat16 *>(grad),
+  const unsigned blocks = unsigned(std::min<int64_t>(ceil_div(R, kT / 32), 8 * 148));
+  k_xpart_dgrad<<<blocks, kT, smem, s>>>(static_cast<const __nv_bfloat16 *>(grad),
                                              static_cast<const __nv_bfloat16 *>(Q), mstride, M,
                                              NG, W, C_in, F_out, R, out);
   return cudaGetLastError();
