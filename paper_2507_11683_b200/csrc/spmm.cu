@@ -510,7 +510,9 @@ __device__ __forceinline__ void mma_bf16_16816(float *d, const uint32_t *a, uint
                : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-template <int NST>
+// ADD: the Chebyshev epilogue Y = alpha acc + beta add (add: bf16, Y's layout), applied to the
+// fp32 fragments before they are rounded and staged
+template <int NST, bool ADD = false>
 __global__ void __launch_bounds__(256, 2) k_spmm_mma(const __grid_constant__ WinParams p, int cpc) {
   // [NST][win_max][32] swizzled stage ring | output tiles [2][16][32] swizzled | P_w hi, lo [16][72]
   extern __shared__ __align__(128) uint4 stage[];
@@ -674,6 +676,24 @@ __global__ void __launch_bounds__(256, 2) k_spmm_mma(const __grid_constant__ Win
         mma_bf16_16816(acc[t], al[ks], b0, b1);
       }
     }
+    if constexpr (ADD) {  // fragment (t, hr): row gq + 8 hr, columns 2 tq, 2 tq + 1 of n-tile t
+      const __nv_bfloat16 *A = reinterpret_cast<const __nv_bfloat16 *>(jb.add) + goff;
+      const float al = jb.alpha, be = jb.beta;
+      const int gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr) {
+        const int n = row0 + gq + 8 * hr;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int col = (c * 32 + warp * 4 + t) * 8 + 2 * tq;
+          float2 a = make_float2(0.f, 0.f);
+          if (n < p.N && col < W)
+            a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(A + int64_t(n) * W + col));
+          acc[t][2 * hr] = fmaf(al, acc[t][2 * hr], be * a.x);
+          acc[t][2 * hr + 1] = fmaf(al, acc[t][2 * hr + 1], be * a.y);
+        }
+      }
+    }
     const uint32_t ob = obase + uint32_t((c - c_lo) & 1) * (kMmaWin * 512);
 #pragma unroll
     for (int q = 0; q < 2; ++q)  // matrices (tile 2q, rows 0-7), (2q, 8-15), (2q+1, 0-7), (2q+1, 8-15)
@@ -825,10 +845,15 @@ cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s) {
     wp = cpc >= 4;
   }
   // tensor-core window SpMM: bf16, 16-row windows, union <= 64, plain hops (store only)
-  bool mma = one_term && bf && w.win_rows == kMmaWin && w.win_max <= kMmaMaxK && !gen;
-  for (int i = 0; i < njobs && mma; ++i)
-    mma = !jobs[i].add && !jobs[i].accumulate && jobs[i].W % 8 == 0 &&
+  // (plain hops, or the Chebyshev form alpha acc + beta add: the ADD instantiation)
+  bool mma = one_term && bf && w.win_rows == kMmaWin && w.win_max <= kMmaMaxK;
+  bool mma_add = false;
+  for (int i = 0; i < njobs && mma; ++i) {
+    mma = !jobs[i].accumulate && !jobs[i].add2 && jobs[i].W % 8 == 0 &&
           int64_t(N) * jobs[i].W < (int64_t(1) << 31);
+    mma_add = mma_add || jobs[i].add || jobs[i].alpha != 1.f || jobs[i].beta != 1.f;
+  }
+  for (int i = 0; i < njobs && mma && mma_add; ++i) mma = jobs[i].add != nullptr;
   {  // default where a CTA walks >= 2 chunks of its window (full PeMS 16, PeMS-All-LA 8,
      // PeMS-Bay 2; METR-LA's 13 windows leave 1 and the per-chunk SIMT kernel is faster there);
      // 0 = off, 1 = wherever eligible
@@ -854,6 +879,7 @@ cudaError_t launch_spmm(SpmmJob *jobs, int njobs, int N, cudaStream_t s) {
       if (r != cudaSuccess) return r;
       return pdl_launch(kern, grid, dim3(256), smem, s, w, cpc);
     };
+    if (mma_add) return go(k_spmm_mma<3, true>);
     return nst == 2 ? go(k_spmm_mma<2>) : nst == 4 ? go(k_spmm_mma<4>) : go(k_spmm_mma<3>);
   }
   if (wp) {
