@@ -138,6 +138,16 @@ def test_cheb_step_metr_la_bf16(env):
     _check(cfg, *_step(env, cfg, 1), tol=2e-2)
 
 
+@pytest.mark.parametrize("name", ["ch_tc_k2", "ch_tc_k3", "metr_la"])
+def test_cheb_step_bf16_mma_vs_oracle(env, name, monkeypatch):
+    """The tensor-core window SpMM's Chebyshev epilogue (alpha acc + beta T_{k-2} on the fp32
+    fragments) forced on every bf16 hop (PGTI_SPMM_MMA=1): K = 2 and 3, and METR-LA B = 16,
+    against the oracle at 2e-2."""
+    cfg = TC.get(name) or synth.CONFIGS["metr_la"].replace(B=16, cheb=True)
+    monkeypatch.setenv("PGTI_SPMM_MMA", "1")
+    _check(cfg, *_step(env, cfg, 1), tol=2e-2)
+
+
 @pytest.mark.parametrize("precision,tol", [(0, 1e-5), (1, 2e-2)])
 def test_cheb_encdec_vs_oracle(env, precision, tol):
     pgti, torch = env
